@@ -1,0 +1,183 @@
+/*
+ * cocob200 — C-ABI of the B200-native module-level scaling data path.
+ *
+ * The reference (arxiv 2507.18006 "CoCoServe", package `modscale`, mounted at
+ * /root/reference) is pure Python and has no FFI: its data path is analytic
+ * (SPEC.md:136,317).  Each entry point below is the native replacement of one
+ * reference Python seam on the north-star path; the citation after each
+ * declaration names the reference function it stands behind.  The Python
+ * binding that a maintainer would add on the reference side is shown in
+ * INTEGRATION.md (ctypes, the reference's own language).
+ *
+ * Conventions
+ *  - Every function returns an int status: CB_OK (0) or a negative CB_E* code;
+ *    cb_last_error() returns the message of the last failure on this thread.
+ *  - Status mapping onto the reference's exception classes (ops.py:24-46):
+ *      CB_EINVAL     -> OpError            (invalid op / placement edit)
+ *      CB_ENOMEM     -> InfeasibleOpError  (shortfall in bytes via out-param)
+ *      CB_ENOREPLICA -> MissingReplicaError
+ *      CB_ECUDA / CB_ESTATE / CB_ENOTSUP -> RuntimeError
+ *    Infeasibility is detected before any byte moves, which keeps
+ *    batch_apply (ops.py:263-296) transactional.
+ *  - Layers are 1-based, as in PlacementState (domain.py:306-459).  Devices
+ *    are logical ids 0..n-1 of the runtime, each bound to a CUDA ordinal
+ *    (several logical devices may share one physical GPU).
+ *  - Host buffers are plain pointers; bf16 tensors are passed as uint16_t.
+ *  - Thread-compatible, not thread-safe: one host thread drives the model
+ *    ("placement mutation is single-writer").
+ */
+#ifndef COCOB200_H
+#define COCOB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CB_ABI_VERSION 1
+
+#define CB_OK 0
+#define CB_EINVAL (-1)
+#define CB_ENOMEM (-2)
+#define CB_ENOREPLICA (-3)
+#define CB_ECUDA (-4)
+#define CB_ESTATE (-5)
+#define CB_ENOTSUP (-6)
+
+/* ModuleKind ids, in the reference enum's declaration order (domain.py:23-36). */
+#define CB_ATTN_PROJ_Q 0
+#define CB_ATTN_PROJ_K 1
+#define CB_ATTN_PROJ_V 2
+#define CB_ATTN_PROJ_O 3
+#define CB_SELF_ATTENTION 4
+#define CB_FFN_PROJ_GATE 5
+#define CB_FFN_PROJ_UP 6
+#define CB_FFN_PROJ_DOWN 7
+#define CB_DECODER_LAYER 8
+#define CB_KV_CACHE 9
+/* extra readable parts of a decoder layer (norm vectors, domain.py:259) */
+#define CB_ATTN_NORM 10
+#define CB_FFN_NORM 11
+
+#define CB_PHASE_PREFILL 0
+#define CB_PHASE_DECODE 1
+
+typedef struct cb_runtime cb_runtime;
+typedef struct cb_model cb_model;
+
+typedef struct {
+  int32_t n_layers;   /* ModelSpec.n_layers   (domain.py:173-191) */
+  int32_t d_model;    /* ModelSpec.d_model */
+  int32_t d_ff;       /* ModelSpec.d_ff */
+  int32_t n_heads;    /* ModelSpec.n_heads */
+  int32_t n_kv_heads; /* == n_heads for the reference's MHA accounting; < for GQA (extension) */
+  int32_t vocab;      /* builder choice: the reference has no vocabulary */
+  int32_t max_slots;  /* concurrent sequences (KV slots) */
+  int32_t max_ctx;    /* KV positions per slot */
+  int32_t max_tokens; /* activation rows per pass (prefill chunk) */
+  float rope_theta;
+  float norm_eps;
+} cb_model_desc;
+
+/* bf16 host tensors of one decoder layer, PyTorch Linear layout [out, in]. */
+typedef struct {
+  const uint16_t* attn_norm; /* [d] */
+  const uint16_t* wq;        /* [H*hd, d] */
+  const uint16_t* wk;        /* [Hkv*hd, d] */
+  const uint16_t* wv;        /* [Hkv*hd, d] */
+  const uint16_t* wo;        /* [d, H*hd] */
+  const uint16_t* ffn_norm;  /* [d] */
+  const uint16_t* w_gate;    /* [d_ff, d] */
+  const uint16_t* w_up;      /* [d_ff, d] */
+  const uint16_t* w_down;    /* [d, d_ff] */
+} cb_layer_weights;
+
+/* Data movement of one scaling op, measured with CUDA events on the copy stream. */
+typedef struct {
+  uint64_t weight_bytes; /* bytes of module weights moved */
+  uint64_t kv_bytes;     /* bytes of KV moved */
+  float device_ms;       /* first copy start -> last copy end */
+  uint64_t shortfall_bytes; /* set on CB_ENOMEM */
+} cb_op_stats;
+
+/* ---- library ---------------------------------------------------------- */
+int cb_abi_version(void);
+const char* cb_last_error(void);
+
+/* Even integer batch split: the first p - (bs mod p) replicas get floor(bs/p),
+ * the rest ceil.  Replaces ops.split_batch (ops.py:151-158); the executor uses
+ * exactly this rule to route rows to replicas (and _kernels.py:29-33). */
+int cb_split_batch(int32_t bs, int32_t p, int32_t* shares_out);
+
+/* ---- runtime: logical devices --------------------------------------------
+ * Replaces the simulated ClusterSpec device list (domain.py:74-170): each
+ * logical device gets a compute stream, a copy stream and P2P access to every
+ * other physical GPU (NVLink through NVSwitch on an HGX B200). */
+int cb_runtime_create(int32_t n_devices, const int32_t* cuda_ordinals, cb_runtime** out);
+int cb_runtime_destroy(cb_runtime* rt);
+int cb_device_info(cb_runtime* rt, int32_t device, int32_t* num_sms, uint64_t* free_bytes,
+                   uint64_t* total_bytes);
+
+/* ---- model: module registry of device buffers -----------------------------
+ * The library owns every device buffer, keyed by (layer, ModuleKind, device). */
+int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home_device, cb_model** out);
+int cb_model_destroy(cb_model* m);
+/* Bytes of one module copy (DECODER_LAYER = ModuleCatalog.decoder_layer_mb*1e6
+ * for MHA shapes, domain.py:241-264; KV_CACHE = bytes per token per layer). */
+uint64_t cb_module_bytes(cb_model* m, int32_t kind);
+
+/* First load of a layer makes `device` its original (PlacementState.sequential,
+ * domain.py:352-359).  Weights are copied; host buffers may be freed after. */
+int cb_layer_load(cb_model* m, int32_t layer, int32_t device, const cb_layer_weights* w);
+int cb_layer_init_random(cb_model* m, int32_t layer, int32_t device, uint64_t seed, float std);
+int cb_head_load(cb_model* m, const uint16_t* embed, const uint16_t* final_norm, const uint16_t* lm_head);
+int cb_head_init_random(cb_model* m, uint64_t seed, float std);
+
+/* Byte readback of one module copy in canonical [out, in] layout (for byte
+ * parity of replication/migration).  `kind` = CB_* module id; DECODER_LAYER
+ * returns the raw contiguous layer block.  nbytes must equal the module size. */
+int cb_module_read(cb_model* m, int32_t layer, int32_t device, int32_t kind, void* host_dst, uint64_t nbytes);
+/* KV of one slot for one layer: [len][2][Hkv*hd] bf16 from the device holding it. */
+int cb_kv_read(cb_model* m, int32_t layer, int32_t slot, void* host_dst, uint64_t nbytes, int32_t* device_out);
+int cb_slot_len(cb_model* m, int32_t slot, int32_t* len_out);
+
+/* Current executor plan = the registry as the device sees it: CSR replica list
+ * (original first) like StepArrays.layer_ptr (sim.py:204-236) plus the KV
+ * device per layer (PlacementState.kv_device, domain.py:380-383). */
+int cb_get_placement(cb_model* m, int64_t* layer_ptr, int32_t* replica_dev, int32_t cap, int32_t* kv_dev);
+
+/* ---- executor hook: replaces step_batch / step_time_s (sim.py:239-300) -----
+ * One pass over `bs` sequences in admission order.  Prefill: tokens holds the
+ * concatenated prompts (prompt_lens[i] each) and the slots must be empty.
+ * Decode: one token per sequence, appended at the slot's current length.
+ * Rows are routed to each layer's replicas with cb_split_batch over sequences
+ * (contiguous ranges in replica order), activations move between devices at
+ * placement changes, and KV rows follow their sequence's replica.
+ * Outputs: greedy next token per sequence, optional fp32 logits [bs][vocab],
+ * device time of the pass. */
+int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const int32_t* tokens,
+            const int32_t* prompt_lens, int32_t* next_tokens_out, float* logits_out, float* device_ms_out);
+int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots);
+/* Routing the last step used for `layer`: per replica (device, first sequence,
+ * sequence count).  p_out = number of replicas. */
+int cb_last_routing(cb_model* m, int32_t layer, int32_t* dev_out, int32_t* seq_begin_out, int32_t* seq_count_out,
+                    int32_t cap, int32_t* p_out);
+
+/* ---- scaling operator data movement: apply() (ops.py:173-260) ------------- */
+/* ReplicateLayer (ops.py:199-211): copy the layer block original -> dst. */
+int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st);
+/* MigrateLayer (ops.py:213-228): move the original to dst; with_kv moves the
+ * layer's KV too, otherwise KV stays resident on its current device. */
+int cb_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, cb_op_stats* st);
+/* MigrateSubModule (ops.py:230-251).  KV_CACHE is supported; projection kinds
+ * return CB_ENOTSUP in this version. */
+int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, cb_op_stats* st);
+/* EvictReplica (ops.py:253-258): drop a non-original copy; KV rows it held move
+ * back to the original first. */
+int cb_evict_replica(cb_model* m, int32_t layer, int32_t device, cb_op_stats* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COCOB200_H */

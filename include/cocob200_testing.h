@@ -1,0 +1,33 @@
+/*
+ * cocob200 kernel-level test entry points.  NOT part of the drop-in boundary
+ * (include/cocob200.h is); these let tests/ drive one kernel at a time on
+ * caller-owned device buffers (torch tensors) and compare it with the CPU
+ * oracle.  All calls run on the current CUDA device's default stream and
+ * synchronize before returning.
+ */
+#ifndef COCOB200_TESTING_H
+#define COCOB200_TESTING_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* out (op)= X[row_off:row_off+T] @ W^T; epi: 0 bf16, 1 fp32, 2 fp32 residual +=, 3 SwiGLU (interleaved rows) */
+int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t row_off,
+             int32_t epi, void* out, int64_t ldo);
+int cbt_rmsnorm(const float* x, const uint16_t* gamma, uint16_t* y, int32_t T, int32_t d, float eps);
+int cbt_rope_kv(uint16_t* qkv, uint16_t* kv, const int32_t* row_slot, const int32_t* row_pos, int32_t T, int32_t H,
+                int32_t Hkv, int32_t hd, int32_t max_ctx, float theta);
+int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* row_slot,
+                  const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx);
+int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
+/* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
+int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
+                   void* out, int64_t ldo, int32_t iters, float* ms_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,271 @@
+"""Generate tests/golden/* from the reference itself.  TEST INFRASTRUCTURE ONLY.
+
+Run in the build container (the reference lives at /root/reference and does
+not travel to the GPU box; the fixtures do):
+
+    python oracle/gen_golden.py
+
+1. ``modscale_golden.json`` -- outputs of the reference package ``modscale``
+   (imported in place from /root/reference/pkg/src) for the routing / registry
+   / operator functions on the north-star path: split_batch (ops.py:151-158),
+   replica_runs (ops.py:349-358), schedule with seeded PCG64 (sim.py:157-184),
+   build_step_arrays (sim.py:216-236), ModuleCatalog.from_model
+   (domain.py:241-264), device_usage (domain.py:481-535), apply / batch_apply /
+   aggregate_cost (ops.py:173-346), PlacementState edits (domain.py:414-459).
+2. ``tiny_llama_hf.npz`` -- greedy tokens and logits of
+   ``transformers.LlamaForCausalLM`` (fp32, CPU) on the config-1 weights from
+   oracle.cpu_llama.init_weights: pins the CPU oracle.
+
+numba's cache is redirected to /tmp and bytecode writing is disabled so the
+read-only reference tree is never written.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.dont_write_bytecode = True
+
+ROOT = Path(__file__).resolve().parent.parent
+REF_SRC = Path("/root/reference/pkg/src")
+OUT = ROOT / "tests" / "golden"
+
+CONFIG1_SEED = 14  # weights seed for config 1 (largest bf16-faithful top-2 margin of seeds 0..23)
+CONFIG1_PROMPT_SEED = 0
+CONFIG1_N_REQ, CONFIG1_PROMPT, CONFIG1_NEW = 15, 16, 32
+
+
+def _placement_to_json(p):
+    return {
+        "replicas": [[[r.device_id, bool(r.is_original)] for r in row] for row in p.replicas],
+        "overrides": [[li, k.value, dev] for li, k, dev in p.overrides],
+    }
+
+
+def _build_placement(ms, spec):
+    """spec: {"n": layers, "home": dev | [devs...], "replicas": [[layer, dev], ...]}"""
+    home = spec["home"]
+    p = ms.PlacementState.sequential(spec["n"], (lambda li: home[li - 1]) if isinstance(home, list) else home)
+    for li, dev in spec.get("replicas", []):
+        p = p.with_replica(li, dev)
+    for li, kind, dev in spec.get("overrides", []):
+        p = p.with_override(li, ms.ModuleKind(kind), dev)
+    return p
+
+
+PLACEMENTS = [
+    {"n": 4, "home": 0},
+    {"n": 4, "home": 0, "replicas": [[2, 1]]},
+    {"n": 8, "home": 0, "replicas": [[3, 1], [4, 1], [7, 1]]},
+    {"n": 6, "home": 0, "replicas": [[3, 1], [4, 1], [5, 1], [3, 2], [5, 2]]},
+    {"n": 32, "home": 0, "replicas": [[li, d] for li in range(1, 17) for d in range(1, 8)]},
+    {"n": 8, "home": [0, 0, 1, 1, 2, 2, 3, 3], "replicas": [[1, 3], [2, 3], [5, 0]]},
+    {"n": 5, "home": 0, "overrides": [[2, "kv_cache", 1], [4, "attn_proj_q", 1]]},
+]
+
+
+def gen_modscale() -> dict:
+    sys.path.insert(0, str(REF_SRC))
+    import numpy as np
+    import modscale as ms
+    from modscale import ops as mops
+    from modscale import sim as msim
+
+    g: dict = {}
+    # -- split_batch
+    cases = [(bs, p) for bs in range(0, 70) for p in range(1, 10)]
+    cases += [(15, 2), (63, 8), (64, 8), (256, 8), (255, 7), (500, 40), (1, 8), (10, 4), (0, 3)]
+    g["split_batch"] = [[bs, p, ms.split_batch(bs, p)] for bs, p in cases]
+
+    # -- placements: replica_runs / build_step_arrays / device_usage / edits
+    cluster = ms.ClusterSpec.uniform([ms.DeviceSpec(i, 312000.0, 40960.0) for i in range(8)], 25000.0, 200000.0)
+    cat13 = ms.ModuleCatalog()
+    out = []
+    for spec in PLACEMENTS:
+        p = _build_placement(ms, spec)
+        arr = msim.build_step_arrays(p, cluster)
+        out.append({
+            "spec": spec,
+            "placement": _placement_to_json(p),
+            "p_vector": list(p.p_vector()),
+            "kv_device": [p.kv_device(li) for li in range(1, p.n_layers + 1)],
+            "replica_runs": {str(d): mops.replica_runs(p, d) for d in range(8)},
+            "layer_ptr": arr.layer_ptr.tolist(),
+            "caps": arr.caps.tolist(),
+            "run_min_p": arr.run_min_p.tolist(),
+            "run_bw": arr.run_bw.tolist(),
+            "busy_devices": list(arr.busy_devices),
+            "kv_layer_count": {str(k): v for k, v in arr.kv_layer_count.items()},
+            "device_usage": {str(k): [u.memory_mb, u.compute_gflops]
+                             for k, u in ms.device_usage(p, cat13, kv_tokens={0: 1234.0, 1: 77.0}).items()},
+        })
+    g["placements"] = out
+
+    # -- schedule: seeded tie-breaking draws and shortest-queue picks
+    sched = []
+    for seed, views in [(42, [(0, 0, 2.0), (1, 0, 1.0)]), (7, [(0, 3, 1.0), (1, 3, 1.0), (2, 3, 1.0)]),
+                        (0, [(0, 5, 1.0), (1, 2, 1.0)]), (0, [(0, 3, 2.0), (1, 2, 1.0)]),
+                        (3, [(2, 4, 2.0), (0, 2, 1.0), (1, 6, 3.0)])]:
+        rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed)))
+        sched.append({"seed": seed, "views": views, "picks": [msim.schedule(views, rng) for _ in range(300)]})
+    g["schedule"] = sched
+
+    # -- catalogs
+    cats = {}
+    for name, m in {"tiny": (4, 256, 768, 4), "7b": (32, 4096, 11008, 32), "13b": (40, 5120, 13824, 40),
+                    "70b": (80, 8192, 28672, 64)}.items():
+        c = ms.ModuleCatalog.from_model(ms.ModelSpec(*m))
+        cats[name] = {k: getattr(c, k) for k in c.__dataclass_fields__}
+    g["catalogs"] = cats
+
+    # -- apply / batch_apply scenarios
+    def run_ops(cat, clus, base, ops_list, kv_mb=None, extra=None, mode=None):
+        rec = []
+        p = base
+        for op in ops_list:
+            try:
+                p2, cost = mops.apply(p, op, cat, clus, kv_mb_by_layer=kv_mb, extra_used_mb=extra)
+                rec.append({"ok": True, "placement": _placement_to_json(p2), "time_s": cost.time_s,
+                            "mem_mb": cost.transient_memory_mb})
+                p = p2
+            except mops.OpError as exc:
+                rec.append({"ok": False, "error": type(exc).__name__,
+                            "shortfall_mb": getattr(exc, "shortfall_mb", None)})
+        return rec
+
+    def op_json(op):
+        d = {"type": type(op).__name__}
+        for k, v in op.__dict__.items():
+            d[k] = v.value if isinstance(v, ms.ModuleKind) else v
+        return d
+
+    small = ms.ClusterSpec.uniform([ms.DeviceSpec(0, 1.0, 10000.0), ms.DeviceSpec(1, 1.0, 1200.0)], 1.0, 10.0)
+    b200 = ms.ClusterSpec.uniform([ms.DeviceSpec(i, 2250000.0, 180000.0) for i in range(8)], 900000.0, 8000000.0)
+    cat7 = ms.ModuleCatalog.from_model(ms.ModelSpec(32, 4096, 11008, 32))
+    K = ms.ModuleKind
+    scen = [
+        ("13b_small", cat13, small, {"n": 3, "home": 0},
+         [ms.ReplicateLayer(1, 1), ms.ReplicateLayer(2, 1), ms.EvictReplica(1, 1), ms.EvictReplica(1, 1),
+          ms.MigrateLayer(3, 1, with_kv=False), ms.MigrateSubModule(2, K.KV_CACHE, 1),
+          ms.MigrateSubModule(1, K.DECODER_LAYER, 1), ms.ReplicateLayer(1, 5)], {2: 60.5}),
+        ("7b_b200", cat7, b200, {"n": 32, "home": 0},
+         [ms.ReplicateLayer(li, d) for li in (1, 2, 3) for d in (1, 2)] +
+         [ms.MigrateLayer(10, 3), ms.MigrateLayer(11, 3, with_kv=False), ms.MigrateSubModule(12, K.KV_CACHE, 4),
+          ms.MigrateSubModule(13, K.ATTN_PROJ_O, 5), ms.ReplicateLayer(13, 6), ms.MigrateSubModule(14, K.SELF_ATTENTION, 2),
+          ms.MigrateSubModule(14, K.ATTN_PROJ_Q, 2), ms.EvictReplica(2, 2), ms.ReplicateLayer(1, 1)],
+         {10: 100.0, 11: 100.0, 12: 33.5}),
+    ]
+    g["apply"] = []
+    for name, cat, clus, spec, ops_list, kv in scen:
+        base = _build_placement(ms, spec)
+        g["apply"].append({"name": name, "catalog": {k: getattr(cat, k) for k in cat.__dataclass_fields__},
+                           "cluster": {"devices": [[d.id, d.compute_gflops, d.memory_mb] for d in clus.devices],
+                                       "bandwidth": [list(r) for r in clus.bandwidth_mbps]},
+                           "base": spec, "ops": [op_json(o) for o in ops_list], "kv_mb": {str(k): v for k, v in kv.items()},
+                           "results": run_ops(cat, clus, base, ops_list, kv)})
+    # batch_apply + aggregate cost modes
+    ba = []
+    for mode in ("batched", "sequential"):
+        p = _build_placement(ms, {"n": 12, "home": 0})
+        big = ms.ClusterSpec.uniform([ms.DeviceSpec(0, 1.0, 50000.0), ms.DeviceSpec(1, 1.0, 50000.0)], 1.0, 10.0)
+        ops_list = [ms.MigrateLayer(i, 1, with_kv=(i % 2 == 0)) for i in range(1, 11)] + [
+            ms.ReplicateLayer(11, 1), ms.ReplicateLayer(12, 1), ms.EvictReplica(11, 1)]
+        p2, total, per = mops.batch_apply(p, ops_list, cat13, big, kv_mb_by_layer={i: 10.0 * i for i in range(1, 13)},
+                                          cost_mode=mode)
+        ba.append({"mode": mode, "ops": [op_json(o) for o in ops_list], "placement": _placement_to_json(p2),
+                   "total": [total.time_s, total.transient_memory_mb],
+                   "per_op": [[c.time_s, c.transient_memory_mb] for c in per]})
+    g["batch_apply"] = ba
+    # transactional failure index
+    tiny_clus = ms.ClusterSpec.uniform([ms.DeviceSpec(0, 1.0, 10000.0), ms.DeviceSpec(1, 1.0, 700.0)], 1.0, 10.0)
+    try:
+        mops.batch_apply(_build_placement(ms, {"n": 3, "home": 0}), [ms.ReplicateLayer(1, 1), ms.ReplicateLayer(2, 1)],
+                         cat13, tiny_clus)
+    except mops.BatchApplyError as exc:
+        g["batch_apply_failure_index"] = exc.index
+    return g
+
+
+def _hf_model(cfg, w):
+    import torch
+    from transformers import LlamaConfig as HFConfig, LlamaForCausalLM
+
+    from oracle.cpu_llama import from_bf16_bits
+
+    hc = HFConfig(vocab_size=cfg.vocab, hidden_size=cfg.d_model, intermediate_size=cfg.d_ff,
+                  num_hidden_layers=cfg.n_layers, num_attention_heads=cfg.n_heads,
+                  num_key_value_heads=cfg.n_kv_heads, rms_norm_eps=cfg.norm_eps, rope_theta=cfg.rope_theta,
+                  max_position_embeddings=512, tie_word_embeddings=False, attention_bias=False, mlp_bias=False,
+                  hidden_act="silu")
+    model = LlamaForCausalLM(hc).float().eval()
+    t = lambda b: torch.from_numpy(from_bf16_bits(b).copy())  # noqa: E731
+    sd = {"model.embed_tokens.weight": t(w.embed), "model.norm.weight": t(w.final_norm), "lm_head.weight": t(w.lm_head)}
+    for i, L in enumerate(w.layers):
+        p = f"model.layers.{i}."
+        sd.update({p + "input_layernorm.weight": t(L.attn_norm), p + "post_attention_layernorm.weight": t(L.ffn_norm),
+                   p + "self_attn.q_proj.weight": t(L.wq), p + "self_attn.k_proj.weight": t(L.wk),
+                   p + "self_attn.v_proj.weight": t(L.wv), p + "self_attn.o_proj.weight": t(L.wo),
+                   p + "mlp.gate_proj.weight": t(L.w_gate), p + "mlp.up_proj.weight": t(L.w_up),
+                   p + "mlp.down_proj.weight": t(L.w_down)})
+    model.load_state_dict(sd, strict=True)
+    return model
+
+
+def weights_digest(w) -> str:
+    h = hashlib.sha256()
+    for arr in [w.embed, w.final_norm, w.lm_head] + [a for L in w.layers for a in L.__dict__.values()]:
+        h.update(arr.tobytes())
+    return h.hexdigest()
+
+
+def config1_prompts():
+    import numpy as np
+
+    from oracle.cpu_llama import TINY
+
+    rng = np.random.default_rng(CONFIG1_PROMPT_SEED)
+    return [rng.integers(0, TINY.vocab, CONFIG1_PROMPT) for _ in range(CONFIG1_N_REQ)]
+
+
+def gen_tiny_hf(path: Path) -> None:
+    import numpy as np
+    import torch
+
+    sys.path.insert(0, str(ROOT))
+    from oracle.cpu_llama import TINY, init_weights
+
+    w = init_weights(TINY, CONFIG1_SEED)
+    prompts = config1_prompts()
+    model = _hf_model(TINY, w)
+    ids = torch.tensor(np.stack(prompts))
+    with torch.no_grad():
+        out = model.generate(ids, max_new_tokens=CONFIG1_NEW, do_sample=False, output_logits=True,
+                             return_dict_in_generate=True, pad_token_id=0)
+    logits = np.stack([lg.numpy() for lg in out.logits], axis=1)  # [n, steps, vocab]
+    np.savez_compressed(
+        path,
+        weights_sha256=np.array(weights_digest(w)),
+        seed=np.array(CONFIG1_SEED),
+        prompts=np.stack(prompts).astype(np.int32),
+        tokens=out.sequences[:, CONFIG1_PROMPT:].numpy().astype(np.int32),
+        logits_first=logits[:, 0].astype(np.float32),
+        logits_last=logits[:, -1].astype(np.float32),
+        logits_rowmax=logits.max(-1).astype(np.float32),
+        logits_rowsum=logits.sum(-1).astype(np.float64),
+    )
+
+
+def main() -> None:
+    OUT.mkdir(parents=True, exist_ok=True)
+    g = gen_modscale()
+    (OUT / "modscale_golden.json").write_text(json.dumps(g, indent=0, sort_keys=True))
+    gen_tiny_hf(OUT / "tiny_llama_hf.npz")
+    print("wrote", sorted(p.name for p in OUT.iterdir()))
+
+
+if __name__ == "__main__":
+    main()

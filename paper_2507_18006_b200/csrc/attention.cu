@@ -1,0 +1,199 @@
+// Warp-shuffle attention over the contiguous per-replica slot KV cache.
+//
+// Cache layout per (layer, device): [slot][max_ctx][2 (k,v)][Hkv * hd] bf16, so
+// one token's K and V rows are adjacent and one slot's live KV is the single
+// contiguous prefix [0, len) -- the byte run the reference prices as
+// `kv_bytes_per_token_per_layer` = 2*d*b (domain.py:263) and that a KV
+// migration moves (ops.py:230-251).
+//
+// Row-parallel: CTA = (row, kv head, context split).  A group of hd/8 lanes owns
+// one position (16 bytes per lane = one 128-bit load of K and of V), a warp
+// covers 32/(hd/8) positions per step, 4 warps stride the context.  Scores use
+// exp2 with q pre-scaled by log2(e)/sqrt(hd); online softmax in fp32; the
+// partial states are merged across lane groups (shuffles), warps (smem) and --
+// for short batches with long context -- across context splits (a second
+// combine kernel).  Decode attention is HBM-bound: every K/V byte is read once.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cb {
+
+static constexpr int kAttnWarps = 4;
+static constexpr int kUnroll = 4;
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq) {
+  constexpr int G = HD / 8;  // lanes per position
+  constexpr int P = 32 / G;  // positions per warp step
+  const int row = a.row_off + blockIdx.x;
+  const int hk = blockIdx.y;
+  const int split = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lg = lane % G, pg = lane / G;
+  const int slot = a.row_slot[row];
+  const int len = a.row_pos[row] + 1;
+  const int p_begin = split * chunk;
+  const int p_end = min(len, p_begin + chunk);
+  const float qscale = a.scale * 1.4426950408889634f;
+  const size_t kvd = size_t(a.Hkv) * HD;
+  const size_t pos_stride = 2 * kvd;
+  const uint16_t* kbase = a.kv + (size_t)slot * a.max_ctx * pos_stride + (size_t)hk * HD + lg * 8;
+  const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
+
+  __shared__ float sm_state[kAttnWarps][G][10];
+
+  for (int g = 0; g < gq; ++g) {
+    const int qh = hk * gq + g;
+    const uint4 qv = *reinterpret_cast<const uint4*>(a.qkv + row * qkv_ld + (size_t)qh * HD + lg * 8);
+    float q[8] = {bf16_lo(qv.x), bf16_hi(qv.x), bf16_lo(qv.y), bf16_hi(qv.y),
+                  bf16_lo(qv.z), bf16_hi(qv.z), bf16_lo(qv.w), bf16_hi(qv.w)};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] *= qscale;
+    float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+    for (int p0 = p_begin + warp * P; p0 < p_end; p0 += kAttnWarps * P * kUnroll) {
+      uint4 kk[kUnroll], vv[kUnroll];
+      bool valid[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int pos = p0 + u * kAttnWarps * P + pg;
+        valid[u] = pos < p_end;
+        if (valid[u]) {
+          const uint16_t* kp = kbase + (size_t)pos * pos_stride;
+          kk[u] = __ldg(reinterpret_cast<const uint4*>(kp));
+          vv[u] = __ldg(reinterpret_cast<const uint4*>(kp + kvd));
+        } else {
+          kk[u] = make_uint4(0, 0, 0, 0);
+          vv[u] = make_uint4(0, 0, 0, 0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        float s = q[0] * bf16_lo(kk[u].x) + q[1] * bf16_hi(kk[u].x) + q[2] * bf16_lo(kk[u].y) +
+                  q[3] * bf16_hi(kk[u].y) + q[4] * bf16_lo(kk[u].z) + q[5] * bf16_hi(kk[u].z) +
+                  q[6] * bf16_lo(kk[u].w) + q[7] * bf16_hi(kk[u].w);
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (valid[u]) {
+          const float mn = fmaxf(m, s);
+          const float cf = exp2f(m - mn);
+          const float p = exp2f(s - mn);
+          l = l * cf + p;
+          const float vf[8] = {bf16_lo(vv[u].x), bf16_hi(vv[u].x), bf16_lo(vv[u].y), bf16_hi(vv[u].y),
+                               bf16_lo(vv[u].z), bf16_hi(vv[u].z), bf16_lo(vv[u].w), bf16_hi(vv[u].w)};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = acc[i] * cf + p * vf[i];
+          m = mn;
+        }
+      }
+    }
+    // merge the P position groups of this warp (lanes with equal lg)
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o);
+      const float ol = __shfl_xor_sync(0xffffffffu, l, o);
+      float oacc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) oacc[i] = __shfl_xor_sync(0xffffffffu, acc[i], o);
+      const float mn = fmaxf(m, om);
+      const float c1 = (m == -INFINITY) ? 0.f : exp2f(m - mn);
+      const float c2 = (om == -INFINITY) ? 0.f : exp2f(om - mn);
+      l = l * c1 + ol * c2;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = acc[i] * c1 + oacc[i] * c2;
+      m = mn;
+    }
+    if (pg == 0) {
+      sm_state[warp][lg][0] = m;
+      sm_state[warp][lg][1] = l;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sm_state[warp][lg][2 + i] = acc[i];
+    }
+    __syncthreads();
+    if (warp == 0 && lane < G) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm_state[w][lane][0]);
+      float L = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int w = 0; w < kAttnWarps; ++w) {
+        const float mw = sm_state[w][lane][0];
+        const float cw = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+        L += sm_state[w][lane][1] * cw;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += sm_state[w][lane][2 + i] * cw;
+      }
+      if (nsplit == 1) {
+        const float inv = 1.f / L;
+        uint4 ov;
+        ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
+        ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
+        ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
+        ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
+        *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lane * 8) = ov;
+      } else {
+        // partial state: [(row_local * H + qh) * nsplit + split] -> (m, l, acc[HD])
+        const size_t idx = ((size_t)blockIdx.x * a.H + qh) * nsplit + split;
+        float* st = a.ws + idx * (HD + 2);
+        if (lane == 0) {
+          st[0] = M;
+          st[1] = L;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st[2 + lane * 8 + i] = o[i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int HD>
+__global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
+  const int rl = blockIdx.x, qh = blockIdx.y, i = threadIdx.x;
+  const float* st = a.ws + ((size_t)rl * a.H + qh) * nsplit * (HD + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, st[s * (HD + 2)]);
+  float L = 0.f, o = 0.f;
+  for (int s = 0; s < nsplit; ++s) {
+    const float ms = st[s * (HD + 2)];
+    const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+    L += st[s * (HD + 2) + 1] * c;
+    o += st[s * (HD + 2) + 2 + i] * c;
+  }
+  const int row = a.row_off + rl;
+  a.out[(size_t)row * a.H * HD + (size_t)qh * HD + i] = f_to_bf16(o / L);
+}
+
+template <int HD>
+static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st) {
+  const int gq = a.H / a.Hkv;
+  int nsplit = 1;
+  const long long ctas = (long long)a.T * a.Hkv;
+  if (ctas < 2LL * num_sms && a.max_len > 256) {
+    nsplit = int((2LL * num_sms + ctas - 1) / ctas);
+    nsplit = min(nsplit, (a.max_len + 255) / 256);
+    nsplit = min(nsplit, 32);
+    while (nsplit > 1 && (size_t)a.T * a.H * nsplit * (HD + 2) > a.ws_floats) --nsplit;
+  }
+  const int chunk = (a.max_len + nsplit - 1) / nsplit;
+  dim3 grid(a.T, a.Hkv, nsplit);
+  attn_kernel<HD><<<grid, kAttnWarps * 32, 0, st>>>(a, nsplit, chunk, gq);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || nsplit == 1) return e;
+  attn_combine_kernel<HD><<<dim3(a.T, a.H), HD, 0, st>>>(a, nsplit);
+  return cudaGetLastError();
+}
+
+cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st) {
+  if (a.T <= 0) return cudaSuccess;
+  switch (a.hd) {
+    case 64: return attention_hd<64>(a, num_sms, st);
+    case 128: return attention_hd<128>(a, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cb

@@ -1,0 +1,86 @@
+// Internal kernel launchers of libcocob200 (not part of the public C-ABI; see
+// include/cocob200.h for that).  All launchers are asynchronous on `st`.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cb {
+
+// ---------------------------------------------------------------- GEMM
+enum EpiKind : int {
+  EPI_BF16 = 0,    // out bf16 [row][n]           = acc
+  EPI_F32 = 1,     // out fp32 [row][n]           = acc          (lm_head logits)
+  EPI_RESID = 2,   // out fp32 [row][n]          += acc          (residual stream)
+  EPI_SWIGLU = 3,  // out bf16 [row][n/2] = silu(acc[2j]) * acc[2j+1]   (gate/up interleaved)
+};
+
+struct GemmArgs {
+  int N;        // weight rows (output features; 2*d_ff for the fused gate/up)
+  int K;        // reduction length
+  int T;        // activation rows in this launch
+  int row_off;  // first activation/output row
+  int epi;      // EpiKind
+  long long ldo;  // output row stride (elements)
+  void* out;
+  float* ws;      // stream-K partials, gemm_ws_floats(num_sms) floats
+  int* counters;  // per-tile arrival counters, zero-initialised, >= n_tiles ints
+  // filled by the launcher
+  int n_mtiles, n_ttiles, kblocks, units;
+};
+
+int make_kmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
+                    uint32_t box_rows);
+int gemm_pick_tn(int T);
+cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, int tn, int num_sms,
+                        cudaStream_t st);
+size_t gemm_ws_floats(int num_sms);
+constexpr int kGemmMaxTiles = 1 << 16;
+
+// ---------------------------------------------------------------- element-wise
+// x[row_off + t, :] = fp32(table[tokens[t], :])
+cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x, int T, int d, int row_off,
+                         cudaStream_t st);
+// y = bf16(x * rsqrt(mean(x^2) + eps) * gamma) for rows [row_off, row_off + T)
+cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, int T, int d, float eps,
+                           int row_off, cudaStream_t st);
+// In place RoPE of q,k inside qkv rows and append of (k, v) to the slot KV cache.
+// qkv row = [q: H*hd | k: Hkv*hd | v: Hkv*hd]; cache = [slot][max_ctx][2][Hkv*hd].
+cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const float2* rope, const int32_t* row_slot,
+                           const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd, int max_ctx,
+                           cudaStream_t st);
+// Row-parallel causal attention over the slot KV cache: row r attends to
+// positions [0, row_pos[r]] of its slot.  Decode (one row per sequence) and
+// prefill (one row per prompt token) share this kernel.
+struct AttnArgs {
+  const uint16_t* qkv;
+  const uint16_t* kv;
+  uint16_t* out;  // [row][H*hd]
+  const int32_t* row_slot;
+  const int32_t* row_pos;
+  float* ws;       // split-context partials
+  size_t ws_floats;
+  int T, row_off, H, Hkv, hd, max_ctx, max_len;
+  float scale;  // 1/sqrt(hd)
+};
+cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
+
+// dst[i, :] = src[idx[i], :] (bf16 rows; prefill keeps only each sequence's last row)
+cudaError_t gather_rows_launch(const uint16_t* src, const int32_t* idx, uint16_t* dst, int n, int d,
+                               cudaStream_t st);
+// logits [T][V] fp32 -> argmax index per row (ties -> lowest index)
+cudaError_t argmax_launch(const float* logits, int32_t* out, int T, int V, cudaStream_t st);
+// deterministic counter-based init: uniform with the given std, plus `mean`
+cudaError_t init_uniform_launch(uint16_t* dst, size_t n, uint64_t seed, float std, float mean, cudaStream_t st);
+// SM-driven gather copy of (src, dst, bytes) segments (16-byte aligned), used for
+// KV row moves; src/dst may be peer pointers.
+struct CopySeg {
+  const void* src;
+  void* dst;
+  unsigned long long bytes;
+};
+cudaError_t copy_segments_launch(const CopySeg* segs_dev, int nseg, cudaStream_t st);
+
+}  // namespace cb

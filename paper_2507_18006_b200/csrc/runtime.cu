@@ -1,0 +1,1110 @@
+// libcocob200 runtime: logical devices, the module registry of device buffers,
+// the decoder-layer executor (cb_step), the replica router / batch splitter and
+// the replication / migration copy engine.  Implements include/cocob200.h.
+//
+// Reference seams replaced (all Python in the reference, /root/reference/pkg):
+//   cb_split_batch        <- ops.split_batch                  ops.py:151-158
+//   cb_step               <- sim.step_batch / step_time_s     sim.py:239-300
+//                            (+ _kernels.work_units/comm_units _kernels.py:17-51)
+//   cb_replicate_layer    <- ops.apply(ReplicateLayer)        ops.py:199-211
+//   cb_migrate_layer      <- ops.apply(MigrateLayer)          ops.py:213-228
+//   cb_migrate_submodule  <- ops.apply(MigrateSubModule)      ops.py:230-251
+//   cb_evict_replica      <- ops.apply(EvictReplica)          ops.py:253-258
+//   cb_get_placement      <- sim.build_step_arrays            sim.py:216-236
+//
+// Executor data layout (per logical device that runs any layer rows):
+//   x    fp32 [max_tokens][d]       residual stream (rows indexed globally)
+//   h    bf16 [max_tokens][d]       RMSNorm output (GEMM B operand)
+//   qkv  bf16 [max_tokens][(H+2Hkv)hd]
+//   att  bf16 [max_tokens][H hd]
+//   act  bf16 [max_tokens][d_ff]    SwiGLU output
+// Layer copy = ONE contiguous block [wqkv | wo | w_gate/up interleaved | w_down
+// | attn_norm | ffn_norm], so replication/migration of a layer is one
+// peer-to-peer copy of exactly ModuleCatalog.decoder_layer_mb bytes (MHA).
+// KV per (layer, device): [slot][max_ctx][2][Hkv hd] bf16.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/cocob200.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CB_CUDA(expr)                                                                    \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(CB_ECUDA, std::string(#expr) + " failed: " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define CB_TRY(expr)          \
+  do {                        \
+    int _r = (expr);          \
+    if (_r != CB_OK) return _r; \
+  } while (0)
+
+struct DeviceCtx {
+  int id = 0;
+  int ordinal = 0;
+  int num_sms = 148;
+  cudaStream_t compute = nullptr;
+  cudaStream_t copy = nullptr;
+  std::vector<cudaEvent_t> ev_pool;  // dependency events (no timing)
+  size_t ev_next = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing events
+};
+
+constexpr int kTnCount = 5;
+int tn_index(int tn) { return tn == 16 ? 0 : tn == 32 ? 1 : tn == 64 ? 2 : tn == 128 ? 3 : 4; }
+constexpr int kTns[kTnCount] = {16, 32, 64, 128, 256};
+
+}  // namespace
+
+struct cb_runtime {
+  std::vector<DeviceCtx> devs;
+};
+
+namespace {
+
+struct LayerCopy {
+  int dev = -1;
+  uint8_t* block = nullptr;
+  CUtensorMap m_qkv, m_o, m_gu, m_d;
+};
+
+struct LayerState {
+  std::vector<LayerCopy> reps;      // original first (Replica order, domain.py:306-317)
+  int kv_override = -1;             // device holding KV when overridden, else -1
+  std::map<int, uint16_t*> kv;      // device -> KV block
+  std::vector<int> owner;           // slot -> device holding that slot's KV (-1 none)
+};
+
+struct Workspace {
+  bool ready = false;
+  float* x = nullptr;
+  uint16_t *h = nullptr, *hl = nullptr, *qkv = nullptr, *att = nullptr, *act = nullptr;
+  float* logits = nullptr;
+  int32_t* meta = nullptr;  // [tokens | row_slot | row_pos | gather]
+  int32_t* next = nullptr;
+  float* gemm_ws = nullptr;
+  int* gemm_cnt = nullptr;
+  float* attn_ws = nullptr;
+  size_t attn_ws_floats = 0;
+  float2* rope = nullptr;
+  CUtensorMap map_h[kTnCount], map_hl[kTnCount], map_att[kTnCount], map_act[kTnCount];
+};
+
+struct Route {
+  int dev, s0, cnt;
+};
+
+struct Seg {
+  int dev;      // logical device computing these rows
+  int rep;      // replica index
+  int r0, r1;   // row range
+  int s0, s1;   // sequence range
+};
+
+}  // namespace
+
+struct cb_model {
+  cb_runtime* rt = nullptr;
+  cb_model_desc d{};
+  int home = 0;
+  int hd = 0, qkv_n = 0, q_n = 0, kv_n = 0;
+  size_t off_qkv = 0, off_o = 0, off_gu = 0, off_d = 0, off_an = 0, off_fn = 0, layer_bytes = 0;
+  size_t kv_block_bytes = 0;
+  std::vector<LayerState> layers;
+  uint16_t *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  CUtensorMap m_head;
+  bool head_loaded = false;
+  std::map<int, Workspace> ws;
+  std::vector<int> slot_len;
+  int32_t* pin_meta = nullptr;
+  int32_t* pin_next = nullptr;
+  std::vector<std::vector<Route>> last_routing;
+};
+
+namespace {
+
+DeviceCtx& devctx(cb_model* m, int dev) { return m->rt->devs[dev]; }
+
+int use(const DeviceCtx& d) {
+  CB_CUDA(cudaSetDevice(d.ordinal));
+  return CB_OK;
+}
+
+// dst stream waits for everything issued so far on src's compute stream
+int depend(DeviceCtx& dst, DeviceCtx& src) {
+  if (&dst == &src) return CB_OK;
+  CB_TRY(use(src));
+  cudaEvent_t ev = src.ev_pool[src.ev_next++ % src.ev_pool.size()];
+  CB_CUDA(cudaEventRecord(ev, src.compute));
+  CB_TRY(use(dst));
+  CB_CUDA(cudaStreamWaitEvent(dst.compute, ev, 0));
+  return CB_OK;
+}
+
+int dev_alloc(const DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullptr) {
+  CB_TRY(use(d));
+  size_t free_b = 0, total_b = 0;
+  CB_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  if (bytes + (64ull << 20) > free_b) {
+    if (shortfall) *shortfall = bytes + (64ull << 20) - free_b;
+    return fail(CB_ENOMEM, "device " + std::to_string(d.id) + " lacks memory for " + std::to_string(bytes) +
+                               " bytes (free " + std::to_string(free_b) + ")");
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (shortfall) *shortfall = bytes;
+    return fail(CB_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  return CB_OK;
+}
+
+void dev_free(cb_model* m, int dev, void* p) {
+  if (!p) return;
+  cudaSetDevice(devctx(m, dev).ordinal);
+  cudaFree(p);
+}
+
+int check_layer(cb_model* m, int layer) {
+  if (layer < 1 || layer > m->d.n_layers)
+    return fail(CB_EINVAL, "unknown layer " + std::to_string(layer));
+  return CB_OK;
+}
+int check_dev(cb_model* m, int dev) {
+  if (dev < 0 || dev >= int(m->rt->devs.size()))
+    return fail(CB_EINVAL, "unknown device " + std::to_string(dev));
+  return CB_OK;
+}
+
+int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  int r = cb::make_kmajor_map(map, base, rows, k, k, box_rows);
+  if (r != 0) return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return CB_OK;
+}
+
+int ensure_ws(cb_model* m, int dev) {
+  Workspace& w = m->ws[dev];
+  if (w.ready) return CB_OK;
+  const DeviceCtx& dc = devctx(m, dev);
+  const cb_model_desc& d = m->d;
+  const size_t T = d.max_tokens;
+  CB_TRY(dev_alloc(dc, (void**)&w.x, T * d.d_model * 4));
+  CB_TRY(dev_alloc(dc, (void**)&w.h, T * d.d_model * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.hl, size_t(d.max_slots) * d.d_model * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.qkv, T * m->qkv_n * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.att, T * m->q_n * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.act, T * d.d_ff * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.meta, (3 * T + d.max_slots) * 4));
+  CB_TRY(dev_alloc(dc, (void**)&w.next, size_t(d.max_slots) * 4));
+  const size_t gws = cb::gemm_ws_floats(dc.num_sms);
+  CB_TRY(dev_alloc(dc, (void**)&w.gemm_ws, gws * 4));
+  CB_TRY(dev_alloc(dc, (void**)&w.gemm_cnt, size_t(cb::kGemmMaxTiles) * 4));
+  CB_CUDA(cudaMemset(w.gemm_cnt, 0, size_t(cb::kGemmMaxTiles) * 4));
+  w.attn_ws_floats = size_t(4 * dc.num_sms) * 8 * (m->hd + 2) * 4;
+  CB_TRY(dev_alloc(dc, (void**)&w.attn_ws, w.attn_ws_floats * 4));
+  // RoPE table, rotate-half convention: angle(pos, i) = pos * theta^(-2i/hd)
+  const int half = m->hd / 2;
+  std::vector<float2> tab(size_t(d.max_ctx) * half);
+  for (int p = 0; p < d.max_ctx; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double inv = std::pow(double(d.rope_theta), -2.0 * i / double(m->hd));
+      const double ang = double(p) * inv;
+      tab[size_t(p) * half + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+    }
+  CB_TRY(dev_alloc(dc, (void**)&w.rope, tab.size() * sizeof(float2)));
+  CB_CUDA(cudaMemcpy(w.rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  if (dev == m->home) {
+    CB_TRY(dev_alloc(dc, (void**)&w.logits, size_t(d.max_slots) * d.vocab * 4));
+  }
+  for (int i = 0; i < kTnCount; ++i) {
+    CB_TRY(make_map(&w.map_h[i], w.h, T, d.d_model, kTns[i]));
+    CB_TRY(make_map(&w.map_hl[i], w.hl, d.max_slots, d.d_model, kTns[i]));
+    CB_TRY(make_map(&w.map_att[i], w.att, T, m->q_n, kTns[i]));
+    CB_TRY(make_map(&w.map_act[i], w.act, T, d.d_ff, kTns[i]));
+  }
+  w.ready = true;
+  return CB_OK;
+}
+
+int make_layer_maps(cb_model* m, LayerCopy& c) {
+  const cb_model_desc& d = m->d;
+  CB_TRY(make_map(&c.m_qkv, c.block + m->off_qkv, m->qkv_n, d.d_model, 128));
+  CB_TRY(make_map(&c.m_o, c.block + m->off_o, d.d_model, m->q_n, 128));
+  CB_TRY(make_map(&c.m_gu, c.block + m->off_gu, 2 * size_t(d.d_ff), d.d_model, 128));
+  CB_TRY(make_map(&c.m_d, c.block + m->off_d, d.d_model, d.d_ff, 128));
+  return CB_OK;
+}
+
+int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr) {
+  if (L.kv.count(dev)) return CB_OK;
+  void* p = nullptr;
+  CB_TRY(dev_alloc(devctx(m, dev), &p, m->kv_block_bytes, shortfall));
+  L.kv[dev] = static_cast<uint16_t*>(p);
+  return CB_OK;
+}
+
+int kv_device(const LayerState& L);
+
+// Free a device's KV block for the layer once no slot's KV lives there and the
+// device no longer runs the layer's attention.
+void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
+  auto it = L.kv.find(dev);
+  if (it == L.kv.end()) return;
+  for (int o : L.owner)
+    if (o == dev) return;
+  const bool attn_here =
+      L.reps.size() > 1
+          ? std::any_of(L.reps.begin(), L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; })
+          : kv_device(L) == dev;
+  if (attn_here) return;
+  dev_free(m, dev, it->second);
+  L.kv.erase(it);
+}
+
+int kv_device(const LayerState& L) { return L.kv_override >= 0 ? L.kv_override : L.reps[0].dev; }
+
+size_t kv_token_bytes(cb_model* m) { return size_t(2) * m->kv_n * 2; }
+size_t kv_slot_offset(cb_model* m, int slot) { return size_t(slot) * m->d.max_ctx * m->kv_n * 2; }  // elements
+
+// copy KV prefix of `slot` from src block to dst block (pulled on dst's stream)
+int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t st, uint64_t* bytes) {
+  const int len = m->slot_len[slot];
+  if (len <= 0 || src == dst) return CB_OK;
+  const size_t nbytes = size_t(len) * kv_token_bytes(m);
+  const size_t off = kv_slot_offset(m, slot);
+  CB_CUDA(cudaMemcpyPeerAsync(L.kv[dst] + off, devctx(m, dst).ordinal, L.kv[src] + off,
+                              devctx(m, src).ordinal, nbytes, st));
+  if (bytes) *bytes += nbytes;
+  return CB_OK;
+}
+
+int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, int N, int K, int T, int row_off,
+         int epi, void* out, long long ldo) {
+  DeviceCtx& dc = devctx(m, dev);
+  Workspace& ws = m->ws[dev];
+  const int tn = cb::gemm_pick_tn(T);
+  cb::GemmArgs a{};
+  a.N = N;
+  a.K = K;
+  a.T = T;
+  a.row_off = row_off;
+  a.epi = epi;
+  a.ldo = ldo;
+  a.out = out;
+  a.ws = ws.gemm_ws;
+  a.counters = ws.gemm_cnt;
+  CB_CUDA(cb::gemm_launch(w, xmaps[tn_index(tn)], a, tn, dc.num_sms, dc.compute));
+  return CB_OK;
+}
+
+// Move residual rows so that every row sits on the device of its new segment.
+int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to) {
+  const size_t row_bytes = size_t(m->d.d_model) * 4;
+  for (const Seg& ns : to)
+    for (const Seg& os : from) {
+      const int a = std::max(ns.r0, os.r0), b = std::min(ns.r1, os.r1);
+      if (a >= b || os.dev == ns.dev) continue;
+      DeviceCtx& dd = devctx(m, ns.dev);
+      DeviceCtx& sd = devctx(m, os.dev);
+      CB_TRY(depend(dd, sd));
+      CB_TRY(use(dd));
+      CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].x + size_t(a) * m->d.d_model, dd.ordinal,
+                                  m->ws[os.dev].x + size_t(a) * m->d.d_model, sd.ordinal,
+                                  size_t(b - a) * row_bytes, dd.compute));
+    }
+  return CB_OK;
+}
+
+int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
+                      const std::vector<int>& row_pos) {
+  const cb_model_desc& d = m->d;
+  const LayerCopy& W = L.reps[s.rep];
+  const int dev = s.dev;
+  const int T = s.r1 - s.r0;
+  DeviceCtx& dc = devctx(m, dev);
+  Workspace& ws = m->ws[dev];
+  CB_TRY(use(dc));
+  const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
+  const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
+  CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n));
+
+  // attention runs where the rows' KV lives: on the replica itself for a
+  // replicated layer, on the KV device (MigrateSubModule KV_CACHE /
+  // MigrateLayer without KV) otherwise.
+  const int ad = L.reps.size() > 1 ? dev : kv_device(L);
+  DeviceCtx& ac = devctx(m, ad);
+  Workspace& wa = m->ws[ad];
+  const size_t qkv_row = size_t(m->qkv_n) * 2, att_row = size_t(m->q_n) * 2;
+  if (ad != dev) {
+    CB_TRY(depend(ac, dc));
+    CB_TRY(use(ac));
+    CB_CUDA(cudaMemcpyPeerAsync(reinterpret_cast<uint8_t*>(wa.qkv) + s.r0 * qkv_row, ac.ordinal,
+                                reinterpret_cast<uint8_t*>(ws.qkv) + s.r0 * qkv_row, dc.ordinal, T * qkv_row,
+                                ac.compute));
+  }
+  CB_TRY(ensure_kv(m, L, ad));
+  // KV rows follow their sequence: move any slot whose KV sits elsewhere.
+  for (int q = s.s0; q < s.s1; ++q) {
+    const int slot = seq_slot[q];
+    const int owner = L.owner[slot];
+    if (owner >= 0 && owner != ad && m->slot_len[slot] > 0) {
+      CB_TRY(depend(ac, devctx(m, owner)));
+      CB_TRY(use(ac));
+      CB_TRY(kv_move(m, L, slot, owner, ad, ac.compute, nullptr));
+    }
+    L.owner[slot] = ad;
+  }
+  CB_TRY(use(ac));
+  uint16_t* kv = L.kv[ad];
+  const int32_t* row_slot = wa.meta + d.max_tokens;
+  const int32_t* rpos = wa.meta + 2 * d.max_tokens;
+  CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
+                             d.max_ctx, ac.compute));
+  int max_len = 0;
+  for (int r = s.r0; r < s.r1; ++r) max_len = std::max(max_len, row_pos[r] + 1);
+  cb::AttnArgs aa{};
+  aa.qkv = wa.qkv;
+  aa.kv = kv;
+  aa.out = wa.att;
+  aa.row_slot = row_slot;
+  aa.row_pos = rpos;
+  aa.ws = wa.attn_ws;
+  aa.ws_floats = wa.attn_ws_floats;
+  aa.T = T;
+  aa.row_off = s.r0;
+  aa.H = d.n_heads;
+  aa.Hkv = d.n_kv_heads;
+  aa.hd = m->hd;
+  aa.max_ctx = d.max_ctx;
+  aa.max_len = max_len;
+  aa.scale = 1.0f / std::sqrt(float(m->hd));
+  CB_CUDA(cb::attention_launch(aa, ac.num_sms, ac.compute));
+  if (ad != dev) {
+    CB_TRY(depend(dc, ac));
+    CB_TRY(use(dc));
+    CB_CUDA(cudaMemcpyPeerAsync(reinterpret_cast<uint8_t*>(ws.att) + s.r0 * att_row, dc.ordinal,
+                                reinterpret_cast<uint8_t*>(wa.att) + s.r0 * att_row, ac.ordinal, T * att_row,
+                                dc.compute));
+  }
+  CB_TRY(use(dc));
+  CB_TRY(gemm(m, dev, W.m_o, ws.map_att, d.d_model, m->q_n, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
+  CB_CUDA(cb::rmsnorm_launch(ws.x, fn, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff));
+  CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
+  return CB_OK;
+}
+
+std::vector<int> split_batch_vec(int bs, int p) {
+  std::vector<int> out(p);
+  const int q = bs / p, r = bs % p;
+  for (int j = 0; j < p; ++j) out[j] = (j >= p - r) ? q + 1 : q;
+  return out;
+}
+
+// One pass over a group of sequences whose rows fit max_tokens.
+int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_t* tokens, const int32_t* lens,
+              int32_t* next_out, float* logits_out, float* ms_out) {
+  const cb_model_desc& d = m->d;
+  const bool prefill = phase == CB_PHASE_PREFILL;
+  std::vector<int> seq_row(bs + 1, 0);
+  for (int i = 0; i < bs; ++i) seq_row[i + 1] = seq_row[i] + (prefill ? lens[i] : 1);
+  const int T = seq_row[bs];
+  std::vector<int> seq_slot(slots, slots + bs);
+  std::vector<int> row_pos(T);
+  int32_t* meta = m->pin_meta;
+  for (int i = 0; i < bs; ++i)
+    for (int r = seq_row[i]; r < seq_row[i + 1]; ++r) {
+      const int pos = prefill ? r - seq_row[i] : m->slot_len[slots[i]];
+      if (pos >= d.max_ctx) return fail(CB_EINVAL, "slot " + std::to_string(slots[i]) + " exceeds max_ctx");
+      row_pos[r] = pos;
+      meta[r] = tokens[r];
+      meta[d.max_tokens + r] = slots[i];
+      meta[2 * d.max_tokens + r] = pos;
+    }
+  for (int i = 0; i < bs; ++i) meta[3 * d.max_tokens + i] = seq_row[i + 1] - 1;
+
+  // participating devices
+  std::vector<int> devs{m->home};
+  for (auto& L : m->layers) {
+    for (auto& c : L.reps) devs.push_back(c.dev);
+    devs.push_back(kv_device(L));
+  }
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  DeviceCtx& hc = devctx(m, m->home);
+  CB_TRY(use(hc));
+  CB_CUDA(cudaEventRecord(hc.t0, hc.compute));
+  const size_t meta_bytes = (3 * size_t(d.max_tokens) + d.max_slots) * 4;
+  for (int dv : devs) {
+    CB_TRY(ensure_ws(m, dv));
+    DeviceCtx& dc = devctx(m, dv);
+    CB_TRY(depend(dc, hc));
+    CB_TRY(use(dc));
+    CB_CUDA(cudaMemcpyAsync(m->ws[dv].meta, meta, meta_bytes, cudaMemcpyHostToDevice, dc.compute));
+  }
+  Workspace& hw = m->ws[m->home];
+  CB_TRY(use(hc));
+  CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
+
+  std::vector<Seg> layout{{m->home, 0, 0, T, 0, bs}};
+  m->last_routing.assign(d.n_layers, {});
+  for (int li = 0; li < d.n_layers; ++li) {
+    LayerState& L = m->layers[li];
+    const int p = int(L.reps.size());
+    const std::vector<int> shares = split_batch_vec(bs, p);
+    std::vector<Seg> segs;
+    int s0 = 0;
+    for (int j = 0; j < p; ++j) {
+      m->last_routing[li].push_back({L.reps[j].dev, s0, shares[j]});
+      if (shares[j] > 0) segs.push_back({L.reps[j].dev, j, seq_row[s0], seq_row[s0 + shares[j]], s0, s0 + shares[j]});
+      s0 += shares[j];
+    }
+    CB_TRY(reshard(m, layout, segs));
+    for (const Seg& s : segs) CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos));
+    layout = segs;
+  }
+  std::vector<Seg> home_layout{{m->home, 0, 0, T, 0, bs}};
+  CB_TRY(reshard(m, layout, home_layout));
+  // every device's trailing work joins the home stream
+  for (int dv : devs) CB_TRY(depend(hc, devctx(m, dv)));
+  CB_TRY(use(hc));
+  CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
+  const CUtensorMap* xm = hw.map_h;
+  if (prefill) {
+    CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * d.max_tokens, hw.hl, bs, d.d_model, hc.compute));
+    xm = hw.map_hl;
+  }
+  CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab));
+  CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
+  CB_CUDA(cudaEventRecord(hc.t1, hc.compute));
+  CB_CUDA(cudaMemcpyAsync(m->pin_next, hw.next, size_t(bs) * 4, cudaMemcpyDeviceToHost, hc.compute));
+  if (logits_out)
+    CB_CUDA(cudaMemcpyAsync(logits_out, hw.logits, size_t(bs) * d.vocab * 4, cudaMemcpyDeviceToHost, hc.compute));
+  CB_CUDA(cudaStreamSynchronize(hc.compute));
+  float ms = 0.f;
+  CB_CUDA(cudaEventElapsedTime(&ms, hc.t0, hc.t1));
+  if (ms_out) *ms_out += ms;
+  std::memcpy(next_out, m->pin_next, size_t(bs) * 4);
+  for (int i = 0; i < bs; ++i) m->slot_len[slots[i]] = prefill ? lens[i] : m->slot_len[slots[i]] + 1;
+  return CB_OK;
+}
+
+int layer_offsets(cb_model* m) {
+  const cb_model_desc& d = m->d;
+  const size_t dm = d.d_model;
+  m->off_qkv = 0;
+  m->off_o = m->off_qkv + size_t(m->qkv_n) * dm * 2;
+  m->off_gu = m->off_o + dm * size_t(m->q_n) * 2;
+  m->off_d = m->off_gu + 2 * size_t(d.d_ff) * dm * 2;
+  m->off_an = m->off_d + dm * size_t(d.d_ff) * 2;
+  m->off_fn = m->off_an + dm * 2;
+  m->layer_bytes = m->off_fn + dm * 2;
+  return CB_OK;
+}
+
+// host-side validation shared by the weight loaders
+int begin_layer_load(cb_model* m, int layer, int dev, LayerCopy& c) {
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dev));
+  LayerState& L = m->layers[layer - 1];
+  if (!L.reps.empty()) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already loaded");
+  c.dev = dev;
+  CB_TRY(dev_alloc(devctx(m, dev), (void**)&c.block, m->layer_bytes));
+  return CB_OK;
+}
+
+int finish_layer_load(cb_model* m, int layer, LayerCopy& c) {
+  LayerState& L = m->layers[layer - 1];
+  CB_TRY(make_layer_maps(m, c));
+  L.reps.push_back(c);
+  L.owner.assign(m->d.max_slots, -1);
+  CB_TRY(ensure_kv(m, L, c.dev));
+  CB_TRY(ensure_ws(m, c.dev));
+  return CB_OK;
+}
+
+int timed_begin(DeviceCtx& dc) {
+  CB_TRY(use(dc));
+  CB_CUDA(cudaStreamSynchronize(dc.compute));
+  CB_CUDA(cudaEventRecord(dc.t0, dc.copy));
+  return CB_OK;
+}
+int timed_end(DeviceCtx& dc, cb_op_stats* st) {
+  CB_TRY(use(dc));
+  CB_CUDA(cudaEventRecord(dc.t1, dc.copy));
+  CB_CUDA(cudaStreamSynchronize(dc.copy));
+  float ms = 0.f;
+  CB_CUDA(cudaEventElapsedTime(&ms, dc.t0, dc.t1));
+  if (st) st->device_ms = ms;
+  return CB_OK;
+}
+
+int copy_block(cb_model* m, const LayerCopy& src, LayerCopy& dst, cudaStream_t st) {
+  CB_CUDA(cudaMemcpyPeerAsync(dst.block, devctx(m, dst.dev).ordinal, src.block, devctx(m, src.dev).ordinal,
+                              m->layer_bytes, st));
+  return CB_OK;
+}
+
+void sync_all(cb_model* m) {
+  for (auto& dc : m->rt->devs) {
+    cudaSetDevice(dc.ordinal);
+    cudaStreamSynchronize(dc.compute);
+    cudaStreamSynchronize(dc.copy);
+  }
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+int cb_abi_version(void) { return CB_ABI_VERSION; }
+const char* cb_last_error(void) { return g_err.c_str(); }
+
+int cb_split_batch(int32_t bs, int32_t p, int32_t* shares_out) {
+  if (bs < 0) return fail(CB_EINVAL, "bs must be >= 0");
+  if (p < 1) return fail(CB_EINVAL, "p must be >= 1");
+  if (!shares_out) return fail(CB_EINVAL, "null output");
+  const std::vector<int> v = split_batch_vec(bs, p);
+  for (int j = 0; j < p; ++j) shares_out[j] = v[j];
+  return CB_OK;
+}
+
+int cb_runtime_create(int32_t n_devices, const int32_t* ordinals, cb_runtime** out) {
+  if (n_devices < 1 || !ordinals || !out) return fail(CB_EINVAL, "bad runtime arguments");
+  int count = 0;
+  CB_CUDA(cudaGetDeviceCount(&count));
+  auto* rt = new cb_runtime();
+  rt->devs.resize(n_devices);
+  for (int i = 0; i < n_devices; ++i) {
+    if (ordinals[i] < 0 || ordinals[i] >= count) {
+      delete rt;
+      return fail(CB_EINVAL, "CUDA ordinal " + std::to_string(ordinals[i]) + " not present");
+    }
+    DeviceCtx& dc = rt->devs[i];
+    dc.id = i;
+    dc.ordinal = ordinals[i];
+    CB_CUDA(cudaSetDevice(dc.ordinal));
+    int major = 0;
+    CB_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dc.ordinal));
+    if (major != 10) {
+      delete rt;
+      return fail(CB_ENOTSUP, "libcocob200 requires an sm_100 (B200) GPU");
+    }
+    CB_CUDA(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.ordinal));
+    CB_CUDA(cudaStreamCreateWithFlags(&dc.compute, cudaStreamNonBlocking));
+    CB_CUDA(cudaStreamCreateWithFlags(&dc.copy, cudaStreamNonBlocking));
+    dc.ev_pool.resize(1024);
+    for (auto& e : dc.ev_pool) CB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CB_CUDA(cudaEventCreate(&dc.t0));
+    CB_CUDA(cudaEventCreate(&dc.t1));
+  }
+  // all-pairs peer access between distinct physical GPUs (NVLink via NVSwitch)
+  for (auto& a : rt->devs)
+    for (auto& b : rt->devs) {
+      if (a.ordinal == b.ordinal) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a.ordinal, b.ordinal);
+      if (can) {
+        cudaSetDevice(a.ordinal);
+        cudaError_t e = cudaDeviceEnablePeerAccess(b.ordinal, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      }
+    }
+  *out = rt;
+  return CB_OK;
+}
+
+int cb_runtime_destroy(cb_runtime* rt) {
+  if (!rt) return CB_OK;
+  for (auto& dc : rt->devs) {
+    cudaSetDevice(dc.ordinal);
+    cudaStreamSynchronize(dc.compute);
+    for (auto e : dc.ev_pool) cudaEventDestroy(e);
+    cudaEventDestroy(dc.t0);
+    cudaEventDestroy(dc.t1);
+    cudaStreamDestroy(dc.compute);
+    cudaStreamDestroy(dc.copy);
+  }
+  delete rt;
+  return CB_OK;
+}
+
+int cb_device_info(cb_runtime* rt, int32_t device, int32_t* num_sms, uint64_t* free_bytes, uint64_t* total_bytes) {
+  if (!rt || device < 0 || device >= int(rt->devs.size())) return fail(CB_EINVAL, "unknown device");
+  DeviceCtx& dc = rt->devs[device];
+  CB_TRY(use(dc));
+  size_t f = 0, t = 0;
+  CB_CUDA(cudaMemGetInfo(&f, &t));
+  if (num_sms) *num_sms = dc.num_sms;
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return CB_OK;
+}
+
+int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home, cb_model** out) {
+  if (!rt || !desc || !out) return fail(CB_EINVAL, "null argument");
+  const cb_model_desc& d = *desc;
+  if (d.n_layers < 1 || d.d_model <= 0 || d.d_ff <= 0 || d.n_heads <= 0 || d.n_kv_heads <= 0)
+    return fail(CB_EINVAL, "model dimensions must be > 0");
+  if (d.d_model % d.n_heads != 0) return fail(CB_EINVAL, "d_model must be divisible by n_heads");
+  if (d.n_heads % d.n_kv_heads != 0) return fail(CB_EINVAL, "n_heads must be divisible by n_kv_heads");
+  const int hd = d.d_model / d.n_heads;
+  if (hd != 64 && hd != 128) return fail(CB_ENOTSUP, "head_dim must be 64 or 128");
+  if (d.d_model % 64 || d.d_ff % 64) return fail(CB_ENOTSUP, "d_model and d_ff must be multiples of 64");
+  if (d.vocab < 1 || d.max_slots < 1 || d.max_ctx < 1 || d.max_tokens < d.max_slots)
+    return fail(CB_EINVAL, "vocab/max_slots/max_ctx/max_tokens invalid");
+  if (home < 0 || home >= int(rt->devs.size())) return fail(CB_EINVAL, "unknown home device");
+  auto* m = new cb_model();
+  m->rt = rt;
+  m->d = d;
+  m->home = home;
+  m->hd = hd;
+  m->q_n = d.n_heads * hd;
+  m->kv_n = d.n_kv_heads * hd;
+  m->qkv_n = m->q_n + 2 * m->kv_n;
+  layer_offsets(m);
+  m->kv_block_bytes = size_t(d.max_slots) * d.max_ctx * kv_token_bytes(m);
+  m->layers.resize(d.n_layers);
+  m->slot_len.assign(d.max_slots, 0);
+  cudaSetDevice(rt->devs[home].ordinal);
+  if (cudaMallocHost(&m->pin_meta, (3 * size_t(d.max_tokens) + d.max_slots) * 4) != cudaSuccess ||
+      cudaMallocHost(&m->pin_next, size_t(d.max_slots) * 4) != cudaSuccess) {
+    delete m;
+    return fail(CB_ECUDA, "pinned host allocation failed");
+  }
+  int r = ensure_ws(m, home);
+  if (r != CB_OK) {
+    cb_model_destroy(m);
+    return r;
+  }
+  *out = m;
+  return CB_OK;
+}
+
+int cb_model_destroy(cb_model* m) {
+  if (!m) return CB_OK;
+  sync_all(m);
+  for (auto& L : m->layers) {
+    for (auto& c : L.reps) dev_free(m, c.dev, c.block);
+    for (auto& kv : L.kv) dev_free(m, kv.first, kv.second);
+  }
+  for (auto& kv : m->ws) {
+    Workspace& w = kv.second;
+    void* ptrs[] = {w.x, w.h, w.hl, w.qkv, w.att, w.act, w.logits, w.meta, w.next, w.gemm_ws, w.gemm_cnt, w.attn_ws, w.rope};
+    for (void* p : ptrs) dev_free(m, kv.first, p);
+  }
+  dev_free(m, m->home, m->embed);
+  dev_free(m, m->home, m->final_norm);
+  dev_free(m, m->home, m->lm_head);
+  if (m->pin_meta) cudaFreeHost(m->pin_meta);
+  if (m->pin_next) cudaFreeHost(m->pin_next);
+  delete m;
+  return CB_OK;
+}
+
+uint64_t cb_module_bytes(cb_model* m, int32_t kind) {
+  if (!m) return 0;
+  const size_t dm = m->d.d_model, ff = m->d.d_ff;
+  switch (kind) {
+    case CB_ATTN_PROJ_Q: return size_t(m->q_n) * dm * 2;
+    case CB_ATTN_PROJ_K:
+    case CB_ATTN_PROJ_V: return size_t(m->kv_n) * dm * 2;
+    case CB_ATTN_PROJ_O: return dm * size_t(m->q_n) * 2;
+    case CB_SELF_ATTENTION: return (size_t(m->qkv_n) * dm + dm * size_t(m->q_n)) * 2;
+    case CB_FFN_PROJ_GATE:
+    case CB_FFN_PROJ_UP:
+    case CB_FFN_PROJ_DOWN: return ff * dm * 2;
+    case CB_DECODER_LAYER: return m->layer_bytes;
+    case CB_KV_CACHE: return kv_token_bytes(m);
+    case CB_ATTN_NORM:
+    case CB_FFN_NORM: return dm * 2;
+  }
+  return 0;
+}
+
+int cb_layer_load(cb_model* m, int32_t layer, int32_t dev, const cb_layer_weights* w) {
+  if (!m || !w) return fail(CB_EINVAL, "null argument");
+  LayerCopy c;
+  CB_TRY(begin_layer_load(m, layer, dev, c));
+  const size_t dm = m->d.d_model, ff = m->d.d_ff;
+  CB_CUDA(cudaMemcpy(c.block + m->off_qkv, w->wq, size_t(m->q_n) * dm * 2, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_qkv + size_t(m->q_n) * dm * 2, w->wk, size_t(m->kv_n) * dm * 2,
+                     cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_qkv + size_t(m->q_n + m->kv_n) * dm * 2, w->wv, size_t(m->kv_n) * dm * 2,
+                     cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_o, w->wo, dm * size_t(m->q_n) * 2, cudaMemcpyHostToDevice));
+  // gate/up interleaved by row: row 2j = gate_j, row 2j+1 = up_j (SwiGLU epilogue pairs)
+  CB_CUDA(cudaMemcpy2D(c.block + m->off_gu, 2 * dm * 2, w->w_gate, dm * 2, dm * 2, ff, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy2D(c.block + m->off_gu + dm * 2, 2 * dm * 2, w->w_up, dm * 2, dm * 2, ff, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_d, w->w_down, dm * ff * 2, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_an, w->attn_norm, dm * 2, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(c.block + m->off_fn, w->ffn_norm, dm * 2, cudaMemcpyHostToDevice));
+  return finish_layer_load(m, layer, c);
+}
+
+int cb_layer_init_random(cb_model* m, int32_t layer, int32_t dev, uint64_t seed, float std) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  LayerCopy c;
+  CB_TRY(begin_layer_load(m, layer, dev, c));
+  DeviceCtx& dc = devctx(m, dev);
+  const size_t mat_elems = m->off_an / 2;
+  const uint64_t s = seed * 1000003ull + uint64_t(layer);
+  CB_CUDA(cb::init_uniform_launch(reinterpret_cast<uint16_t*>(c.block), mat_elems, s, std, 0.f, dc.compute));
+  CB_CUDA(cb::init_uniform_launch(reinterpret_cast<uint16_t*>(c.block + m->off_an), 2 * size_t(m->d.d_model), s + 7,
+                                  0.f, 1.f, dc.compute));
+  CB_CUDA(cudaStreamSynchronize(dc.compute));
+  return finish_layer_load(m, layer, c);
+}
+
+int cb_head_load(cb_model* m, const uint16_t* embed, const uint16_t* final_norm, const uint16_t* lm_head) {
+  if (!m || !embed || !final_norm || !lm_head) return fail(CB_EINVAL, "null argument");
+  const DeviceCtx& dc = devctx(m, m->home);
+  const size_t ve = size_t(m->d.vocab) * m->d.d_model * 2;
+  if (!m->embed) {
+    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve));
+    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve));
+    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2));
+  }
+  CB_TRY(use(dc));
+  CB_CUDA(cudaMemcpy(m->embed, embed, ve, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(m->lm_head, lm_head, ve, cudaMemcpyHostToDevice));
+  CB_CUDA(cudaMemcpy(m->final_norm, final_norm, size_t(m->d.d_model) * 2, cudaMemcpyHostToDevice));
+  CB_TRY(make_map(&m->m_head, m->lm_head, m->d.vocab, m->d.d_model, 128));
+  m->head_loaded = true;
+  return CB_OK;
+}
+
+int cb_head_init_random(cb_model* m, uint64_t seed, float std) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  DeviceCtx& dc = devctx(m, m->home);
+  const size_t ve = size_t(m->d.vocab) * m->d.d_model;
+  if (!m->embed) {
+    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve * 2));
+    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve * 2));
+    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2));
+  }
+  CB_TRY(use(dc));
+  CB_CUDA(cb::init_uniform_launch(m->embed, ve, seed * 31 + 1, 1.0f, 0.f, dc.compute));
+  CB_CUDA(cb::init_uniform_launch(m->lm_head, ve, seed * 31 + 2, std, 0.f, dc.compute));
+  CB_CUDA(cb::init_uniform_launch(m->final_norm, m->d.d_model, seed * 31 + 3, 0.f, 1.f, dc.compute));
+  CB_CUDA(cudaStreamSynchronize(dc.compute));
+  CB_TRY(make_map(&m->m_head, m->lm_head, m->d.vocab, m->d.d_model, 128));
+  m->head_loaded = true;
+  return CB_OK;
+}
+
+int cb_module_read(cb_model* m, int32_t layer, int32_t dev, int32_t kind, void* dst, uint64_t nbytes) {
+  if (!m || !dst) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_layer(m, layer));
+  LayerState& L = m->layers[layer - 1];
+  const LayerCopy* c = nullptr;
+  for (auto& r : L.reps)
+    if (r.dev == dev) c = &r;
+  if (!c) return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no copy on device " + std::to_string(dev));
+  const uint64_t want = cb_module_bytes(m, kind);
+  if (kind == CB_KV_CACHE || want == 0) return fail(CB_EINVAL, "kind not readable here (use cb_kv_read)");
+  if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
+  CB_TRY(use(devctx(m, dev)));
+  sync_all(m);
+  const size_t dm = m->d.d_model, ff = m->d.d_ff;
+  uint8_t* out = static_cast<uint8_t*>(dst);
+  const uint8_t* b = c->block;
+  switch (kind) {
+    case CB_ATTN_PROJ_Q: CB_CUDA(cudaMemcpy(out, b + m->off_qkv, want, cudaMemcpyDeviceToHost)); break;
+    case CB_ATTN_PROJ_K:
+      CB_CUDA(cudaMemcpy(out, b + m->off_qkv + size_t(m->q_n) * dm * 2, want, cudaMemcpyDeviceToHost));
+      break;
+    case CB_ATTN_PROJ_V:
+      CB_CUDA(cudaMemcpy(out, b + m->off_qkv + size_t(m->q_n + m->kv_n) * dm * 2, want, cudaMemcpyDeviceToHost));
+      break;
+    case CB_ATTN_PROJ_O: CB_CUDA(cudaMemcpy(out, b + m->off_o, want, cudaMemcpyDeviceToHost)); break;
+    case CB_SELF_ATTENTION: CB_CUDA(cudaMemcpy(out, b + m->off_qkv, want, cudaMemcpyDeviceToHost)); break;
+    case CB_FFN_PROJ_GATE:
+      CB_CUDA(cudaMemcpy2D(out, dm * 2, b + m->off_gu, 2 * dm * 2, dm * 2, ff, cudaMemcpyDeviceToHost));
+      break;
+    case CB_FFN_PROJ_UP:
+      CB_CUDA(cudaMemcpy2D(out, dm * 2, b + m->off_gu + dm * 2, 2 * dm * 2, dm * 2, ff, cudaMemcpyDeviceToHost));
+      break;
+    case CB_FFN_PROJ_DOWN: CB_CUDA(cudaMemcpy(out, b + m->off_d, want, cudaMemcpyDeviceToHost)); break;
+    case CB_DECODER_LAYER: CB_CUDA(cudaMemcpy(out, b, want, cudaMemcpyDeviceToHost)); break;
+    case CB_ATTN_NORM: CB_CUDA(cudaMemcpy(out, b + m->off_an, want, cudaMemcpyDeviceToHost)); break;
+    case CB_FFN_NORM: CB_CUDA(cudaMemcpy(out, b + m->off_fn, want, cudaMemcpyDeviceToHost)); break;
+    default: return fail(CB_EINVAL, "unknown kind");
+  }
+  return CB_OK;
+}
+
+int cb_kv_read(cb_model* m, int32_t layer, int32_t slot, void* dst, uint64_t nbytes, int32_t* dev_out) {
+  if (!m || !dst) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_layer(m, layer));
+  if (slot < 0 || slot >= m->d.max_slots) return fail(CB_EINVAL, "unknown slot");
+  LayerState& L = m->layers[layer - 1];
+  const int owner = L.owner.empty() ? -1 : L.owner[slot];
+  const uint64_t want = uint64_t(m->slot_len[slot]) * kv_token_bytes(m);
+  if (owner < 0 || want == 0) return fail(CB_ESTATE, "slot holds no KV for this layer");
+  if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
+  sync_all(m);
+  CB_TRY(use(devctx(m, owner)));
+  CB_CUDA(cudaMemcpy(dst, L.kv[owner] + kv_slot_offset(m, slot), want, cudaMemcpyDeviceToHost));
+  if (dev_out) *dev_out = owner;
+  return CB_OK;
+}
+
+int cb_slot_len(cb_model* m, int32_t slot, int32_t* len_out) {
+  if (!m || !len_out || slot < 0 || slot >= m->d.max_slots) return fail(CB_EINVAL, "bad slot");
+  *len_out = m->slot_len[slot];
+  return CB_OK;
+}
+
+int cb_get_placement(cb_model* m, int64_t* layer_ptr, int32_t* replica_dev, int32_t cap, int32_t* kv_dev) {
+  if (!m || !layer_ptr || !replica_dev || !kv_dev) return fail(CB_EINVAL, "null argument");
+  int64_t n = 0;
+  layer_ptr[0] = 0;
+  for (int li = 0; li < m->d.n_layers; ++li) {
+    const LayerState& L = m->layers[li];
+    for (const auto& c : L.reps) {
+      if (n >= cap) return fail(CB_EINVAL, "replica_dev capacity too small");
+      replica_dev[n++] = c.dev;
+    }
+    layer_ptr[li + 1] = n;
+    kv_dev[li] = L.reps.empty() ? -1 : kv_device(L);
+  }
+  return CB_OK;
+}
+
+int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const int32_t* tokens,
+            const int32_t* prompt_lens, int32_t* next_out, float* logits_out, float* ms_out) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (ms_out) *ms_out = 0.f;
+  if (bs == 0) return CB_OK;
+  if (bs < 0 || bs > m->d.max_slots || !slots || !tokens || !next_out)
+    return fail(CB_EINVAL, "bad batch arguments");
+  if (phase != CB_PHASE_PREFILL && phase != CB_PHASE_DECODE) return fail(CB_EINVAL, "unknown phase");
+  if (!m->head_loaded) return fail(CB_ESTATE, "embedding / lm_head not loaded");
+  for (auto& L : m->layers)
+    if (L.reps.empty()) return fail(CB_ESTATE, "a decoder layer is not loaded");
+  std::vector<char> seen(m->d.max_slots, 0);
+  for (int i = 0; i < bs; ++i) {
+    if (slots[i] < 0 || slots[i] >= m->d.max_slots) return fail(CB_EINVAL, "slot out of range");
+    if (seen[slots[i]]++) return fail(CB_EINVAL, "duplicate slot in batch");
+    const int len = m->slot_len[slots[i]];
+    if (phase == CB_PHASE_PREFILL && len != 0) return fail(CB_EINVAL, "prefill into a non-empty slot");
+    if (phase == CB_PHASE_DECODE && len == 0) return fail(CB_EINVAL, "decode on an empty slot");
+  }
+  if (phase == CB_PHASE_DECODE) return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out);
+  if (!prompt_lens) return fail(CB_EINVAL, "prefill needs prompt_lens");
+  // prefill: group sequences so each pass fits max_tokens rows
+  int i = 0, tok_off = 0;
+  while (i < bs) {
+    int j = i, rows = 0;
+    while (j < bs && rows + prompt_lens[j] <= m->d.max_tokens) {
+      if (prompt_lens[j] < 1 || prompt_lens[j] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
+      rows += prompt_lens[j++];
+    }
+    if (j == i) return fail(CB_EINVAL, "prompt longer than max_tokens");
+    CB_TRY(step_pass(m, phase, j - i, slots + i, tokens + tok_off, prompt_lens + i, next_out + i,
+                     logits_out ? logits_out + size_t(i) * m->d.vocab : nullptr, ms_out));
+    tok_off += rows;
+    i = j;
+  }
+  return CB_OK;
+}
+
+int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots) {
+  if (!m || (n > 0 && !slots)) return fail(CB_EINVAL, "null argument");
+  for (int i = 0; i < n; ++i) {
+    if (slots[i] < 0 || slots[i] >= m->d.max_slots) return fail(CB_EINVAL, "slot out of range");
+    m->slot_len[slots[i]] = 0;
+    for (auto& L : m->layers)
+      if (!L.owner.empty()) L.owner[slots[i]] = -1;
+  }
+  return CB_OK;
+}
+
+int cb_last_routing(cb_model* m, int32_t layer, int32_t* dev_out, int32_t* s0_out, int32_t* cnt_out, int32_t cap,
+                    int32_t* p_out) {
+  if (!m || !p_out) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_layer(m, layer));
+  if (m->last_routing.empty()) return fail(CB_ESTATE, "no step has run");
+  const auto& r = m->last_routing[layer - 1];
+  *p_out = int(r.size());
+  if (int(r.size()) > cap) return fail(CB_EINVAL, "capacity too small");
+  for (size_t j = 0; j < r.size(); ++j) {
+    dev_out[j] = r[j].dev;
+    s0_out[j] = r[j].s0;
+    cnt_out[j] = r[j].cnt;
+  }
+  return CB_OK;
+}
+
+int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dst));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  for (auto& c : L.reps)
+    if (c.dev == dst) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
+  if (L.kv_override >= 0) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
+  LayerCopy c;
+  c.dev = dst;
+  uint64_t shortfall = 0;
+  int r = dev_alloc(devctx(m, dst), (void**)&c.block, m->layer_bytes, &shortfall);
+  if (r == CB_OK) r = ensure_kv(m, L, dst, &shortfall);
+  if (r != CB_OK) {
+    if (c.block) dev_free(m, dst, c.block);
+    if (st) st->shortfall_bytes = shortfall;
+    return r;
+  }
+  CB_TRY(ensure_ws(m, dst));
+  sync_all(m);
+  DeviceCtx& dc = devctx(m, dst);
+  CB_TRY(timed_begin(dc));
+  CB_TRY(copy_block(m, L.reps[0], c, dc.copy));
+  CB_TRY(timed_end(dc, st));
+  if (st) st->weight_bytes = m->layer_bytes;
+  CB_TRY(make_layer_maps(m, c));
+  L.reps.push_back(c);
+  return CB_OK;
+}
+
+int cb_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dst));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  const int src = L.reps[0].dev;
+  if (dst == src) return fail(CB_EINVAL, "layer original already on device " + std::to_string(dst));
+  for (auto& c : L.reps)
+    if (c.dev == dst) return fail(CB_EINVAL, "layer already has a copy on device " + std::to_string(dst));
+  if (!with_kv && L.reps.size() > 1) return fail(CB_EINVAL, "cannot detach KV from a replicated layer");
+  const int kv_src = kv_device(L);
+  LayerCopy c;
+  c.dev = dst;
+  uint64_t shortfall = 0;
+  int r = dev_alloc(devctx(m, dst), (void**)&c.block, m->layer_bytes, &shortfall);
+  if (r == CB_OK && with_kv) r = ensure_kv(m, L, dst, &shortfall);
+  if (r != CB_OK) {
+    if (c.block) dev_free(m, dst, c.block);
+    if (st) st->shortfall_bytes = shortfall;
+    return r;
+  }
+  CB_TRY(ensure_ws(m, dst));
+  sync_all(m);
+  DeviceCtx& dc = devctx(m, dst);
+  CB_TRY(timed_begin(dc));
+  CB_TRY(copy_block(m, L.reps[0], c, dc.copy));
+  uint64_t kvb = 0;
+  if (with_kv) {
+    for (int slot = 0; slot < m->d.max_slots; ++slot) {
+      // KV held by the layer's KV device follows the layer; replica-held rows stay
+      if (L.owner[slot] == kv_src) {
+        CB_TRY(kv_move(m, L, slot, kv_src, dst, dc.copy, &kvb));
+        L.owner[slot] = dst;
+      }
+    }
+  }
+  CB_TRY(timed_end(dc, st));
+  if (st) {
+    st->weight_bytes = m->layer_bytes;
+    st->kv_bytes = kvb;
+  }
+  CB_TRY(make_layer_maps(m, c));
+  LayerCopy old = L.reps[0];
+  L.reps[0] = c;
+  dev_free(m, old.dev, old.block);
+  if (with_kv) {
+    L.kv_override = -1;
+  } else {
+    L.kv_override = kv_src;  // KV stays resident where it was (domain.py:445-451)
+  }
+  for (int dv : std::vector<int>{old.dev, kv_src}) drop_kv_if_unused(m, L, dv);
+  return CB_OK;
+}
+
+int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dst));
+  if (kind == CB_DECODER_LAYER) return fail(CB_EINVAL, "whole layers move via MigrateLayer");
+  if (kind != CB_KV_CACHE) return fail(CB_ENOTSUP, "projection / attention sub-module migration not supported yet");
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
+  uint64_t shortfall = 0;
+  int r = ensure_kv(m, L, dst, &shortfall);
+  if (r != CB_OK) {
+    if (st) st->shortfall_bytes = shortfall;
+    return r;
+  }
+  CB_TRY(ensure_ws(m, dst));
+  const int old_kv = kv_device(L);
+  sync_all(m);
+  DeviceCtx& dc = devctx(m, dst);
+  CB_TRY(timed_begin(dc));
+  uint64_t kvb = 0;
+  for (int slot = 0; slot < m->d.max_slots; ++slot) {
+    const int o = L.owner[slot];
+    if (o >= 0 && o != dst) {
+      CB_TRY(kv_move(m, L, slot, o, dst, dc.copy, &kvb));
+      L.owner[slot] = dst;
+    }
+  }
+  CB_TRY(timed_end(dc, st));
+  if (st) st->kv_bytes = kvb;
+  L.kv_override = dst;
+  drop_kv_if_unused(m, L, old_kv);
+  return CB_OK;
+}
+
+int cb_evict_replica(cb_model* m, int32_t layer, int32_t dev, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  CB_TRY(check_layer(m, layer));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (L.reps[0].dev == dev) return fail(CB_ENOREPLICA, "cannot evict the original replica");
+  auto it = std::find_if(L.reps.begin() + 1, L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; });
+  if (it == L.reps.end())
+    return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no replica on device " + std::to_string(dev));
+  const int orig = L.reps[0].dev;
+  sync_all(m);
+  DeviceCtx& oc = devctx(m, orig);
+  CB_TRY(timed_begin(oc));
+  uint64_t kvb = 0;
+  for (int slot = 0; slot < m->d.max_slots; ++slot)
+    if (L.owner[slot] == dev) {
+      CB_TRY(kv_move(m, L, slot, dev, orig, oc.copy, &kvb));
+      L.owner[slot] = orig;
+    }
+  CB_TRY(timed_end(oc, st));
+  if (st) st->kv_bytes = kvb;
+  dev_free(m, dev, it->block);
+  L.reps.erase(it);
+  drop_kv_if_unused(m, L, dev);
+  return CB_OK;
+}
+
+}  // extern "C"
