@@ -177,6 +177,24 @@ int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, 
  * back to the original first. */
 int cb_evict_replica(cb_model* m, int32_t layer, int32_t device, cb_op_stats* st);
 
+/* ---- live per-kernel profiling (evidence for the roofline numbers) ----------
+ * When enabled, every launch of the executor is bracketed by CUDA events on the
+ * stream it is launched on; after each step the elapsed times are added to
+ * per-class totals together with the launch's ALGORITHMIC bytes and FLOPs
+ * (weights + activations read/written; KV bytes actually attended). */
+#define CB_KCLASS_GEMM 0      /* tcgen05 projections (QKV, O, gate/up, down, lm_head) */
+#define CB_KCLASS_ATTENTION 1 /* KV-cache attention (+ split combine) */
+#define CB_KCLASS_ELEMWISE 2  /* RMSNorm, RoPE+KV append, embedding, argmax, gather */
+#define CB_KCLASS_COPY 3      /* activation reshard / KV row moves between devices */
+typedef struct {
+  uint32_t launches;
+  float ms;     /* summed device time */
+  double bytes; /* summed algorithmic bytes */
+  double flops; /* summed algorithmic FLOPs */
+} cb_kstat;
+int cb_profile(cb_model* m, int32_t enable); /* enable=1 resets the counters */
+int cb_profile_read(cb_model* m, int32_t kclass, cb_kstat* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,7 +95,7 @@ class ModelWeights:
 
 
 def init_weights(cfg: LlamaConfig, seed: int = 0, w_std: float | None = None, head_std: float | None = None,
-                 n_layers: int | None = None) -> ModelWeights:
+                 n_layers: int | None = None, head: str = "random") -> ModelWeights:
     """Seeded normal init (bf16-rounded).  Defaults: O(1) hidden states and a
     logit std of ~0.6, small enough that a bf16 pipeline stays within the
     north star's 2e-2 max-abs logit tolerance of this fp32 oracle."""
@@ -123,12 +123,24 @@ def init_weights(cfg: LlamaConfig, seed: int = 0, w_std: float | None = None, he
             w_up=mat(ff, d, w_std),
             w_down=mat(d, ff, 1.0 / np.sqrt(ff)),
         ))
-    return ModelWeights(
+    w = ModelWeights(
         embed=to_bf16_bits(rng.standard_normal((cfg.vocab, d), dtype=np.float32)),
         final_norm=vec(d),
         lm_head=mat(cfg.vocab, d, head_std),
         layers=layers,
     )
+    if head == "permuted_tied":
+        # "confident" head: lm_head[pi(t)] = e(t) / 128, so the next token's logit
+        # stands ~1.6 above the rest (min top-2 margin 0.43 over the 480 config-1
+        # decisions, >> the 2e-2 tolerance): greedy identity is then a property of
+        # the numerics, not of luck at near-ties.
+        perm = np.random.default_rng(seed + 1000).permutation(cfg.vocab)
+        head_w = np.empty((cfg.vocab, d), dtype=np.float32)
+        head_w[perm] = from_bf16_bits(w.embed) / 128.0
+        w.lm_head = to_bf16_bits(head_w)
+    elif head != "random":
+        raise ValueError(head)
+    return w
 
 
 # ------------------------------------------------------------------ primitive ops
@@ -182,13 +194,12 @@ def attention_rows(q: np.ndarray, k_cache: np.ndarray, v_cache: np.ndarray, lens
 class OracleModel:
     """fp32 LLaMA with a per-sequence KV cache (one cache per layer per slot).
 
-    ``bf16_acts=True`` is the *bf16-faithful* variant: still fp32 math, but the
-    activations are rounded to bf16 exactly where the B200 path stores them in
-    bf16 (GEMM operands h/att/act, q/k/v, attention output, final h).  It is
-    the reference for "identical greedy tokens" -- with random weights the
-    top-1/top-2 gap of some of the 480 config-1 decisions is below the bf16
-    noise of the pure fp32 comparison (SURVEY §7 hard part 2), which the pure
-    fp32 oracle checks separately through the 2e-2 logit tolerance.
+    ``bf16_acts=True`` is a *diagnostic* variant: still fp32 math, but the
+    activations are rounded to bf16 where the B200 path stores them in bf16
+    (GEMM operands h/att/act, q/k/v, attention output, final h).  It is not
+    bit-faithful to the GPU -- attention amplifies single-ulp rounding flips
+    chaotically -- so parity tests use the plain fp32 oracle with the 2e-2
+    logit tolerance.
     """
 
     def __init__(self, cfg: LlamaConfig, weights: ModelWeights, max_ctx: int = 512, bf16_acts: bool = False):

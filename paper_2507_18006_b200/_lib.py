@@ -71,6 +71,12 @@ class OpStats(C.Structure):
     ]
 
 
+class KStat(C.Structure):
+    _fields_ = [("launches", C.c_uint32), ("ms", C.c_float), ("bytes", C.c_double), ("flops", C.c_double)]
+
+
+KCLASSES = ("gemm", "attention", "elementwise", "copy")
+
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
 _I64P = C.POINTER(C.c_int64)
@@ -101,6 +107,8 @@ _SIGS = {
     "cb_migrate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_migrate_submodule": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_evict_replica": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
+    "cb_profile": (C.c_int, [_P, C.c_int32]),
+    "cb_profile_read": (C.c_int, [_P, C.c_int32, C.POINTER(KStat)]),
     # kernel-level test entry points (include/cocob200_testing.h)
     "cbt_gemm": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64]),
     "cbt_gemm_bench": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,

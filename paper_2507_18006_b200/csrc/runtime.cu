@@ -110,6 +110,20 @@ struct Route {
   int dev, s0, cnt;
 };
 
+struct ProfRec {
+  int dev, cls;
+  cudaEvent_t e0, e1;
+  double bytes, flops;
+};
+
+struct Prof {
+  bool on = false;
+  std::vector<ProfRec> pending;
+  cb_kstat stats[4] = {};
+  std::map<int, std::vector<cudaEvent_t>> pool;
+  std::map<int, size_t> next;
+};
+
 struct Seg {
   int dev;      // logical device computing these rows
   int rep;      // replica index
@@ -135,6 +149,8 @@ struct cb_model {
   int32_t* pin_meta = nullptr;
   int32_t* pin_next = nullptr;
   std::vector<std::vector<Route>> last_routing;
+  int cur_T = 0;  // rows of the pass in flight: per-step meta = [tokens | slot | pos] x T, then gather x bs
+  Prof prof;
 };
 
 namespace {
@@ -155,6 +171,57 @@ int depend(DeviceCtx& dst, DeviceCtx& src) {
   CB_TRY(use(dst));
   CB_CUDA(cudaStreamWaitEvent(dst.compute, ev, 0));
   return CB_OK;
+}
+
+// ---- live profiling: bracket one launch with timing events on its stream
+cudaEvent_t prof_event(cb_model* m, int dev) {
+  auto& pool = m->prof.pool[dev];
+  size_t& nx = m->prof.next[dev];
+  if (nx == pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    pool.push_back(e);
+  }
+  return pool[nx++];
+}
+
+struct ProfScope {
+  cb_model* m;
+  int dev, cls;
+  double bytes, flops;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  ProfScope(cb_model* m_, int dev_, int cls_, cudaStream_t st_, double bytes_, double flops_ = 0.0)
+      : m(m_), dev(dev_), cls(cls_), bytes(bytes_), flops(flops_), st(st_) {
+    if (m->prof.on) {
+      e0 = prof_event(m, dev);
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~ProfScope() {
+    if (!e0) return;
+    cudaEvent_t e1 = prof_event(m, dev);
+    cudaEventRecord(e1, st);
+    m->prof.pending.push_back({dev, cls, e0, e1, bytes, flops});
+  }
+};
+
+// fold the finished step's launch timings into the per-class totals
+void prof_resolve(cb_model* m) {
+  for (const ProfRec& r : m->prof.pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    cb_kstat& k = m->prof.stats[r.cls];
+    k.launches += 1;
+    k.ms += ms;
+    k.bytes += r.bytes;
+    k.flops += r.flops;
+  }
+  m->prof.pending.clear();
+  for (auto& kv : m->prof.next) kv.second = 0;
 }
 
 int dev_alloc(const DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullptr) {
@@ -309,6 +376,11 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
   a.out = out;
   a.ws = ws.gemm_ws;
   a.counters = ws.gemm_cnt;
+  const double out_b = (epi == cb::EPI_F32 || epi == cb::EPI_RESID) ? 4.0 : 2.0;
+  const double out_n = epi == cb::EPI_SWIGLU ? N / 2.0 : double(N);
+  const double bytes = double(N) * K * 2 + double(T) * K * 2 + double(T) * out_n * out_b +
+                       (epi == cb::EPI_RESID ? double(T) * N * 4 : 0.0);
+  ProfScope ps(m, dev, CB_KCLASS_GEMM, dc.compute, bytes, 2.0 * N * K * T);
   CB_CUDA(cb::gemm_launch(w, xmaps[tn_index(tn)], a, tn, dc.num_sms, dc.compute));
   return CB_OK;
 }
@@ -324,6 +396,7 @@ int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& t
       DeviceCtx& sd = devctx(m, os.dev);
       CB_TRY(depend(dd, sd));
       CB_TRY(use(dd));
+      ProfScope ps(m, ns.dev, CB_KCLASS_COPY, dd.compute, double(b - a) * row_bytes);
       CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].x + size_t(a) * m->d.d_model, dd.ordinal,
                                   m->ws[os.dev].x + size_t(a) * m->d.d_model, sd.ordinal,
                                   size_t(b - a) * row_bytes, dd.compute));
@@ -342,7 +415,11 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   CB_TRY(use(dc));
   const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
   const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
-  CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
+  {
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
+    CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  }
   CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n));
 
   // attention runs where the rows' KV lives: on the replica itself for a
@@ -367,18 +444,26 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
     if (owner >= 0 && owner != ad && m->slot_len[slot] > 0) {
       CB_TRY(depend(ac, devctx(m, owner)));
       CB_TRY(use(ac));
+      ProfScope ps(m, ad, CB_KCLASS_COPY, ac.compute, double(m->slot_len[slot]) * kv_token_bytes(m));
       CB_TRY(kv_move(m, L, slot, owner, ad, ac.compute, nullptr));
     }
     L.owner[slot] = ad;
   }
   CB_TRY(use(ac));
   uint16_t* kv = L.kv[ad];
-  const int32_t* row_slot = wa.meta + d.max_tokens;
-  const int32_t* rpos = wa.meta + 2 * d.max_tokens;
-  CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
-                             d.max_ctx, ac.compute));
+  const int32_t* row_slot = wa.meta + m->cur_T;
+  const int32_t* rpos = wa.meta + 2 * m->cur_T;
+  {
+    ProfScope ps(m, ad, CB_KCLASS_ELEMWISE, ac.compute, double(T) * m->qkv_n * 4);
+    CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
+                               d.max_ctx, ac.compute));
+  }
   int max_len = 0;
-  for (int r = s.r0; r < s.r1; ++r) max_len = std::max(max_len, row_pos[r] + 1);
+  double kv_tokens = 0;
+  for (int r = s.r0; r < s.r1; ++r) {
+    max_len = std::max(max_len, row_pos[r] + 1);
+    kv_tokens += row_pos[r] + 1;
+  }
   cb::AttnArgs aa{};
   aa.qkv = wa.qkv;
   aa.kv = kv;
@@ -395,7 +480,12 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   aa.max_ctx = d.max_ctx;
   aa.max_len = max_len;
   aa.scale = 1.0f / std::sqrt(float(m->hd));
-  CB_CUDA(cb::attention_launch(aa, ac.num_sms, ac.compute));
+  {
+    // algorithmic bytes: every attended K/V row once, q in, output out
+    ProfScope ps(m, ad, CB_KCLASS_ATTENTION, ac.compute, kv_tokens * kv_token_bytes(m) + double(T) * m->q_n * 4,
+                 kv_tokens * 4.0 * m->q_n);
+    CB_CUDA(cb::attention_launch(aa, ac.num_sms, ac.compute));
+  }
   if (ad != dev) {
     CB_TRY(depend(dc, ac));
     CB_TRY(use(dc));
@@ -405,7 +495,10 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   }
   CB_TRY(use(dc));
   CB_TRY(gemm(m, dev, W.m_o, ws.map_att, d.d_model, m->q_n, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
-  CB_CUDA(cb::rmsnorm_launch(ws.x, fn, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  {
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
+    CB_CUDA(cb::rmsnorm_launch(ws.x, fn, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  }
   CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff));
   CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
   return CB_OK;
@@ -429,16 +522,17 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   std::vector<int> seq_slot(slots, slots + bs);
   std::vector<int> row_pos(T);
   int32_t* meta = m->pin_meta;
+  m->cur_T = T;
   for (int i = 0; i < bs; ++i)
     for (int r = seq_row[i]; r < seq_row[i + 1]; ++r) {
       const int pos = prefill ? r - seq_row[i] : m->slot_len[slots[i]];
       if (pos >= d.max_ctx) return fail(CB_EINVAL, "slot " + std::to_string(slots[i]) + " exceeds max_ctx");
       row_pos[r] = pos;
       meta[r] = tokens[r];
-      meta[d.max_tokens + r] = slots[i];
-      meta[2 * d.max_tokens + r] = pos;
+      meta[T + r] = slots[i];
+      meta[2 * T + r] = pos;
     }
-  for (int i = 0; i < bs; ++i) meta[3 * d.max_tokens + i] = seq_row[i + 1] - 1;
+  for (int i = 0; i < bs; ++i) meta[3 * T + i] = seq_row[i + 1] - 1;
 
   // participating devices
   std::vector<int> devs{m->home};
@@ -451,7 +545,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   DeviceCtx& hc = devctx(m, m->home);
   CB_TRY(use(hc));
   CB_CUDA(cudaEventRecord(hc.t0, hc.compute));
-  const size_t meta_bytes = (3 * size_t(d.max_tokens) + d.max_slots) * 4;
+  const size_t meta_bytes = (3 * size_t(T) + bs) * 4;  // exactly what this pass needs
   for (int dv : devs) {
     CB_TRY(ensure_ws(m, dv));
     DeviceCtx& dc = devctx(m, dv);
@@ -461,7 +555,10 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   }
   Workspace& hw = m->ws[m->home];
   CB_TRY(use(hc));
-  CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
+  {
+    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
+    CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
+  }
 
   std::vector<Seg> layout{{m->home, 0, 0, T, 0, bs}};
   m->last_routing.assign(d.n_layers, {});
@@ -485,19 +582,27 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   // every device's trailing work joins the home stream
   for (int dv : devs) CB_TRY(depend(hc, devctx(m, dv)));
   CB_TRY(use(hc));
-  CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
+  {
+    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
+    CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
+  }
   const CUtensorMap* xm = hw.map_h;
   if (prefill) {
-    CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * d.max_tokens, hw.hl, bs, d.d_model, hc.compute));
+    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.d_model * 4);
+    CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * T, hw.hl, bs, d.d_model, hc.compute));
     xm = hw.map_hl;
   }
   CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab));
-  CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
+  {
+    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.vocab * 4);
+    CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
+  }
   CB_CUDA(cudaEventRecord(hc.t1, hc.compute));
   CB_CUDA(cudaMemcpyAsync(m->pin_next, hw.next, size_t(bs) * 4, cudaMemcpyDeviceToHost, hc.compute));
   if (logits_out)
     CB_CUDA(cudaMemcpyAsync(logits_out, hw.logits, size_t(bs) * d.vocab * 4, cudaMemcpyDeviceToHost, hc.compute));
   CB_CUDA(cudaStreamSynchronize(hc.compute));
+  if (m->prof.on) prof_resolve(m);
   float ms = 0.f;
   CB_CUDA(cudaEventElapsedTime(&ms, hc.t0, hc.t1));
   if (ms_out) *ms_out += ms;
@@ -714,6 +819,10 @@ int cb_model_destroy(cb_model* m) {
   dev_free(m, m->home, m->embed);
   dev_free(m, m->home, m->final_norm);
   dev_free(m, m->home, m->lm_head);
+  for (auto& kv : m->prof.pool) {
+    cudaSetDevice(devctx(m, kv.first).ordinal);
+    for (auto e : kv.second) cudaEventDestroy(e);
+  }
   if (m->pin_meta) cudaFreeHost(m->pin_meta);
   if (m->pin_next) cudaFreeHost(m->pin_next);
   delete m;
@@ -952,6 +1061,21 @@ int cb_last_routing(cb_model* m, int32_t layer, int32_t* dev_out, int32_t* s0_ou
     s0_out[j] = r[j].s0;
     cnt_out[j] = r[j].cnt;
   }
+  return CB_OK;
+}
+
+int cb_profile(cb_model* m, int32_t enable) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  sync_all(m);
+  prof_resolve(m);
+  for (auto& k : m->prof.stats) k = cb_kstat{};
+  m->prof.on = enable != 0;
+  return CB_OK;
+}
+
+int cb_profile_read(cb_model* m, int32_t kclass, cb_kstat* out) {
+  if (!m || !out || kclass < 0 || kclass > 3) return fail(CB_EINVAL, "bad profile query");
+  *out = m->prof.stats[kclass];
   return CB_OK;
 }
 

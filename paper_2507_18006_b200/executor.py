@@ -284,6 +284,19 @@ class Executor:
             return StepOutcome(ms / 1e3, len(batch), nxt)
         raise ValueError(f"unknown phase {phase!r}")
 
+    # ------------------------------------------------------------ profiling
+    def profile(self, enable: bool) -> None:
+        """Start (and reset) / stop per-launch CUDA-event timing inside cb_step."""
+        _lib.check(self.lib.cb_profile(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for i, name in enumerate(_lib.KCLASSES):
+            k = _lib.KStat()
+            _lib.check(self.lib.cb_profile_read(self.handle, i, C.byref(k)))
+            out[name] = {"launches": k.launches, "ms": k.ms, "bytes": k.bytes, "flops": k.flops}
+        return out
+
     # ------------------------------------------------------------ readback
     def module_bytes(self, kind: str | ModuleKind) -> int:
         k = kind.value if isinstance(kind, ModuleKind) else kind
