@@ -25,7 +25,7 @@ int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const 
 int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
 /* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
-                   void* out, int64_t ldo, int32_t iters, float* ms_per_launch);
+                   void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch);
 
 #ifdef __cplusplus
 }

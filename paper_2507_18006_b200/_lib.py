@@ -112,7 +112,7 @@ _SIGS = {
     # kernel-level test entry points (include/cocob200_testing.h)
     "cbt_gemm": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64]),
     "cbt_gemm_bench": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,
-                                 C.c_int32, _F32P]),
+                                 C.c_int32, C.c_int32, _F32P]),
     "cbt_rmsnorm": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float]),
     "cbt_rope_kv": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float]),
     "cbt_attention": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),

@@ -34,41 +34,65 @@ cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x,
 // ---------------------------------------------------------------- RMSNorm
 // reference composition: LLaMA decoder (norm vectors counted in
 // ModuleCatalog.from_model, domain.py:259).  fp32 residual in, bf16 out.
+// One CTA per row; the row is held in registers (<= 8 float4 per thread), so
+// it is read once and every load of the row is in flight at the same time.
+static constexpr int kNormVec = 8;
+
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gamma,
-                               uint16_t* __restrict__ y, int T, int d, float eps, int row_off) {
-  const int warps = blockDim.x >> 5;
-  const int t = blockIdx.x * warps + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)(row_off + t) * d);
+                               uint16_t* __restrict__ y, int d, float eps, int row_off) {
+  const int row = row_off + blockIdx.x;
+  const int n4 = d / 4;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
+  float4 v[kNormVec];
   float ss = 0.f;
-  for (int i = lane; i < d / 4; i += 32) {
-    float4 v = xr[i];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < n4) {
+      v[k] = xr[i];
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+    }
   }
+  __shared__ float red[32];
   ss = warp_sum(ss);
-  const float r = rsqrtf(ss / float(d) + eps);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+  }
+  __syncthreads();
+  const float r = rsqrtf(red[0] / float(d) + eps);
   const uint2* g = reinterpret_cast<const uint2*>(gamma);
-  uint2* yr = reinterpret_cast<uint2*>(y + (size_t)(row_off + t) * d);
-  for (int i = lane; i < d / 4; i += 32) {
-    float4 v = xr[i];
-    uint2 gg = __ldg(g + i);
-    uint2 o;
-    o.x = pack_bf16x2(v.x * r * bf16_lo(gg.x), v.y * r * bf16_hi(gg.x));
-    o.y = pack_bf16x2(v.z * r * bf16_lo(gg.y), v.w * r * bf16_hi(gg.y));
-    yr[i] = o;
+  uint2* yr = reinterpret_cast<uint2*>(y + (size_t)row * d);
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = threadIdx.x + k * blockDim.x;
+    if (i < n4) {
+      const uint2 gg = __ldg(g + i);
+      uint2 o;
+      o.x = pack_bf16x2(v[k].x * r * bf16_lo(gg.x), v[k].y * r * bf16_hi(gg.x));
+      o.y = pack_bf16x2(v[k].z * r * bf16_lo(gg.y), v[k].w * r * bf16_hi(gg.y));
+      yr[i] = o;
+    }
   }
 }
 
 cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, int T, int d, float eps,
                            int row_off, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  rmsnorm_kernel<<<(T + 3) / 4, 128, 0, st>>>(x, gamma, y, T, d, eps, row_off);
+  const int n4 = d / 4;
+  int threads = ((n4 + kNormVec - 1) / kNormVec + 31) / 32 * 32;
+  threads = threads < 32 ? 32 : threads;
+  if (threads > 1024) return cudaErrorInvalidValue;
+  rmsnorm_kernel<<<T, threads, 0, st>>>(x, gamma, y, d, eps, row_off);
   return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- RoPE + KV append
-// One CTA per row.  Thread j handles rotation pair j of a head: (i, i + hd/2)
+// One CTA per row, 128-bit accesses.  A work item is 8 consecutive elements of
+// one head's first half plus their rotation partners in the second half
 // (rotate-half convention).  q is rotated in place; rotated k and raw v are
 // appended at cache[slot][pos].
 __global__ void rope_kv_kernel(uint16_t* __restrict__ qkv, uint16_t* __restrict__ kv,
@@ -79,33 +103,49 @@ __global__ void rope_kv_kernel(uint16_t* __restrict__ qkv, uint16_t* __restrict_
   const int slot = row_slot[row];
   const int pos = row_pos[row];
   const int half = hd / 2;
+  const int cph = half / 8;  // 8-element chunks per half head
   const size_t qkv_ld = size_t(H + 2 * Hkv) * hd;
-  uint16_t* q = qkv + row * qkv_ld;
+  uint16_t* q = qkv + (size_t)row * qkv_ld;
   uint16_t* k = q + size_t(H) * hd;
   const uint16_t* v = k + size_t(Hkv) * hd;
   const size_t kvd = size_t(Hkv) * hd;
   uint16_t* kc = kv + ((size_t)slot * max_ctx + pos) * 2 * kvd;
   uint16_t* vc = kc + kvd;
   const float2* rp = rope + (size_t)pos * half;
-  const int npairs = (H + Hkv) * half;
-  for (int j = threadIdx.x; j < npairs; j += blockDim.x) {
-    const int head = j / half, i = j % half;
-    const float2 cs = rp[i];
-    uint16_t* base = (head < H) ? (q + (size_t)head * hd) : (k + (size_t)(head - H) * hd);
-    const float x1 = bf16_to_f(base[i]), x2 = bf16_to_f(base[i + half]);
-    const uint16_t o1 = f_to_bf16(x1 * cs.x - x2 * cs.y);
-    const uint16_t o2 = f_to_bf16(x2 * cs.x + x1 * cs.y);
-    if (head < H) {
-      base[i] = o1;
-      base[i + half] = o2;
-    } else {
-      const size_t off = (size_t)(head - H) * hd;
-      kc[off + i] = o1;
-      kc[off + i + half] = o2;
+  const int nrot = (H + Hkv) * cph;
+  const int nv = int(kvd / 8);
+  for (int c = threadIdx.x; c < nrot + nv; c += blockDim.x) {
+    if (c >= nrot) {  // v: straight copy into the cache
+      reinterpret_cast<uint4*>(vc)[c - nrot] = reinterpret_cast<const uint4*>(v)[c - nrot];
+      continue;
     }
+    const int head = c / cph, i0 = (c % cph) * 8;
+    const uint16_t* src = head < H ? q + (size_t)head * hd : k + (size_t)(head - H) * hd;
+    const uint4 a = *reinterpret_cast<const uint4*>(src + i0);
+    const uint4 b = *reinterpret_cast<const uint4*>(src + i0 + half);
+    const float4* cs4 = reinterpret_cast<const float4*>(rp + i0);
+    const float x1[8] = {bf16_lo(a.x), bf16_hi(a.x), bf16_lo(a.y), bf16_hi(a.y),
+                         bf16_lo(a.z), bf16_hi(a.z), bf16_lo(a.w), bf16_hi(a.w)};
+    const float x2[8] = {bf16_lo(b.x), bf16_hi(b.x), bf16_lo(b.y), bf16_hi(b.y),
+                         bf16_lo(b.z), bf16_hi(b.z), bf16_lo(b.w), bf16_hi(b.w)};
+    float o1[8], o2[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 cs = __ldg(cs4 + j);  // (cos, sin) of elements 2j and 2j+1
+      o1[2 * j] = x1[2 * j] * cs.x - x2[2 * j] * cs.y;
+      o2[2 * j] = x2[2 * j] * cs.x + x1[2 * j] * cs.y;
+      o1[2 * j + 1] = x1[2 * j + 1] * cs.z - x2[2 * j + 1] * cs.w;
+      o2[2 * j + 1] = x2[2 * j + 1] * cs.z + x1[2 * j + 1] * cs.w;
+    }
+    uint4 r1, r2;
+    r1.x = pack_bf16x2(o1[0], o1[1]); r1.y = pack_bf16x2(o1[2], o1[3]);
+    r1.z = pack_bf16x2(o1[4], o1[5]); r1.w = pack_bf16x2(o1[6], o1[7]);
+    r2.x = pack_bf16x2(o2[0], o2[1]); r2.y = pack_bf16x2(o2[2], o2[3]);
+    r2.z = pack_bf16x2(o2[4], o2[5]); r2.w = pack_bf16x2(o2[6], o2[7]);
+    uint16_t* dst = head < H ? q + (size_t)head * hd : kc + (size_t)(head - H) * hd;
+    *reinterpret_cast<uint4*>(dst + i0) = r1;
+    *reinterpret_cast<uint4*>(dst + i0 + half) = r2;
   }
-  for (int j = threadIdx.x; j < int(kvd / 8); j += blockDim.x)
-    reinterpret_cast<uint4*>(vc)[j] = reinterpret_cast<const uint4*>(v)[j];
 }
 
 cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const float2* rope, const int32_t* row_slot,

@@ -228,8 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (whole) {
           emit16(a, n, row0 + c0, min(16, ncols_tile - c0), v);
         } else {
+          float4* dst = reinterpret_cast<float4*>(part + (size_t)row_in_tile * TN + c0);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) part[(c0 + i) * kBM + row_in_tile] = v[i];
+          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
       }
       tc_fence_before();
@@ -250,15 +251,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (*bcast) {
           __threadfence();
+          // fixed part order -> deterministic; 16-column chunks, 128-bit loads,
+          // all of a part's chunk loads in flight before they are summed
           for (int c0 = 0; c0 < ncols_tile; c0 += 16) {
             float v[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = 0.f;
             for (int cc = c_first; cc <= c_last; ++cc) {
               const int w = (sk.u0(cc) / sk.kb == tile) ? 0 : 1;
-              const float* p = a.ws + ((size_t)cc * 2 + w) * (size_t)(kBM * TN);
+              const float4* p = reinterpret_cast<const float4*>(
+                  a.ws + ((size_t)cc * 2 + w) * (size_t)(kBM * TN) + (size_t)row_in_tile * TN + c0);
+              float4 q[4];
 #pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] += __ldcg(p + (c0 + i) * kBM + row_in_tile);
+              for (int i = 0; i < 4; ++i) q[i] = __ldcg(p + i);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                v[4 * i] += q[i].x;
+                v[4 * i + 1] += q[i].y;
+                v[4 * i + 2] += q[i].z;
+                v[4 * i + 3] += q[i].w;
+              }
             }
             emit16(a, n, row0 + c0, min(16, ncols_tile - c0), v);
           }
@@ -326,10 +338,15 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK - 1) / kBK;
-  long long units = (long long)a.n_mtiles * a.n_ttiles * a.kblocks;
+  const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
+  long long units = tiles * a.kblocks;
   a.units = int(units);
-  int grid = int(units < num_sms ? units : num_sms);
-  gemm_tc_kernel<TN><<<grid, kThreads, Cfg::kSmemBytes, st>>>(w, x, a);
+  // HBM-bound weight streaming needs enough bytes in flight, not every SM:
+  // cap the split so a tile is shared by <= ~max_parts CTAs (short fixups).
+  long long grid = units < num_sms ? units : num_sms;
+  const int max_parts = a.max_parts > 0 ? a.max_parts : 2;
+  if (grid > tiles * max_parts) grid = tiles * max_parts;
+  gemm_tc_kernel<TN><<<int(grid), kThreads, Cfg::kSmemBytes, st>>>(w, x, a);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,7 @@ struct GemmArgs {
   void* out;
   float* ws;      // stream-K partials, gemm_ws_floats(num_sms) floats
   int* counters;  // per-tile arrival counters, zero-initialised, >= n_tiles ints
+  int max_parts;  // stream-K: max average CTAs per tile (0 = default 2)
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
 };

@@ -75,7 +75,7 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
 }
 
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
-                   void* out, int64_t ldo, int32_t iters, float* ms_per_launch) {
+                   void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch) {
   TestWs* ws;
   int r = ws_for_current(&ws);
   if (r) return r;
@@ -91,6 +91,7 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
+  a.max_parts = max_parts;
   for (int i = 0; i < 3; ++i) cb::gemm_launch(mw, mx, a, tn, ws->sms, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
