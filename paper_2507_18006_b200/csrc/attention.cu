@@ -24,6 +24,8 @@ static constexpr int kUnroll = 4;
 template <int HD>
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int G = HD / 8;  // lanes per position
   constexpr int P = 32 / G;  // positions per warp step
   const int row = a.row_off + blockIdx.x;
@@ -152,6 +154,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 
 template <int HD>
 __global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
+  pdl_trigger();
+  pdl_wait();
   const int rl = blockIdx.x, qh = blockIdx.y, i = threadIdx.x;
   const float* st = a.ws + ((size_t)rl * a.H + qh) * nsplit * (HD + 2);
   float M = -INFINITY;
@@ -180,11 +184,9 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
   }
   const int chunk = (a.max_len + nsplit - 1) / nsplit;
   dim3 grid(a.T, a.Hkv, nsplit);
-  attn_kernel<HD><<<grid, kAttnWarps * 32, 0, st>>>(a, nsplit, chunk, gq);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(attn_kernel<HD>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq);
   if (e != cudaSuccess || nsplit == 1) return e;
-  attn_combine_kernel<HD><<<dim3(a.T, a.H), HD, 0, st>>>(a, nsplit);
-  return cudaGetLastError();
+  return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);
 }
 
 cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st) {

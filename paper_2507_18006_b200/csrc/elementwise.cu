@@ -11,6 +11,8 @@ namespace cb {
 // ---------------------------------------------------------------- embedding
 __global__ void embed_kernel(const uint16_t* __restrict__ table, const int32_t* __restrict__ tokens,
                              float* __restrict__ x, int T, int d, int row_off) {
+  pdl_trigger();
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int t = blockIdx.x * warps + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -27,8 +29,7 @@ __global__ void embed_kernel(const uint16_t* __restrict__ table, const int32_t* 
 cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x, int T, int d, int row_off,
                          cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  embed_kernel<<<(T + 3) / 4, 128, 0, st>>>(table, tokens, x, T, d, row_off);
-  return cudaGetLastError();
+  return launch_pdl(embed_kernel, dim3((T + 3) / 4), dim3(128), 0, st, table, tokens, x, T, d, row_off);
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -40,6 +41,8 @@ static constexpr int kNormVec = 8;
 
 __global__ void rmsnorm_kernel(const float* __restrict__ x, const uint16_t* __restrict__ gamma,
                                uint16_t* __restrict__ y, int d, float eps, int row_off) {
+  pdl_trigger();
+  pdl_wait();
   const int row = row_off + blockIdx.x;
   const int n4 = d / 4;
   const float4* xr = reinterpret_cast<const float4*>(x + (size_t)row * d);
@@ -86,8 +89,7 @@ cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, i
   int threads = ((n4 + kNormVec - 1) / kNormVec + 31) / 32 * 32;
   threads = threads < 32 ? 32 : threads;
   if (threads > 1024) return cudaErrorInvalidValue;
-  rmsnorm_kernel<<<T, threads, 0, st>>>(x, gamma, y, d, eps, row_off);
-  return cudaGetLastError();
+  return launch_pdl(rmsnorm_kernel, dim3(T), dim3(threads), 0, st, x, gamma, y, d, eps, row_off);
 }
 
 // ---------------------------------------------------------------- RoPE + KV append
@@ -99,6 +101,8 @@ __global__ void rope_kv_kernel(uint16_t* __restrict__ qkv, uint16_t* __restrict_
                                const float2* __restrict__ rope, const int32_t* __restrict__ row_slot,
                                const int32_t* __restrict__ row_pos, int row_off, int H, int Hkv, int hd,
                                int max_ctx) {
+  pdl_trigger();
+  pdl_wait();
   const int row = row_off + blockIdx.x;
   const int slot = row_slot[row];
   const int pos = row_pos[row];
@@ -152,13 +156,15 @@ cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const float2* rope, cons
                            const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd, int max_ctx,
                            cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  rope_kv_kernel<<<T, 256, 0, st>>>(qkv, kv, rope, row_slot, row_pos, row_off, H, Hkv, hd, max_ctx);
-  return cudaGetLastError();
+  return launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, st, qkv, kv, rope, row_slot, row_pos, row_off, H, Hkv,
+                    hd, max_ctx);
 }
 
 // ---------------------------------------------------------------- row gather
 __global__ void gather_rows_kernel(const uint16_t* __restrict__ src, const int32_t* __restrict__ idx,
                                    uint16_t* __restrict__ dst, int d) {
+  pdl_trigger();
+  pdl_wait();
   const uint4* s = reinterpret_cast<const uint4*>(src + (size_t)idx[blockIdx.x] * d);
   uint4* o = reinterpret_cast<uint4*>(dst + (size_t)blockIdx.x * d);
   for (int i = threadIdx.x; i < d / 8; i += blockDim.x) o[i] = s[i];
@@ -167,12 +173,13 @@ __global__ void gather_rows_kernel(const uint16_t* __restrict__ src, const int32
 cudaError_t gather_rows_launch(const uint16_t* src, const int32_t* idx, uint16_t* dst, int n, int d,
                                cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  gather_rows_kernel<<<n, 128, 0, st>>>(src, idx, dst, d);
-  return cudaGetLastError();
+  return launch_pdl(gather_rows_kernel, dim3(n), dim3(128), 0, st, src, idx, dst, d);
 }
 
 // ---------------------------------------------------------------- argmax
 __global__ void argmax_kernel(const float* __restrict__ logits, int32_t* __restrict__ out, int V) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const float* row = logits + (size_t)t * V;
   float best = -INFINITY;
@@ -208,8 +215,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int32_t* __restr
 
 cudaError_t argmax_launch(const float* logits, int32_t* out, int T, int V, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  argmax_kernel<<<T, 512, 0, st>>>(logits, out, V);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(T), dim3(512), 0, st, logits, out, V);
 }
 
 // ---------------------------------------------------------------- init

@@ -96,6 +96,31 @@ CB_DEVICE void emit16(const GemmArgs& a, int n, int row0, int ncols, const float
   }
 }
 
+// Epilogue of a (row pair, token column) of a finished tile: rows n, n+1 of
+// the weight (an interleaved gate/up pair for SwiGLU).
+CB_DEVICE void emit_pair(const GemmArgs& a, int n, int row, float v0, float v1) {
+  if (n >= a.N) return;
+  const size_t base = (size_t)row * a.ldo;
+  if (a.epi == EPI_SWIGLU) {
+    reinterpret_cast<uint16_t*>(a.out)[base + (n >> 1)] = f_to_bf16(v0 / (1.0f + __expf(-v0)) * v1);
+  } else if (a.epi == EPI_BF16) {
+    uint16_t* o = reinterpret_cast<uint16_t*>(a.out) + base + n;
+    if (n + 1 < a.N) {
+      *reinterpret_cast<uint32_t*>(o) = pack_bf16x2(v0, v1);
+    } else {
+      o[0] = f_to_bf16(v0);
+    }
+  } else if (a.epi == EPI_F32) {
+    float* o = reinterpret_cast<float*>(a.out) + base + n;
+    o[0] = v0;
+    if (n + 1 < a.N) o[1] = v1;
+  } else {
+    float* o = reinterpret_cast<float*>(a.out) + base + n;
+    o[0] += v0;
+    if (n + 1 < a.N) o[1] += v1;
+  }
+}
+
 template <int TN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -120,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int c = blockIdx.x;
   const int ubeg = sk.u0(c), uend = sk.u0(c + 1);
 
+  pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
@@ -144,21 +170,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream through once
       const uint64_t pol_x = policy_evict_last();   // activations are re-read by every tile
+      // Weights do not depend on the previous kernel: fill the first stages'
+      // weight tiles before waiting on it (programmatic dependent launch).
+      const int npre = min(S, uend - ubeg);
+      for (int i = 0; i < npre; ++i) {
+        const int u = ubeg + i, tile = u / sk.kb, kb = u % sk.kb;
+        mbar_arrive_expect_tx(&full_bar[i], Cfg::kStageBytes);
+        tma_load_2d(&tmW, &full_bar[i], sW + i * Cfg::kWBytes, kb * kBK, (tile / n_ttiles) * kBM, pol_w);
+      }
+      pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = ubeg; u < uend;) {
-        const int tile = u / sk.kb, kb0 = u % sk.kb;
-        const int kb1 = min(sk.kb, kb0 + (uend - u));
+      for (int u = ubeg; u < uend; ++u) {
+        const int tile = u / sk.kb, kb = u % sk.kb;
         const int mt = tile / n_ttiles, tt = tile % n_ttiles;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        if (u - ubeg >= npre) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt * kBM, pol_w);
-          tma_load_2d(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
-                      a.row_off + tt * TN, pol_x);
-          if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        u += kb1 - kb0;
+        tma_load_2d(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -199,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------------------------------------------------- epilogue
+    pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row_in_tile = q * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
@@ -217,6 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TN);
       // which workspace slot: 0 if this is the CTA's first segment, else 1
       const int which = (u == ubeg) ? 0 : 1;
+      // partials are column-major [col][128 rows]: coalesced stores here and
+      // coalesced row-pair loads in the fixup
       float* part = a.ws + ((size_t)c * 2 + which) * (size_t)(kBM * TN);
       for (int c0 = 0; c0 < ncols_tile; c0 += 16) {
         uint32_t r[16];
@@ -228,9 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (whole) {
           emit16(a, n, row0 + c0, min(16, ncols_tile - c0), v);
         } else {
-          float4* dst = reinterpret_cast<float4*>(part + (size_t)row_in_tile * TN + c0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          for (int i = 0; i < 16; ++i) part[(size_t)(c0 + i) * kBM + row_in_tile] = v[i];
         }
       }
       tc_fence_before();
@@ -251,28 +285,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         named_bar_sync(1, kEpiThreads);
         if (*bcast) {
           __threadfence();
-          // fixed part order -> deterministic; 16-column chunks, 128-bit loads,
-          // all of a part's chunk loads in flight before they are summed
-          for (int c0 = 0; c0 < ncols_tile; c0 += 16) {
-            float v[16];
+          // work item = (row pair, token column); parts summed in fixed CTA
+          // order (deterministic); 8 items per thread in flight per round trip.
+          const int n_items = 64 * ncols_tile;
+          for (int base = et; base < n_items; base += 8 * kEpiThreads) {
+            float2 sum[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = 0.f;
+            for (int j = 0; j < 8; ++j) sum[j] = make_float2(0.f, 0.f);
             for (int cc = c_first; cc <= c_last; ++cc) {
               const int w = (sk.u0(cc) / sk.kb == tile) ? 0 : 1;
-              const float4* p = reinterpret_cast<const float4*>(
-                  a.ws + ((size_t)cc * 2 + w) * (size_t)(kBM * TN) + (size_t)row_in_tile * TN + c0);
-              float4 q[4];
+              const float* p = a.ws + ((size_t)cc * 2 + w) * (size_t)(kBM * TN);
+              float2 ld[8];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) q[i] = __ldcg(p + i);
+              for (int j = 0; j < 8; ++j) ld[j] = make_float2(0.f, 0.f);
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                v[4 * i] += q[i].x;
-                v[4 * i + 1] += q[i].y;
-                v[4 * i + 2] += q[i].z;
-                v[4 * i + 3] += q[i].w;
+              for (int j = 0; j < 8; ++j) {
+                const int it = base + j * kEpiThreads;
+                if (it < n_items)
+                  ld[j] = __ldcg(reinterpret_cast<const float2*>(p + (size_t)(it >> 6) * kBM + 2 * (it & 63)));
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                sum[j].x += ld[j].x;
+                sum[j].y += ld[j].y;
               }
             }
-            emit16(a, n, row0 + c0, min(16, ncols_tile - c0), v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int it = base + j * kEpiThreads;
+              if (it < n_items) emit_pair(a, mt * kBM + 2 * (it & 63), row0 + (it >> 6), sum[j].x, sum[j].y);
+            }
           }
           if (et == 0) a.counters[tile] = 0;
         }
@@ -344,10 +386,19 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   // HBM-bound weight streaming needs enough bytes in flight, not every SM:
   // cap the split so a tile is shared by <= ~max_parts CTAs (short fixups).
   long long grid = units < num_sms ? units : num_sms;
-  const int max_parts = a.max_parts > 0 ? a.max_parts : 2;
+  // Split rule (depends only on the tile count and TN bucket, so for decode
+  // batches in one bucket a row's bits do not depend on how many rows share
+  // the launch): few tiles -> spread each over <= 4 CTAs so every SM streams
+  // weights; many tiles or wide TN -> no split (the fixup would cost more).
+  int max_parts = a.max_parts;
+  if (max_parts <= 0) {
+    if (TN > 64 || tiles * 10 >= (long long)num_sms * 6)
+      max_parts = 1;
+    else
+      max_parts = int((num_sms + tiles - 1) / tiles) < 4 ? int((num_sms + tiles - 1) / tiles) : 4;
+  }
   if (grid > tiles * max_parts) grid = tiles * max_parts;
-  gemm_tc_kernel<TN><<<int(grid), kThreads, Cfg::kSmemBytes, st>>>(w, x, a);
-  return cudaGetLastError();
+  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(grid)), dim3(kThreads), Cfg::kSmemBytes, st, w, x, a);
 }
 
 cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, int tn, int num_sms,
