@@ -188,7 +188,7 @@ def build_instance(args, n_dev: int, ordinal0: int):
     from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
 
     batch = args.batch * n_dev
-    max_ctx = args.prompt + args.warmup + args.steps + 8
+    max_ctx = args.prompt + args.warmup + 2 * args.steps + 8  # timed pass + profiled pass
     # two logical devices on one GPU at N=1 so the replication/migration copy
     # engine can be measured too (device 1 holds no layer during decode)
     ordinals = list(range(ordinal0, ordinal0 + n_dev)) if n_dev > 1 else [ordinal0, ordinal0]

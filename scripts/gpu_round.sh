@@ -11,7 +11,7 @@ fi
 timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   # every launch of two timed decode steps (cold-cache, serialised: compare shares)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 588 -c 520 --csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 588 -c 260 --csv \
       --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
   # full sections of the decode GEMMs (qkv, o, gate/up, down) and attention
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 258 -c 4 \
