@@ -143,7 +143,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_ttiles = a.n_ttiles;
   const StreamK sk{a.units, int(gridDim.x), a.kblocks};
   const int c = blockIdx.x;
-  const int ubeg = sk.u0(c), uend = sk.u0(c + 1);
+  // Work range: stream-K slice of the (tile, k-block) space, or -- in cluster
+  // split mode -- k-slice r of tile c / S (the cluster = the tile's S CTAs).
+  const int csplit = a.cluster_split > 1 ? a.cluster_split : 1;
+  int ubeg, uend;
+  if (csplit > 1) {
+    const int tile = c / csplit, r = c % csplit;
+    ubeg = tile * sk.kb + (r * sk.kb) / csplit;
+    uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
+  } else {
+    ubeg = sk.u0(c);
+    uend = sk.u0(c + 1);
+  }
 
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
   if (warp == 0 && lane == 0) {
@@ -252,7 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int which = (u == ubeg) ? 0 : 1;
       // partials are column-major [col][128 rows]: coalesced stores here and
       // coalesced row-pair loads in the fixup
-      float* part = a.ws + ((size_t)c * 2 + which) * (size_t)(kBM * TN);
+      float* part = csplit > 1 ? reinterpret_cast<float*>(sW)  // cluster mode: partial stays in smem
+                               : a.ws + ((size_t)c * 2 + which) * (size_t)(kBM * TN);
       for (int c0 = 0; c0 < ncols_tile; c0 += 16) {
         uint32_t r[16];
         tmem_ld16(t_addr + uint32_t(c0), r);
@@ -272,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
 
-      if (!whole) {
+      if (!whole && csplit == 1) {
         // stream-K fixup: the last CTA to deposit its part finishes the tile.
         const int c_first = sk.cta_of(tile * sk.kb);
         const int c_last = sk.cta_of(tile * sk.kb + sk.kb - 1);
@@ -322,6 +334,39 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       u += kb1 - kb0;
     }
+  }
+  if (csplit > 1) {
+    // Cluster split-K: every CTA of the cluster holds a partial [TN][128] in
+    // its shared memory; CTA r reduces rows [r*128/S, (r+1)*128/S) across the
+    // S partials through DSMEM in fixed rank order and runs the epilogue.
+    const int tile = c / csplit;
+    const int mt = tile / n_ttiles, tt = tile % n_ttiles;
+    const int ncols_tile = min(TN, a.T - tt * TN);
+    if (uend == ubeg && warp >= 2) {  // empty k-slice (kb < S): contribute zeros
+      float* part = reinterpret_cast<float*>(sW);
+      for (int i = threadIdx.x - 64; i < TN * kBM; i += kEpiThreads) part[i] = 0.f;
+    }
+    cluster_sync_all();
+    if (warp >= 2) {
+      const int et = threadIdx.x - 64;
+      const uint32_t rank = cluster_ctarank();
+      const int rows_per = kBM / csplit, pairs = rows_per / 2;
+      const int row_base = int(rank) * rows_per;
+      const int row0 = a.row_off + tt * TN;
+      const uint32_t base = smem_u32(sW);
+      for (int it = et; it < pairs * ncols_tile; it += kEpiThreads) {
+        const int col = it / pairs, row = row_base + 2 * (it % pairs);
+        const uint32_t off = base + uint32_t((col * kBM + row) * 4);
+        float2 sum = make_float2(0.f, 0.f);
+        for (int src = 0; src < csplit; ++src) {
+          const float2 v = dsmem_ld_f2(dsmem_map(off, uint32_t(src)));
+          sum.x += v.x;
+          sum.y += v.y;
+        }
+        emit_pair(a, mt * kBM + row, row0 + col, sum.x, sum.y);
+      }
+    }
+    cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
   tc_fence_before();
   __syncthreads();
@@ -380,6 +425,22 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK - 1) / kBK;
+  const long long tiles0 = (long long)a.n_mtiles * a.n_ttiles;
+  // Cluster split-K for few wide-K tiles (decode O / down projections): each
+  // tile's K is cut over S CTAs of one cluster, partials reduced through DSMEM.
+  int cs = a.cluster_split;
+  if (cs == 0) {
+    cs = 1;
+    if (TN <= 64 && tiles0 * 10 < (long long)num_sms * 6) {
+      while (cs < 8 && tiles0 * cs * 2 <= num_sms && cs * 2 <= a.kblocks) cs *= 2;
+    }
+  }
+  a.cluster_split = cs;
+  if (cs > 1) {
+    a.units = int(tiles0 * a.kblocks);
+    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles0 * cs)), dim3(kThreads), Cfg::kSmemBytes, st,
+                              unsigned(cs), w, x, a);
+  }
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   long long units = tiles * a.kblocks;
   a.units = int(units);

@@ -27,7 +27,8 @@ struct GemmArgs {
   void* out;
   float* ws;      // stream-K partials, gemm_ws_floats(num_sms) floats
   int* counters;  // per-tile arrival counters, zero-initialised, >= n_tiles ints
-  int max_parts;  // stream-K: max average CTAs per tile (0 = default 2)
+  int max_parts;  // stream-K: max average CTAs per tile (0 = automatic)
+  int cluster_split;  // >1: each tile split over a cluster of this many CTAs, DSMEM reduce (0 = automatic)
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
 };

@@ -91,7 +91,8 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
-  a.max_parts = max_parts;
+  a.max_parts = max_parts < 0 ? 1 : max_parts;
+  a.cluster_split = max_parts < 0 ? -max_parts : 0;  // negative max_parts selects a fixed cluster split
   for (int i = 0; i < 3; ++i) cb::gemm_launch(mw, mx, a, tn, ws->sms, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);

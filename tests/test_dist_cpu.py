@@ -1,0 +1,56 @@
+"""Multi-process plumbing on CPU (gloo, world_size 2).
+
+``bench.py`` under ``torch.distributed.run`` with two ranks: the reference arm
+must run on rank 0 only and print exactly one JSON line; the rendezvous uses
+127.0.0.1.  (The GPU arm's N>1 path needs GPUs and is exercised on the box.)
+"""
+from __future__ import annotations
+
+import json
+import socket
+import subprocess
+import sys
+
+from conftest import ROOT
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_torchrun_reference_arm_rank0_only():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--batch", "2", "--prompt", "8"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
+    assert rec["e2e"]["h2d_bytes_per_step"] == 0 and rec["cpu_baseline"]["kind"] == "port"
+
+
+def test_gloo_barrier_world2():
+    """The barrier/max-over-ranks pattern bench.py relies on, with gloo."""
+    code = r'''
+import os, torch, torch.distributed as dist
+dist.init_process_group("gloo")
+r = dist.get_rank()
+t = torch.tensor([float(r + 1)])
+dist.all_reduce(t, op=dist.ReduceOp.MAX)
+dist.barrier()
+if r == 0:
+    print("MAX", t.item())
+dist.destroy_process_group()
+'''
+    script = ROOT / "build" / "gloo_probe.py"
+    script.parent.mkdir(exist_ok=True)
+    script.write_text(code)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(script)]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "MAX 2.0" in out.stdout
