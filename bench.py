@@ -188,7 +188,7 @@ def build_instance(args, n_dev: int, ordinal0: int):
     from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
 
     batch = args.batch * n_dev
-    max_ctx = args.prompt + args.warmup + 2 * args.steps + 8  # timed pass + profiled pass
+    max_ctx = max(args.prompt + args.warmup + 2 * args.steps, args.prompt + args.serve_gen) + 8
     # two logical devices on one GPU at N=1 so the replication/migration copy
     # engine can be measured too (device 1 holds no layer during decode)
     ordinals = list(range(ordinal0, ordinal0 + n_dev)) if n_dev > 1 else [ordinal0, ordinal0]
@@ -218,6 +218,23 @@ def measure_migration(ex, cat, cluster, n_dev: int) -> dict:
     path = "NVLink P2P (cudaMemcpyPeerAsync)" if n_dev > 1 else "same-GPU D2D copy (HBM read+write; NVLink needs N>1)"
     return {"bytes": m.weight_bytes, "ms": m.device_ms, "gbps": m.gbps, "path": path,
             "nvlink_peak_gbps_per_dir": 900.0}
+
+
+def serving_window(ex, args, batch: int) -> dict:
+    """Continuous batching (reference Engine semantics, serving.py) under Poisson
+    arrivals for a bounded window: per-request p50/p99 latency and tok/s."""
+    from paper_2507_18006_b200.serving import InstanceState, ServingEngine, poisson_arrivals
+
+    reqs = poisson_arrivals(args.serve_rps, args.serve_s, args.prompt, args.serve_gen, seed=7)
+    inst = InstanceState(0, ex, max_batch_size=batch)
+    eng = ServingEngine([inst], seed=7)
+    res = eng.run(reqs)
+    s = res.summary()
+    s.update({"rps": args.serve_rps, "arrival_window_s": args.serve_s, "requests": len(reqs),
+              "prompt_len": args.prompt, "gen_len": args.serve_gen, "max_batch_size": batch,
+              "what": "wall-clock serving run: Poisson arrivals (seed 7), FIFO admission, prefill-then-decode "
+                      "continuous batching (sim.py:624-736 semantics); latency = completion - arrival"})
+    return s
 
 
 def run_ours(args, rank: int, world: int, dist) -> None:
@@ -264,6 +281,8 @@ def run_ours(args, rank: int, world: int, dist) -> None:
     prof = ex.profile_read()
     ex.profile(False)
     mig = measure_migration(ex, cat, cluster, n_dev)
+    ex.release_all()
+    serving = serving_window(ex, args, batch) if args.serve_s > 0 else None
     total_dev_s = sum(dev_ms) / 1e3
     value = batch * args.steps / total_dev_s
     e2e = batch * args.steps / sum(wall_s)
@@ -304,6 +323,7 @@ def run_ours(args, rank: int, world: int, dist) -> None:
                      "attention": {"achieved": attn_gbs, "frac": attn_gbs / peaks["hbm_gbs"],
                                    "bytes_per_launch": a["bytes"] / max(1, a["launches"])}},
         "migrate": mig,
+        "serving": serving,
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -326,6 +346,9 @@ def main() -> None:
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--replicate-layers", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--serve-s", type=float, default=8.0, help="serving window (0 = skip)")
+    ap.add_argument("--serve-rps", type=float, default=40.0)
+    ap.add_argument("--serve-gen", type=int, default=64)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -22,6 +22,10 @@ int cbt_rope_kv(uint16_t* qkv, uint16_t* kv, const int32_t* row_slot, const int3
                 int32_t Hkv, int32_t hd, int32_t max_ctx, float theta);
 int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* row_slot,
                   const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx);
+/* decode path: RoPE of q/k + KV append fused into the attention kernel */
+int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* out, const int32_t* row_slot,
+                        const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,
+                        float theta);
 int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
 /* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,

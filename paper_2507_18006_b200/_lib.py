@@ -116,6 +116,8 @@ _SIGS = {
     "cbt_rmsnorm": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float]),
     "cbt_rope_kv": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_float]),
     "cbt_attention": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    "cbt_attention_fused": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_float]),
     "cbt_argmax": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
 }
 

@@ -42,14 +42,65 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   const size_t pos_stride = 2 * kvd;
   const uint16_t* kbase = a.kv + (size_t)slot * a.max_ctx * pos_stride + (size_t)hk * HD + lg * 8;
   const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
+  const int cur = len - 1;  // position of this row's own token
 
   __shared__ float sm_state[kAttnWarps][G][10];
+
+  if (a.rope != nullptr && warp == 0 && p_begin <= cur && cur < p_end) {
+    // Fused decode path: the CTA whose context split holds the newest position
+    // appends this row's rotated k and raw v for kv head hk to the cache.
+    uint16_t* kc = const_cast<uint16_t*>(a.kv) + ((size_t)slot * a.max_ctx + cur) * pos_stride + (size_t)hk * HD;
+    const uint16_t* ksrc = a.qkv + row * qkv_ld + (size_t)(a.H + hk) * HD;
+    const uint16_t* vsrc = ksrc + (size_t)a.Hkv * HD;
+    constexpr int half = HD / 2, cph = half / 8;
+    const float2* rp = a.rope + (size_t)cur * half;
+    if (lane < cph) {
+      const int i0 = lane * 8;
+      const uint4 x = *reinterpret_cast<const uint4*>(ksrc + i0);
+      const uint4 y = *reinterpret_cast<const uint4*>(ksrc + i0 + half);
+      const float x1[8] = {bf16_lo(x.x), bf16_hi(x.x), bf16_lo(x.y), bf16_hi(x.y),
+                           bf16_lo(x.z), bf16_hi(x.z), bf16_lo(x.w), bf16_hi(x.w)};
+      const float x2[8] = {bf16_lo(y.x), bf16_hi(y.x), bf16_lo(y.y), bf16_hi(y.y),
+                           bf16_lo(y.z), bf16_hi(y.z), bf16_lo(y.w), bf16_hi(y.w)};
+      float o1[8], o2[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 cs = rp[i0 + j];
+        o1[j] = x1[j] * cs.x - x2[j] * cs.y;
+        o2[j] = x2[j] * cs.x + x1[j] * cs.y;
+      }
+      uint4 r1, r2;
+      r1.x = pack_bf16x2(o1[0], o1[1]); r1.y = pack_bf16x2(o1[2], o1[3]);
+      r1.z = pack_bf16x2(o1[4], o1[5]); r1.w = pack_bf16x2(o1[6], o1[7]);
+      r2.x = pack_bf16x2(o2[0], o2[1]); r2.y = pack_bf16x2(o2[2], o2[3]);
+      r2.z = pack_bf16x2(o2[4], o2[5]); r2.w = pack_bf16x2(o2[6], o2[7]);
+      *reinterpret_cast<uint4*>(kc + i0) = r1;
+      *reinterpret_cast<uint4*>(kc + i0 + half) = r2;
+    }
+    if (lane < HD / 8)
+      reinterpret_cast<uint4*>(kc + kvd)[lane] = reinterpret_cast<const uint4*>(vsrc)[lane];
+  }
+  if (a.rope != nullptr) __syncthreads();  // the appended row is read back by the loop below
 
   for (int g = 0; g < gq; ++g) {
     const int qh = hk * gq + g;
     const uint4 qv = *reinterpret_cast<const uint4*>(a.qkv + row * qkv_ld + (size_t)qh * HD + lg * 8);
     float q[8] = {bf16_lo(qv.x), bf16_hi(qv.x), bf16_lo(qv.y), bf16_hi(qv.y),
                   bf16_lo(qv.z), bf16_hi(qv.z), bf16_lo(qv.w), bf16_hi(qv.w)};
+    if (a.rope != nullptr) {
+      // rotate-half RoPE of q in registers: the partner chunk lives G/2 lanes away;
+      // rounded to bf16 exactly like the stand-alone rope_kv kernel
+      const int hl = lg % (G / 2);
+      const bool first = lg < G / 2;
+      const float2* rp = a.rope + (size_t)cur * (HD / 2) + hl * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float other = __shfl_xor_sync(0xffffffffu, q[i], G / 2);
+        const float2 cs = rp[i];
+        const float r = first ? q[i] * cs.x - other * cs.y : q[i] * cs.x + other * cs.y;
+        q[i] = bf16_to_f(f_to_bf16(r));
+      }
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[i] *= qscale;
     float m = -INFINITY, l = 0.f, acc[8];
@@ -65,8 +116,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         valid[u] = pos < p_end;
         if (valid[u]) {
           const uint16_t* kp = kbase + (size_t)pos * pos_stride;
-          kk[u] = __ldg(reinterpret_cast<const uint4*>(kp));
-          vv[u] = __ldg(reinterpret_cast<const uint4*>(kp + kvd));
+          // coherent loads: the fused path appended this row's K/V in this kernel
+          kk[u] = *reinterpret_cast<const uint4*>(kp);
+          vv[u] = *reinterpret_cast<const uint4*>(kp + kvd);
         } else {
           kk[u] = make_uint4(0, 0, 0, 0);
           vv[u] = make_uint4(0, 0, 0, 0);

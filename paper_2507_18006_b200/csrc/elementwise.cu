@@ -184,9 +184,22 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int32_t* __restr
   const float* row = logits + (size_t)t * V;
   float best = -INFINITY;
   int idx = 0x7fffffff;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    float v = row[i];
-    if (v > best) { best = v; idx = i; }  // strided ascending: first max per thread
+  // 128-bit loads, all in flight at once; each thread scans ascending indices so
+  // its first maximum is its lowest index
+  if ((V & 3) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    for (int i = threadIdx.x; i < V / 4; i += blockDim.x) {
+      const float4 v = r4[i];
+      if (v.x > best) { best = v.x; idx = 4 * i; }
+      if (v.y > best) { best = v.y; idx = 4 * i + 1; }
+      if (v.z > best) { best = v.z; idx = 4 * i + 2; }
+      if (v.w > best) { best = v.w; idx = 4 * i + 3; }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+      const float v = row[i];
+      if (v > best) { best = v; idx = i; }
+    }
   }
   __shared__ float sv[32];
   __shared__ int si[32];
@@ -215,7 +228,7 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int32_t* __restr
 
 cudaError_t argmax_launch(const float* logits, int32_t* out, int T, int V, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  return launch_pdl(argmax_kernel, dim3(T), dim3(512), 0, st, logits, out, V);
+  return launch_pdl(argmax_kernel, dim3(T), dim3(1024), 0, st, logits, out, V);
 }
 
 // ---------------------------------------------------------------- init

@@ -64,6 +64,7 @@ struct AttnArgs {
   const int32_t* row_pos;
   float* ws;       // split-context partials
   size_t ws_floats;
+  const float2* rope;  // non-null: fused decode path (RoPE of q/k + KV append inside the kernel)
   int T, row_off, H, Hkv, hd, max_ctx, max_len;
   float scale;  // 1/sqrt(hd)
 };

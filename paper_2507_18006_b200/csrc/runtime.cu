@@ -149,6 +149,7 @@ struct cb_model {
   int32_t* pin_meta = nullptr;
   int32_t* pin_next = nullptr;
   std::vector<std::vector<Route>> last_routing;
+  int cur_phase = 0;  // CB_PHASE_* of the pass in flight
   int cur_T = 0;  // rows of the pass in flight: per-step meta = [tokens | slot | pos] x T, then gather x bs
   Prof prof;
 };
@@ -453,7 +454,9 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   uint16_t* kv = L.kv[ad];
   const int32_t* row_slot = wa.meta + m->cur_T;
   const int32_t* rpos = wa.meta + 2 * m->cur_T;
-  {
+  // decode rows are one per sequence: RoPE + KV append fuse into the attention kernel
+  const bool fused = m->cur_phase == CB_PHASE_DECODE;
+  if (!fused) {
     ProfScope ps(m, ad, CB_KCLASS_ELEMWISE, ac.compute, double(T) * m->qkv_n * 4);
     CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
                                d.max_ctx, ac.compute));
@@ -480,6 +483,7 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   aa.max_ctx = d.max_ctx;
   aa.max_len = max_len;
   aa.scale = 1.0f / std::sqrt(float(m->hd));
+  aa.rope = fused ? wa.rope : nullptr;
   {
     // algorithmic bytes: every attended K/V row once, q in, output out
     ProfScope ps(m, ad, CB_KCLASS_ATTENTION, ac.compute, kv_tokens * kv_token_bytes(m) + double(T) * m->q_n * 4,
@@ -523,6 +527,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   std::vector<int> row_pos(T);
   int32_t* meta = m->pin_meta;
   m->cur_T = T;
+  m->cur_phase = phase;
   for (int i = 0; i < bs; ++i)
     for (int r = seq_row[i]; r < seq_row[i + 1]; ++r) {
       const int pos = prefill ? r - seq_row[i] : m->slot_len[slots[i]];

@@ -113,6 +113,59 @@ int cbt_rmsnorm(const float* x, const uint16_t* gamma, uint16_t* y, int32_t T, i
   return finish(cb::rmsnorm_launch(x, gamma, y, T, d, eps, 0, 0));
 }
 
+}  // extern "C"
+
+namespace {
+float2* rope_table_dev(int max_ctx, int hd, float theta) {
+  const int half = hd / 2;
+  std::vector<float2> tab(size_t(max_ctx) * half);
+  for (int p = 0; p < max_ctx; ++p)
+    for (int i = 0; i < half; ++i) {
+      const double ang = double(p) * std::pow(double(theta), -2.0 * i / double(hd));
+      tab[size_t(p) * half + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+    }
+  float2* dtab = nullptr;
+  if (cudaMalloc(&dtab, tab.size() * sizeof(float2)) != cudaSuccess) return nullptr;
+  cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
+  return dtab;
+}
+}  // namespace
+
+extern "C" int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* out, const int32_t* row_slot,
+                                   const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd,
+                                   int32_t max_ctx, float theta) {
+  TestWs* ws;
+  int r = ws_for_current(&ws);
+  if (r) return r;
+  float2* dtab = rope_table_dev(max_ctx, hd, theta);
+  if (!dtab) return CB_ECUDA;
+  std::vector<int32_t> pos(T);
+  cudaMemcpy(pos.data(), row_pos, size_t(T) * 4, cudaMemcpyDeviceToHost);
+  int max_len = 0;
+  for (int v : pos) max_len = std::max(max_len, v + 1);
+  cb::AttnArgs a{};
+  a.qkv = qkv;
+  a.kv = kv;
+  a.out = out;
+  a.row_slot = row_slot;
+  a.row_pos = row_pos;
+  a.ws = ws->attn_ws;
+  a.ws_floats = ws->attn_floats;
+  a.T = T;
+  a.H = H;
+  a.Hkv = Hkv;
+  a.hd = hd;
+  a.max_ctx = max_ctx;
+  a.max_len = max_len;
+  a.scale = 1.0f / std::sqrt(float(hd));
+  a.rope = dtab;
+  r = finish(cb::attention_launch(a, ws->sms, 0));
+  cudaFree(dtab);
+  return r;
+}
+
+extern "C" {
+
 int cbt_rope_kv(uint16_t* qkv, uint16_t* kv, const int32_t* row_slot, const int32_t* row_pos, int32_t T, int32_t H,
                 int32_t Hkv, int32_t hd, int32_t max_ctx, float theta) {
   const int half = hd / 2;

@@ -224,6 +224,12 @@ class Executor:
         for r in requests:
             r.slot = None
 
+    def release_all(self) -> None:
+        """Free every KV slot (end of a benchmark phase)."""
+        arr = np.arange(self.cfg.max_slots, dtype=np.int32)
+        _lib.check(self.lib.cb_release_slots(self.handle, len(arr), _lib.i32(arr)))
+        self._slots = list(range(self.cfg.max_slots - 1, -1, -1))
+
     # ------------------------------------------------------------ passes
     def prefill(self, slots: np.ndarray, tokens: np.ndarray, prompt_lens: np.ndarray,
                 want_logits: bool = False) -> tuple[np.ndarray, np.ndarray | None, float]:

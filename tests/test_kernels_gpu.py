@@ -196,3 +196,29 @@ def test_argmax_ties_lowest_index(lib, cuda):
     ref = logits.cpu().numpy().argmax(-1)
     assert out.cpu().numpy().tolist() == ref.tolist()
     assert int(out[1]) == 100
+
+
+@pytest.mark.parametrize("H,Hkv,hd,lens", [(4, 4, 64, [1, 16, 17, 40]), (32, 32, 128, [300, 1, 129, 900]),
+                                           (8, 2, 128, [5, 700])])
+def test_fused_decode_attention_bit_identical(lib, cuda, H, Hkv, hd, lens):
+    """Decode path: RoPE + KV append fused into attention == rope_kv kernel then
+    attention, bit for bit (output and appended cache row)."""
+    torch = cuda
+    T = len(lens)
+    max_ctx = max(lens) + 2
+    qkv = _bf16(torch, (T, (H + 2 * Hkv) * hd), 1.0, 21).cuda()
+    kv = _bf16(torch, (T, max_ctx, 2, Hkv * hd), 1.0, 22).cuda()
+    row_slot = torch.arange(T, dtype=torch.int32, device="cuda")
+    row_pos = torch.tensor([L - 1 for L in lens], dtype=torch.int32, device="cuda")
+    q1, kv1 = qkv.clone(), kv.clone()
+    out1 = torch.zeros(T, H * hd, dtype=torch.bfloat16, device="cuda")
+    assert lib.cbt_rope_kv(_ptr(q1), _ptr(kv1), _ptr(row_slot), _ptr(row_pos), T, H, Hkv, hd, max_ctx,
+                           C.c_float(1e4)) == 0
+    assert lib.cbt_attention(_ptr(q1), _ptr(kv1), _ptr(out1), _ptr(row_slot), _ptr(row_pos), T, H, Hkv, hd,
+                             max_ctx) == 0
+    q2, kv2 = qkv.clone(), kv.clone()
+    out2 = torch.zeros_like(out1)
+    assert lib.cbt_attention_fused(_ptr(q2), _ptr(kv2), _ptr(out2), _ptr(row_slot), _ptr(row_pos), T, H, Hkv, hd,
+                                   max_ctx, C.c_float(1e4)) == 0
+    assert torch.equal(out1, out2)
+    assert torch.equal(kv1, kv2)
