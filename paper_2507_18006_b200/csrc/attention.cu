@@ -19,7 +19,7 @@
 namespace cb {
 
 static constexpr int kAttnWarps = 4;
-static constexpr int kUnroll = 4;
+static constexpr int kUnroll = 8;
 
 template <int HD>
 __global__ void __launch_bounds__(kAttnWarps * 32)
@@ -108,13 +108,12 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 
     for (int p0 = p_begin + warp * P; p0 < p_end; p0 += kAttnWarps * P * kUnroll) {
+      // all kUnroll positions' K and V rows in flight before any is used
       uint4 kk[kUnroll], vv[kUnroll];
-      bool valid[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const int pos = p0 + u * kAttnWarps * P + pg;
-        valid[u] = pos < p_end;
-        if (valid[u]) {
+        if (pos < p_end) {
           const uint16_t* kp = kbase + (size_t)pos * pos_stride;
           // coherent loads: the fused path appended this row's K/V in this kernel
           kk[u] = *reinterpret_cast<const uint4*>(kp);
@@ -124,24 +123,42 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
           vv[u] = make_uint4(0, 0, 0, 0);
         }
       }
+      float s[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        s[u] = q[0] * bf16_lo(kk[u].x) + q[1] * bf16_hi(kk[u].x) + q[2] * bf16_lo(kk[u].y) +
+               q[3] * bf16_hi(kk[u].y) + q[4] * bf16_lo(kk[u].z) + q[5] * bf16_hi(kk[u].z) +
+               q[6] * bf16_lo(kk[u].w) + q[7] * bf16_hi(kk[u].w);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+      // one online-softmax update for the kUnroll positions
+      float mx = m;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        float s = q[0] * bf16_lo(kk[u].x) + q[1] * bf16_hi(kk[u].x) + q[2] * bf16_lo(kk[u].y) +
-                  q[3] * bf16_hi(kk[u].y) + q[4] * bf16_lo(kk[u].z) + q[5] * bf16_hi(kk[u].z) +
-                  q[6] * bf16_lo(kk[u].w) + q[7] * bf16_hi(kk[u].w);
+        if (p0 + u * kAttnWarps * P + pg >= p_end) s[u] = -INFINITY;
+        mx = fmaxf(mx, s[u]);
+      }
+      if (mx != -INFINITY) {
+        const float cf = exp2f(m - mx);  // m == -inf -> 0
+        l *= cf;
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (valid[u]) {
-          const float mn = fmaxf(m, s);
-          const float cf = exp2f(m - mn);
-          const float p = exp2f(s - mn);
-          l = l * cf + p;
-          const float vf[8] = {bf16_lo(vv[u].x), bf16_hi(vv[u].x), bf16_lo(vv[u].y), bf16_hi(vv[u].y),
-                               bf16_lo(vv[u].z), bf16_hi(vv[u].z), bf16_lo(vv[u].w), bf16_hi(vv[u].w)};
+        for (int i = 0; i < 8; ++i) acc[i] *= cf;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = acc[i] * cf + p * vf[i];
-          m = mn;
+        for (int u = 0; u < kUnroll; ++u) {
+          const float p = exp2f(s[u] - mx);  // invalid positions: exp2(-inf) = 0
+          l += p;
+          acc[0] += p * bf16_lo(vv[u].x);
+          acc[1] += p * bf16_hi(vv[u].x);
+          acc[2] += p * bf16_lo(vv[u].y);
+          acc[3] += p * bf16_hi(vv[u].y);
+          acc[4] += p * bf16_lo(vv[u].z);
+          acc[5] += p * bf16_hi(vv[u].z);
+          acc[6] += p * bf16_lo(vv[u].w);
+          acc[7] += p * bf16_hi(vv[u].w);
         }
+        m = mx;
       }
     }
     // merge the P position groups of this warp (lanes with equal lg)
