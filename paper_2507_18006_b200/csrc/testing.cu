@@ -210,6 +210,43 @@ int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const 
   return finish(cb::attention_launch(a, ws->sms, 0));
 }
 
+int cbt_attention_bench(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* row_slot,
+                        const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,
+                        int32_t max_len, int32_t iters, float* ms_per_launch) {
+  TestWs* ws;
+  int r = ws_for_current(&ws);
+  if (r) return r;
+  cb::AttnArgs a{};
+  a.qkv = qkv;
+  a.kv = kv;
+  a.out = out;
+  a.row_slot = row_slot;
+  a.row_pos = row_pos;
+  a.ws = ws->attn_ws;
+  a.ws_floats = ws->attn_floats;
+  a.T = T;
+  a.H = H;
+  a.Hkv = Hkv;
+  a.hd = hd;
+  a.max_ctx = max_ctx;
+  a.max_len = max_len;
+  a.scale = 1.0f / std::sqrt(float(hd));
+  for (int i = 0; i < 3; ++i) cb::attention_launch(a, ws->sms, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
+  for (int i = 0; i < iters; ++i) cb::attention_launch(a, ws->sms, 0);
+  cudaEventRecord(e1, 0);
+  if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_per_launch = ms / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return finish(cudaGetLastError());
+}
+
 int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V) {
   return finish(cb::argmax_launch(logits, out, T, V, 0));
 }
