@@ -23,25 +23,28 @@ namespace cb {
 static constexpr int kAttnWarps = 4;
 static constexpr int kUnroll = 4;
 
-// positions in flight per lane group per step: fewer for wide GQA groups so the
-// per-head q / accumulator registers fit
-template <int GQ>
-struct AttnUnroll {
-  static constexpr int value = GQ >= 4 ? 2 : 4;
-};
-
-template <int HD, int GQ, int U>
+// CTA = (row, kv head, context split), 4 warps.  Lane group j (hd/8 lanes,
+// 16 bytes of a K/V row each) owns q-head  j % gq  of the KV group and the
+// positions  p == j / gq  (mod  n_groups / gq).  For MHA (gq = 1) the groups
+// split the positions 8 (hd 128) ways; for GQA the groups of one warp read the
+// same K/V addresses (one transaction) for different q-heads, so every K/V
+// byte is fetched once for the whole head group.
+template <int HD, int U>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-    attn_kernel(const AttnArgs a, int nsplit, int chunk) {
+    attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq) {
   pdl_trigger();
   pdl_wait();
-  constexpr int G = HD / 8;  // lanes per position
-  constexpr int P = 32 / G;  // positions per warp step
+  constexpr int G = HD / 8;               // lanes per group
+  constexpr int P = 32 / G;               // groups per warp
+  constexpr int NG = kAttnWarps * P;      // groups per CTA
   const int row = a.row_off + blockIdx.x;
   const int hk = blockIdx.y;
   const int split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lg = lane % G, pg = lane / G;
+  const int grp = warp * P + pg;
+  const int head = grp % gq, phase = grp / gq, nph = NG / gq;
+  const int qh = hk * gq + head;
   const int slot = a.row_slot[row];
   const int len = a.row_pos[row] + 1;
   const int p_begin = split * chunk;
@@ -53,7 +56,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
   const int cur = len - 1;  // position of this row's own token
 
-  __shared__ float sm_state[kAttnWarps][GQ][G][10];
+  __shared__ float sm_state[NG][G][10];
 
   if (a.rope != nullptr && warp == 0 && p_begin <= cur && cur < p_end) {
     // Fused decode path: the CTA whose context split holds the newest position
@@ -91,14 +94,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
   if (a.rope != nullptr) __syncthreads();  // the appended row is read back by the loop below
 
-  // q of every head of this KV group: this lane's 8 elements of each
-  float q[GQ][8];
-#pragma unroll
-  for (int g = 0; g < GQ; ++g) {
-    const int qh = hk * GQ + g;
+  float q[8];
+  {
     const uint4 qv = *reinterpret_cast<const uint4*>(a.qkv + row * qkv_ld + (size_t)qh * HD + lg * 8);
-    q[g][0] = bf16_lo(qv.x); q[g][1] = bf16_hi(qv.x); q[g][2] = bf16_lo(qv.y); q[g][3] = bf16_hi(qv.y);
-    q[g][4] = bf16_lo(qv.z); q[g][5] = bf16_hi(qv.z); q[g][6] = bf16_lo(qv.w); q[g][7] = bf16_hi(qv.w);
+    q[0] = bf16_lo(qv.x); q[1] = bf16_hi(qv.x); q[2] = bf16_lo(qv.y); q[3] = bf16_hi(qv.y);
+    q[4] = bf16_lo(qv.z); q[5] = bf16_hi(qv.z); q[6] = bf16_lo(qv.w); q[7] = bf16_hi(qv.w);
     if (a.rope != nullptr) {
       // rotate-half RoPE of q in registers: the partner chunk lives G/2 lanes away;
       // rounded to bf16 exactly like the stand-alone rope_kv kernel
@@ -107,31 +107,30 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       const float2* rp = a.rope + (size_t)cur * (HD / 2) + hl * 8;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float other = __shfl_xor_sync(0xffffffffu, q[g][i], G / 2);
+        const float other = __shfl_xor_sync(0xffffffffu, q[i], G / 2);
         const float2 cs = rp[i];
-        const float r = first ? q[g][i] * cs.x - other * cs.y : q[g][i] * cs.x + other * cs.y;
-        q[g][i] = bf16_to_f(f_to_bf16(r));
+        const float r = first ? q[i] * cs.x - other * cs.y : q[i] * cs.x + other * cs.y;
+        q[i] = bf16_to_f(f_to_bf16(r));
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[g][i] *= qscale;
+    for (int i = 0; i < 8; ++i) q[i] *= qscale;
   }
-  float m[GQ], l[GQ], acc[GQ][8];
+  float m = -INFINITY, l = 0.f, acc[8];
 #pragma unroll
-  for (int g = 0; g < GQ; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
-  }
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 
-  // every K/V row of the group is read once for all GQ heads
-  for (int p0 = p_begin + warp * P; p0 < p_end; p0 += kAttnWarps * P * U) {
+  // the loop trip count is uniform within a warp (groups of a warp share the
+  // phase when gq >= P; for gq < P they differ by < nph, handled by predication)
+  const int wphase = (warp * P) / gq;
+  for (int pb = p_begin + wphase; pb < p_end; pb += nph * U) {
     uint4 kk[U], vv[U];
+    bool ok[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int pos = p0 + u * kAttnWarps * P + pg;
-      if (pos < p_end) {
+      const int pos = pb + (phase - wphase) + u * nph;
+      ok[u] = pos < p_end;
+      if (ok[u]) {
         const uint16_t* kp = kbase + (size_t)pos * pos_stride;
         // coherent loads: the fused path appended this row's K/V in this kernel
         kk[u] = *reinterpret_cast<const uint4*>(kp);
@@ -141,97 +140,59 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         vv[u] = make_uint4(0, 0, 0, 0);
       }
     }
-    float kf[U][8];
+    float s[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      s[u] = q[0] * bf16_lo(kk[u].x) + q[1] * bf16_hi(kk[u].x) + q[2] * bf16_lo(kk[u].y) +
+             q[3] * bf16_hi(kk[u].y) + q[4] * bf16_lo(kk[u].z) + q[5] * bf16_hi(kk[u].z) +
+             q[6] * bf16_lo(kk[u].w) + q[7] * bf16_hi(kk[u].w);
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+    float mx = m;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      kf[u][0] = bf16_lo(kk[u].x); kf[u][1] = bf16_hi(kk[u].x); kf[u][2] = bf16_lo(kk[u].y);
-      kf[u][3] = bf16_hi(kk[u].y); kf[u][4] = bf16_lo(kk[u].z); kf[u][5] = bf16_hi(kk[u].z);
-      kf[u][6] = bf16_lo(kk[u].w); kf[u][7] = bf16_hi(kk[u].w);
+      if (!ok[u]) s[u] = -INFINITY;
+      mx = fmaxf(mx, s[u]);
     }
+    if (mx != -INFINITY) {
+      const float cf = exp2f(m - mx);  // m == -inf -> 0
+      l *= cf;
 #pragma unroll
-    for (int g = 0; g < GQ; ++g) {
-      float s[U];
+      for (int i = 0; i < 8; ++i) acc[i] *= cf;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        float t = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) t += q[g][i] * kf[u][i];
-        s[u] = t;
+        const float p = exp2f(s[u] - mx);  // invalid positions: exp2(-inf) = 0
+        l += p;
+        acc[0] += p * bf16_lo(vv[u].x);
+        acc[1] += p * bf16_hi(vv[u].x);
+        acc[2] += p * bf16_lo(vv[u].y);
+        acc[3] += p * bf16_hi(vv[u].y);
+        acc[4] += p * bf16_lo(vv[u].z);
+        acc[5] += p * bf16_hi(vv[u].z);
+        acc[6] += p * bf16_lo(vv[u].w);
+        acc[7] += p * bf16_hi(vv[u].w);
       }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1)
-#pragma unroll
-        for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-      // one online-softmax update for the U positions
-      float mx = m[g];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (p0 + u * kAttnWarps * P + pg >= p_end) s[u] = -INFINITY;
-        mx = fmaxf(mx, s[u]);
-      }
-      if (mx != -INFINITY) {
-        const float cf = exp2f(m[g] - mx);  // m == -inf -> 0
-        l[g] *= cf;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[g][i] *= cf;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const float p = exp2f(s[u] - mx);  // invalid positions: exp2(-inf) = 0
-          l[g] += p;
-          acc[g][0] += p * bf16_lo(vv[u].x);
-          acc[g][1] += p * bf16_hi(vv[u].x);
-          acc[g][2] += p * bf16_lo(vv[u].y);
-          acc[g][3] += p * bf16_hi(vv[u].y);
-          acc[g][4] += p * bf16_lo(vv[u].z);
-          acc[g][5] += p * bf16_hi(vv[u].z);
-          acc[g][6] += p * bf16_lo(vv[u].w);
-          acc[g][7] += p * bf16_hi(vv[u].w);
-        }
-        m[g] = mx;
-      }
+      m = mx;
     }
   }
+  sm_state[grp][lg][0] = m;
+  sm_state[grp][lg][1] = l;
 #pragma unroll
-  for (int g = 0; g < GQ; ++g) {
-    // merge the P position groups of this warp (lanes with equal lg)
-#pragma unroll
-    for (int o = G; o < 32; o <<= 1) {
-      const float om = __shfl_xor_sync(0xffffffffu, m[g], o);
-      const float ol = __shfl_xor_sync(0xffffffffu, l[g], o);
-      float oacc[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) oacc[i] = __shfl_xor_sync(0xffffffffu, acc[g][i], o);
-      const float mn = fmaxf(m[g], om);
-      const float c1 = (m[g] == -INFINITY) ? 0.f : exp2f(m[g] - mn);
-      const float c2 = (om == -INFINITY) ? 0.f : exp2f(om - mn);
-      l[g] = l[g] * c1 + ol * c2;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[g][i] = acc[g][i] * c1 + oacc[i] * c2;
-      m[g] = mn;
-    }
-    if (pg == 0) {
-      sm_state[warp][g][lg][0] = m[g];
-      sm_state[warp][g][lg][1] = l[g];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) sm_state[warp][g][lg][2 + i] = acc[g][i];
-    }
-  }
+  for (int i = 0; i < 8; ++i) sm_state[grp][lg][2 + i] = acc[i];
   __syncthreads();
-  // warp w finalises heads g = w, w + 4, ... (lanes < G)
-  for (int g = warp; g < GQ; g += kAttnWarps) {
-    if (lane >= G) continue;
-    const int qh = hk * GQ + g;
+  // group j < gq finalises head j over its nph phases (groups j, j+gq, ...)
+  if (grp < gq) {
     float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kAttnWarps; ++w) M = fmaxf(M, sm_state[w][g][lane][0]);
+    for (int f = 0; f < nph; ++f) M = fmaxf(M, sm_state[grp + f * gq][lg][0]);
     float L = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int f = 0; f < nph; ++f) {
+      const float* stt = sm_state[grp + f * gq][lg];
+      const float cw = (stt[0] == -INFINITY) ? 0.f : exp2f(stt[0] - M);
+      L += stt[1] * cw;
 #pragma unroll
-    for (int w = 0; w < kAttnWarps; ++w) {
-      const float mw = sm_state[w][g][lane][0];
-      const float cw = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-      L += sm_state[w][g][lane][1] * cw;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] += sm_state[w][g][lane][2 + i] * cw;
+      for (int i = 0; i < 8; ++i) o[i] += stt[2 + i] * cw;
     }
     if (nsplit == 1) {
       const float inv = 1.f / L;
@@ -240,17 +201,17 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
       ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
       ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
-      *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lane * 8) = ov;
+      *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
     } else {
       // partial state: [(row_local * H + qh) * nsplit + split] -> (m, l, acc[HD])
       const size_t idx = ((size_t)blockIdx.x * a.H + qh) * nsplit + split;
       float* st = a.ws + idx * (HD + 2);
-      if (lane == 0) {
+      if (lg == 0) {
         st[0] = M;
         st[1] = L;
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) st[2 + lane * 8 + i] = o[i];
+      for (int i = 0; i < 8; ++i) st[2 + lg * 8 + i] = o[i];
     }
   }
 }
@@ -274,24 +235,11 @@ __global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
   a.out[(size_t)row * a.H * HD + (size_t)qh * HD + i] = f_to_bf16(o / L);
 }
 
-template <int HD, int GQ>
-static cudaError_t attention_launch_t(const AttnArgs& a, dim3 grid, int nsplit, int chunk, cudaStream_t st) {
-  if (GQ == 1) {
-    // positions in flight per lane group (tunable for experiments: CB_ATTN_UNROLL=2|4|8)
-    static const int u = [] {
-      const char* e = getenv("CB_ATTN_UNROLL");
-      return e ? atoi(e) : 4;
-    }();
-    if (u == 2) return launch_pdl(attn_kernel<HD, GQ, 2>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk);
-    if (u == 8) return launch_pdl(attn_kernel<HD, GQ, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk);
-  }
-  return launch_pdl(attn_kernel<HD, GQ, AttnUnroll<GQ>::value>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit,
-                    chunk);
-}
-
 template <int HD>
 static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st) {
   const int gq = a.H / a.Hkv;
+  constexpr int NG = kAttnWarps * (32 / (HD / 8));
+  if (gq < 1 || NG % gq != 0) return cudaErrorInvalidValue;
   int nsplit = 1;
   const long long ctas = (long long)a.T * a.Hkv;
   if (ctas < 2LL * num_sms && a.max_len > 256) {
@@ -302,14 +250,16 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
   }
   const int chunk = (a.max_len + nsplit - 1) / nsplit;
   dim3 grid(a.T, a.Hkv, nsplit);
-  cudaError_t e;
-  switch (gq) {
-    case 1: e = attention_launch_t<HD, 1>(a, grid, nsplit, chunk, st); break;
-    case 2: e = attention_launch_t<HD, 2>(a, grid, nsplit, chunk, st); break;
-    case 4: e = attention_launch_t<HD, 4>(a, grid, nsplit, chunk, st); break;
-    case 8: e = attention_launch_t<HD, 8>(a, grid, nsplit, chunk, st); break;
-    default: return cudaErrorInvalidValue;
-  }
+  // positions in flight per lane group: 4 when there are enough CTAs to fill
+  // the GPU (measured best for decode batches), 8 for few long rows
+  static const int forced = [] {
+    const char* e = getenv("CB_ATTN_UNROLL");
+    return e ? atoi(e) : 0;
+  }();
+  const long long total = ctas * nsplit;
+  const int u = forced ? forced : (total >= 8LL * num_sms ? 4 : 8);
+  cudaError_t e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq)
+                         : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq);
   if (e != cudaSuccess || nsplit == 1) return e;
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);
 }

@@ -158,7 +158,8 @@ def test_rope_kv_append(lib, cuda, H, Hkv, hd):
 
 
 @pytest.mark.parametrize("H,Hkv,hd,lens", [(4, 4, 64, [1, 16, 17, 63]), (32, 32, 128, [300, 1, 128, 2000]),
-                                           (8, 2, 128, [5, 700]), (32, 32, 128, [4096])])
+                                           (8, 2, 128, [5, 700]), (32, 32, 128, [4096]), (16, 2, 128, [33, 260]),
+                                           (64, 8, 128, [129, 7, 1000]), (8, 4, 64, [70, 3])])
 def test_attention(lib, cuda, H, Hkv, hd, lens):
     torch = cuda
     T = len(lens)
