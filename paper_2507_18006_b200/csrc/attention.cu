@@ -242,9 +242,13 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
   if (gq < 1 || NG % gq != 0) return cudaErrorInvalidValue;
   int nsplit = 1;
   const long long ctas = (long long)a.T * a.Hkv;
-  if (ctas < 2LL * num_sms && a.max_len > 256) {
-    nsplit = int((2LL * num_sms + ctas - 1) / ctas);
-    nsplit = min(nsplit, (a.max_len + 255) / 256);
+  // enough CTAs to keep HBM busy: MHA needs 2 waves; a GQA CTA carries gq
+  // heads' work, so aim for 8 waves of CTAs there
+  const long long want = (gq > 1 ? 8LL : 2LL) * num_sms;
+  const int min_chunk = gq > 1 ? 128 : 256;
+  if (ctas < want && a.max_len > min_chunk) {
+    nsplit = int((want + ctas - 1) / ctas);
+    nsplit = min(nsplit, (a.max_len + min_chunk - 1) / min_chunk);
     nsplit = min(nsplit, 32);
     while (nsplit > 1 && (size_t)a.T * a.H * nsplit * (HD + 2) > a.ws_floats) --nsplit;
   }
@@ -257,7 +261,7 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
     return e ? atoi(e) : 0;
   }();
   const long long total = ctas * nsplit;
-  const int u = forced ? forced : (total >= 8LL * num_sms ? 4 : 8);
+  const int u = forced ? forced : (gq == 1 && total >= 8LL * num_sms ? 4 : 8);
   cudaError_t e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq)
                          : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq);
   if (e != cudaSuccess || nsplit == 1) return e;

@@ -431,7 +431,9 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   int cs = a.cluster_split;
   if (cs == 0) {
     cs = 1;
-    if (TN <= 64 && tiles0 * 10 < (long long)num_sms * 6) {
+    // depends on the tile count only (n_ttiles == 1 for every decode batch <= 256
+    // rows), so a row's bits do not depend on how many rows share the launch
+    if (a.n_ttiles == 1 && tiles0 * 10 < (long long)num_sms * 6) {
       while (cs < 8 && tiles0 * cs * 2 <= num_sms && cs * 2 <= a.kblocks) cs *= 2;
     }
   }
