@@ -141,9 +141,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_ttiles = a.n_ttiles;
-  const StreamK sk{a.units, int(gridDim.x), a.kblocks};
   const int c = blockIdx.x;
-  // Work range: stream-K slice of the (tile, k-block) space, or -- in cluster
+  // Multicast clusters (mc > 1): the mc CTAs of a cluster own mc neighbouring
+  // weight tiles ("a group") and walk the group's k-blocks in lockstep; CTA r
+  // loads 1/mc of each activation tile and multicasts it to the whole cluster,
+  // so an activation k-block is read from L2 once per cluster.  Stream-K units
+  // are (group, k-block) and are dealt out per cluster.
+  const int mc = a.mcast > 1 ? a.mcast : 1;
+  const int mrank = c % mc;
+  const StreamK sk{a.units, int(gridDim.x) / mc, a.kblocks};
+  const int cl = c / mc;
+  // Work range: stream-K slice of the (group, k-block) space, or -- in cluster
   // split mode -- k-slice r of tile c / S (the cluster = the tile's S CTAs).
   const int csplit = a.cluster_split > 1 ? a.cluster_split : 1;
   int ubeg, uend;
@@ -152,9 +160,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     ubeg = tile * sk.kb + (r * sk.kb) / csplit;
     uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
   } else {
-    ubeg = sk.u0(c);
-    uend = sk.u0(c + 1);
+    ubeg = sk.u0(cl);
+    uend = sk.u0(cl + 1);
   }
+  const uint16_t mc_mask = uint16_t((1u << mc) - 1);
 
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
   if (warp == 0 && lane == 0) {
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], 1);
+      mbar_init(&empty_bar[i], mc);  // a stage is free once every CTA of the cluster consumed it
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -172,7 +181,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if (mc > 1)
+    cluster_sync_all();  // peers' barriers exist before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -185,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // weight tiles before waiting on it (programmatic dependent launch).
       const int npre = min(S, uend - ubeg);
       for (int i = 0; i < npre; ++i) {
-        const int u = ubeg + i, tile = u / sk.kb, kb = u % sk.kb;
+        const int u = ubeg + i, tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
         mbar_arrive_expect_tx(&full_bar[i], Cfg::kStageBytes);
         tma_load_2d(&tmW, &full_bar[i], sW + i * Cfg::kWBytes, kb * kBK, (tile / n_ttiles) * kBM, pol_w);
       }
@@ -193,14 +205,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
-        const int tile = u / sk.kb, kb = u % sk.kb;
+        const int tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
         const int mt = tile / n_ttiles, tt = tile % n_ttiles;
         if (u - ubeg >= npre) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt * kBM, pol_w);
         }
-        tma_load_2d(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
+        if (mc > 1)
+          tma_load_2d_mc(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes + mrank * (Cfg::kXBytes / mc), kb * kBK,
+                         a.row_off + tt * TN + mrank * (TN / mc), mc_mask, pol_x);
+        else
+          tma_load_2d(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -229,7 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(d_tmem, dw + uint64_t(2 * k), dx + uint64_t(2 * k), idesc,
                       (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty_bar[stage]);
+          if (mc > 1)
+            umma_commit_mc(&empty_bar[stage], mc_mask);  // the stage's X slices came from every CTA
+          else
+            umma_commit(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -249,7 +268,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = ubeg; u < uend;) {
-      const int tile = u / sk.kb, kb0 = u % sk.kb;
+      const int grp = u / sk.kb, kb0 = u % sk.kb;
+      const int tile = grp * mc + mrank;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
       const int mt = tile / n_ttiles, tt = tile % n_ttiles;
       const int n = mt * kBM + row_in_tile;
@@ -286,8 +306,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
       if (!whole && csplit == 1) {
         // stream-K fixup: the last CTA to deposit its part finishes the tile.
-        const int c_first = sk.cta_of(tile * sk.kb);
-        const int c_last = sk.cta_of(tile * sk.kb + sk.kb - 1);
+        const int c_first = sk.cta_of(grp * sk.kb);  // clusters sharing this group
+        const int c_last = sk.cta_of(grp * sk.kb + sk.kb - 1);
         __threadfence();
         named_bar_sync(1, kEpiThreads);
         if (et == 0) {
@@ -305,8 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < 8; ++j) sum[j] = make_float2(0.f, 0.f);
             for (int cc = c_first; cc <= c_last; ++cc) {
-              const int w = (sk.u0(cc) / sk.kb == tile) ? 0 : 1;
-              const float* p = a.ws + ((size_t)cc * 2 + w) * (size_t)(kBM * TN);
+              const int w = (sk.u0(cc) / sk.kb == grp) ? 0 : 1;
+              const float* p = a.ws + ((size_t)(cc * mc + mrank) * 2 + w) * (size_t)(kBM * TN);
               float2 ld[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) ld[j] = make_float2(0.f, 0.f);
@@ -369,9 +389,158 @@ __global__ void __launch_bounds__(kThreads, 1)
     cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
   tc_fence_before();
-  __syncthreads();
+  if (mc > 1)
+    cluster_sync_all();  // no CTA leaves while peers may still multicast into it / arrive on it
+  else
+    __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+}
+
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM for prefill-sized batches (T > 256): one tcgen05.mma.cta_group::2
+// computes a 256 (weight rows) x 256 (tokens) tile across the two SMs of a
+// cluster pair.  Each CTA stages its own 128 weight rows and 128 token rows
+// per k-block (both TMA loads signal the leader's barrier), so every byte of
+// the B operand feeds twice the MMA work of the 1-CTA kernel -- the prefill
+// GEMMs are L2-bandwidth / tensor bound, not HBM bound.  Persistent over pair
+// tiles; accumulators double buffered in TMEM (2 x 256 columns per CTA).
+static constexpr int kPairTN = 256;
+static constexpr int kPairStageBytes = 2 * kBM * kBK * 2;  // 16 KB weights + 16 KB tokens per CTA
+static constexpr int kPairStages = 6;
+static constexpr size_t kPairSmemBytes = size_t(kPairStages) * kPairStageBytes + 1024 + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                    const GemmArgs a) {
+  constexpr int S = kPairStages;
+  constexpr int HB = kBM * kBK * 2;  // one half-tile (128 rows x 64 k) in bytes
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + S * HB;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sX + S * HB);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int n_mt = (a.N + 2 * kBM - 1) / (2 * kBM);
+  const int n_tt = (a.T + kPairTN - 1) / kPairTN;
+  const int n_tiles = n_mt * n_tt;
+  const int kb_n = (a.K + kBK - 1) / kBK;
+
+  pdl_trigger();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 2 * kEpiThreads);  // both CTAs' epilogue threads report to the leader
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync_all();  // barriers of both CTAs exist before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_last();  // a weight tile is reused by consecutive token tiles
+      const uint64_t pol_x = policy_evict_last();
+      pdl_wait();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < n_tiles; tile += npairs) {
+        const int mt = tile / n_tt, tt = tile % n_tt;
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kPairStageBytes);
+          tma_load_2d_pair(&tmW, &full_bar[stage], sW + stage * HB, kb * kBK, mt * 2 * kBM + int(rank) * kBM, pol_w);
+          tma_load_2d_pair(&tmX, &full_bar[stage], sX + stage * HB, kb * kBK,
+                           a.row_off + tt * kPairTN + int(rank) * kBM, pol_x);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, kPairTN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = pair; tile < n_tiles; tile += npairs) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * kPairTN);
+        for (int kb = 0; kb < kb_n; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint64_t dw = make_sw128_desc(smem_u32(sW + stage * HB));
+            const uint64_t dx = make_sw128_desc(smem_u32(sX + stage * HB));
+#pragma unroll
+            for (int k = 0; k < kBK / kUmmaK; ++k)
+              umma_bf16_pair(d_tmem, dw + uint64_t(2 * k), dx + uint64_t(2 * k), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit_pair(&empty_bar[stage]);  // frees the stage in both CTAs
+          }
+          __syncwarp();
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit_pair(&tfull_bar[acc]);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    pdl_wait();
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t tempty_leader0 = dsmem_map(smem_u32(&tempty_bar[0]), 0);
+    const uint32_t tempty_leader1 = dsmem_map(smem_u32(&tempty_bar[1]), 0);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = pair; tile < n_tiles; tile += npairs) {
+      const int mt = tile / n_tt, tt = tile % n_tt;
+      const int n = mt * 2 * kBM + int(rank) * kBM + row_in_tile;
+      const int row0 = a.row_off + tt * kPairTN;
+      const int ncols = min(kPairTN, a.T - tt * kPairTN);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kPairTN);
+      for (int c0 = 0; c0 < ncols; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(t_addr + uint32_t(c0), r);
+        tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        emit16(a, n, row0 + c0, min(16, ncols - c0), v);
+      }
+      tc_fence_before();
+      mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
 }
 
 // ------------------------------------------------------------------ host side
@@ -406,12 +575,42 @@ int gemm_pick_tn(int T) {
   if (T <= 32) return 32;
   if (T <= 64) return 64;
   if (T <= 128) return 128;
-  return 256;
+  if (T <= 256) return 256;
+  return kPairTileMarker;  // CTA-pair kernel; its token box is 128 rows per CTA
+}
+
+// Work split of one launch.  Everything but the TN bucket depends on (N, K) and
+// the tile count only, so for decode batches (T <= 256, one token tile) a row's
+// result does not depend on how many rows share the launch.
+GemmPlan gemm_plan(int N, int K, int T, int num_sms) {
+  GemmPlan p{};
+  p.tn = gemm_pick_tn(T);
+  if (p.tn == kPairTileMarker) {
+    p.box_rows = kBM;
+    p.mcast = 1;
+    p.csplit = 1;
+    return p;
+  }
+  const long long tiles = (N + kBM - 1) / kBM;  // one token tile
+  const int kb = (K + kBK - 1) / kBK;
+  p.csplit = 1;
+  p.mcast = 1;
+  if (tiles * 10 < (long long)num_sms * 6) {
+    // few wide-K tiles (O / down projections): cluster split-K
+    while (p.csplit < 8 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
+  } else {
+    // many tiles: stream the weights, multicast the activation tile across a
+    // cluster of neighbouring weight tiles (slices of >= 8 rows)
+    p.mcast = p.tn >= 32 ? 4 : 2;
+    while (p.mcast > 1 && tiles < p.mcast * 8) p.mcast /= 2;
+  }
+  p.box_rows = p.tn / p.mcast;
+  return p;
 }
 
 template <int TN>
-static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, int num_sms,
-                             cudaStream_t st) {
+static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, const GemmPlan& plan,
+                             int num_sms, cudaStream_t st) {
   using Cfg = GemmCfg<TN>;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -420,59 +619,62 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Cfg::kSmemBytes));
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(gemm_tc_kernel<TN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) cudaGetLastError();
     attr_set[dev & 63] = true;
   }
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK - 1) / kBK;
-  const long long tiles0 = (long long)a.n_mtiles * a.n_ttiles;
-  // Cluster split-K for few wide-K tiles (decode O / down projections): each
-  // tile's K is cut over S CTAs of one cluster, partials reduced through DSMEM.
-  int cs = a.cluster_split;
-  if (cs == 0) {
-    cs = 1;
-    // depends on the tile count only (n_ttiles == 1 for every decode batch <= 256
-    // rows), so a row's bits do not depend on how many rows share the launch
-    if (a.n_ttiles == 1 && tiles0 * 10 < (long long)num_sms * 6) {
-      while (cs < 8 && tiles0 * cs * 2 <= num_sms && cs * 2 <= a.kblocks) cs *= 2;
-    }
-  }
-  a.cluster_split = cs;
-  if (cs > 1) {
-    a.units = int(tiles0 * a.kblocks);
-    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles0 * cs)), dim3(kThreads), Cfg::kSmemBytes, st,
-                              unsigned(cs), w, x, a);
-  }
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
-  long long units = tiles * a.kblocks;
-  a.units = int(units);
-  // HBM-bound weight streaming needs enough bytes in flight, not every SM:
-  // cap the split so a tile is shared by <= ~max_parts CTAs (short fixups).
-  long long grid = units < num_sms ? units : num_sms;
-  // Split rule (depends only on the tile count and TN bucket, so for decode
-  // batches in one bucket a row's bits do not depend on how many rows share
-  // the launch): few tiles -> spread each over <= 4 CTAs so every SM streams
-  // weights; many tiles or wide TN -> no split (the fixup would cost more).
-  int max_parts = a.max_parts;
-  if (max_parts <= 0) {
-    if (TN > 64 || tiles * 10 >= (long long)num_sms * 6)
-      max_parts = 1;
-    else
-      max_parts = int((num_sms + tiles - 1) / tiles) < 4 ? int((num_sms + tiles - 1) / tiles) : 4;
+  a.cluster_split = plan.csplit;
+  a.mcast = plan.mcast;
+  if (plan.csplit > 1) {
+    a.units = int(tiles * a.kblocks);
+    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads),
+                              Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, a);
   }
-  if (grid > tiles * max_parts) grid = tiles * max_parts;
-  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(grid)), dim3(kThreads), Cfg::kSmemBytes, st, w, x, a);
+  const int mc = plan.mcast;
+  const long long groups = (tiles + mc - 1) / mc;
+  a.units = int(groups * a.kblocks);
+  // persistent stream-K over clusters; a group is spread over <= max_parts clusters
+  long long clusters = num_sms / mc;
+  if (clusters > a.units) clusters = a.units;
+  const int max_parts = a.max_parts > 0 ? a.max_parts : 1;
+  if (clusters > groups * max_parts) clusters = groups * max_parts;
+  if (mc == 1)
+    return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(clusters)), dim3(kThreads), Cfg::kSmemBytes, st, w, x, a);
+  return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(clusters * mc)), dim3(kThreads), Cfg::kSmemBytes, st,
+                            unsigned(mc), w, x, a);
 }
 
-cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, int tn, int num_sms,
-                        cudaStream_t st) {
+static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, int num_sms, cudaStream_t st) {
+  static bool attr_set[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(kPairSmemBytes));
+    if (e != cudaSuccess) return e;
+    attr_set[dev & 63] = true;
+  }
+  const long long tiles = (long long)((a.N + 2 * kBM - 1) / (2 * kBM)) * ((a.T + kPairTN - 1) / kPairTN);
+  long long pairs = num_sms / 2;
+  if (pairs > tiles) pairs = tiles;
+  return launch_pdl_cluster(gemm_tc2_kernel, dim3(unsigned(2 * pairs)), dim3(kThreads), kPairSmemBytes, st, 2u,
+                            w, x, a);
+}
+
+cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
+                        int num_sms, cudaStream_t st) {
   if (a.T <= 0 || a.N <= 0) return cudaSuccess;
-  switch (tn) {
-    case 16: return launch_tn<16>(w, x, a, num_sms, st);
-    case 32: return launch_tn<32>(w, x, a, num_sms, st);
-    case 64: return launch_tn<64>(w, x, a, num_sms, st);
-    case 128: return launch_tn<128>(w, x, a, num_sms, st);
-    case 256: return launch_tn<256>(w, x, a, num_sms, st);
+  switch (plan.tn) {
+    case 16: return launch_tn<16>(w, x, a, plan, num_sms, st);
+    case 32: return launch_tn<32>(w, x, a, plan, num_sms, st);
+    case 64: return launch_tn<64>(w, x, a, plan, num_sms, st);
+    case 128: return launch_tn<128>(w, x, a, plan, num_sms, st);
+    case 256: return launch_tn<256>(w, x, a, plan, num_sms, st);
+    case kPairTileMarker: return launch_pair(w, x, a, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

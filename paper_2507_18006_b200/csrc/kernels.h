@@ -27,17 +27,28 @@ struct GemmArgs {
   void* out;
   float* ws;      // stream-K partials, gemm_ws_floats(num_sms) floats
   int* counters;  // per-tile arrival counters, zero-initialised, >= n_tiles ints
-  int max_parts;  // stream-K: max average CTAs per tile (0 = automatic)
-  int cluster_split;  // >1: each tile split over a cluster of this many CTAs, DSMEM reduce (0 = automatic)
+  int max_parts;      // stream-K: max clusters per tile group (0 = 1)
+  int cluster_split;  // set from the plan: >1 = tile split over a cluster, DSMEM reduce
+  int mcast;          // set from the plan: >1 = activation tile multicast across a cluster
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
                     uint32_t box_rows);
+// TN bucket of a launch: 16..256 for the 1-CTA kernel, kPairTileMarker for the
+// CTA-pair kernel (T > 256, activation map boxes of 128 rows).
+constexpr int kPairTileMarker = 512;
 int gemm_pick_tn(int T);
-cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, int tn, int num_sms,
-                        cudaStream_t st);
+struct GemmPlan {
+  int tn;        // token tile (16..256) or kPairTileMarker
+  int box_rows;  // activation tensor-map box height this plan needs
+  int mcast;     // activation multicast cluster size (1, 2, 4)
+  int csplit;    // cluster split-K size (1, 2, 4, 8)
+};
+GemmPlan gemm_plan(int N, int K, int T, int num_sms);
+cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
+                        int num_sms, cudaStream_t st);
 size_t gemm_ws_floats(int num_sms);
 constexpr int kGemmMaxTiles = 1 << 16;
 

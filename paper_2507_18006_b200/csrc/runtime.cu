@@ -66,9 +66,14 @@ struct DeviceCtx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing events
 };
 
-constexpr int kTnCount = 5;
-int tn_index(int tn) { return tn == 16 ? 0 : tn == 32 ? 1 : tn == 64 ? 2 : tn == 128 ? 3 : 4; }
-constexpr int kTns[kTnCount] = {16, 32, 64, 128, 256};
+// activation tensor maps per box height (GEMM plans need 8..256-row boxes)
+constexpr int kTnCount = 6;
+constexpr int kTns[kTnCount] = {8, 16, 32, 64, 128, 256};
+int box_index(int rows) {
+  for (int i = 0; i < kTnCount; ++i)
+    if (kTns[i] == rows) return i;
+  return kTnCount - 1;
+}
 
 }  // namespace
 
@@ -371,7 +376,7 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
          int epi, void* out, long long ldo) {
   DeviceCtx& dc = devctx(m, dev);
   Workspace& ws = m->ws[dev];
-  const int tn = cb::gemm_pick_tn(T);
+  const cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms);
   cb::GemmArgs a{};
   a.N = N;
   a.K = K;
@@ -387,7 +392,7 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
   const double bytes = double(N) * K * 2 + double(T) * K * 2 + double(T) * out_n * out_b +
                        (epi == cb::EPI_RESID ? double(T) * N * 4 : 0.0);
   ProfScope ps(m, dev, CB_KCLASS_GEMM, dc.compute, bytes, 2.0 * N * K * T);
-  CB_CUDA(cb::gemm_launch(w, xmaps[tn_index(tn)], a, tn, dc.num_sms, dc.compute));
+  CB_CUDA(cb::gemm_launch(w, xmaps[box_index(plan.box_rows)], a, plan, dc.num_sms, dc.compute));
   return CB_OK;
 }
 

@@ -42,10 +42,10 @@ int finish(cudaError_t e) {
   return cudaDeviceSynchronize() == cudaSuccess ? CB_OK : CB_ECUDA;
 }
 
-int gemm_setup(const void* w, const void* x, int64_t x_rows, int N, int K, int T, int tn, CUtensorMap* mw,
-               CUtensorMap* mx) {
+int gemm_setup(const void* w, const void* x, int64_t x_rows, int N, int K, const cb::GemmPlan& plan,
+               CUtensorMap* mw, CUtensorMap* mx) {
   if (cb::make_kmajor_map(mw, w, N, K, K, 128) != 0) return CB_ECUDA;
-  if (cb::make_kmajor_map(mx, x, x_rows, K, K, tn) != 0) return CB_ECUDA;
+  if (cb::make_kmajor_map(mx, x, x_rows, K, K, plan.box_rows) != 0) return CB_ECUDA;
   return CB_OK;
 }
 
@@ -58,9 +58,9 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   TestWs* ws;
   int r = ws_for_current(&ws);
   if (r) return r;
-  const int tn = cb::gemm_pick_tn(T);
+  const cb::GemmPlan plan = cb::gemm_plan(N, K, T, ws->sms);
   CUtensorMap mw, mx;
-  if ((r = gemm_setup(w, x, x_rows, N, K, T, tn, &mw, &mx))) return r;
+  if ((r = gemm_setup(w, x, x_rows, N, K, plan, &mw, &mx))) return r;
   cb::GemmArgs a{};
   a.N = N;
   a.K = K;
@@ -71,7 +71,7 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
-  return finish(cb::gemm_launch(mw, mx, a, tn, ws->sms, 0));
+  return finish(cb::gemm_launch(mw, mx, a, plan, ws->sms, 0));
 }
 
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
@@ -79,9 +79,17 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   TestWs* ws;
   int r = ws_for_current(&ws);
   if (r) return r;
-  const int tn = cb::gemm_pick_tn(T);
+  cb::GemmPlan plan = cb::gemm_plan(N, K, T, ws->sms);
+  if (max_parts < 0 && plan.tn != cb::kPairTileMarker) {  // experiments: force cluster split -max_parts
+    plan.csplit = -max_parts;
+    plan.mcast = 1;
+    plan.box_rows = plan.tn;
+  } else if (max_parts == 100 && plan.tn != cb::kPairTileMarker) {  // experiments: no multicast
+    plan.mcast = 1;
+    plan.box_rows = plan.tn;
+  }
   CUtensorMap mw, mx;
-  if ((r = gemm_setup(w, x, x_rows, N, K, T, tn, &mw, &mx))) return r;
+  if ((r = gemm_setup(w, x, x_rows, N, K, plan, &mw, &mx))) return r;
   cb::GemmArgs a{};
   a.N = N;
   a.K = K;
@@ -91,14 +99,13 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
-  a.max_parts = max_parts < 0 ? 1 : max_parts;
-  a.cluster_split = max_parts < 0 ? -max_parts : 0;  // negative max_parts selects a fixed cluster split
-  for (int i = 0; i < 3; ++i) cb::gemm_launch(mw, mx, a, tn, ws->sms, 0);
+  a.max_parts = (max_parts < 0 || max_parts == 100) ? 1 : max_parts;
+  for (int i = 0; i < 3; ++i) cb::gemm_launch(mw, mx, a, plan, ws->sms, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
-  for (int i = 0; i < iters; ++i) cb::gemm_launch(mw, mx, a, tn, ws->sms, 0);
+  for (int i = 0; i < iters; ++i) cb::gemm_launch(mw, mx, a, plan, ws->sms, 0);
   cudaEventRecord(e1, 0);
   if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
   float ms = 0;

@@ -16,6 +16,9 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   # full sections of the decode GEMMs (qkv, o, gate/up, down) and attention
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 258 -c 4 \
       -o $OUT/prof_gemm -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_gemm.log 2>&1
+  # prefill GEMMs of layer 1 (T = 64 x 128 = 8192 rows): the tensor-bound case
+  timeout 900 ncu --set full --clock-control none -k regex:gemm_tc_kernel -s 0 -c 4 \
+      -o $OUT/prof_prefill -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_prefill.log 2>&1
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 64 -c 1 \
       -o $OUT/prof_attn -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_attn.log 2>&1
 fi

@@ -51,7 +51,8 @@ def raw(rep):
     return out
 
 
-for rep, key in [("prof_gemm.ncu-rep", "gemm_full"), ("prof_attn.ncu-rep", "attention_full")]:
+for rep, key in [("prof_gemm.ncu-rep", "gemm_full"), ("prof_attn.ncu-rep", "attention_full"),
+                 ("prof_prefill.ncu-rep", "prefill_gemm_full")]:
     if (g / rep).exists():
         res[key] = raw(g / rep)
 out_dir.mkdir(exist_ok=True)

@@ -47,7 +47,9 @@ def test_gemm_bf16_out(lib, cuda, N, K, T):
 
 
 @pytest.mark.parametrize("N,K,T,row_off", [(4096, 4096, 64, 0), (12288, 4096, 16, 3), (4096, 11008, 64, 0),
-                                           (22016, 4096, 8, 0), (1024, 4096, 1, 5)])
+                                           (22016, 4096, 8, 0), (1024, 4096, 1, 5), (12288, 4096, 200, 0),
+                                           (32000, 4096, 128, 2), (4096, 11008, 256, 0), (22016, 4096, 1000, 0),
+                                           (4096, 4096, 2100, 7)])
 def test_gemm_f32_7b_shapes(lib, cuda, N, K, T, row_off):
     """7B projection shapes (QKV / O / down / gate+up): stream-K splits across SMs."""
     torch = cuda
@@ -92,11 +94,12 @@ def test_gemm_swiglu_epilogue(lib, cuda):
     assert err <= 1e-2 * ref.abs().max().item() + 1e-3, err
 
 
-def test_gemm_deterministic_and_row_split_invariant(lib, cuda):
+@pytest.mark.parametrize("N,K", [(4096, 4096), (12288, 4096), (22016, 4096)])
+def test_gemm_deterministic_and_row_split_invariant(lib, cuda, N, K):
     """Bit-identical reruns, and rows give the same bits whether computed as one
-    batch of 15 or as the 7 + 8 replica micro-batches split_batch produces."""
+    batch of 15 or as the 7 + 8 replica micro-batches split_batch produces
+    (cluster split-K, multicast and stream-K plans)."""
     torch = cuda
-    N, K = 4096, 4096
     w = _bf16(torch, (N, K), 0.02, 10).cuda()
     x = _bf16(torch, (15, K), 1.0, 11).cuda()
     a = torch.zeros(15, N, dtype=torch.float32, device="cuda")
