@@ -33,7 +33,8 @@ namespace cb {
 static constexpr int kBM = 128;          // weight rows per tile (UMMA M)
 static constexpr int kBK = 64;           // k-block: 64 bf16 = one 128-byte swizzle row
 static constexpr int kUmmaK = 16;        // K per tcgen05.mma (bf16)
-static constexpr int kThreads = 192;
+static constexpr int kThreads = 192;   // CTA-pair kernel: TMA, MMA, 4 epilogue warps
+static constexpr int kThreads1 = 224;  // 1-CTA kernel: + a second producer warp for the activation ring
 static constexpr int kEpiThreads = 128;
 static constexpr size_t kSmemBudget = 200 * 1024;
 
@@ -49,7 +50,7 @@ struct GemmCfg {
                                         : (2 * TN <= 128) ? 128
                                         : (2 * TN <= 256) ? 256
                                                           : 512;
-  static constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align slack*/ + 256;
+  static constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/;
 };
 
 struct StreamK {
@@ -122,7 +123,7 @@ CB_DEVICE void emit_pair(const GemmArgs& a, int n, int row, float v0, float v1) 
 }
 
 template <int TN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const GemmArgs a) {
   using Cfg = GemmCfg<TN>;
@@ -131,9 +132,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sX + S * Cfg::kXBytes);
-  uint64_t* empty_bar = full_bar + S;
-  uint64_t* tfull_bar = empty_bar + S;
+  // Two stage rings with a shared index: weights (local TMA, its own barriers,
+  // never coupled to other CTAs) and activations (possibly cluster multicast).
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sX + S * Cfg::kXBytes);  // weights landed
+  uint64_t* empty_bar = full_bar + S;                                        // weights consumed
+  uint64_t* xfull_bar = empty_bar + S;                                       // activations landed
+  uint64_t* xempty_bar = xfull_bar + S;                                      // activations consumed (whole cluster)
+  uint64_t* tfull_bar = xempty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* bcast = reinterpret_cast<int*>(tmem_slot + 1);
@@ -171,7 +176,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);
-      mbar_init(&empty_bar[i], mc);  // a stage is free once every CTA of the cluster consumed it
+      mbar_init(&empty_bar[i], 1);
+      mbar_init(&xfull_bar[i], 1);
+      mbar_init(&xempty_bar[i], mc);  // an activation slot is free once every CTA of the cluster consumed it
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -195,28 +202,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = policy_evict_last();   // activations are re-read by every tile
       // Weights do not depend on the previous kernel: fill the first stages'
       // weight tiles before waiting on it (programmatic dependent launch).
-      const int npre = min(S, uend - ubeg);
-      for (int i = 0; i < npre; ++i) {
-        const int u = ubeg + i, tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
-        mbar_arrive_expect_tx(&full_bar[i], Cfg::kStageBytes);
-        tma_load_2d(&tmW, &full_bar[i], sW + i * Cfg::kWBytes, kb * kBK, (tile / n_ttiles) * kBM, pol_w);
+      (void)pol_x;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = ubeg; u < uend; ++u) {
+        const int tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
+        if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full_bar[stage], Cfg::kWBytes);
+        tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, (tile / n_ttiles) * kBM, pol_w);
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------------- activation producer
+    // Activations belong to the previous kernel: wait for it (programmatic
+    // dependent launch) -- the weight ring above was filled without waiting.
+    if (elect_one()) {
+      const uint64_t pol_x = policy_evict_last();   // activations are re-read by every tile
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
         const int tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
-        const int mt = tile / n_ttiles, tt = tile % n_ttiles;
-        if (u - ubeg >= npre) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full_bar[stage], Cfg::kStageBytes);
-          tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt * kBM, pol_w);
-        }
+        const int tt = tile % n_ttiles;
+        mbar_wait(&xempty_bar[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&xfull_bar[stage], Cfg::kXBytes);
         if (mc > 1)
-          tma_load_2d_mc(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes + mrank * (Cfg::kXBytes / mc), kb * kBK,
+          tma_load_2d_mc(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes + mrank * (Cfg::kXBytes / mc), kb * kBK,
                          a.row_off + tt * TN + mrank * (TN / mc), mc_mask, pol_x);
         else
-          tma_load_2d(&tmX, &full_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
+          tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -235,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t d_tmem = tmem_base + uint32_t(acc * TN);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
+        mbar_wait(&xfull_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {  // the same lane issues and commits (commit tracks its own MMAs)
           const uint64_t dw = make_sw128_desc(smem_u32(sW + stage * Cfg::kWBytes));
@@ -245,10 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_bf16(d_tmem, dw + uint64_t(2 * k), dx + uint64_t(2 * k), idesc,
                       (kb > kb0 || k > 0) ? 1u : 0u);
           }
+          umma_commit(&empty_bar[stage]);
           if (mc > 1)
-            umma_commit_mc(&empty_bar[stage], mc_mask);  // the stage's X slices came from every CTA
+            umma_commit_mc(&xempty_bar[stage], mc_mask);  // the slot's X slices came from every CTA
           else
-            umma_commit(&empty_bar[stage]);
+            umma_commit(&xempty_bar[stage]);
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -362,12 +379,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tile = c / csplit;
     const int mt = tile / n_ttiles, tt = tile % n_ttiles;
     const int ncols_tile = min(TN, a.T - tt * TN);
-    if (uend == ubeg && warp >= 2) {  // empty k-slice (kb < S): contribute zeros
+    const bool epi_warp = warp >= 2 && warp < 6;
+    if (uend == ubeg && epi_warp) {  // empty k-slice (kb < S): contribute zeros
       float* part = reinterpret_cast<float*>(sW);
       for (int i = threadIdx.x - 64; i < TN * kBM; i += kEpiThreads) part[i] = 0.f;
     }
     cluster_sync_all();
-    if (warp >= 2) {
+    if (epi_warp) {
       const int et = threadIdx.x - 64;
       const uint32_t rank = cluster_ctarank();
       const int rows_per = kBM / csplit, pairs = rows_per / 2;
@@ -631,7 +649,7 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   a.mcast = plan.mcast;
   if (plan.csplit > 1) {
     a.units = int(tiles * a.kblocks);
-    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads),
+    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
                               Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, a);
   }
   const int mc = plan.mcast;
@@ -643,8 +661,8 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   const int max_parts = a.max_parts > 0 ? a.max_parts : 1;
   if (clusters > groups * max_parts) clusters = groups * max_parts;
   if (mc == 1)
-    return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(clusters)), dim3(kThreads), Cfg::kSmemBytes, st, w, x, a);
-  return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(clusters * mc)), dim3(kThreads), Cfg::kSmemBytes, st,
+    return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(clusters)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, a);
+  return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(clusters * mc)), dim3(kThreads1), Cfg::kSmemBytes, st,
                             unsigned(mc), w, x, a);
 }
 
