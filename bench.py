@@ -188,12 +188,16 @@ def build_instance(args, n_dev: int, ordinal0: int):
     from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
 
     batch = args.batch * n_dev
-    max_ctx = max(args.prompt + args.warmup + 2 * args.steps, args.prompt + args.serve_gen) + 8
+    sweep = [s * n_dev for s in args.sweep if s * n_dev != batch]
+    sweep_tokens = sum(args.sweep_steps + 2 for _ in sweep)
+    max_ctx = max(args.prompt + args.warmup + 2 * args.steps + sweep_tokens, args.prompt + args.serve_gen) + 8
+    max_slots = max([batch] + sweep)
     # two logical devices on one GPU at N=1 so the replication/migration copy
     # engine can be measured too (device 1 holds no layer during decode)
     ordinals = list(range(ordinal0, ordinal0 + n_dev)) if n_dev > 1 else [ordinal0, ordinal0]
     rt = Runtime(ordinals)
-    cfg = ExecutorConfig(**LLAMA2_7B, max_slots=batch, max_ctx=max_ctx, max_tokens=max(batch * args.prompt, 256))
+    cfg = ExecutorConfig(**LLAMA2_7B, max_slots=max_slots, max_ctx=max_ctx,
+                         max_tokens=max(min(max_slots, 64) * args.prompt, 256))
     ex = Executor(rt, cfg, home_device=0, seed=7)
     ex.init_head_random(std=0.02)
     for li in range(1, cfg.n_layers + 1):
@@ -204,7 +208,7 @@ def build_instance(args, n_dev: int, ordinal0: int):
         for li in range(1, args.replicate_layers + 1):
             for dv in range(1, n_dev):
                 ex.apply(O.ReplicateLayer(li, dv), cat, cluster)
-    return rt, ex, cat, cluster, batch
+    return rt, ex, cat, cluster, batch, sweep
 
 
 def measure_migration(ex, cat, cluster, n_dev: int) -> dict:
@@ -251,11 +255,27 @@ def run_ours(args, rank: int, world: int, dist) -> None:
         dist.barrier()  # timed region end
         return
     n_dev = world
-    rt, ex, cat, cluster, batch = build_instance(args, n_dev, 0)
+    rt, ex, cat, cluster, batch, sweep = build_instance(args, n_dev, 0)
     rng = np.random.default_rng(11)
-    slots = np.arange(batch, dtype=np.int32)
-    prompts = rng.integers(0, ex.cfg.vocab, batch * args.prompt).astype(np.int32)
-    nxt, _, prefill_ms = ex.prefill(slots, prompts, np.full(batch, args.prompt, np.int32))
+    n_slots = ex.cfg.max_slots
+    all_slots = np.arange(n_slots, dtype=np.int32)
+    prompts = rng.integers(0, ex.cfg.vocab, n_slots * args.prompt).astype(np.int32)
+    all_next, _, prefill_ms = ex.prefill(all_slots, prompts, np.full(n_slots, args.prompt, np.int32))
+    # decode throughput at other batch sizes on the same instance (slot subsets)
+    sweep_res = {}
+    for sb in sorted(sweep):
+        s_slots = all_slots[:sb]
+        s_next = all_next[:sb]
+        for _ in range(2):
+            s_next, _, _ = ex.decode(s_slots, s_next)
+        ms = []
+        for _ in range(args.sweep_steps):
+            s_next, _, m = ex.decode(s_slots, s_next)
+            ms.append(m)
+        all_next[:sb] = s_next
+        sweep_res[str(sb)] = {"tokens_per_s": sb * len(ms) / (sum(ms) / 1e3), "ms_per_step": float(np.mean(ms))}
+    slots = all_slots[:batch]
+    nxt = all_next[:batch]
     for _ in range(args.warmup):
         nxt, _, _ = ex.decode(slots, nxt)
     if world > 1:
@@ -322,6 +342,7 @@ def run_ours(args, rank: int, world: int, dist) -> None:
                      "step_share": step_share,
                      "attention": {"achieved": attn_gbs, "frac": attn_gbs / peaks["hbm_gbs"],
                                    "bytes_per_launch": a["bytes"] / max(1, a["launches"])}},
+        "batch_sweep": sweep_res,
         "migrate": mig,
         "serving": serving,
         "clocks": clocks.summary(),
@@ -342,7 +363,10 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64, help="sequences per GPU")
+    ap.add_argument("--batch", type=int, default=64, help="sequences per GPU (headline)")
+    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",") if x], default=[64, 128, 256],
+                    help="other batch sizes timed on the same instance")
+    ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--prompt", type=int, default=128)
     ap.add_argument("--replicate-layers", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -626,6 +626,35 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms) {
   return p;
 }
 
+// How many clusters of `cs` CTAs of this kernel can be resident at once (GPCs
+// are not multiples of 4 SMs: clusters of 4 fit on 132 of the 148 SMs).
+template <typename K>
+static int max_active_clusters(K kernel, int cs, size_t smem, int threads) {
+  static int cache[64][9] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slot = cache[dev & 63][cs & 7];
+  if (slot) return slot;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(cs));
+  cfg.blockDim = dim3(unsigned(threads));
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(cs);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 148 / cs;
+  }
+  slot = n;
+  return n;
+}
+
 template <int TN>
 static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, const GemmPlan& plan,
                              int num_sms, cudaStream_t st) {
@@ -657,6 +686,10 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   a.units = int(groups * a.kblocks);
   // persistent stream-K over clusters; a group is spread over <= max_parts clusters
   long long clusters = num_sms / mc;
+  if (mc > 1) {
+    const int resident = max_active_clusters(gemm_tc_kernel<TN>, mc, Cfg::kSmemBytes, kThreads1);
+    if (clusters > resident) clusters = resident;  // one wave: no cluster waits for another to finish
+  }
   if (clusters > a.units) clusters = a.units;
   const int max_parts = a.max_parts > 0 ? a.max_parts : 1;
   if (clusters > groups * max_parts) clusters = groups * max_parts;
