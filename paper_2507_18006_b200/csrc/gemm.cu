@@ -616,12 +616,9 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms) {
   if (tiles * 10 < (long long)num_sms * 6) {
     // few wide-K tiles (O / down projections): cluster split-K
     while (p.csplit < 8 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
-  } else {
-    // many tiles: stream the weights, multicast the activation tile across a
-    // cluster of neighbouring weight tiles (slices of >= 8 rows)
-    p.mcast = p.tn >= 32 ? 4 : 2;
-    while (p.mcast > 1 && tiles < p.mcast * 8) p.mcast /= 2;
   }
+  // (activation multicast across clusters -- a.mcast > 1 -- is implemented and
+  // correct but measured no faster than plain loads on B200, so plans keep 1)
   p.box_rows = p.tn / p.mcast;
   return p;
 }
