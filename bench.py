@@ -144,7 +144,7 @@ class CpuDecodeSample:
                 f"layer time scaled x{self.cfg.n_layers // self.sample_layers}; BLAS threads = all host cores")
 
 
-def cpu_decode_sample(batch: int, ctx: int, repeats: int = 3) -> dict:
+def cpu_decode_sample(batch: int, ctx: int, repeats: int = 2) -> dict:
     s = CpuDecodeSample(batch, ctx)
     s.step()  # warm
     step_s = min(s.step() for _ in range(repeats))
@@ -162,7 +162,7 @@ def run_reference(args, rank: int, world: int) -> None:
     s = CpuDecodeSample(args.batch, args.prompt)
     for _ in range(max(1, min(args.warmup, 2))):
         s.step()
-    steps = min(args.steps, 10)  # bounded: each sampled step is ~0.3-1 s of CPU work
+    steps = max(1, min(args.steps, 3 if args.batch > 64 else 10))  # bounded: each sampled step is 1-10 s of CPU work
     steps_s = [s.step() for _ in range(steps)]
     value = args.batch * len(steps_s) / sum(steps_s)
     line = {
@@ -363,8 +363,8 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=64, help="sequences per GPU (headline)")
-    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",") if x], default=[64, 128, 256],
+    ap.add_argument("--batch", type=int, default=256, help="sequences per GPU (headline; BASELINE config 2 lists 1..256)")
+    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",") if x], default=[64, 128],
                     help="other batch sizes timed on the same instance")
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--prompt", type=int, default=128)
