@@ -34,6 +34,16 @@ int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
 /* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
                    void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch);
+/* cbt_gemm_bench rotates over n weight copies stride_bytes apart (weights larger than L2, as in a step) */
+int cbt_gemm_set_wcopies(int32_t n, int64_t stride_bytes);
+/* tcgen05.mma issue-rate probe: cycles per 128 x N x 16 bf16 MMA (smem operands), grid CTAs */
+int cbt_mma_probe(int32_t N, int32_t n, int32_t grid, int32_t kstep, double* cyc_per_mma);
+/* per-CTA timeline (globaltimer ns, 64 slots per CTA) of the last traced cbt_gemm_bench launch */
+int cbt_gemm_trace(unsigned long long* out, int32_t n);
+/* TMA read-bandwidth probe: `grid` CTAs, `nw` issuing warps each, stream `iters` boxes of
+ * box_rows x (kd x 64) bf16 (kd > 1: 3-D boxes) through a `stages`-deep ring per warp; device ms */
+int cbt_tma_probe(const void* buf, int64_t rows, int32_t box_rows, int32_t stages, int32_t grid, int32_t iters,
+                  int32_t kd, int32_t nw, int32_t mma_n, float* ms_out);
 
 #ifdef __cplusplus
 }

@@ -4,24 +4,31 @@
 //
 // W is a PyTorch-layout weight [N, K] (K contiguous), X the activation rows
 // [rows, K].  Both are K-major, the native tcgen05 operand layout.  The MMA's
-// M dimension is the weight rows (128 per tile) and its N dimension the tokens
-// (TN = 16..256 per tile): "swap-AB", so a decode step with a handful of rows
-// still drives the tensor pipe while the kernel streams the weight at HBM rate
-// (decode GEMMs are HBM-bound, prefill GEMMs tensor-bound).
+// M dimension is the weight rows (128 per CTA) and its N dimension the tokens
+// ("swap-AB"), so a decode step with a handful of rows still drives the tensor
+// pipe while the kernel streams the weight at HBM rate (decode
+// GEMMs are HBM-bound, prefill GEMMs tensor-bound).
 //
-// Work split: persistent stream-K.  The (tile, k-block) unit space is cut into
-// `grid` contiguous ranges, one per CTA (grid <= #SMs, one CTA per SM), so all
-// SMs pull weight bytes for the whole launch regardless of N.  A tile split
-// across CTAs is finished by the last CTA to arrive: every part writes an fp32
-// partial to a (L2-resident) workspace and the finisher sums the parts in a
-// fixed order -> deterministic, and for T <= 256 the split points do not depend
-// on T, so a row's result is identical whether it runs unreplicated or inside
-// a replica's micro-batch (reference batch split: ops.py:151-158).
+// Two kernels share the warp roles and the epilogue:
+//  * gemm_tc_kernel<TN>  -- 1 CTA per 128 weight rows x TN tokens (T <= 128);
+//  * gemm_tc2_kernel<TNP> -- CTA pair (tcgen05 cta_group::2): 256 weight rows x
+//    TNP tokens per pair, each CTA stages 128 weight rows and TNP/2 token rows,
+//    so the activation bytes read from L2 per weight byte halve (T > 128).
+// Work split: persistent stream-K over (tile, k-block) units -- one contiguous
+// range per CTA (pair), so every SM streams weight bytes for the whole launch --
+// or, for few wide-K tiles, cluster split-K with a DSMEM reduction.  A tile
+// split across CTAs is finished by the last CTA to arrive, summing the parts in
+// fixed CTA order: deterministic, and for T <= one token tile the split points
+// do not depend on T, so a row's result is identical whether it runs
+// unreplicated or inside a replica's micro-batch (ops.py:151-158).
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
-// issuer (one elected lane), warps 2..5 = epilogue (TMEM -> registers -> global,
-// with the fused epilogue ops below).  TMEM accumulators are double buffered so
-// the epilogue of one tile overlaps the main loop of the next.
+// Warp roles (224 threads): warp 0 = TMA producer of the weight ring (filled
+// before griddepcontrol.wait: weights do not depend on the previous kernel),
+// warp 1 = TMEM owner + MMA issuer (converged warp, elect.sync picks the issuing
+// lane), warps 2..5 = epilogue (TMEM -> registers -> smem transpose -> 16-byte
+// global stores), warp 6 = TMA producer of the activation ring.  TMEM
+// accumulators are double buffered so a tile's epilogue overlaps the next
+// tile's main loop.
 //
 // Stand-in replaced: reference `_kernels._work_units` (`_kernels.py:17-38`) and
 // the per-module GEMM FLOPs of `ModuleCatalog.from_model` (`domain.py:241-264`).
@@ -30,27 +37,37 @@
 
 namespace cb {
 
-static constexpr int kBM = 128;          // weight rows per tile (UMMA M)
+static constexpr int kBM = 128;          // weight rows per CTA tile (UMMA M per CTA)
 static constexpr int kBK = 64;           // k-block: 64 bf16 = one 128-byte swizzle row
-static constexpr int kUmmaK = 16;        // K per tcgen05.mma (bf16)
-static constexpr int kThreads = 192;   // CTA-pair kernel: TMA, MMA, 4 epilogue warps
-static constexpr int kThreads1 = 224;  // 1-CTA kernel: + a second producer warp for the activation ring
+static constexpr int kThreads1 = 224;    // TMA weights, MMA, 4 epilogue warps, TMA activations
 static constexpr int kEpiThreads = 128;
-static constexpr size_t kSmemBudget = 200 * 1024;
+static constexpr size_t kSmemBudget = 224 * 1024;  // of the 227 KB opt-in maximum
+static constexpr int kTbRow = 36;  // transpose buffer row stride (floats): 32 + 4 pad -> conflict-free 16-byte reads
+static constexpr int kTbufBytes = 4 * 16 * kTbRow * 4;  // epilogue transpose buffers: 4 warps x 16 x 36 fp32
+static constexpr int kMaxStages = 16;
 
+template <int WB, int XB>
+struct RingCfg {
+  static constexpr int kWBytes = WB;
+  static constexpr int kXBytes = XB;
+  static constexpr int kStageBytes = WB + XB;
+  static constexpr int kStagesRaw = int((kSmemBudget - 2048 - kTbufBytes) / kStageBytes);
+  static constexpr int kStages = kStagesRaw > kMaxStages ? kMaxStages : kStagesRaw;
+  static constexpr int kRingBytes = kStages * kStageBytes;
+  // ring | transpose buffers | barriers
+  static constexpr size_t kSmemBytes = size_t(kRingBytes) + kTbufBytes + 1024 /*align slack*/ + 1024 /*barriers*/;
+};
 template <int TN>
-struct GemmCfg {
-  static constexpr int kWBytes = kBM * kBK * 2;
-  static constexpr int kXBytes = TN * kBK * 2;
-  static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kStagesRaw = int((kSmemBudget - 2048) / kStageBytes);
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+struct GemmCfg : RingCfg<kBM * kBK * 2, TN * kBK * 2> {
   static constexpr uint32_t kTmemCols = (2 * TN <= 32)    ? 32
                                         : (2 * TN <= 64)  ? 64
                                         : (2 * TN <= 128) ? 128
                                         : (2 * TN <= 256) ? 256
                                                           : 512;
-  static constexpr size_t kSmemBytes = size_t(kStages) * kStageBytes + 1024 /*align slack*/ + 512 /*barriers*/;
+};
+template <int TNP>
+struct PairCfg : RingCfg<kBM * kBK * 2, (TNP / 2) * kBK * 2> {
+  static constexpr uint32_t kTmemCols = 2 * TNP <= 256 ? 256 : 512;
 };
 
 struct StreamK {
@@ -59,7 +76,15 @@ struct StreamK {
   CB_DEVICE int cta_of(int u) const { return int(((long long)(u + 1) * grid - 1) / units); }
 };
 
-// Apply the fused epilogue to 16 consecutive token columns of one weight row.
+// ------------------------------------------------------------------ epilogue
+// SwiGLU: silu(gate) * up.  Fast divide: an IEEE divide by the huge 1 + exp(-g)
+// of a very negative gate takes the slow path (measured 3x slower epilogue);
+// __fdividef returns the correct limit 0 there.  Every epilogue path uses this
+// one function, so a row's bits do not depend on which path finished its tile.
+CB_DEVICE float silu_mul(float g, float u) { return __fdividef(g, 1.0f + __expf(-g)) * u; }
+
+// Scalar fallback (shapes whose outputs are not 16-byte aligned): 16 token
+// columns of weight row n.
 CB_DEVICE void emit16(const GemmArgs& a, int n, int row0, int ncols, const float (&v)[16]) {
   const int lane = threadIdx.x & 31;
   if (a.epi == EPI_SWIGLU) {
@@ -68,9 +93,7 @@ CB_DEVICE void emit16(const GemmArgs& a, int n, int row0, int ncols, const float
     for (int i = 0; i < 16; ++i) {
       float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
       if (!(lane & 1) && n < a.N && i < ncols) {
-        float g = v[i];
-        float s = g / (1.0f + __expf(-g));
-        reinterpret_cast<uint16_t*>(a.out)[(size_t)(row0 + i) * a.ldo + (n >> 1)] = f_to_bf16(s * other);
+        reinterpret_cast<uint16_t*>(a.out)[(size_t)(row0 + i) * a.ldo + (n >> 1)] = f_to_bf16(silu_mul(v[i], other));
       }
     }
     return;
@@ -97,13 +120,12 @@ CB_DEVICE void emit16(const GemmArgs& a, int n, int row0, int ncols, const float
   }
 }
 
-// Epilogue of a (row pair, token column) of a finished tile: rows n, n+1 of
-// the weight (an interleaved gate/up pair for SwiGLU).
+// Scalar: weight rows n, n+1 (an interleaved gate/up pair for SwiGLU) of token `row`.
 CB_DEVICE void emit_pair(const GemmArgs& a, int n, int row, float v0, float v1) {
   if (n >= a.N) return;
   const size_t base = (size_t)row * a.ldo;
   if (a.epi == EPI_SWIGLU) {
-    reinterpret_cast<uint16_t*>(a.out)[base + (n >> 1)] = f_to_bf16(v0 / (1.0f + __expf(-v0)) * v1);
+    reinterpret_cast<uint16_t*>(a.out)[base + (n >> 1)] = f_to_bf16(silu_mul(v0, v1));
   } else if (a.epi == EPI_BF16) {
     uint16_t* o = reinterpret_cast<uint16_t*>(a.out) + base + n;
     if (n + 1 < a.N) {
@@ -122,6 +144,272 @@ CB_DEVICE void emit_pair(const GemmArgs& a, int n, int row, float v0, float v1) 
   }
 }
 
+
+// Vector: weight rows n0..n0+7 (n0 % 8 == 0) of token `row`, one 16-byte store
+// (8-byte for SwiGLU, 2 x 16 bytes for fp32 outputs).  For EPI_RESID the
+// caller passes the residual already loaded (res): loads of a batch are issued
+// before its stores, since a store may alias a later load in the compiler's view.
+CB_DEVICE float* out_f32(const GemmArgs& a, int n0, int row) {
+  return reinterpret_cast<float*>(a.out) + (size_t)row * a.ldo + n0;
+}
+CB_DEVICE void emit8(const GemmArgs& a, int n0, int row, const float (&s)[8], const float4* res = nullptr) {
+  if (n0 >= a.N) return;
+  const size_t base = (size_t)row * a.ldo;
+  if (a.epi == EPI_BF16) {
+    uint4 o;
+    o.x = pack_bf16x2(s[0], s[1]);
+    o.y = pack_bf16x2(s[2], s[3]);
+    o.z = pack_bf16x2(s[4], s[5]);
+    o.w = pack_bf16x2(s[6], s[7]);
+    *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.out) + base + n0) = o;
+  } else if (a.epi == EPI_SWIGLU) {
+    uint2 o;
+    o.x = pack_bf16x2(silu_mul(s[0], s[1]), silu_mul(s[2], s[3]));
+    o.y = pack_bf16x2(silu_mul(s[4], s[5]), silu_mul(s[6], s[7]));
+    *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.out) + base + (n0 >> 1)) = o;
+  } else {
+    float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + base + n0);
+    float4 x0 = make_float4(s[0], s[1], s[2], s[3]), x1 = make_float4(s[4], s[5], s[6], s[7]);
+    if (a.epi == EPI_RESID) {
+      const float4 y0 = res[0], y1 = res[1];
+      x0 = make_float4(y0.x + x0.x, y0.y + x0.y, y0.z + x0.z, y0.w + x0.w);
+      x1 = make_float4(y1.x + x1.x, y1.y + x1.y, y1.z + x1.z, y1.w + x1.w);
+    }
+    o[0] = x0;
+    o[1] = x1;
+  }
+}
+
+CB_DEVICE void load8(const float* src, float (&s)[8]) {
+  const float4 x0 = *reinterpret_cast<const float4*>(src);
+  const float4 x1 = *reinterpret_cast<const float4*>(src + 4);
+  s[0] = x0.x; s[1] = x0.y; s[2] = x0.z; s[3] = x0.w;
+  s[4] = x1.x; s[5] = x1.y; s[6] = x1.z; s[7] = x1.w;
+}
+
+// One warp's 32 weight rows (lane = row) x 16 token columns, transposed through
+// the warp's smem buffer so every lane stores whole 16-byte runs of one token
+// row: 2 store instructions per chunk instead of 16 scalar ones.
+CB_DEVICE void emit_warp_vec(const GemmArgs& a, float* tb, int nw0, int row, int nc, const float (&v)[16],
+                             int lane) {
+  // fp32 outputs: lane -> (token p*4 + lane/8, 4 rows at (lane%8)*4); residual loads issued first
+  float4 res[4];
+  if (a.epi == EPI_RESID) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
+      res[p] = (i < nc && nw0 + f0 < a.N) ? __ldcg(reinterpret_cast<const float4*>(out_f32(a, nw0 + f0, row + i)))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tb[i * kTbRow + lane] = v[i];
+  __syncwarp();
+  if (a.epi == EPI_SWIGLU) {
+    const int i = lane >> 1, f0 = (lane & 1) * 16;
+    if (i < nc) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float s[8];
+        load8(tb + i * kTbRow + f0 + 8 * h, s);
+        emit8(a, nw0 + f0 + 8 * h, row + i, s);
+      }
+    }
+  } else if (a.epi == EPI_BF16) {
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int i = p * 8 + (lane >> 2), f0 = (lane & 3) * 8;
+      if (i < nc) {
+        float s[8];
+        load8(tb + i * kTbRow + f0, s);
+        emit8(a, nw0 + f0, row + i, s);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
+      if (i < nc && nw0 + f0 < a.N) {
+        float4 x = *reinterpret_cast<const float4*>(tb + i * kTbRow + f0);
+        if (a.epi == EPI_RESID) x = make_float4(res[p].x + x.x, res[p].y + x.y, res[p].z + x.z, res[p].w + x.w);
+        *reinterpret_cast<float4*>(out_f32(a, nw0 + f0, row + i)) = x;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Stream-K / split-K partial of one warp chunk into the [col][128 rows] fp32
+// layout (part already offset to this chunk's first column and warp's rows).
+CB_DEVICE void write_part_vec(float* part, float* tb, const float (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tb[i * kTbRow + lane] = v[i];
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
+    *reinterpret_cast<float4*>(part + (size_t)i * kBM + f0) = *reinterpret_cast<const float4*>(tb + i * kTbRow + f0);
+  }
+  __syncwarp();
+}
+
+// TMEM accumulator (this warp's 32 lanes) -> output (whole tile) or partial.
+CB_DEVICE void epi_drain(const GemmArgs& a, uint32_t t_addr, int m0, int row0, int ncols, bool whole, float* part,
+                         float* tb, int q, int lane) {
+  const int nw0 = m0 + q * 32;
+  for (int c0 = 0; c0 < ncols; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(t_addr + uint32_t(c0), r);
+    tmem_ld_wait();
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    const int nc = min(16, ncols - c0);
+    if (!whole)
+      write_part_vec(part + (size_t)c0 * kBM + q * 32, tb, v, lane);
+    else if (a.vec)
+      emit_warp_vec(a, tb, nw0, row0 + c0, nc, v, lane);
+    else
+      emit16(a, nw0 + lane, row0 + c0, nc, v);
+  }
+}
+
+// Where the parts of a split tile live: CTA (or pair) cc's slot for `tile`.
+struct PartMap {
+  const float* ws;
+  StreamK sk;
+  int tile, cstride, coff, tn;
+  CB_DEVICE const float* of(int cc) const {
+    const int w = (sk.u0(cc) / sk.kb == tile) ? 0 : 1;  // slot 0 = the CTA's first segment
+    return ws + ((size_t)(cc * cstride + coff) * 2 + w) * (size_t)(kBM * tn);
+  }
+};
+
+// Stream-K fixup of one (tile, 128-row half): every part is in the workspace;
+// the last CTA to arrive sums the parts in CTA order (deterministic).  When that
+// CTA has finished its whole range (ring_idle) the parts are bulk-copied into
+// its idle stage ring and summed from shared memory -- one round trip per
+// ring-full -- otherwise they are read from L2 directly.
+CB_DEVICE void epi_fixup(const GemmArgs& a, int* counter, const PartMap& pm, int c_first, int c_last, int m0,
+                         int row0, int ncols, bool ring_idle, uint8_t* ring, uint32_t ring_bytes, uint64_t* fix_bar,
+                         uint32_t& fix_phase, int* bcast, int et, unsigned long long* tr = nullptr) {
+  const int nparts = c_last - c_first + 1;
+  __threadfence();
+  named_bar_sync(1, kEpiThreads);
+  if (et == 0) {
+    const int prev = atomicAdd(counter, 1);
+    *bcast = (prev == nparts - 1) ? 1 : 0;
+  }
+  named_bar_sync(1, kEpiThreads);
+  const bool finisher = *bcast != 0;
+  if (tr) tr[2] = globaltimer_ns() | (finisher ? (1ull << 63) : 0) | (ring_idle ? (1ull << 62) : 0);
+  if (finisher) {
+    __threadfence();
+    const int cols_cap = int(ring_bytes / uint32_t(nparts * kBM * 4)) & ~7;
+    if (ring_idle && a.vec && cols_cap >= 8) {
+      for (int cs = 0; cs < ncols; cs += cols_cap) {
+        const int nc = min(cols_cap, ncols - cs);
+        const uint32_t bytes = uint32_t(nc) * kBM * 4;
+        if (et == 0) {
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(fix_bar, bytes * uint32_t(nparts));
+          for (int p = 0; p < nparts; ++p)
+            bulk_g2s(ring + p * bytes, pm.of(c_first + p) + (size_t)cs * kBM, bytes, fix_bar);
+        }
+        mbar_wait(fix_bar, fix_phase);
+        fix_phase ^= 1;
+        // item = (token column, 8 consecutive weight rows); 4 items per thread per
+        // batch, residual loads of the batch issued before its stores
+        for (int it0 = et; it0 < nc * 16; it0 += 4 * kEpiThreads) {
+          float4 res[4][2];
+          if (a.epi == EPI_RESID) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int it = it0 + j * kEpiThreads;
+              const int col = it >> 4, g = it & 15;
+              if (it < nc * 16 && m0 + g * 8 < a.N) {
+                const float4* y = reinterpret_cast<const float4*>(out_f32(a, m0 + g * 8, row0 + cs + col));
+                res[j][0] = __ldcg(y);
+                res[j][1] = __ldcg(y + 1);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int it = it0 + j * kEpiThreads;
+            if (it >= nc * 16) break;
+            const int col = it >> 4, g = it & 15;
+            float s[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s[e] = 0.f;
+            for (int p = 0; p < nparts; ++p) {
+              float x[8];
+              load8(reinterpret_cast<const float*>(ring + p * bytes) + col * kBM + g * 8, x);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) s[e] += x[e];
+            }
+            emit8(a, m0 + g * 8, row0 + cs + col, s, res[j]);
+          }
+        }
+        named_bar_sync(1, kEpiThreads);  // every read of this round is done before the next copy lands
+        if (et == 0) fence_proxy_async_smem();
+      }
+    } else {
+      // work item = (row pair, token column); 8 items per thread in flight per round trip.
+      const int n_items = 64 * ncols;
+      for (int base = et; base < n_items; base += 8 * kEpiThreads) {
+        float2 sum[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sum[j] = make_float2(0.f, 0.f);
+        for (int cc = c_first; cc <= c_last; ++cc) {
+          const float* p = pm.of(cc);
+          float2 ld[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ld[j] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int it = base + j * kEpiThreads;
+            if (it < n_items) ld[j] = __ldcg(reinterpret_cast<const float2*>(p + (size_t)(it >> 6) * kBM + 2 * (it & 63)));
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            sum[j].x += ld[j].x;
+            sum[j].y += ld[j].y;
+          }
+        }
+        if (a.epi == EPI_RESID && a.vec) {  // residual loads of the round first, then the stores
+          float2 y[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int it = base + j * kEpiThreads, n = m0 + 2 * (it & 63);
+            y[j] = (it < n_items && n + 1 < a.N) ? __ldcg(reinterpret_cast<const float2*>(out_f32(a, n, row0 + (it >> 6))))
+                                                 : make_float2(0.f, 0.f);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int it = base + j * kEpiThreads, n = m0 + 2 * (it & 63);
+            if (it < n_items && n + 1 < a.N)
+              *reinterpret_cast<float2*>(out_f32(a, n, row0 + (it >> 6))) =
+                  make_float2(y[j].x + sum[j].x, y[j].y + sum[j].y);
+            else if (it < n_items)
+              emit_pair(a, n, row0 + (it >> 6), sum[j].x, sum[j].y);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int it = base + j * kEpiThreads;
+            if (it < n_items) emit_pair(a, m0 + 2 * (it & 63), row0 + (it >> 6), sum[j].x, sum[j].y);
+          }
+        }
+      }
+    }
+    if (et == 0) *counter = 0;
+  }
+  named_bar_sync(1, kEpiThreads);
+  if (tr) tr[3] = globaltimer_ns();
+}
+
+// ------------------------------------------------------------------ 1-CTA kernel
 template <int TN>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
@@ -132,31 +420,26 @@ __global__ void __launch_bounds__(kThreads1, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
-  // Two stage rings with a shared index: weights (local TMA, its own barriers,
-  // never coupled to other CTAs) and activations (possibly cluster multicast).
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sX + S * Cfg::kXBytes);  // weights landed
-  uint64_t* empty_bar = full_bar + S;                                        // weights consumed
-  uint64_t* xfull_bar = empty_bar + S;                                       // activations landed
-  uint64_t* xempty_bar = xfull_bar + S;                                      // activations consumed (whole cluster)
+  float* tbuf_all = reinterpret_cast<float*>(smem + Cfg::kRingBytes);
+  // Two stage rings with a shared index: weights and activations, each with
+  // its own full/empty barriers, so the weight ring fills before the
+  // activations of the previous kernel exist.
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + kTbufBytes);  // weights landed
+  uint64_t* empty_bar = full_bar + S;                                                     // weights consumed
+  uint64_t* xfull_bar = empty_bar + S;                                                    // activations landed
+  uint64_t* xempty_bar = xfull_bar + S;                                                   // activations consumed
   uint64_t* tfull_bar = xempty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* fix_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
   int* bcast = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int n_ttiles = a.n_ttiles;
   const int c = blockIdx.x;
-  // Multicast clusters (mc > 1): the mc CTAs of a cluster own mc neighbouring
-  // weight tiles ("a group") and walk the group's k-blocks in lockstep; CTA r
-  // loads 1/mc of each activation tile and multicasts it to the whole cluster,
-  // so an activation k-block is read from L2 once per cluster.  Stream-K units
-  // are (group, k-block) and are dealt out per cluster.
-  const int mc = a.mcast > 1 ? a.mcast : 1;
-  const int mrank = c % mc;
-  const StreamK sk{a.units, int(gridDim.x) / mc, a.kblocks};
-  const int cl = c / mc;
-  // Work range: stream-K slice of the (group, k-block) space, or -- in cluster
+  const StreamK sk{a.units, int(gridDim.x), a.kblocks};
+  // Work range: stream-K slice of the (tile, k-block) space, or -- in cluster
   // split mode -- k-slice r of tile c / S (the cluster = the tile's S CTAs).
   const int csplit = a.cluster_split > 1 ? a.cluster_split : 1;
   int ubeg, uend;
@@ -165,12 +448,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
     ubeg = tile * sk.kb + (r * sk.kb) / csplit;
     uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
   } else {
-    ubeg = sk.u0(cl);
-    uend = sk.u0(cl + 1);
+    ubeg = sk.u0(c);
+    uend = sk.u0(c + 1);
   }
-  const uint16_t mc_mask = uint16_t((1u << mc) - 1);
 
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
+  if (a.trace && threadIdx.x == 0) a.trace[(size_t)c * 512] = globaltimer_ns();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
@@ -178,38 +461,36 @@ __global__ void __launch_bounds__(kThreads1, 1)
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
       mbar_init(&xfull_bar[i], 1);
-      mbar_init(&xempty_bar[i], mc);  // an activation slot is free once every CTA of the cluster consumed it
+      mbar_init(&xempty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], kEpiThreads);
     }
+    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
-  if (mc > 1)
-    cluster_sync_all();  // peers' barriers exist before any multicast lands
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------------------------------------------------- TMA producer
+    // ---------------------------------------------------------- weight producer
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights stream through once
-      const uint64_t pol_x = policy_evict_last();   // activations are re-read by every tile
-      // Weights do not depend on the previous kernel: fill the first stages'
-      // weight tiles before waiting on it (programmatic dependent launch).
-      (void)pol_x;
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
-        const int tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
+        const int tile = u / sk.kb, kb = u % sk.kb;
+        const int mt = tile / n_ttiles;
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full_bar[stage], Cfg::kWBytes);
-        tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, (tile / n_ttiles) * kBM, pol_w);
+        if (a.w_tiled)
+          tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, 0, (mt * sk.kb + kb) * kBM, pol_w);
+        else
+          tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt * kBM, pol_w);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -218,26 +499,27 @@ __global__ void __launch_bounds__(kThreads1, 1)
     // Activations belong to the previous kernel: wait for it (programmatic
     // dependent launch) -- the weight ring above was filled without waiting.
     if (elect_one()) {
-      const uint64_t pol_x = policy_evict_last();   // activations are re-read by every tile
+      const uint64_t pol_x = policy_evict_last();  // activations are re-read by every tile
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
-        const int tile = (u / sk.kb) * mc + mrank, kb = u % sk.kb;
+        const int tile = u / sk.kb, kb = u % sk.kb;
         const int tt = tile % n_ttiles;
         mbar_wait(&xempty_bar[stage], phase ^ 1);
         mbar_arrive_expect_tx(&xfull_bar[stage], Cfg::kXBytes);
-        if (mc > 1)
-          tma_load_2d_mc(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes + mrank * (Cfg::kXBytes / mc), kb * kBK,
-                         a.row_off + tt * TN + mrank * (TN / mc), mc_mask, pol_x);
-        else
-          tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
+        tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
+    // The whole warp runs this loop converged; elect.sync inside the issue
+    // helper picks the lane that issues (and commits: a commit tracks the MMAs
+    // of its own thread, and elect.sync of a converged warp is always lane 0).
     constexpr uint32_t idesc = make_idesc_bf16(kBM, TN);
+    const uint64_t dw0 = make_sw128_desc(smem_u32(sW));
+    const uint64_t dx0 = make_sw128_desc(smem_u32(sX));
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -252,26 +534,29 @@ __global__ void __launch_bounds__(kThreads1, 1)
         mbar_wait(&full_bar[stage], phase);
         mbar_wait(&xfull_bar[stage], phase);
         tc_fence_after();
-        if (lane == 0) {  // the same lane issues and commits (commit tracks its own MMAs)
-          const uint64_t dw = make_sw128_desc(smem_u32(sW + stage * Cfg::kWBytes));
-          const uint64_t dx = make_sw128_desc(smem_u32(sX + stage * Cfg::kXBytes));
-#pragma unroll
-          for (int k = 0; k < kBK / kUmmaK; ++k) {
-            // +32 bytes per K=16 step inside the 128-byte swizzle row (>>4 encoded)
-            umma_bf16(d_tmem, dw + uint64_t(2 * k), dx + uint64_t(2 * k), idesc,
-                      (kb > kb0 || k > 0) ? 1u : 0u);
-          }
-          umma_commit(&empty_bar[stage]);
-          if (mc > 1)
-            umma_commit_mc(&xempty_bar[stage], mc_mask);  // the slot's X slices came from every CTA
-          else
-            umma_commit(&xempty_bar[stage]);
-        }
+        const int i = u + (kb - kb0) - ubeg;
+        if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 2 + i] = globaltimer_ns();
         __syncwarp();
+        if (a.dbg & 1) {  // experiments: no MMAs, release the stage at once
+          if (lane == 0) {
+            mbar_arrive(&empty_bar[stage]);
+            mbar_arrive(&xempty_bar[stage]);
+          }
+        } else {
+          // descriptor start address += stage offset (>> 4 encoded, stays inside its 14-bit field)
+          const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
+          const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
+          umma_kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage]);
+        }
+        if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
-      if (lane == 0) umma_commit(&tfull_bar[acc]);
       __syncwarp();
+      if (a.dbg & 1) {
+        if (lane == 0) mbar_arrive(&tfull_bar[acc]);
+      } else {
+        umma_commit_elect(&tfull_bar[acc]);
+      }
       u += kb1 - kb0;
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
@@ -280,97 +565,43 @@ __global__ void __launch_bounds__(kThreads1, 1)
     // ---------------------------------------------------------- epilogue
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row_in_tile = q * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127
+    float* tb = tbuf_all + q * (16 * kTbRow);
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t fix_phase = 0;
+    int seg_i = 0;
     for (int u = ubeg; u < uend;) {
-      const int grp = u / sk.kb, kb0 = u % sk.kb;
-      const int tile = grp * mc + mrank;
+      const int tile = u / sk.kb, kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
       const int mt = tile / n_ttiles, tt = tile % n_ttiles;
-      const int n = mt * kBM + row_in_tile;
       const int row0 = a.row_off + tt * TN;
-      const int ncols_tile = min(TN, a.T - tt * TN);
+      const int ncols = min(TN, a.T - tt * TN);
       const bool whole = (kb0 == 0 && kb1 == sk.kb);
+      const bool last_seg = (u + (kb1 - kb0) == uend);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      unsigned long long* tr = (a.trace && et == 0 && seg_i < 4) ? a.trace + (size_t)c * 512 + 130 + 4 * seg_i : nullptr;
+      ++seg_i;
+      if (tr) tr[0] = globaltimer_ns() | (whole ? (1ull << 62) : 0);
       const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TN);
-      // which workspace slot: 0 if this is the CTA's first segment, else 1
-      const int which = (u == ubeg) ? 0 : 1;
-      // partials are column-major [col][128 rows]: coalesced stores here and
-      // coalesced row-pair loads in the fixup
+      // partials are column-major [col][128 rows]: slot 0 = the CTA's first segment
       float* part = csplit > 1 ? reinterpret_cast<float*>(sW)  // cluster mode: partial stays in smem
-                               : a.ws + ((size_t)c * 2 + which) * (size_t)(kBM * TN);
-      for (int c0 = 0; c0 < ncols_tile; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_addr + uint32_t(c0), r);
-        tmem_ld_wait();
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-        if (whole) {
-          emit16(a, n, row0 + c0, min(16, ncols_tile - c0), v);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) part[(size_t)(c0 + i) * kBM + row_in_tile] = v[i];
-        }
-      }
+                               : a.ws + ((size_t)c * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TN);
+      if (!(a.dbg & 2)) epi_drain(a, t_addr, mt * kBM, row0, ncols, whole, part, tb, q, lane);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-
+      if (tr) tr[1] = globaltimer_ns();
       if (!whole && csplit == 1) {
-        // stream-K fixup: the last CTA to deposit its part finishes the tile.
-        const int c_first = sk.cta_of(grp * sk.kb);  // clusters sharing this group
-        const int c_last = sk.cta_of(grp * sk.kb + sk.kb - 1);
-        __threadfence();
-        named_bar_sync(1, kEpiThreads);
-        if (et == 0) {
-          int prev = atomicAdd(&a.counters[tile], 1);
-          *bcast = (prev == c_last - c_first) ? 1 : 0;
-        }
-        named_bar_sync(1, kEpiThreads);
-        if (*bcast) {
-          __threadfence();
-          // work item = (row pair, token column); parts summed in fixed CTA
-          // order (deterministic); 8 items per thread in flight per round trip.
-          const int n_items = 64 * ncols_tile;
-          for (int base = et; base < n_items; base += 8 * kEpiThreads) {
-            float2 sum[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sum[j] = make_float2(0.f, 0.f);
-            for (int cc = c_first; cc <= c_last; ++cc) {
-              const int w = (sk.u0(cc) / sk.kb == grp) ? 0 : 1;
-              const float* p = a.ws + ((size_t)(cc * mc + mrank) * 2 + w) * (size_t)(kBM * TN);
-              float2 ld[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) ld[j] = make_float2(0.f, 0.f);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const int it = base + j * kEpiThreads;
-                if (it < n_items)
-                  ld[j] = __ldcg(reinterpret_cast<const float2*>(p + (size_t)(it >> 6) * kBM + 2 * (it & 63)));
-              }
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                sum[j].x += ld[j].x;
-                sum[j].y += ld[j].y;
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int it = base + j * kEpiThreads;
-              if (it < n_items) emit_pair(a, mt * kBM + 2 * (it & 63), row0 + (it >> 6), sum[j].x, sum[j].y);
-            }
-          }
-          if (et == 0) a.counters[tile] = 0;
-        }
-        named_bar_sync(1, kEpiThreads);
+        const PartMap pm{a.ws, sk, tile, 1, 0, TN};
+        epi_fixup(a, &a.counters[tile], pm, sk.cta_of(tile * sk.kb), sk.cta_of(tile * sk.kb + sk.kb - 1), mt * kBM,
+                  row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes), fix_bar, fix_phase, bcast, et, tr);
       }
       u += kb1 - kb0;
     }
+    if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
   }
   if (csplit > 1) {
     // Cluster split-K: every CTA of the cluster holds a partial [TN][128] in
@@ -388,177 +619,237 @@ __global__ void __launch_bounds__(kThreads1, 1)
     if (epi_warp) {
       const int et = threadIdx.x - 64;
       const uint32_t rank = cluster_ctarank();
-      const int rows_per = kBM / csplit, pairs = rows_per / 2;
+      const int rows_per = kBM / csplit;
       const int row_base = int(rank) * rows_per;
       const int row0 = a.row_off + tt * TN;
       const uint32_t base = smem_u32(sW);
-      for (int it = et; it < pairs * ncols_tile; it += kEpiThreads) {
-        const int col = it / pairs, row = row_base + 2 * (it % pairs);
-        const uint32_t off = base + uint32_t((col * kBM + row) * 4);
-        float2 sum = make_float2(0.f, 0.f);
-        for (int src = 0; src < csplit; ++src) {
-          const float2 v = dsmem_ld_f2(dsmem_map(off, uint32_t(src)));
-          sum.x += v.x;
-          sum.y += v.y;
+      if (a.vec) {
+        // item = (token column, 8 consecutive rows of this rank's share); 4 items
+        // per thread per batch, residual loads of a batch before its stores
+        const int gpr = rows_per / 8, n_items = gpr * ncols_tile;
+        for (int it0 = et; it0 < n_items; it0 += 4 * kEpiThreads) {
+          float4 res[4][2];
+          if (a.epi == EPI_RESID) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int it = it0 + j * kEpiThreads;
+              const int n0 = mt * kBM + row_base + 8 * (it % gpr);
+              if (it < n_items && n0 < a.N) {
+                const float4* y = reinterpret_cast<const float4*>(out_f32(a, n0, row0 + it / gpr));
+                res[j][0] = __ldcg(y);
+                res[j][1] = __ldcg(y + 1);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int it = it0 + j * kEpiThreads;
+            if (it >= n_items) break;
+            const int col = it / gpr, row = row_base + 8 * (it % gpr);
+            const uint32_t off = base + uint32_t((col * kBM + row) * 4);
+            float s8[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s8[e] = 0.f;
+            for (int src = 0; src < csplit; ++src) {
+              const uint32_t ra = dsmem_map(off, uint32_t(src));
+              const float4 x0 = dsmem_ld_f4(ra), x1 = dsmem_ld_f4(ra + 16);
+              s8[0] += x0.x; s8[1] += x0.y; s8[2] += x0.z; s8[3] += x0.w;
+              s8[4] += x1.x; s8[5] += x1.y; s8[6] += x1.z; s8[7] += x1.w;
+            }
+            emit8(a, mt * kBM + row, row0 + col, s8, res[j]);
+          }
         }
-        emit_pair(a, mt * kBM + row, row0 + col, sum.x, sum.y);
+      } else {
+        const int pairs = rows_per / 2;
+        for (int it = et; it < pairs * ncols_tile; it += kEpiThreads) {
+          const int col = it / pairs, row = row_base + 2 * (it % pairs);
+          const uint32_t off = base + uint32_t((col * kBM + row) * 4);
+          float2 sum = make_float2(0.f, 0.f);
+          for (int src = 0; src < csplit; ++src) {
+            const float2 v = dsmem_ld_f2(dsmem_map(off, uint32_t(src)));
+            sum.x += v.x;
+            sum.y += v.y;
+          }
+          emit_pair(a, mt * kBM + row, row0 + col, sum.x, sum.y);
+        }
       }
     }
     cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
   tc_fence_before();
-  if (mc > 1)
-    cluster_sync_all();  // no CTA leaves while peers may still multicast into it / arrive on it
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
 }
 
-
-// ---------------------------------------------------------------------------
-// CTA-pair GEMM for prefill-sized batches (T > 256): one tcgen05.mma.cta_group::2
-// computes a 256 (weight rows) x 256 (tokens) tile across the two SMs of a
-// cluster pair.  Each CTA stages its own 128 weight rows and 128 token rows
-// per k-block (both TMA loads signal the leader's barrier), so every byte of
-// the B operand feeds twice the MMA work of the 1-CTA kernel -- the prefill
-// GEMMs are L2-bandwidth / tensor bound, not HBM bound.  Persistent over pair
-// tiles; accumulators double buffered in TMEM (2 x 256 columns per CTA).
-static constexpr int kPairTN = 256;
-static constexpr int kPairStageBytes = 2 * kBM * kBK * 2;  // 16 KB weights + 16 KB tokens per CTA
-static constexpr int kPairStages = 6;
-static constexpr size_t kPairSmemBytes = size_t(kPairStages) * kPairStageBytes + 1024 + 256;
-
-__global__ void __launch_bounds__(kThreads, 1)
+// ------------------------------------------------------------------ CTA-pair kernel
+// One MMA computes a 256 (weight rows) x TNP (tokens) tile across the two SMs of
+// a cluster pair; each CTA stages its own 128 weight rows and TNP/2 token rows
+// per k-block (both TMA loads complete on the leader's barriers).  At T = 256
+// the 1-CTA kernel would re-read the activation tile once per 128 weight rows
+// (L2 traffic 3x the weight bytes); the pair kernel once per 256 rows.  Same
+// stream-K split (over pairs) and fixup as the 1-CTA kernel; each CTA finishes
+// its own 128-row half.
+template <int TNP>
+__global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const GemmArgs a) {
-  constexpr int S = kPairStages;
-  constexpr int HB = kBM * kBK * 2;  // one half-tile (128 rows x 64 k) in bytes
+  using Cfg = PairCfg<TNP>;
+  constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  uint8_t* sX = smem + S * HB;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(sX + S * HB);
-  uint64_t* empty_bar = full_bar + S;
-  uint64_t* tfull_bar = empty_bar + S;
-  uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint8_t* sX = smem + S * Cfg::kWBytes;
+  float* tbuf_all = reinterpret_cast<float*>(smem + Cfg::kRingBytes);
+  uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + kTbufBytes);  // leader: weights landed
+  uint64_t* xfull_bar = wfull_bar + S;   // leader: both CTAs' tokens landed
+  uint64_t* empty_bar = xfull_bar + S;   // each CTA: stage consumed
+  uint64_t* tfull_bar = empty_bar + S;   // each CTA: accumulator ready
+  uint64_t* tempty_bar = tfull_bar + 2;  // leader: both epilogues drained
+  uint64_t* fix_bar = tempty_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
+  int* bcast = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int n_mt = (a.N + 2 * kBM - 1) / (2 * kBM);
-  const int n_tt = (a.T + kPairTN - 1) / kPairTN;
-  const int n_tiles = n_mt * n_tt;
-  const int kb_n = (a.K + kBK - 1) / kBK;
+  const int pair = blockIdx.x >> 1;
+  const int n_tt = a.n_ttiles;
+  const StreamK sk{a.units, int(gridDim.x) >> 1, a.kblocks};
+  const int ubeg = sk.u0(pair), uend = sk.u0(pair + 1);
 
   pdl_trigger();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full_bar[i], 1);
+      mbar_init(&wfull_bar[i], 1);
+      mbar_init(&xfull_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 2 * kEpiThreads);  // both CTAs' epilogue threads report to the leader
     }
+    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc_pair<512>(tmem_slot);
+  if (warp == 1) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
   cluster_sync_all();  // barriers of both CTAs exist before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
+    // ---------------------------------------------------------- weight producer
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_last();  // a weight tile is reused by consecutive token tiles
-      const uint64_t pol_x = policy_evict_last();
-      pdl_wait();
+      const uint64_t pol_w = n_tt > 1 ? policy_evict_last() : policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = pair; tile < n_tiles; tile += npairs) {
-        const int mt = tile / n_tt, tt = tile % n_tt;
-        for (int kb = 0; kb < kb_n; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kPairStageBytes);
-          tma_load_2d_pair(&tmW, &full_bar[stage], sW + stage * HB, kb * kBK, mt * 2 * kBM + int(rank) * kBM, pol_w);
-          tma_load_2d_pair(&tmX, &full_bar[stage], sX + stage * HB, kb * kBK,
-                           a.row_off + tt * kPairTN + int(rank) * kBM, pol_x);
-          if (++stage == S) { stage = 0; phase ^= 1; }
-        }
+      for (int u = ubeg; u < uend; ++u) {
+        const int mt = (u / sk.kb) / n_tt, kb = u % sk.kb;
+        if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], 2 * Cfg::kWBytes);
+        const int mt128 = mt * 2 + int(rank);
+        if (a.w_tiled)
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, 0, (mt128 * sk.kb + kb) * kBM, pol_w);
+        else
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt128 * kBM, pol_w);
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------------------------------------------------- activation producer
+    if (elect_one()) {
+      const uint64_t pol_x = policy_evict_last();
+      pdl_wait();  // activations belong to the previous kernel
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = ubeg; u < uend; ++u) {
+        const int tt = (u / sk.kb) % n_tt, kb = u % sk.kb;
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * Cfg::kXBytes);
+        tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
+                         a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
+        if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer (leader, converged warp)
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, kPairTN);
+      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, TNP);
+      const uint64_t dw0 = make_sw128_desc(smem_u32(sW));
+      const uint64_t dx0 = make_sw128_desc(smem_u32(sX));
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = pair; tile < n_tiles; tile += npairs) {
+      for (int u = ubeg; u < uend;) {
+        const int kb0 = u % sk.kb;
+        const int kb1 = min(sk.kb, kb0 + (uend - u));
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * kPairTN);
-        for (int kb = 0; kb < kb_n; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * TNP);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&wfull_bar[stage], phase);
+          mbar_wait(&xfull_bar[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
-            const uint64_t dw = make_sw128_desc(smem_u32(sW + stage * HB));
-            const uint64_t dx = make_sw128_desc(smem_u32(sX + stage * HB));
-#pragma unroll
-            for (int k = 0; k < kBK / kUmmaK; ++k)
-              umma_bf16_pair(d_tmem, dw + uint64_t(2 * k), dx + uint64_t(2 * k), idesc, (kb > 0 || k > 0) ? 1u : 0u);
-            umma_commit_pair(&empty_bar[stage]);  // frees the stage in both CTAs
-          }
           __syncwarp();
+          const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
+          const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
+          umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        if (lane == 0) umma_commit_pair(&tfull_bar[acc]);
         __syncwarp();
+        umma_commit_pair_elect(&tfull_bar[acc]);
+        u += kb1 - kb0;
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
   } else {
-    pdl_wait();
+    // ---------------------------------------------------------- epilogue (both CTAs)
+    pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;
-    const int row_in_tile = q * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127
+    float* tb = tbuf_all + q * (16 * kTbRow);
     const uint32_t tempty_leader0 = dsmem_map(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = dsmem_map(smem_u32(&tempty_bar[1]), 0);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = pair; tile < n_tiles; tile += npairs) {
+    uint32_t fix_phase = 0;
+    for (int u = ubeg; u < uend;) {
+      const int tile = u / sk.kb, kb0 = u % sk.kb;
+      const int kb1 = min(sk.kb, kb0 + (uend - u));
       const int mt = tile / n_tt, tt = tile % n_tt;
-      const int n = mt * 2 * kBM + int(rank) * kBM + row_in_tile;
-      const int row0 = a.row_off + tt * kPairTN;
-      const int ncols = min(kPairTN, a.T - tt * kPairTN);
+      const int m0 = mt * 2 * kBM + int(rank) * kBM;  // this CTA's first weight row
+      const int row0 = a.row_off + tt * TNP;
+      const int ncols = min(TNP, a.T - tt * TNP);
+      const bool whole = (kb0 == 0 && kb1 == sk.kb);
+      const bool last_seg = (u + (kb1 - kb0) == uend);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * kPairTN);
-      for (int c0 = 0; c0 < ncols; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_addr + uint32_t(c0), r);
-        tmem_ld_wait();
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-        emit16(a, n, row0 + c0, min(16, ncols - c0), v);
-      }
+      const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TNP);
+      float* part = a.ws + ((size_t)blockIdx.x * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TNP);
+      epi_drain(a, t_addr, m0, row0, ncols, whole, part, tb, q, lane);
       tc_fence_before();
       mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (!whole) {
+        const PartMap pm{a.ws, sk, tile, 2, int(rank), TNP};
+        epi_fixup(a, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
+                  sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes),
+                  fix_bar, fix_phase, bcast, et);
+      }
+      u += kb1 - kb0;
     }
   }
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+  if (warp == 1) tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
 }
 
 // ------------------------------------------------------------------ host side
@@ -593,63 +884,60 @@ int gemm_pick_tn(int T) {
   if (T <= 32) return 32;
   if (T <= 64) return 64;
   if (T <= 128) return 128;
-  if (T <= 256) return 256;
-  return kPairTileMarker;  // CTA-pair kernel; its token box is 128 rows per CTA
+  return 256;
 }
 
-// Work split of one launch.  Everything but the TN bucket depends on (N, K) and
-// the tile count only, so for decode batches (T <= 256, one token tile) a row's
+// Work split of one launch.  Everything but the TN bucket depends on (N, K),
+// the kernel kind and the tile count only, so within one kind a decode row's
 // result does not depend on how many rows share the launch.
-GemmPlan gemm_plan(int N, int K, int T, int num_sms) {
+//   T <= 128: 1-CTA kernel (128 weight rows x TN tokens), stream-K or cluster
+//             split-K -- HBM-bound weight streaming;
+//   T  > 128: CTA-pair kernel (256 weight rows x 256 tokens per pair tile),
+//             stream-K -- halves the activation re-reads from L2.
+//
+// Stream-K fixups (partials through L2, last arriver sums) cost several us per
+// split tile at the end of a launch (measured), so a launch whose tiles fit in
+// one wave runs one tile per CTA (pair) instead (max_parts = 1); stream-K is
+// kept where tiles outnumber the SMs (gate/up, lm_head) or K is long enough to
+// pay for the fixup (down projection on the pair kernel).
+//
+// kind_T = rows of the whole pass the launch belongs to: a replica's
+// micro-batch (split_batch share) runs the kernel and split the unreplicated
+// pass would run, so replication does not change a row's bits (T <= 256).
+GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   GemmPlan p{};
-  p.tn = gemm_pick_tn(T);
-  if (p.tn == kPairTileMarker) {
-    p.box_rows = kBM;
-    p.mcast = 1;
-    p.csplit = 1;
+  p.csplit = 1;
+  p.max_parts = 0;
+  if (kind_T < T) kind_T = T;
+  const int kb = (K + kBK - 1) / kBK;
+  if (kind_T > kPairMinT) {
+    p.pair = 1;
+    p.tn = 256;
+    p.box_rows = p.tn / 2;
+    const long long ptiles = (long long)((N + 2 * kBM - 1) / (2 * kBM)) * ((kind_T + p.tn - 1) / p.tn);
+    if (ptiles <= num_sms / 2 && kb < 128) p.max_parts = 1;
     return p;
   }
+  p.pair = 0;
+  p.tn = gemm_pick_tn(T);
   const long long tiles = (N + kBM - 1) / kBM;  // one token tile
-  const int kb = (K + kBK - 1) / kBK;
-  p.csplit = 1;
-  p.mcast = 1;
   if (tiles * 10 < (long long)num_sms * 6) {
     // few wide-K tiles (O / down projections): cluster split-K
     while (p.csplit < 8 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
+  } else if (tiles <= num_sms) {
+    p.max_parts = 1;  // QKV: one wave of whole tiles
   }
-  // (activation multicast across clusters -- a.mcast > 1 -- is implemented and
-  // correct but measured no faster than plain loads on B200, so plans keep 1)
-  p.box_rows = p.tn / p.mcast;
+  p.box_rows = p.tn;
   return p;
 }
 
-// How many clusters of `cs` CTAs of this kernel can be resident at once (GPCs
-// are not multiples of 4 SMs: clusters of 4 fit on 132 of the 148 SMs).
-template <typename K>
-static int max_active_clusters(K kernel, int cs, size_t smem, int threads) {
-  static int cache[64][9] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int& slot = cache[dev & 63][cs & 7];
-  if (slot) return slot;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(cs));
-  cfg.blockDim = dim3(unsigned(threads));
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(cs);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = 148 / cs;
-  }
-  slot = n;
-  return n;
+// 16-byte vector epilogue stores are legal: 8-row groups never straddle N, and
+// every output row start is 16-byte aligned.
+static int vec_ok(const GemmArgs& a) {
+  const uintptr_t o = reinterpret_cast<uintptr_t>(a.out);
+  if (a.N % 16 != 0 || (o & 15) != 0) return 0;
+  if (a.epi == EPI_SWIGLU || a.epi == EPI_BF16) return (a.ldo % 8 == 0) ? 1 : 0;
+  return (a.ldo % 4 == 0) ? 1 : 0;
 }
 
 template <int TN>
@@ -670,59 +958,62 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK - 1) / kBK;
+  a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;
-  a.mcast = plan.mcast;
-  if (plan.csplit > 1) {
-    a.units = int(tiles * a.kblocks);
+  a.units = int(tiles * a.kblocks);
+  if (plan.csplit > 1)
     return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
                               Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, a);
-  }
-  const int mc = plan.mcast;
-  const long long groups = (tiles + mc - 1) / mc;
-  a.units = int(groups * a.kblocks);
-  // persistent stream-K over clusters; a group is spread over <= max_parts clusters
-  long long clusters = num_sms / mc;
-  if (mc > 1) {
-    const int resident = max_active_clusters(gemm_tc_kernel<TN>, mc, Cfg::kSmemBytes, kThreads1);
-    if (clusters > resident) clusters = resident;  // one wave: no cluster waits for another to finish
-  }
-  if (clusters > a.units) clusters = a.units;
-  const int max_parts = a.max_parts > 0 ? a.max_parts : 1;
-  if (clusters > groups * max_parts) clusters = groups * max_parts;
-  if (mc == 1)
-    return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(clusters)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, a);
-  return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(clusters * mc)), dim3(kThreads1), Cfg::kSmemBytes, st,
-                            unsigned(mc), w, x, a);
+  // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
+  long long ctas = num_sms;
+  if (ctas > a.units) ctas = a.units;
+  const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
+  if (mp > 0 && ctas > tiles * mp) ctas = tiles * mp;
+  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, a);
 }
 
-static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, int num_sms, cudaStream_t st) {
+template <int TNP>
+static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, const GemmPlan& plan,
+                               int num_sms, cudaStream_t st) {
+  using Cfg = PairCfg<TNP>;
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(kPairSmemBytes));
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(Cfg::kSmemBytes));
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
-  const long long tiles = (long long)((a.N + 2 * kBM - 1) / (2 * kBM)) * ((a.T + kPairTN - 1) / kPairTN);
+  a.n_ttiles = (a.T + TNP - 1) / TNP;
+  a.n_mtiles = (a.N + 2 * kBM - 1) / (2 * kBM);
+  a.kblocks = (a.K + kBK - 1) / kBK;
+  a.vec = vec_ok(a);
+  const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
+  a.units = int(tiles * a.kblocks);
   long long pairs = num_sms / 2;
-  if (pairs > tiles) pairs = tiles;
-  return launch_pdl_cluster(gemm_tc2_kernel, dim3(unsigned(2 * pairs)), dim3(kThreads), kPairSmemBytes, st, 2u,
-                            w, x, a);
+  if (pairs > a.units) pairs = a.units;
+  const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
+  if (mp > 0 && pairs > tiles * mp) pairs = tiles * mp;
+  return launch_pdl_cluster(gemm_tc2_kernel<TNP>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes, st,
+                            2u, w, x, a);
 }
 
 cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
                         int num_sms, cudaStream_t st) {
   if (a.T <= 0 || a.N <= 0) return cudaSuccess;
+  if (plan.pair) {
+    if (plan.tn == 128) return launch_pair<128>(w, x, a, plan, num_sms, st);
+    if (plan.tn == 256) return launch_pair<256>(w, x, a, plan, num_sms, st);
+    return cudaErrorInvalidValue;
+  }
   switch (plan.tn) {
     case 16: return launch_tn<16>(w, x, a, plan, num_sms, st);
     case 32: return launch_tn<32>(w, x, a, plan, num_sms, st);
     case 64: return launch_tn<64>(w, x, a, plan, num_sms, st);
     case 128: return launch_tn<128>(w, x, a, plan, num_sms, st);
     case 256: return launch_tn<256>(w, x, a, plan, num_sms, st);
-    case kPairTileMarker: return launch_pair(w, x, a, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -27,26 +27,32 @@ struct GemmArgs {
   void* out;
   float* ws;      // stream-K partials, gemm_ws_floats(num_sms) floats
   int* counters;  // per-tile arrival counters, zero-initialised, >= n_tiles ints
-  int max_parts;      // stream-K: max clusters per tile group (0 = 1)
+  int max_parts;      // stream-K: max CTAs (pairs) per tile (0 = no cap)
   int cluster_split;  // set from the plan: >1 = tile split over a cluster, DSMEM reduce
-  int mcast;          // set from the plan: >1 = activation tile multicast across a cluster
+  int w_tiled;        // 1 = weight stored tile-major [N/128][K/64][128][64] (each TMA box contiguous)
+  unsigned long long* trace;  // experiments only: per-CTA event timestamps (globaltimer ns) when non-null
+  int vec;            // set by the launcher: 16-byte vector epilogue stores are legal for out/N/ldo
+  int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
 };
 
 int make_kmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
                     uint32_t box_rows);
-// TN bucket of a launch: 16..256 for the 1-CTA kernel, kPairTileMarker for the
-// CTA-pair kernel (T > 256, activation map boxes of 128 rows).
-constexpr int kPairTileMarker = 512;
+// TN bucket of a 1-CTA launch (16..256).
 int gemm_pick_tn(int T);
+// Launches with more rows than this use the CTA-pair kernel (tunable for experiments).
+constexpr int kPairMinT = 128;
 struct GemmPlan {
-  int tn;        // token tile (16..256) or kPairTileMarker
-  int box_rows;  // activation tensor-map box height this plan needs
-  int mcast;     // activation multicast cluster size (1, 2, 4)
+  int tn;        // token tile: 16..256 (1-CTA) or the pair tile (128 / 256 tokens per pair)
+  int pair;      // 1 = CTA-pair kernel (tcgen05 cta_group::2, 256 weight rows per tile)
+  int box_rows;  // activation tensor-map box height this plan needs (pair: tn / 2)
   int csplit;    // cluster split-K size (1, 2, 4, 8)
+  int max_parts; // stream-K: max CTAs (pairs) sharing a tile (0 = no cap; 1 = one tile per CTA, no fixups)
 };
-GemmPlan gemm_plan(int N, int K, int T, int num_sms);
+// kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
+// micro-batches compute exactly what the unreplicated pass would.
+GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T = 0);
 cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
                         int num_sms, cudaStream_t st);
 size_t gemm_ws_floats(int num_sms);

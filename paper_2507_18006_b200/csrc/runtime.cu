@@ -376,7 +376,7 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
          int epi, void* out, long long ldo) {
   DeviceCtx& dc = devctx(m, dev);
   Workspace& ws = m->ws[dev];
-  const cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms);
+  const cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms, m->cur_T);
   cb::GemmArgs a{};
   a.N = N;
   a.K = K;

@@ -1,12 +1,15 @@
 // Kernel-level test entry points (include/cocob200_testing.h).  Thin wrappers
 // that build tensor maps / workspaces for caller-owned device buffers.
 #include <cmath>
+#include <cstring>
+#include <algorithm>
 #include <map>
 #include <string>
 #include <vector>
 
 #include "../../include/cocob200.h"
 #include "../../include/cocob200_testing.h"
+#include "common.cuh"
 #include "kernels.h"
 
 namespace {
@@ -20,6 +23,9 @@ struct TestWs {
 };
 
 std::map<int, TestWs> g_ws;
+unsigned long long g_trace[148 * 512];
+int g_wcopies = 1;          // experiments: rotate over this many weight copies ...
+int64_t g_wcopy_stride = 0; // ... this many bytes apart (defeats L2 residency of the weight)
 
 int ws_for_current(TestWs** out) {
   int dev = 0;
@@ -80,17 +86,34 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   int r = ws_for_current(&ws);
   if (r) return r;
   cb::GemmPlan plan = cb::gemm_plan(N, K, T, ws->sms);
-  if (max_parts < 0 && plan.tn != cb::kPairTileMarker) {  // experiments: force cluster split -max_parts
+  const int dbg_bits = max_parts / 1000;
+  max_parts %= 1000;
+  // experiment knobs: 201 / 202 force the CTA-pair kernel (256 / 128-token
+  // tiles), 203 forces the 1-CTA kernel, < 0 forces cluster split -max_parts,
+  // 1..99 cap the stream-K parts per tile
+  if (max_parts == 201 || max_parts == 202) {
+    plan = cb::GemmPlan{max_parts == 201 ? 256 : 128, 1, max_parts == 201 ? 128 : 64, 1, 0};
+  } else if (max_parts == 203 && plan.pair) {
+    plan = cb::GemmPlan{cb::gemm_pick_tn(T), 0, cb::gemm_pick_tn(T), 1, 0};
+  } else if (max_parts < 0 && !plan.pair) {
     plan.csplit = -max_parts;
-    plan.mcast = 1;
-    plan.box_rows = plan.tn;
-  } else if (max_parts == 100 && plan.tn != cb::kPairTileMarker) {  // experiments: no multicast
-    plan.mcast = 1;
-    plan.box_rows = plan.tn;
+  } else if (max_parts > 0 && max_parts < 100 && !plan.pair) {
+    plan.csplit = 1;
+  } else if (max_parts == 99) {
+    plan.max_parts = 0;  // experiments: force stream-K
   }
   CUtensorMap mw, mx;
   if ((r = gemm_setup(w, x, x_rows, N, K, plan, &mw, &mx))) return r;
+  const bool tiled = (dbg_bits & 4) != 0;  // w holds the tile-major layout
+  std::vector<CUtensorMap> mws(std::max(1, g_wcopies));
+  for (size_t i = 0; i < mws.size(); ++i) {
+    const void* wi = static_cast<const uint8_t*>(w) + i * g_wcopy_stride;
+    int e = tiled ? cb::make_kmajor_map(&mws[i], wi, uint64_t(N) * (K / 64), 64, 64, 128)
+                  : cb::make_kmajor_map(&mws[i], wi, N, K, K, 128);
+    if (e != 0) return CB_ECUDA;
+  }
   cb::GemmArgs a{};
+  a.w_tiled = tiled ? 1 : 0;
   a.N = N;
   a.K = K;
   a.T = T;
@@ -99,18 +122,31 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
-  a.max_parts = (max_parts < 0 || max_parts == 100) ? 1 : max_parts;
-  for (int i = 0; i < 3; ++i) cb::gemm_launch(mw, mx, a, plan, ws->sms, 0);
+  a.max_parts = (max_parts > 0 && max_parts < 100) ? max_parts : 0;
+  static unsigned long long* trace = nullptr;
+  if (dbg_bits & 8) {  // experiments: per-CTA timeline of the last launch -> g_trace
+    if (!trace) cudaMalloc(&trace, 148 * 512 * 8);
+    cudaMemset(trace, 0, 148 * 512 * 8);
+    a.trace = trace;
+  }
+  a.dbg = dbg_bits & ~(4 | 8);  // experiments: knob + 1000 * dbg bits (4 = tile-major weight)
+  for (int i = 0; i < 3; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
-  for (int i = 0; i < iters; ++i) cb::gemm_launch(mw, mx, a, plan, ws->sms, 0);
+  for (int i = 0; i < iters; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0);
   cudaEventRecord(e1, 0);
   if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   *ms_per_launch = ms / iters;
+  if (a.trace) {
+    cudaMemset(trace, 0, 148 * 512 * 8);
+    cb::gemm_launch(mws[iters % mws.size()], mx, a, plan, ws->sms, 0);
+    cudaDeviceSynchronize();
+    cudaMemcpy(g_trace, trace, sizeof(g_trace), cudaMemcpyDeviceToHost);
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return finish(cudaGetLastError());
@@ -259,3 +295,213 @@ int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// TMA read-bandwidth probe (experiments only): every CTA streams `iters` boxes
+// of box_rows x 64 bf16 through an S-stage smem ring (one thread issues, the
+// same thread waits), from a rows x 64 K-major region.  Small regions stay in
+// L2, large ones stream from HBM: the per-SM and chip-wide TMA fill rates the
+// GEMM kernels are bounded by.
+namespace {
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int c1,
+                                            int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(cb::smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cb::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+
+// warp w (< nw) streams its own S-stage ring; kd > 1 = 3-D boxes of kd k-slices
+template <int S>
+__global__ void __launch_bounds__(128, 1) tma_probe_kernel(const __grid_constant__ CUtensorMap tm, int rows,
+                                                           int box_rows, int kd, int nw, int iters, int mma_n) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int box_bytes = box_rows * 128 * kd;
+  const int w = threadIdx.x >> 5;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + nw * S * box_bytes) + w * S;
+  __shared__ volatile int done;
+  __shared__ uint32_t tslot;
+  __shared__ uint64_t mbar;
+  if (mma_n > 0) {
+    // warp 3: back-to-back 128 x mma_n x 16 MMAs on a separate smem region while warps < nw stream TMA
+    if (threadIdx.x == 0) done = 0;
+    if (w == 3) cb::tmem_alloc<256>(&tslot);
+    cb::tc_fence_before();
+    __syncthreads();
+    cb::tc_fence_after();
+    if (w == 3) {
+      if ((threadIdx.x & 31) == 0) {
+        cb::mbar_init(&mbar, 1);
+        cb::fence_barrier_init();
+        uint8_t* ops = smem + nw * S * box_bytes + 4096;
+        ops = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ops) + 1023) & ~uintptr_t(1023));
+        const uint64_t da = cb::make_sw128_desc(cb::smem_u32(ops));
+        const uint64_t db = cb::make_sw128_desc(cb::smem_u32(ops + 16384));
+        const uint32_t idesc = cb::make_idesc_bf16(128, uint32_t(mma_n));
+        uint32_t ph = 0;
+        while (!done) {
+          for (int i = 0; i < 64; ++i) cb::umma_bf16(tslot, da + uint64_t(2 * (i & 3)), db + uint64_t(2 * (i & 3)), idesc, 1u);
+          cb::umma_commit(&mbar);
+          cb::mbar_wait(&mbar, ph);
+          ph ^= 1;
+        }
+      }
+      __syncwarp();
+      cb::tc_fence_before();
+      cb::tmem_dealloc<256>(tslot);
+      return;
+    }
+  }
+  if (w >= nw || (threadIdx.x & 31) != 0) return;
+  uint8_t* ring = smem + w * S * box_bytes;
+  for (int i = 0; i < S; ++i) cb::mbar_init(&bar[i], 1);
+  cb::fence_barrier_init();
+  const uint64_t pol = cb::policy_evict_first();
+  const int nbox = rows / box_rows;
+  int next = 0;
+  auto issue = [&](int i) {
+    const int s = i % S;
+    const int b = int(((long long)(blockIdx.x * nw + w) * iters + i) % nbox);  // disjoint chunks (HBM) / wraps (L2)
+    cb::mbar_arrive_expect_tx(&bar[s], box_bytes);
+    if (kd == 1)
+      cb::tma_load_2d(&tm, &bar[s], ring + s * box_bytes, 0, b * box_rows, pol);
+    else
+      tma_load_3d(&tm, &bar[s], ring + s * box_bytes, 0, b * box_rows, 0, pol);
+  };
+  for (; next < S && next < iters; ++next) issue(next);
+  for (int i = 0; i < iters; ++i) {
+    cb::mbar_wait(&bar[i % S], (i / S) & 1);
+    if (next < iters) issue(next++);
+  }
+  if (mma_n > 0 && w == 0) done = 1;
+}
+
+}
+
+extern "C" int cbt_tma_probe(const void* buf, int64_t rows, int32_t box_rows, int32_t stages, int32_t grid,
+                             int32_t iters, int32_t kd, int32_t nw, int32_t mma_n, float* ms_out) {
+  CUtensorMap tm;
+  // region viewed as [rows][kd * 64] bf16; a 3-D box = (64, box_rows, kd) lands as kd SW128 sub-tiles
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return CB_ECUDA;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const int64_t r = rows / kd;
+  cuuint64_t dims[3] = {64, cuuint64_t(r), cuuint64_t(kd)};
+  cuuint64_t strides[2] = {cuuint64_t(kd) * 128, 128};
+  cuuint32_t box[3] = {64, uint32_t(box_rows), uint32_t(kd)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, kd == 1 ? 2 : 3, const_cast<void*>(buf), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return CB_EINVAL;
+  const size_t smem = size_t(nw) * stages * box_rows * 128 * kd + 1024 + 512 + (mma_n > 0 ? 4096 + 1024 + 49152 : 0);
+  auto run = [&](auto kern) -> int {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, 128, smem>>>(tm, int(r), box_rows, kd, nw, iters, mma_n);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    kern<<<grid, 128, smem>>>(tm, int(r), box_rows, kd, nw, iters, mma_n);
+    cudaEventRecord(e1);
+    if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
+    cudaEventElapsedTime(ms_out, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return cudaGetLastError() == cudaSuccess ? CB_OK : CB_ECUDA;
+  };
+  switch (stages) {
+    case 1: return run(tma_probe_kernel<1>);
+    case 2: return run(tma_probe_kernel<2>);
+    case 4: return run(tma_probe_kernel<4>);
+    case 8: return run(tma_probe_kernel<8>);
+    case 16: return run(tma_probe_kernel<16>);
+  }
+  return CB_EINVAL;
+}
+
+extern "C" int cbt_gemm_trace(unsigned long long* out, int32_t n) {
+  if (n > 148 * 512) n = 148 * 512;
+  std::memcpy(out, g_trace, size_t(n) * 8);
+  return CB_OK;
+}
+
+extern "C" int cbt_gemm_set_wcopies(int32_t n, int64_t stride_bytes) {
+  g_wcopies = n < 1 ? 1 : n;
+  g_wcopy_stride = stride_bytes;
+  return CB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05.mma issue-rate probe (experiments only): one CTA per SM issues `n`
+// kind::f16 MMAs of 128 x N x 16 from shared memory (SW128 K-major operands,
+// garbage data) into TMEM, then waits for completion; cycles per MMA.
+namespace {
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_probe_kernel(int n, int kstep, unsigned long long* cyc) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    cb::mbar_init(&bar, 1);
+    cb::fence_barrier_init();
+  }
+  if (warp == 0) cb::tmem_alloc<256>(&tslot);
+  cb::tc_fence_before();
+  __syncthreads();
+  cb::tc_fence_after();
+  const uint32_t tm = tslot;
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = cb::make_idesc_bf16(128, N);
+    const uint64_t da = cb::make_sw128_desc(cb::smem_u32(smem));
+    const uint64_t db = cb::make_sw128_desc(cb::smem_u32(smem + 16384));
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+      const int k = (i % 4) * kstep;
+      cb::umma_bf16(tm, da + uint64_t(2 * k), db + uint64_t(2 * k), idesc, i > 0 ? 1u : 0u);
+    }
+    cb::umma_commit(&bar);
+    cb::mbar_wait(&bar, 0);
+    const unsigned long long t1 = clock64();
+    cyc[blockIdx.x] = t1 - t0;
+  }
+  cb::tc_fence_before();
+  __syncthreads();
+  cb::tc_fence_after();
+  if (warp == 0) cb::tmem_dealloc<256>(tm);
+}
+}  // namespace
+
+extern "C" int cbt_mma_probe(int32_t N, int32_t n, int32_t grid, int32_t kstep, double* cyc_per_mma) {
+  unsigned long long* d = nullptr;
+  cudaMalloc(&d, size_t(grid) * 8);
+  const size_t smem = 16384 + 32768 + 1024;
+  auto run = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, 128, smem>>>(n, kstep, d);
+    kern<<<grid, 128, smem>>>(n, kstep, d);
+  };
+  switch (N) {
+    case 16: run(mma_probe_kernel<16>); break;
+    case 64: run(mma_probe_kernel<64>); break;
+    case 128: run(mma_probe_kernel<128>); break;
+    case 256: run(mma_probe_kernel<256>); break;
+    default: cudaFree(d); return CB_EINVAL;
+  }
+  std::vector<unsigned long long> h(grid);
+  if (cudaMemcpy(h.data(), d, size_t(grid) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return CB_ECUDA;
+  cudaFree(d);
+  double s = 0;
+  for (auto v : h) s += double(v);
+  *cyc_per_mma = s / grid / n;
+  return CB_OK;
+}
