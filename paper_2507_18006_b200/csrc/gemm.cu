@@ -718,8 +718,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
   const int n_tt = a.n_ttiles;
   const StreamK sk{a.units, int(gridDim.x) >> 1, a.kblocks};
   const int ubeg = sk.u0(pair), uend = sk.u0(pair + 1);
+  const int c = blockIdx.x;
 
   pdl_trigger();
+  if (a.trace && threadIdx.x == 0) a.trace[(size_t)c * 512] = globaltimer_ns();
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
@@ -750,6 +752,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       for (int u = ubeg; u < uend; ++u) {
         const int mt = (u / sk.kb) / n_tt, kb = u % sk.kb;
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 66 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], 2 * Cfg::kWBytes);
         const int mt128 = mt * 2 + int(rank);
         if (a.w_tiled)
@@ -769,6 +772,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       for (int u = ubeg; u < uend; ++u) {
         const int tt = (u / sk.kb) % n_tt, kb = u % sk.kb;
         mbar_wait(&empty_bar[stage], phase ^ 1);
+        if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * Cfg::kXBytes);
         tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
                          a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
@@ -792,13 +796,17 @@ __global__ void __launch_bounds__(kThreads1, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * TNP);
         for (int kb = kb0; kb < kb1; ++kb) {
+          const int i = u + (kb - kb0) - ubeg;
           mbar_wait(&wfull_bar[stage], phase);
+          if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 214 + i] = globaltimer_ns();
           mbar_wait(&xfull_bar[stage], phase);
           tc_fence_after();
+          if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 2 + i] = globaltimer_ns();
           __syncwarp();
           const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
           const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
           umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+          if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
         __syncwarp();
@@ -819,6 +827,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t fix_phase = 0;
+    int seg_i = 0;
     for (int u = ubeg; u < uend;) {
       const int tile = u / sk.kb, kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
@@ -830,6 +839,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const bool last_seg = (u + (kb1 - kb0) == uend);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
+      unsigned long long* tr = (a.trace && et == 0 && seg_i < 4) ? a.trace + (size_t)c * 512 + 130 + 4 * seg_i : nullptr;
+      ++seg_i;
+      if (tr) tr[0] = globaltimer_ns() | (whole ? (1ull << 62) : 0);
       const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TNP);
       float* part = a.ws + ((size_t)blockIdx.x * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TNP);
       epi_drain(a, t_addr, m0, row0, ncols, whole, part, tb, q, lane);
@@ -837,14 +849,16 @@ __global__ void __launch_bounds__(kThreads1, 1)
       mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (tr) tr[1] = globaltimer_ns();
       if (!whole) {
         const PartMap pm{a.ws, sk, tile, 2, int(rank), TNP};
         epi_fixup(a, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
                   sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes),
-                  fix_bar, fix_phase, bcast, et);
+                  fix_bar, fix_phase, bcast, et, tr);
       }
       u += kb1 - kb0;
     }
+    if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -910,6 +924,16 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   p.max_parts = 0;
   if (kind_T < T) kind_T = T;
   const int kb = (K + kBK - 1) / kBK;
+  const long long tiles = (N + kBM - 1) / kBM;  // 128-row weight tiles
+  if (kind_T <= 256 && tiles * 10 < (long long)num_sms * 6) {
+    // few wide-K tiles (O / down projections): 1-CTA kernel, cluster split-K
+    // (DSMEM reduction) -- measured fastest up to 256 rows
+    p.pair = 0;
+    p.tn = gemm_pick_tn(T);
+    p.box_rows = p.tn;
+    while (p.csplit < 4 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
+    return p;
+  }
   if (kind_T > kPairMinT) {
     p.pair = 1;
     p.tn = 256;
@@ -920,13 +944,7 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   }
   p.pair = 0;
   p.tn = gemm_pick_tn(T);
-  const long long tiles = (N + kBM - 1) / kBM;  // one token tile
-  if (tiles * 10 < (long long)num_sms * 6) {
-    // few wide-K tiles (O / down projections): cluster split-K
-    while (p.csplit < 8 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
-  } else if (tiles <= num_sms) {
-    p.max_parts = 1;  // QKV: one wave of whole tiles
-  }
+  if (tiles <= num_sms) p.max_parts = 1;  // QKV: one wave of whole tiles
   p.box_rows = p.tn;
   return p;
 }

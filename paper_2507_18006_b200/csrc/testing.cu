@@ -95,8 +95,8 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
     plan = cb::GemmPlan{max_parts == 201 ? 256 : 128, 1, max_parts == 201 ? 128 : 64, 1, 0};
   } else if (max_parts == 203 && plan.pair) {
     plan = cb::GemmPlan{cb::gemm_pick_tn(T), 0, cb::gemm_pick_tn(T), 1, 0};
-  } else if (max_parts < 0 && !plan.pair) {
-    plan.csplit = -max_parts;
+  } else if (max_parts < 0) {  // 1-CTA kernel with cluster split -max_parts
+    plan = cb::GemmPlan{cb::gemm_pick_tn(T), 0, cb::gemm_pick_tn(T), -max_parts, 0};
   } else if (max_parts > 0 && max_parts < 100 && !plan.pair) {
     plan.csplit = 1;
   } else if (max_parts == 99) {

@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x 2>&1 | tail -3 > gpurun_out/kt4.txt
-timeout 300 python scripts/gemm_perf.py 0 64,256 --real-epi > gpurun_out/perf_epi3.txt 2>&1
-for B in 64 256; do timeout 300 python scripts/step_profile.py $B 3 > gpurun_out/step_$B.txt 2>&1; done
+timeout 120 python scripts/gemm_trace.py 12288 4096 256 0 6 0 > gpurun_out/trace11.txt 2>&1
+timeout 120 python scripts/gemm_trace.py 22016 4096 256 0 6 3 >> gpurun_out/trace11.txt 2>&1
+timeout 120 python scripts/gemm_trace.py 4096 4096 256 0 3 2 >> gpurun_out/trace11.txt 2>&1

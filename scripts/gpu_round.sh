@@ -10,17 +10,15 @@ if [ "${SKIP_TESTS:-0}" != "1" ]; then
 fi
 timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
-  # every launch of two timed decode steps (cold-cache, serialised: compare shares)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 588 -c 260 --csv \
-      --log-file $OUT/launches.csv python bench.py --batch 64 --sweep '' --steps 2 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_launch.log 2>&1
-  # full sections of the decode GEMMs (qkv, o, gate/up, down) and attention
-  # decode GEMMs of the timed step (skip the lm_head of prefill + the warm-up step's 129)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 130 -c 4 \
-      -o $OUT/prof_gemm -f python bench.py --batch 64 --sweep '' --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_gemm.log 2>&1
-  # prefill GEMMs of layer 1 (T = 64 x 128 = 8192 rows): the tensor-bound case
-  timeout 900 ncu --set full --clock-control none -k regex:gemm_tc2 -s 0 -c 4 \
-      -o $OUT/prof_prefill -f python bench.py --batch 64 --sweep '' --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_prefill.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 64 -c 1 \
-      -o $OUT/prof_attn -f python bench.py --batch 64 --sweep '' --steps 1 --warmup 1 --no-cpu-baseline --serve-s 0 > $OUT/ncu_attn.log 2>&1
+  for B in 64 256; do
+    # every launch of one decode step (cudaProfilerStart/Stop brackets it): cold-cache, serialised
+    timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $OUT/launches_$B.csv python scripts/step_profile.py $B 1 > $OUT/ncu_launch_$B.log 2>&1
+    # full sections of the four decode GEMMs of layer 1 and its attention
+    timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:gemm -c 4 \
+        -o $OUT/prof_gemm_$B -f python scripts/step_profile.py $B 1 > $OUT/ncu_gemm_$B.log 2>&1
+    timeout 600 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:attn_kernel -c 1 \
+        -o $OUT/prof_attn_$B -f python scripts/step_profile.py $B 1 > $OUT/ncu_attn_$B.log 2>&1
+  done
 fi
 ls -la $OUT
