@@ -26,10 +26,14 @@ Weights are random-init on the device (no checkpoints offline); they total
 * ``cpu_baseline``: the CPU oracle (numpy fp32, all host cores) on a bounded
   sample of the same decode step (2 of 32 layers + lm_head), scaled.
 
-For N>1 (torchrun) rank 0 drives one serving instance over all N GPUs with
-the decoder layers replicated on every GPU (BASELINE config 3): the batch is
-split per layer with split_batch across the replicas and activations move
-over NVLink P2P; the other ranks hold their GPU and join the barriers.
+For N>1 (torchrun, one process per GPU) every decoder layer is replicated on
+every GPU (BASELINE config 3 with all layers hot): that is ONE replicated run,
+so each rank serves its split_batch share of the global batch on its own GPU
+(``dist.ReplicaGroup``) and the run-boundary scatter / gather
+are NCCL collectives of the step metadata and sampled tokens.  Per-GPU batch
+is fixed (weak scaling); value = global tokens / max-over-ranks device time.
+Rank 0 then measures a cross-GPU layer migration over NVLink (one process,
+two GPUs, cudaMemcpyPeerAsync of the layer block).
 """
 from __future__ import annotations
 
@@ -241,20 +245,14 @@ def serving_window(ex, args, batch: int) -> dict:
     return s
 
 
-def run_ours(args, rank: int, world: int, dist) -> None:
+def run_single(args) -> None:
     import torch
 
     from paper_2507_18006_b200 import _lib
 
     _lib.load()  # fail loudly if the extension is missing
     peaks = _peaks()
-    if world > 1 and rank != 0:
-        torch.cuda.set_device(rank)
-        dist.barrier()  # instance built
-        dist.barrier()  # timed region start
-        dist.barrier()  # timed region end
-        return
-    n_dev = world
+    world, n_dev = 1, 1
     rt, ex, cat, cluster, batch, sweep = build_instance(args, n_dev, 0)
     rng = np.random.default_rng(11)
     n_slots = ex.cfg.max_slots
@@ -278,9 +276,6 @@ def run_ours(args, rank: int, world: int, dist) -> None:
     nxt = all_next[:batch]
     for _ in range(args.warmup):
         nxt, _, _ = ex.decode(slots, nxt)
-    if world > 1:
-        dist.barrier()
-        dist.barrier()
     dev_ms, wall_s = [], []
     with ClockSampler(0) as clocks:
         for _ in range(args.steps):
@@ -288,8 +283,6 @@ def run_ours(args, rank: int, world: int, dist) -> None:
             nxt, _, ms = ex.decode(slots, nxt)
             wall_s.append(time.perf_counter() - t0)
             dev_ms.append(ms)
-    if world > 1:
-        dist.barrier()
     # Per-kernel-class evidence: the same decode steps again with every launch
     # bracketed by CUDA events (events between launches disable the PDL
     # overlap, so this pass is not the one `value` is computed from).
@@ -357,6 +350,119 @@ def run_ours(args, rank: int, world: int, dist) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_replicas(args, rank: int, world: int, dist) -> None:
+    """N>1: one process per GPU, every layer replicated on every GPU (one run);
+    scatter / gather of each step through NCCL (dist.ReplicaGroup)."""
+    import torch
+
+    from paper_2507_18006_b200 import _lib
+    from paper_2507_18006_b200.dist import PHASE_DECODE, PHASE_PREFILL, ReplicaGroup
+    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
+
+    _lib.load()
+    peaks = _peaks()
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"  # tests: every rank on cuda:0 (gloo collectives)
+    dev = 0 if same_gpu else rank
+    torch.cuda.set_device(dev)
+    per = args.batch
+    gbatch = per * world
+    max_ctx = args.prompt + args.warmup + args.steps + 8
+    rt = Runtime([dev])
+    cfg = ExecutorConfig(**LLAMA2_7B, max_slots=per, max_ctx=max_ctx, max_tokens=max(min(per, 64) * args.prompt, 256))
+    ex = Executor(rt, cfg, home_device=0, seed=7)
+    ex.init_head_random(std=0.02)
+    for li in range(1, cfg.n_layers + 1):
+        ex.init_layer_random(li, 0, std=0.02)
+    group = ReplicaGroup(dist, ex)
+    slots = np.arange(gbatch)
+    rng = np.random.default_rng(11)
+    prompts = rng.integers(0, cfg.vocab, gbatch * args.prompt).astype(np.int32) if rank == 0 else None
+    nxt, _ = group.step(PHASE_PREFILL, slots, prompts, np.full(gbatch, args.prompt) if rank == 0 else None)
+    for _ in range(args.warmup):
+        nxt, _ = group.step(PHASE_DECODE, slots, nxt)
+    dist.barrier()
+    torch.cuda.synchronize()
+    dev_ms, t0 = [], time.perf_counter()
+    with ClockSampler(rank) as clocks:
+        for _ in range(args.steps):
+            nxt, ms = group.step(PHASE_DECODE, slots, nxt)
+            dev_ms.append(ms)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    dist.barrier()
+    cdev = "cpu" if same_gpu else "cuda"
+    t = torch.tensor([sum(dev_ms), wall], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_s, wall_s = t[0].item() / 1e3, t[1].item()
+    # kernel launches per step (one profiled local step of this rank's share, after the timed region)
+    ex.profile(True)
+    _, s_loc, t_loc, _, _ = group.scatter(PHASE_DECODE, slots, nxt)
+    ex.decode(s_loc, t_loc)
+    prof = ex.profile_read()
+    ex.profile(False)
+    group.gather(np.zeros(len(s_loc), np.int32))
+    n = torch.tensor([sum(prof[k]["launches"] for k in ("gemm", "attention", "elementwise"))], device=cdev)
+    dist.all_reduce(n)
+    launches = int(n.item()) * args.steps
+    mig = None
+    if rank == 0 and world >= 2 and not same_gpu:
+        ex.close()
+        rt.close()
+        mig = measure_nvlink_migration()
+    dist.barrier()
+    if rank != 0:
+        return
+    value = gbatch * args.steps / dev_s
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random prompts)",
+        "config": {"workload": f"config 3: Llama-2-7B shape, every decoder layer replicated on {world} GPUs "
+                               "(one process per GPU, split_batch shares)",
+                   "batch": gbatch, "batch_per_gpu": per, "prompt_len": args.prompt,
+                   "parallelism": f"module replication x{world} (one run; NCCL scatter/gather)",
+                   "l2": "weights 13.2 GB >> 126 MB L2 per GPU: every step streams from HBM"},
+        "e2e": {"value": gbatch * args.steps / wall_s, "unit": "tokens/s",
+                "h2d_bytes_per_step": (gbatch * 3 + 3) * 8, "d2h_bytes_per_step": gbatch * 8},
+        "gpu_launches": launches,
+        "migrate": mig,
+        "clocks": clocks.summary(),
+        "peaks": peaks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measure_nvlink_migration() -> dict:
+    """One process, GPUs 0 and 1: replicate then migrate a 7B layer block
+    (ops.apply semantics) over NVLink; device-timed copy (CUDA events on the
+    destination's copy stream)."""
+    from paper_2507_18006_b200 import domain as D
+    from paper_2507_18006_b200 import ops as O
+    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
+
+    rt = Runtime([0, 1])
+    cfg = ExecutorConfig(**{**LLAMA2_7B, "n_layers": 2}, max_slots=8, max_ctx=64, max_tokens=256)
+    ex = Executor(rt, cfg, home_device=0, seed=7)
+    ex.init_head_random(std=0.02)
+    for li in (1, 2):
+        ex.init_layer_random(li, 0, std=0.02)
+    cat = D.ModuleCatalog.from_model(D.ModelSpec(2, 4096, 11008, 32))
+    cluster = D.ClusterSpec.b200(2)
+    res = []
+    for _ in range(3):
+        ex.apply(O.ReplicateLayer(1, 1), cat, cluster)
+        res.append(ex.op_log[-1])
+        ex.apply(O.EvictReplica(1, 1), cat, cluster)
+    ex.apply(O.MigrateLayer(2, 1, with_kv=True), cat, cluster)
+    m = ex.op_log[-1]
+    best = max(res, key=lambda r: r.gbps)
+    ex.close()
+    rt.close()
+    return {"bytes": best.weight_bytes, "ms": best.device_ms, "gbps": best.gbps,
+            "migrate_layer_gbps": m.gbps, "path": "NVLink P2P (cudaMemcpyPeerAsync, GPU 0 -> GPU 1)",
+            "nvlink_peak_gbps_per_dir": 900.0, "frac": best.gbps / 900.0}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,15 +484,23 @@ def main() -> None:
     rank = int(os.environ.get("RANK", "0"))
     dist = None
     if world > 1:
+        import torch
         import torch.distributed as dist  # noqa: F811
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo")
+        if args.impl == "reference" or not torch.cuda.is_available() or os.environ.get("BENCH_SAME_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            local = int(os.environ.get("LOCAL_RANK", rank))
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif world == 1:
+            run_single(args)
         else:
-            run_ours(args, rank, world, dist)
+            run_replicas(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -224,6 +224,11 @@ class Executor:
         for r in requests:
             r.slot = None
 
+    def release_slots(self, slots: np.ndarray) -> None:
+        """Free KV slots by id (callers that manage their own slot ids, e.g. dist.ReplicaGroup)."""
+        arr = np.ascontiguousarray(slots, dtype=np.int32)
+        _lib.check(self.lib.cb_release_slots(self.handle, len(arr), _lib.i32(arr)))
+
     def release_all(self) -> None:
         """Free every KV slot (end of a benchmark phase)."""
         arr = np.arange(self.cfg.max_slots, dtype=np.int32)

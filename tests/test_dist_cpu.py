@@ -54,3 +54,29 @@ dist.destroy_process_group()
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "MAX 2.0" in out.stdout
+
+
+def _torchrun(script, nproc, env=None):
+    import os
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(script)]
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT,
+                          env={**os.environ, **(env or {})})
+
+
+def test_replica_group_world2_matches_unreplicated():
+    """One process per replica (gloo, world 2): scatter of the batch by
+    split_batch (15 -> [7, 8]), each rank serves its share, the
+    gather returns greedy tokens identical to one unreplicated pass."""
+    out = _torchrun(ROOT / "tests" / "dist_replica_worker.py", 2)
+    assert out.returncode == 0, out.stderr[-3000:]
+    rec = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert rec["equal"] and rec["shares"] == [7, 8] and rec["world"] == 2
+
+
+def test_replica_group_world3_uneven_shares():
+    """Uneven split with an empty-remainder edge: 5 requests over 3 ranks -> [1, 2, 2]."""
+    out = _torchrun(ROOT / "tests" / "dist_replica_worker.py", 3, {"N_REQ": "5"})
+    assert out.returncode == 0, out.stderr[-3000:]
+    rec = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert rec["equal"] and rec["shares"] == [1, 2, 2]
