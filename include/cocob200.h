@@ -170,8 +170,11 @@ int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st)
 /* MigrateLayer (ops.py:213-228): move the original to dst; with_kv moves the
  * layer's KV too, otherwise KV stays resident on its current device. */
 int cb_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, cb_op_stats* st);
-/* MigrateSubModule (ops.py:230-251).  KV_CACHE is supported; projection kinds
- * return CB_ENOTSUP in this version. */
+/* MigrateSubModule (ops.py:230-251).  KV_CACHE moves the layer's KV rows (the
+ * attention core then runs on that device); a projection kind (Q/K/V/O, GATE,
+ * UP, DOWN) or SELF_ATTENTION copies the module's weights ([out, in] layout) to
+ * dst, after which that projection's GEMM runs there with its input rows (and
+ * the fp32 residual rows for O / DOWN) hopping to dst and its output rows back. */
 int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, cb_op_stats* st);
 /* EvictReplica (ops.py:253-258): drop a non-original copy; KV rows it held move
  * back to the original first. */

@@ -3,6 +3,8 @@
 //
 // Each is HBM/L2-bound (SURVEY.md §8(d) "RMSNorm/RoPE, KV append: HBM"):
 // 128-bit vector accesses, one warp per row so every row is read once.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -30,6 +32,37 @@ cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x,
                          cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
   return launch_pdl(embed_kernel, dim3((T + 3) / 4), dim3(128), 0, st, table, tokens, x, T, d, row_off);
+}
+
+// ---------------------------------------------------------------- SwiGLU combine
+// act[r] = bf16(silu(gate[r]) * up[r]) in place over act, rows [row_off, row_off + T):
+// the gate/up pair of a layer whose FFN_PROJ_GATE / FFN_PROJ_UP was migrated
+// to another device (MigrateSubModule, ops.py:230-251) runs as two GEMMs, so the
+// fused SwiGLU epilogue is replaced by this pass (same silu formula).
+__global__ void swiglu_kernel(const uint16_t* __restrict__ gate, uint16_t* __restrict__ act, size_t n8) {
+  pdl_trigger();
+  pdl_wait();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 g = reinterpret_cast<const uint4*>(gate)[i];
+    uint4 u = reinterpret_cast<uint4*>(act)[i];
+    const uint32_t gw[4] = {g.x, g.y, g.z, g.w};
+    uint32_t* uw = &u.x;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float g0 = bf16_lo(gw[j]), g1 = bf16_hi(gw[j]);
+      const float u0 = bf16_lo(uw[j]), u1 = bf16_hi(uw[j]);
+      uw[j] = pack_bf16x2(__fdividef(g0, 1.0f + __expf(-g0)) * u0, __fdividef(g1, 1.0f + __expf(-g1)) * u1);
+    }
+    reinterpret_cast<uint4*>(act)[i] = u;
+  }
+}
+
+cudaError_t swiglu_launch(const uint16_t* gate, uint16_t* act, int T, int d_ff, int row_off, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  const size_t off = size_t(row_off) * d_ff;
+  const size_t n8 = size_t(T) * d_ff / 8;
+  const unsigned blocks = unsigned(std::min<size_t>((n8 + 255) / 256, 148 * 8));
+  return launch_pdl(swiglu_kernel, dim3(blocks), dim3(256), 0, st, gate + off, act + off, n8);
 }
 
 // ---------------------------------------------------------------- RMSNorm

@@ -89,17 +89,29 @@ struct LayerCopy {
   CUtensorMap m_qkv, m_o, m_gu, m_d;
 };
 
+// A sub-module moved off its layer by MigrateSubModule (ops.py:230-251): its
+// weights in canonical [out, in] layout on `dev`.  Index = CB_* kind id
+// (Q, K, V, O, SELF_ATTENTION = [wqkv | wo], GATE, UP, DOWN).
+struct ModCopy {
+  int dev = -1;
+  uint8_t* buf = nullptr;
+};
+constexpr int kModKinds = CB_FFN_PROJ_DOWN + 1;
+
 struct LayerState {
   std::vector<LayerCopy> reps;      // original first (Replica order, domain.py:306-317)
   int kv_override = -1;             // device holding KV when overridden, else -1
   std::map<int, uint16_t*> kv;      // device -> KV block
   std::vector<int> owner;           // slot -> device holding that slot's KV (-1 none)
+  ModCopy mod[kModKinds];           // projection / self-attention overrides
+  bool proj_ov = false;             // any entry of mod[] in use
 };
 
 struct Workspace {
   bool ready = false;
   float* x = nullptr;
   uint16_t *h = nullptr, *hl = nullptr, *qkv = nullptr, *att = nullptr, *act = nullptr;
+  uint16_t* gbuf = nullptr;  // [max_tokens][d_ff] gate output when gate / up run as separate GEMMs
   float* logits = nullptr;
   int32_t* meta = nullptr;  // [tokens | row_slot | row_pos | gather]
   int32_t* next = nullptr;
@@ -415,29 +427,117 @@ int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& t
   return CB_OK;
 }
 
-int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
-                      const std::vector<int>& row_pos) {
+// ---- sub-module (projection) overrides: where each projection's weights live
+struct ProjView {
+  int dev;
+  const uint8_t* base;
+  uint64_t row_stride;  // elements
+  int rows, k;
+  int col0;  // column offset inside the fused qkv output (Q, K, V)
+};
+
+size_t block_offset(cb_model* m, int kind) {
+  const size_t dm = m->d.d_model;
+  switch (kind) {
+    case CB_ATTN_PROJ_Q: return m->off_qkv;
+    case CB_ATTN_PROJ_K: return m->off_qkv + size_t(m->q_n) * dm * 2;
+    case CB_ATTN_PROJ_V: return m->off_qkv + size_t(m->q_n + m->kv_n) * dm * 2;
+    case CB_ATTN_PROJ_O: return m->off_o;
+    case CB_SELF_ATTENTION: return m->off_qkv;
+    case CB_FFN_PROJ_GATE: return m->off_gu;
+    case CB_FFN_PROJ_UP: return m->off_gu + dm * 2;  // odd rows of the interleaved gate/up block
+    case CB_FFN_PROJ_DOWN: return m->off_d;
+  }
+  return 0;
+}
+
+ProjView proj_view(cb_model* m, const LayerState& L, int kind) {
   const cb_model_desc& d = m->d;
-  const LayerCopy& W = L.reps[s.rep];
+  ProjView v{};
+  v.col0 = 0;
+  switch (kind) {
+    case CB_ATTN_PROJ_Q: v.rows = m->q_n; v.k = d.d_model; break;
+    case CB_ATTN_PROJ_K: v.rows = m->kv_n; v.k = d.d_model; v.col0 = m->q_n; break;
+    case CB_ATTN_PROJ_V: v.rows = m->kv_n; v.k = d.d_model; v.col0 = m->q_n + m->kv_n; break;
+    case CB_ATTN_PROJ_O: v.rows = d.d_model; v.k = m->q_n; break;
+    case CB_FFN_PROJ_GATE:
+    case CB_FFN_PROJ_UP: v.rows = d.d_ff; v.k = d.d_model; break;
+    case CB_FFN_PROJ_DOWN: v.rows = d.d_model; v.k = d.d_ff; break;
+  }
+  const ModCopy& own = L.mod[kind];
+  const ModCopy& sa = L.mod[CB_SELF_ATTENTION];
+  if (own.dev >= 0) {
+    v.dev = own.dev;
+    v.base = own.buf;
+    v.row_stride = uint64_t(v.k);
+  } else if (kind <= CB_ATTN_PROJ_O && sa.dev >= 0) {
+    v.dev = sa.dev;  // SELF_ATTENTION copy = block[off_qkv, off_o + |wo|)
+    v.base = sa.buf + (block_offset(m, kind) - m->off_qkv);
+    v.row_stride = uint64_t(v.k);
+  } else {
+    v.dev = L.reps[0].dev;
+    v.base = L.reps[0].block + block_offset(m, kind);
+    v.row_stride = uint64_t(v.k) * ((kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP) ? 2 : 1);
+  }
+  return v;
+}
+
+int ensure_gbuf(cb_model* m, int dev) {
+  Workspace& w = m->ws[dev];
+  if (w.gbuf) return CB_OK;
+  return dev_alloc(devctx(m, dev), (void**)&w.gbuf, size_t(m->d.max_tokens) * m->d.d_ff * 2);
+}
+
+// rows [r0, r0 + T) of a row-major buffer, device src -> dst (pulled on dst's stream)
+int hop_rows(cb_model* m, int src, int dst, const void* sbase, void* dbase, size_t row_bytes, int r0, int T) {
+  if (src == dst || T <= 0) return CB_OK;
+  DeviceCtx& dd = devctx(m, dst);
+  DeviceCtx& sd = devctx(m, src);
+  CB_TRY(depend(dd, sd));
+  CB_TRY(use(dd));
+  ProfScope ps(m, dst, CB_KCLASS_COPY, dd.compute, double(T) * row_bytes);
+  CB_CUDA(cudaMemcpyPeerAsync(static_cast<uint8_t*>(dbase) + size_t(r0) * row_bytes, dd.ordinal,
+                              static_cast<const uint8_t*>(sbase) + size_t(r0) * row_bytes, sd.ordinal,
+                              size_t(T) * row_bytes, dd.compute));
+  return CB_OK;
+}
+
+// columns [c0, c0 + nc) (bf16) of rows [r0, r0 + T) of a [rows][pitch] buffer, src -> dst
+int hop_cols(cb_model* m, int src, int dst, const uint16_t* sbase, uint16_t* dbase, int pitch, int c0, int nc, int r0,
+             int T) {
+  if (src == dst || T <= 0) return CB_OK;
+  DeviceCtx& dd = devctx(m, dst);
+  CB_TRY(depend(dd, devctx(m, src)));
+  CB_TRY(use(dd));
+  ProfScope ps(m, dst, CB_KCLASS_COPY, dd.compute, double(T) * nc * 2);
+  const size_t off = size_t(r0) * pitch + c0;
+  CB_CUDA(cudaMemcpy2DAsync(dbase + off, size_t(pitch) * 2, sbase + off, size_t(pitch) * 2, size_t(nc) * 2, T,
+                            cudaMemcpyDefault, dd.compute));
+  return CB_OK;
+}
+
+int proj_gemm(cb_model* m, const ProjView& v, const CUtensorMap* xmaps, int T, int r0, int epi, void* out,
+              long long ldo) {
+  CUtensorMap wm;
+  CB_TRY(use(devctx(m, v.dev)));
+  if (cb::make_kmajor_map(&wm, v.base, uint64_t(v.rows), uint64_t(v.k), v.row_stride, 128) != 0)
+    return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed for a migrated projection");
+  return gemm(m, v.dev, wm, xmaps, v.rows, v.k, T, r0, epi, out, ldo);
+}
+
+// RoPE + KV append + attention for the segment's rows: qkv on `dev` -> att on `dev`.
+// Runs where the rows' KV lives: on the replica itself for a replicated layer,
+// on the KV device (MigrateSubModule KV_CACHE / MigrateLayer without KV) otherwise.
+int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
+                   const std::vector<int>& row_pos) {
+  const cb_model_desc& d = m->d;
   const int dev = s.dev;
   const int T = s.r1 - s.r0;
   DeviceCtx& dc = devctx(m, dev);
   Workspace& ws = m->ws[dev];
-  CB_TRY(use(dc));
-  const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
-  const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
-  const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
-  {
-    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
-    CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
-  }
-  CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n));
-
-  // attention runs where the rows' KV lives: on the replica itself for a
-  // replicated layer, on the KV device (MigrateSubModule KV_CACHE /
-  // MigrateLayer without KV) otherwise.
   const int ad = L.reps.size() > 1 ? dev : kv_device(L);
   DeviceCtx& ac = devctx(m, ad);
+  CB_TRY(ensure_ws(m, ad));
   Workspace& wa = m->ws[ad];
   const size_t qkv_row = size_t(m->qkv_n) * 2, att_row = size_t(m->q_n) * 2;
   if (ad != dev) {
@@ -507,6 +607,133 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
                                 reinterpret_cast<uint8_t*>(wa.att) + s.r0 * att_row, ac.ordinal, T * att_row,
                                 dc.compute));
   }
+  return CB_OK;
+}
+
+// A projection that runs on another device: its input rows hop there, the
+// fp32 residual rows too for the += epilogues (O, down), and the output rows
+// hop back -- the "module on another device" of PAPER.md:182-189.
+int remote_resid_proj(cb_model* m, const ProjView& v, int dev, const uint16_t* in_local, size_t in_row_bytes,
+                      uint16_t* in_remote, const CUtensorMap* xmaps_remote, int T, int r0) {
+  const size_t x_row = size_t(m->d.d_model) * 4;
+  CB_TRY(hop_rows(m, dev, v.dev, in_local, in_remote, in_row_bytes, r0, T));
+  CB_TRY(hop_rows(m, dev, v.dev, m->ws[dev].x, m->ws[v.dev].x, x_row, r0, T));
+  CB_TRY(proj_gemm(m, v, xmaps_remote, T, r0, cb::EPI_RESID, m->ws[v.dev].x, m->d.d_model));
+  return hop_rows(m, v.dev, dev, m->ws[v.dev].x, m->ws[dev].x, x_row, r0, T);
+}
+
+// Decoder layer with migrated projections (the layer is not replicated: the
+// registry forbids overrides on replicated layers, domain.py:339-340).
+int run_layer_overridden(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
+                         const std::vector<int>& row_pos) {
+  const cb_model_desc& d = m->d;
+  const LayerCopy& W = L.reps[s.rep];
+  const int dev = s.dev;
+  const int T = s.r1 - s.r0;
+  DeviceCtx& dc = devctx(m, dev);
+  Workspace& ws = m->ws[dev];
+  const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
+  const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
+  const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
+  const size_t h_row = size_t(d.d_model) * 2;
+  CB_TRY(use(dc));
+  {
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
+    CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  }
+  // ---- Q, K, V: each projection where its weights live, into its column slice of qkv
+  const bool qkv_moved = L.mod[CB_SELF_ATTENTION].dev >= 0 || L.mod[CB_ATTN_PROJ_Q].dev >= 0 ||
+                         L.mod[CB_ATTN_PROJ_K].dev >= 0 || L.mod[CB_ATTN_PROJ_V].dev >= 0;
+  if (!qkv_moved) {
+    CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n));
+  } else {
+    std::vector<int> h_at{dev};
+    for (int kind : {CB_ATTN_PROJ_Q, CB_ATTN_PROJ_K, CB_ATTN_PROJ_V}) {
+      const ProjView v = proj_view(m, L, kind);
+      CB_TRY(ensure_ws(m, v.dev));
+      Workspace& we = m->ws[v.dev];
+      if (std::find(h_at.begin(), h_at.end(), v.dev) == h_at.end()) {
+        CB_TRY(hop_rows(m, dev, v.dev, ws.h, we.h, h_row, s.r0, T));
+        h_at.push_back(v.dev);
+      }
+      CB_TRY(proj_gemm(m, v, we.map_h, T, s.r0, cb::EPI_BF16, we.qkv + v.col0, m->qkv_n));
+      CB_TRY(hop_cols(m, v.dev, dev, we.qkv, ws.qkv, m->qkv_n, v.col0, v.rows, s.r0, T));
+    }
+  }
+  CB_TRY(attention_part(m, L, s, seq_slot, row_pos));
+  // ---- O (+= residual)
+  {
+    const ProjView v = proj_view(m, L, CB_ATTN_PROJ_O);
+    if (v.dev == dev) {
+      CB_TRY(proj_gemm(m, v, ws.map_att, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
+    } else {
+      CB_TRY(ensure_ws(m, v.dev));
+      CB_TRY(remote_resid_proj(m, v, dev, ws.att, size_t(m->q_n) * 2, m->ws[v.dev].att, m->ws[v.dev].map_att, T,
+                               s.r0));
+    }
+  }
+  CB_TRY(use(dc));
+  {
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
+    CB_CUDA(cb::rmsnorm_launch(ws.x, fn, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  }
+  // ---- gate / up: fused SwiGLU GEMM unless one of them moved
+  if (L.mod[CB_FFN_PROJ_GATE].dev < 0 && L.mod[CB_FFN_PROJ_UP].dev < 0) {
+    CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff));
+  } else {
+    CB_TRY(ensure_gbuf(m, dev));
+    std::vector<int> h_at{dev};
+    for (int kind : {CB_FFN_PROJ_GATE, CB_FFN_PROJ_UP}) {
+      const ProjView v = proj_view(m, L, kind);
+      CB_TRY(ensure_ws(m, v.dev));
+      CB_TRY(ensure_gbuf(m, v.dev));
+      Workspace& we = m->ws[v.dev];
+      if (std::find(h_at.begin(), h_at.end(), v.dev) == h_at.end()) {
+        CB_TRY(hop_rows(m, dev, v.dev, ws.h, we.h, h_row, s.r0, T));
+        h_at.push_back(v.dev);
+      }
+      uint16_t* out_e = kind == CB_FFN_PROJ_GATE ? we.gbuf : we.act;
+      uint16_t* out_d = kind == CB_FFN_PROJ_GATE ? ws.gbuf : ws.act;
+      CB_TRY(proj_gemm(m, v, we.map_h, T, s.r0, cb::EPI_BF16, out_e, d.d_ff));
+      CB_TRY(hop_rows(m, v.dev, dev, out_e, out_d, size_t(d.d_ff) * 2, s.r0, T));
+    }
+    CB_TRY(use(dc));
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, double(T) * d.d_ff * 6);
+    CB_CUDA(cb::swiglu_launch(ws.gbuf, ws.act, T, d.d_ff, s.r0, dc.compute));
+  }
+  // ---- down (+= residual)
+  {
+    const ProjView v = proj_view(m, L, CB_FFN_PROJ_DOWN);
+    if (v.dev == dev) {
+      CB_TRY(proj_gemm(m, v, ws.map_act, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
+    } else {
+      CB_TRY(ensure_ws(m, v.dev));
+      CB_TRY(remote_resid_proj(m, v, dev, ws.act, size_t(d.d_ff) * 2, m->ws[v.dev].act, m->ws[v.dev].map_act, T,
+                               s.r0));
+    }
+  }
+  return CB_OK;
+}
+
+int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
+                      const std::vector<int>& row_pos) {
+  if (L.proj_ov) return run_layer_overridden(m, L, s, seq_slot, row_pos);
+  const cb_model_desc& d = m->d;
+  const LayerCopy& W = L.reps[s.rep];
+  const int dev = s.dev;
+  const int T = s.r1 - s.r0;
+  DeviceCtx& dc = devctx(m, dev);
+  Workspace& ws = m->ws[dev];
+  CB_TRY(use(dc));
+  const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
+  const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
+  const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
+  {
+    ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
+    CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
+  }
+  CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n));
+  CB_TRY(attention_part(m, L, s, seq_slot, row_pos));
   CB_TRY(use(dc));
   CB_TRY(gemm(m, dev, W.m_o, ws.map_att, d.d_model, m->q_n, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
   {
@@ -554,6 +781,8 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   for (auto& L : m->layers) {
     for (auto& c : L.reps) devs.push_back(c.dev);
     devs.push_back(kv_device(L));
+    for (auto& mc : L.mod)
+      if (mc.dev >= 0) devs.push_back(mc.dev);
   }
   std::sort(devs.begin(), devs.end());
   devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
@@ -688,6 +917,57 @@ void sync_all(cb_model* m) {
     cudaStreamSynchronize(dc.compute);
     cudaStreamSynchronize(dc.copy);
   }
+}
+
+// MigrateSubModule of a projection / SELF_ATTENTION (ops.py:230-251): copy the
+// module's weights (canonical [out, in] layout) to `dst`; the layer's kernels
+// then run that projection there with activation hops (run_layer_overridden).
+// The layer block keeps its bytes (it is one allocation); the registry does
+// the reference's memory accounting (device_usage, domain.py:481-535).
+int migrate_projection(cb_model* m, int layer, int kind, int dst, cb_op_stats* st) {
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
+  const bool attn_part = kind <= CB_ATTN_PROJ_O;
+  if ((kind == CB_SELF_ATTENTION && (L.mod[0].dev >= 0 || L.mod[1].dev >= 0 || L.mod[2].dev >= 0 ||
+                                     L.mod[3].dev >= 0)) ||
+      (attn_part && L.mod[CB_SELF_ATTENTION].dev >= 0))
+    return fail(CB_EINVAL, "projection override conflicts with a self_attention override (domain.py:298-303)");
+  const uint64_t bytes = cb_module_bytes(m, kind);
+  ModCopy& mc = L.mod[kind];
+  ModCopy nc;
+  nc.dev = dst;
+  uint64_t shortfall = 0;
+  int r = dev_alloc(devctx(m, dst), (void**)&nc.buf, bytes, &shortfall);
+  if (r != CB_OK) {
+    if (st) st->shortfall_bytes = shortfall;
+    return r;
+  }
+  CB_TRY(ensure_ws(m, dst));
+  sync_all(m);
+  DeviceCtx& dc = devctx(m, dst);
+  CB_TRY(timed_begin(dc));
+  CB_TRY(use(dc));
+  if (mc.dev >= 0) {  // already moved once: copy from the current override
+    CB_CUDA(cudaMemcpyPeerAsync(nc.buf, dc.ordinal, mc.buf, devctx(m, mc.dev).ordinal, bytes, dc.copy));
+  } else {
+    const LayerCopy& src = L.reps[0];
+    const uint8_t* from = src.block + block_offset(m, kind);
+    if (kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP) {  // every other row of the interleaved block
+      const size_t row = size_t(m->d.d_model) * 2;
+      CB_CUDA(cudaMemcpy2DAsync(nc.buf, row, from, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
+    } else {
+      CB_CUDA(cudaMemcpyPeerAsync(nc.buf, dc.ordinal, from, devctx(m, src.dev).ordinal, bytes, dc.copy));
+    }
+  }
+  CB_TRY(timed_end(dc, st));
+  if (st) st->weight_bytes = bytes;
+  if (mc.dev >= 0) dev_free(m, mc.dev, mc.buf);
+  mc = nc;
+  L.proj_ov = false;
+  for (const ModCopy& x : L.mod)
+    if (x.dev >= 0) L.proj_ov = true;
+  return CB_OK;
 }
 
 }  // namespace
@@ -838,10 +1118,12 @@ int cb_model_destroy(cb_model* m) {
   for (auto& L : m->layers) {
     for (auto& c : L.reps) dev_free(m, c.dev, c.block);
     for (auto& kv : L.kv) dev_free(m, kv.first, kv.second);
+    for (auto& mc : L.mod) dev_free(m, mc.dev, mc.buf);
   }
   for (auto& kv : m->ws) {
     Workspace& w = kv.second;
-    void* ptrs[] = {w.x, w.h, w.hl, w.qkv, w.att, w.act, w.logits, w.meta, w.next, w.gemm_ws, w.gemm_cnt, w.attn_ws, w.rope};
+    void* ptrs[] = {w.x, w.h, w.hl, w.qkv, w.att, w.act, w.gbuf, w.logits, w.meta, w.next, w.gemm_ws, w.gemm_cnt,
+                    w.attn_ws, w.rope};
     for (void* p : ptrs) dev_free(m, kv.first, p);
   }
   dev_free(m, m->home, m->embed);
@@ -952,13 +1234,19 @@ int cb_module_read(cb_model* m, int32_t layer, int32_t dev, int32_t kind, void* 
   if (!m || !dst) return fail(CB_EINVAL, "null argument");
   CB_TRY(check_layer(m, layer));
   LayerState& L = m->layers[layer - 1];
+  const uint64_t want = cb_module_bytes(m, kind);
+  if (kind == CB_KV_CACHE || want == 0) return fail(CB_EINVAL, "kind not readable here (use cb_kv_read)");
+  if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
+  if (kind >= 0 && kind < kModKinds && L.mod[kind].dev >= 0 && L.mod[kind].dev == dev) {  // migrated sub-module
+    sync_all(m);
+    CB_TRY(use(devctx(m, dev)));
+    CB_CUDA(cudaMemcpy(dst, L.mod[kind].buf, want, cudaMemcpyDeviceToHost));
+    return CB_OK;
+  }
   const LayerCopy* c = nullptr;
   for (auto& r : L.reps)
     if (r.dev == dev) c = &r;
   if (!c) return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no copy on device " + std::to_string(dev));
-  const uint64_t want = cb_module_bytes(m, kind);
-  if (kind == CB_KV_CACHE || want == 0) return fail(CB_EINVAL, "kind not readable here (use cb_kv_read)");
-  if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
   CB_TRY(use(devctx(m, dev)));
   sync_all(m);
   const size_t dm = m->d.d_model, ff = m->d.d_ff;
@@ -1116,7 +1404,7 @@ int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st)
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
   for (auto& c : L.reps)
     if (c.dev == dst) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
-  if (L.kv_override >= 0) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
+  if (L.kv_override >= 0 || L.proj_ov) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
   LayerCopy c;
   c.dev = dst;
   uint64_t shortfall = 0;
@@ -1201,7 +1489,8 @@ int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, 
   CB_TRY(check_layer(m, layer));
   CB_TRY(check_dev(m, dst));
   if (kind == CB_DECODER_LAYER) return fail(CB_EINVAL, "whole layers move via MigrateLayer");
-  if (kind != CB_KV_CACHE) return fail(CB_ENOTSUP, "projection / attention sub-module migration not supported yet");
+  if (kind < 0 || kind > CB_KV_CACHE) return fail(CB_EINVAL, "unknown module kind");
+  if (kind != CB_KV_CACHE) return migrate_projection(m, layer, kind, dst, st);
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
   if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");

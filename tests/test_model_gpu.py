@@ -298,3 +298,35 @@ def test_gqa_sharded_layers_match_oracle(cuda):
     assert ex.module_bytes("kv_cache") == 2 * 2 * 64 * 2  # 2 x Hkv x hd x bf16
     ex.close()
     rt.close()
+
+
+def test_projection_submodule_migration_matches_oracle(runtime, confident):
+    """MigrateSubModule of projections / self_attention (ops.py:230-251; the
+    compute-bound relief path of the reference's scale-down, autoscaler.py:407-419):
+    the moved weights are byte-identical on the destination, and the layer --
+    now running those projections on the other device with activation hops --
+    still produces the oracle's greedy tokens and logits within 2e-2."""
+    prompts = config1_prompts()
+    ex = Executor(runtime, _tiny_cfg())
+    ex.load_model(confident, device_of_layer=0)
+    cat, cl = _catalog_cluster()
+    moves = [(1, D.ModuleKind.FFN_PROJ_GATE), (1, D.ModuleKind.ATTN_PROJ_O), (2, D.ModuleKind.ATTN_PROJ_Q),
+             (2, D.ModuleKind.FFN_PROJ_DOWN), (3, D.ModuleKind.SELF_ATTENTION), (4, D.ModuleKind.FFN_PROJ_UP),
+             (4, D.ModuleKind.ATTN_PROJ_V)]
+    for layer, kind in moves:
+        before = ex.read_module(layer, 0, kind)
+        ex.apply(O.MigrateSubModule(layer, kind, 1), cat, cl)
+        assert np.array_equal(ex.read_module(layer, 1, kind), before), (layer, kind)
+        assert ex.op_log[-1].weight_bytes == before.nbytes
+    assert ex.placement.override_device(2, D.ModuleKind.ATTN_PROJ_Q) == 1
+    got, logits = _greedy_gpu(ex, prompts, 8)
+    ref, ref_logits = greedy_generate(OracleModel(TINY, confident, 64), prompts, 8)
+    assert np.array_equal(got, ref)
+    assert max(np.abs(a - b).max() for a, b in zip(logits, ref_logits)) <= LOGIT_TOL
+    # a second move of the same module (device 1 -> 0) keeps the bytes
+    before = ex.read_module(2, 1, D.ModuleKind.ATTN_PROJ_Q)
+    ex.apply(O.MigrateSubModule(2, D.ModuleKind.ATTN_PROJ_Q, 0), cat, cl)
+    assert np.array_equal(ex.read_module(2, 0, D.ModuleKind.ATTN_PROJ_Q), before)
+    with pytest.raises(O.OpError):  # replicated layers cannot carry overrides (domain.py:339-340)
+        ex.apply(O.ReplicateLayer(1, 1), cat, cl)
+    ex.close()
