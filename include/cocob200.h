@@ -180,6 +180,12 @@ int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, 
  * back to the original first. */
 int cb_evict_replica(cb_model* m, int32_t layer, int32_t device, cb_op_stats* st);
 
+/* Phase-3 KV offload (autoscaler.py:568-583 PerformanceReduction): move the
+ * layer's KV blocks to (to_host=1) or back from (0) mapped pinned host memory.
+ * Attention reads an offloaded block in place (zero-copy); kv_bytes = live KV moved. */
+int cb_kv_offload(cb_model* m, int32_t layer, int32_t to_host, cb_op_stats* st);
+int cb_kv_offloaded(cb_model* m, int32_t layer, int32_t* offloaded_out);
+
 /* ---- live per-kernel profiling (evidence for the roofline numbers) ----------
  * When enabled, every launch of the executor is bracketed by CUDA events on the
  * stream it is launched on; after each step the elapsed times are added to

@@ -107,6 +107,8 @@ _SIGS = {
     "cb_migrate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_migrate_submodule": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_evict_replica": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
+    "cb_kv_offload": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
+    "cb_kv_offloaded": (C.c_int, [_P, C.c_int32, _I32P]),
     "cb_profile": (C.c_int, [_P, C.c_int32]),
     "cb_profile_read": (C.c_int, [_P, C.c_int32, C.POINTER(KStat)]),
     # kernel-level test entry points (include/cocob200_testing.h)

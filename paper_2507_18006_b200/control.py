@@ -106,6 +106,7 @@ class ReferenceController:
         self.cfg = cfg or A.ControllerConfig()
         self.params = params or self.ms.SpeedupParams()
         self.log: list = []
+        self.bs_cap: int | None = None  # last Phase-3 batch cap decided
 
     def view(self, bs: int, kv_tokens: float = 0.0, violation_rate: float = 0.0, busy: dict | None = None,
              mean_prompt_len: float = 0.0, mean_gen_len: float = 0.0, offload_fraction: float = 0.0):
@@ -127,8 +128,15 @@ class ReferenceController:
         done = []
         for phased in decision.ops:
             op = from_ref_op(phased.op)
+            if type(op).__name__ == "PerformanceReduction":
+                # Phase 3: the batch cap is the serving loop's (``self.bs_cap``); the
+                # KV offload fraction is applied physically (host-resident KV blocks)
+                self.bs_cap = op.new_bs
+                if op.new_offload_fraction != self.ex.kv_offload_fraction:
+                    self.ex.set_kv_offload(op.new_offload_fraction)
+                continue
             if not isinstance(op, (O.ReplicateLayer, O.MigrateLayer, O.MigrateSubModule, O.EvictReplica)):
-                continue  # PerformanceReduction: batch size / offload knobs belong to the serving loop
+                continue
             _, cost = self.ex.apply(op, self.catalog, self.cluster, kv_mb_by_layer=kv_mb_by_layer)
             done.append((op, cost))
         if decision.placement is not None:

@@ -105,6 +105,7 @@ struct LayerState {
   std::vector<int> owner;           // slot -> device holding that slot's KV (-1 none)
   ModCopy mod[kModKinds];           // projection / self-attention overrides
   bool proj_ov = false;             // any entry of mod[] in use
+  std::map<int, bool> kv_host;      // device -> its KV block lives in mapped pinned host memory (offloaded)
 };
 
 struct Workspace {
@@ -350,9 +351,20 @@ int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr
 }
 
 int kv_device(const LayerState& L);
+void sync_all_devices(cb_model* m);
 
 // Free a device's KV block for the layer once no slot's KV lives there and the
 // device no longer runs the layer's attention.
+void free_kv_block(cb_model* m, LayerState& L, int dev, uint16_t* p) {
+  if (L.kv_host.count(dev) && L.kv_host[dev]) {
+    sync_all_devices(m);
+    cudaFreeHost(p);
+    L.kv_host.erase(dev);
+  } else {
+    dev_free(m, dev, p);
+  }
+}
+
 void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
   auto it = L.kv.find(dev);
   if (it == L.kv.end()) return;
@@ -363,7 +375,7 @@ void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
           ? std::any_of(L.reps.begin(), L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; })
           : kv_device(L) == dev;
   if (attn_here) return;
-  dev_free(m, dev, it->second);
+  free_kv_block(m, L, dev, it->second);
   L.kv.erase(it);
 }
 
@@ -378,8 +390,8 @@ int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t
   if (len <= 0 || src == dst) return CB_OK;
   const size_t nbytes = size_t(len) * kv_token_bytes(m);
   const size_t off = kv_slot_offset(m, slot);
-  CB_CUDA(cudaMemcpyPeerAsync(L.kv[dst] + off, devctx(m, dst).ordinal, L.kv[src] + off,
-                              devctx(m, src).ordinal, nbytes, st));
+  // cudaMemcpyDefault: either block may be offloaded to mapped pinned host memory
+  CB_CUDA(cudaMemcpyAsync(L.kv[dst] + off, L.kv[src] + off, nbytes, cudaMemcpyDefault, st));
   if (bytes) *bytes += nbytes;
   return CB_OK;
 }
@@ -918,6 +930,58 @@ void sync_all(cb_model* m) {
     cudaStreamSynchronize(dc.copy);
   }
 }
+void sync_all_devices(cb_model* m) { sync_all(m); }
+
+// Phase-3 KV offload (autoscaler.py:568-583 PerformanceReduction; the
+// reference prices it as a latency multiplier, sim.py:258): the layer's KV
+// blocks move between device memory and mapped pinned host memory.  The
+// attention kernel reads an offloaded block in place through its UVA address
+// (zero-copy over PCIe / C2C), so nothing else in the executor changes.
+int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  sync_all(m);
+  uint64_t moved = 0;
+  float ms = 0.f;
+  for (auto& kv : L.kv) {
+    const int dev = kv.first;
+    const bool on_host = L.kv_host.count(dev) && L.kv_host[dev];
+    if (on_host == to_host) continue;
+    DeviceCtx& dc = devctx(m, dev);
+    CB_TRY(use(dc));
+    uint16_t* nb = nullptr;
+    if (to_host) {
+      CB_CUDA(cudaHostAlloc((void**)&nb, m->kv_block_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    } else {
+      uint64_t shortfall = 0;
+      int r = dev_alloc(dc, (void**)&nb, m->kv_block_bytes, &shortfall);
+      if (r != CB_OK) {
+        if (st) st->shortfall_bytes = shortfall;
+        return r;
+      }
+    }
+    CB_TRY(timed_begin(dc));
+    for (int slot = 0; slot < m->d.max_slots; ++slot) {
+      if (L.owner[slot] != dev || m->slot_len[slot] <= 0) continue;
+      const size_t nbytes = size_t(m->slot_len[slot]) * kv_token_bytes(m);
+      const size_t off = kv_slot_offset(m, slot);
+      CB_CUDA(cudaMemcpyAsync(nb + off, kv.second + off, nbytes, cudaMemcpyDefault, dc.copy));
+      moved += nbytes;
+    }
+    cb_op_stats one{};
+    CB_TRY(timed_end(dc, &one));
+    ms += one.device_ms;
+    uint16_t* old = kv.second;
+    free_kv_block(m, L, dev, old);
+    kv.second = nb;
+    if (to_host) L.kv_host[dev] = true;
+  }
+  if (st) {
+    st->kv_bytes = moved;
+    st->device_ms = ms;
+  }
+  return CB_OK;
+}
 
 // MigrateSubModule of a projection / SELF_ATTENTION (ops.py:230-251): copy the
 // module's weights (canonical [out, in] layout) to `dst`; the layer's kernels
@@ -1117,7 +1181,7 @@ int cb_model_destroy(cb_model* m) {
   sync_all(m);
   for (auto& L : m->layers) {
     for (auto& c : L.reps) dev_free(m, c.dev, c.block);
-    for (auto& kv : L.kv) dev_free(m, kv.first, kv.second);
+    for (auto& kv : L.kv) free_kv_block(m, L, kv.first, kv.second);
     for (auto& mc : L.mod) dev_free(m, mc.dev, mc.buf);
   }
   for (auto& kv : m->ws) {
@@ -1288,7 +1352,7 @@ int cb_kv_read(cb_model* m, int32_t layer, int32_t slot, void* dst, uint64_t nby
   if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
   sync_all(m);
   CB_TRY(use(devctx(m, owner)));
-  CB_CUDA(cudaMemcpy(dst, L.kv[owner] + kv_slot_offset(m, slot), want, cudaMemcpyDeviceToHost));
+  CB_CUDA(cudaMemcpy(dst, L.kv[owner] + kv_slot_offset(m, slot), want, cudaMemcpyDefault));
   if (dev_out) *dev_out = owner;
   return CB_OK;
 }
@@ -1377,6 +1441,23 @@ int cb_last_routing(cb_model* m, int32_t layer, int32_t* dev_out, int32_t* s0_ou
     s0_out[j] = r[j].s0;
     cnt_out[j] = r[j].cnt;
   }
+  return CB_OK;
+}
+
+int cb_kv_offload(cb_model* m, int32_t layer, int32_t to_host, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  CB_TRY(check_layer(m, layer));
+  return kv_offload(m, layer, to_host != 0, st);
+}
+
+int cb_kv_offloaded(cb_model* m, int32_t layer, int32_t* out) {
+  if (!m || !out) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_layer(m, layer));
+  const LayerState& L = m->layers[layer - 1];
+  *out = 0;
+  for (auto& h : L.kv_host)
+    if (h.second) *out = 1;
   return CB_OK;
 }
 

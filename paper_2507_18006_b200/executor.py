@@ -118,6 +118,7 @@ class Executor:
         self._slots = list(range(cfg.max_slots - 1, -1, -1))
         self.op_log: list[OpMeasurement] = []
         self.last_step_ms = 0.0
+        self.kv_offload_fraction = 0.0
 
     # ------------------------------------------------------------ weights
     def load_layer(self, layer: int, device: int, w) -> None:
@@ -294,6 +295,34 @@ class Executor:
                 r.output_tokens.append(int(t))
             return StepOutcome(ms / 1e3, len(batch), nxt)
         raise ValueError(f"unknown phase {phase!r}")
+
+    # ------------------------------------------------------------ Phase-3 KV offload
+    def set_kv_offload(self, fraction: float) -> list[OpMeasurement]:
+        """Offload a fraction of the KV cache off-device (the reference's Phase-3
+        ``PerformanceReduction.new_offload_fraction``, autoscaler.py:568-583).
+
+        The reference scales every layer's KV by (1 - f) (sim.py:500-505); the
+        physical unit here is a layer's KV block, so layers 1..round(f * n_layers)
+        keep their KV in mapped pinned host memory (attention reads it in place)
+        and the rest return to HBM.  Returns the per-layer move measurements."""
+        if not 0.0 <= fraction <= 1.0:
+            raise ValueError("offload fraction must be in [0, 1]")
+        n_off = int(round(fraction * self.cfg.n_layers))
+        self.kv_offload_fraction = fraction
+        out = []
+        for li in range(1, self.cfg.n_layers + 1):
+            want = li <= n_off
+            if want == self.kv_offloaded(li):
+                continue
+            st = _lib.OpStats()
+            _lib.check(self.lib.cb_kv_offload(self.handle, li, int(want), C.byref(st)), "cb_kv_offload")
+            out.append(OpMeasurement(("kv_offload" if want else "kv_reload", li), 0, st.kv_bytes, st.device_ms))
+        return out
+
+    def kv_offloaded(self, layer: int) -> bool:
+        v = C.c_int32()
+        _lib.check(self.lib.cb_kv_offloaded(self.handle, layer, C.byref(v)))
+        return bool(v.value)
 
     # ------------------------------------------------------------ profiling
     def profile(self, enable: bool) -> None:

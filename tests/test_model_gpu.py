@@ -330,3 +330,35 @@ def test_projection_submodule_migration_matches_oracle(runtime, confident):
     with pytest.raises(O.OpError):  # replicated layers cannot carry overrides (domain.py:339-340)
         ex.apply(O.ReplicateLayer(1, 1), cat, cl)
     ex.close()
+
+
+def test_kv_offload_to_host_and_back_matches_oracle(runtime, confident):
+    """Phase-3 KV offload (PerformanceReduction, autoscaler.py:568-583): half the
+    layers' KV moves to mapped pinned host memory mid-decode, attention reads it
+    there in place; KV bytes are unchanged and tokens keep matching the oracle,
+    before and after the KV returns to HBM."""
+    prompts = config1_prompts()
+    ex = Executor(runtime, _tiny_cfg())
+    ex.load_model(confident, device_of_layer=0)
+    oracle = OracleModel(TINY, confident, 64)
+    live = list(range(N_REQ))
+    slots = np.array(live, np.int32)
+    nxt, _, _ = ex.prefill(slots, np.concatenate(prompts), np.full(N_REQ, PROMPT, np.int32))
+    oracle.forward(live, np.concatenate(prompts), [PROMPT] * N_REQ)
+    for step in range(6):
+        if step == 2:
+            before = [ex.read_kv(li, 5)[0] for li in (1, 2)]
+            moves = ex.set_kv_offload(0.5)
+            assert [m.op for m in moves] == [("kv_offload", 1), ("kv_offload", 2)]
+            assert ex.kv_offloaded(1) and ex.kv_offloaded(2) and not ex.kv_offloaded(3)
+            assert all(m.kv_bytes == N_REQ * (PROMPT + 2) * 2 * TINY.d_model * 2 for m in moves)
+            assert all(np.array_equal(ex.read_kv(li, 5)[0], b) for li, b in zip((1, 2), before))
+        if step == 4:
+            ex.set_kv_offload(0.0)
+            assert not ex.kv_offloaded(1)
+        inp = nxt
+        nxt, lg, _ = ex.decode(slots, inp, want_logits=True)
+        ref = oracle.forward(live, inp, None)
+        assert np.array_equal(nxt, ref.argmax(-1)), step
+        assert np.abs(lg - ref).max() <= LOGIT_TOL
+    ex.close()
