@@ -237,6 +237,13 @@ def serving_window(ex, args, batch: int) -> dict:
     inst = InstanceState(0, ex, max_batch_size=batch)
     eng = ServingEngine([inst], seed=7)
     res = eng.run(reqs)
+    if args.telemetry:  # reference-schema artefacts (outputs.py layout) of this serving window
+        from paper_2507_18006_b200 import telemetry as T
+
+        trace = T.trace_rows(res.completed, res.step_log, window_s=1.0, devices=(0,))
+        ops = T.op_rows(ex.op_log)
+        T.write_run(args.telemetry, trace, ops, [], T.summary(trace, ops, res.completed, 7, args.serve_s,
+                                                              {"0": list(ex.placement.p_vector())}))
     s = res.summary()
     s.update({"rps": args.serve_rps, "arrival_window_s": args.serve_s, "requests": len(reqs),
               "prompt_len": args.prompt, "gen_len": args.serve_gen, "max_batch_size": batch,
@@ -479,6 +486,7 @@ def main() -> None:
     ap.add_argument("--serve-s", type=float, default=8.0, help="serving window (0 = skip)")
     ap.add_argument("--serve-rps", type=float, default=40.0)
     ap.add_argument("--serve-gen", type=int, default=64)
+    ap.add_argument("--telemetry", default="", help="write the serving window's trace/ops/summary (reference schema) here")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
