@@ -32,6 +32,8 @@
 //
 // Stand-in replaced: reference `_kernels._work_units` (`_kernels.py:17-38`) and
 // the per-module GEMM FLOPs of `ModuleCatalog.from_model` (`domain.py:241-264`).
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -43,7 +45,10 @@ static constexpr int kThreads1 = 224;    // TMA weights, MMA, 4 epilogue warps, 
 static constexpr int kEpiThreads = 128;
 static constexpr size_t kSmemBudget = 224 * 1024;  // of the 227 KB opt-in maximum
 static constexpr int kTbRow = 36;  // transpose buffer row stride (floats): 32 + 4 pad -> conflict-free 16-byte reads
-static constexpr int kTbufBytes = 4 * 16 * kTbRow * 4;  // epilogue transpose buffers: 4 warps x 16 x 36 fp32
+static constexpr int kChunkBytes = 16 * 32 * 4;  // one epilogue warp chunk: 16 tokens x 32 weight rows, fp32
+// per epilogue warp: padded transpose buffer (register-store path) + 2 TMA staging chunks
+static constexpr int kEpiWarpBytes = 16 * kTbRow * 4 + 2 * kChunkBytes;
+static constexpr int kTbufBytes = 4 * kEpiWarpBytes;
 static constexpr int kMaxStages = 16;
 
 template <int WB, int XB>
@@ -239,24 +244,89 @@ CB_DEVICE void emit_warp_vec(const GemmArgs& a, float* tb, int nw0, int row, int
   __syncwarp();
 }
 
-// Stream-K / split-K partial of one warp chunk into the [col][128 rows] fp32
-// layout (part already offset to this chunk's first column and warp's rows).
-CB_DEVICE void write_part_vec(float* part, float* tb, const float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) tb[i * kTbRow + lane] = v[i];
-  __syncwarp();
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
-    *reinterpret_cast<float4*>(part + (size_t)i * kBM + f0) = *reinterpret_cast<const float4*>(tb + i * kTbRow + f0);
+// Per epilogue warp state: transpose buffer, two TMA staging chunks.
+struct EpiWarp {
+  float* tb;    // padded [16][kTbRow] fp32 (register-store path)
+  uint8_t* st;  // 2 x kChunkBytes staging for TMA stores / bulk partial stores
+  int sb;       // staging chunk to use next
+  int q, lane;
+  CB_DEVICE EpiWarp(uint8_t* base, int q_, int lane_)
+      : tb(reinterpret_cast<float*>(base)), st(base + 16 * kTbRow * 4), sb(0), q(q_), lane(lane_) {}
+  // a staging chunk whose previous TMA store has finished reading it
+  CB_DEVICE uint8_t* next_stage() {
+    uint8_t* p = st + sb * kChunkBytes;
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    sb ^= 1;
+    return p;
   }
-  __syncwarp();
+  CB_DEVICE void drain() {
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+};
+
+// One warp chunk of output: weight rows nw0..nw0+31 (lane = row) x tokens
+// row..row+nc-1 (register i = token).  Full chunks go through smem and one TMA
+// store (EPI_RESID: TMA reduce-add = the fp32 residual +=) issued by lane 0 --
+// the LSU never sees the output; a partial chunk (token tail) uses 16-byte
+// register stores (or scalar ones for unaligned shapes).
+CB_DEVICE void emit_chunk(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, int nw0, int row, int nc,
+                          const float (&v)[16]) {
+  if (a.tma && nc == 16) {
+    uint8_t* stg = e.next_stage();
+    if (a.epi == EPI_SWIGLU) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float other = __shfl_xor_sync(0xffffffffu, v[i], 1);
+        if (!(e.lane & 1)) reinterpret_cast<uint16_t*>(stg)[i * 16 + (e.lane >> 1)] = f_to_bf16(silu_mul(v[i], other));
+      }
+    } else if (a.epi == EPI_BF16) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) reinterpret_cast<uint16_t*>(stg)[i * 32 + e.lane] = f_to_bf16(v[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) reinterpret_cast<float*>(stg)[i * 32 + e.lane] = v[i];
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (e.lane == 0) {
+      const int x = a.epi == EPI_SWIGLU ? (nw0 >> 1) : nw0;
+      if (a.epi == EPI_RESID)
+        tma_reduce_add_2d(tmO, stg, x, row);
+      else
+        tma_store_2d(tmO, stg, x, row);
+      bulk_commit();
+    }
+    return;
+  }
+  if (a.vec)
+    emit_warp_vec(a, e.tb, nw0, row, nc, v, e.lane);
+  else
+    emit16(a, nw0 + e.lane, row, nc, v);
 }
 
-// TMEM accumulator (this warp's 32 lanes) -> output (whole tile) or partial.
-CB_DEVICE void epi_drain(const GemmArgs& a, uint32_t t_addr, int m0, int row0, int ncols, bool whole, float* part,
-                         float* tb, int q, int lane) {
-  const int nw0 = m0 + q * 32;
+// Partial tiles (stream-K / split-K): fp32, chunk-major [ncol/16][4 warps][16][32]
+// so every warp chunk is one contiguous 2 KB block -- written with one bulk
+// store from smem, summed by the finisher with one bulk load per part.
+CB_DEVICE size_t part_chunk(int c0, int q) { return size_t((c0 >> 4) * 4 + q) * (kChunkBytes / 4); }
+
+CB_DEVICE void write_part_chunk(EpiWarp& e, float* gdst, const float (&v)[16]) {
+  uint8_t* stg = e.next_stage();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) reinterpret_cast<float*>(stg)[i * 32 + e.lane] = v[i];
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (e.lane == 0) {
+    bulk_s2g(gdst, stg, kChunkBytes);
+    bulk_commit();
+  }
+}
+
+// TMEM accumulator (this warp's 32 lanes) -> output (whole tile) or partial
+// (global workspace, or -- cluster split-K -- this CTA's shared memory).
+CB_DEVICE void epi_drain(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, uint32_t t_addr, int m0, int row0,
+                         int ncols, bool whole, float* part, bool part_in_smem) {
   for (int c0 = 0; c0 < ncols; c0 += 16) {
     uint32_t r[16];
     tmem_ld16(t_addr + uint32_t(c0), r);
@@ -264,13 +334,15 @@ CB_DEVICE void epi_drain(const GemmArgs& a, uint32_t t_addr, int m0, int row0, i
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-    const int nc = min(16, ncols - c0);
-    if (!whole)
-      write_part_vec(part + (size_t)c0 * kBM + q * 32, tb, v, lane);
-    else if (a.vec)
-      emit_warp_vec(a, tb, nw0, row0 + c0, nc, v, lane);
-    else
-      emit16(a, nw0 + lane, row0 + c0, nc, v);
+    if (whole) {
+      emit_chunk(a, tmO, e, m0 + e.q * 32, row0 + c0, min(16, ncols - c0), v);
+    } else if (part_in_smem) {
+      float* pc = part + part_chunk(c0, e.q);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pc[i * 32 + e.lane] = v[i];
+    } else {
+      write_part_chunk(e, part + part_chunk(c0, e.q), v);
+    }
   }
 }
 
@@ -285,15 +357,18 @@ struct PartMap {
   }
 };
 
-// Stream-K fixup of one (tile, 128-row half): every part is in the workspace;
-// the last CTA to arrive sums the parts in CTA order (deterministic).  When that
-// CTA has finished its whole range (ring_idle) the parts are bulk-copied into
-// its idle stage ring and summed from shared memory -- one round trip per
-// ring-full -- otherwise they are read from L2 directly.
-CB_DEVICE void epi_fixup(const GemmArgs& a, int* counter, const PartMap& pm, int c_first, int c_last, int m0,
-                         int row0, int ncols, bool ring_idle, uint8_t* ring, uint32_t ring_bytes, uint64_t* fix_bar,
-                         uint32_t& fix_phase, int* bcast, int et, unsigned long long* tr = nullptr) {
+// Stream-K fixup of one (tile, 128-row half): every CTA wrote its part; the
+// last to arrive sums all parts in CTA order (deterministic, independent of
+// who finishes) and emits the tile like a whole one.  When that CTA has
+// finished its whole range (ring_idle) the parts are bulk-copied into its idle
+// stage ring, one round per ring-full; otherwise they are read from L2.
+CB_DEVICE void epi_fixup(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, int* counter, const PartMap& pm,
+                         int c_first, int c_last, int m0, int row0, int ncols, bool ring_idle, uint8_t* ring,
+                         uint32_t ring_bytes, uint64_t* fix_bar, uint32_t& fix_phase, int* bcast, int et,
+                         unsigned long long* tr = nullptr) {
   const int nparts = c_last - c_first + 1;
+  e.drain();  // this warp's bulk partial stores have landed
+  fence_proxy_async_global();
   __threadfence();
   named_bar_sync(1, kEpiThreads);
   if (et == 0) {
@@ -305,102 +380,49 @@ CB_DEVICE void epi_fixup(const GemmArgs& a, int* counter, const PartMap& pm, int
   if (tr) tr[2] = globaltimer_ns() | (finisher ? (1ull << 63) : 0) | (ring_idle ? (1ull << 62) : 0);
   if (finisher) {
     __threadfence();
-    const int cols_cap = int(ring_bytes / uint32_t(nparts * kBM * 4)) & ~7;
-    if (ring_idle && a.vec && cols_cap >= 8) {
-      for (int cs = 0; cs < ncols; cs += cols_cap) {
-        const int nc = min(cols_cap, ncols - cs);
-        const uint32_t bytes = uint32_t(nc) * kBM * 4;
+    const int nchunks = (ncols + 15) >> 4;
+    const uint32_t chunk4 = 4 * kChunkBytes;  // one 16-column chunk of all 4 warps of one part
+    const int cap = int(ring_bytes / (uint32_t(nparts) * chunk4));
+    if (ring_idle && cap >= 1) {
+      for (int ch0 = 0; ch0 < nchunks; ch0 += cap) {
+        const int nch = min(cap, nchunks - ch0);
+        const uint32_t bytes = uint32_t(nch) * chunk4;
         if (et == 0) {
           fence_proxy_async_global();
           mbar_arrive_expect_tx(fix_bar, bytes * uint32_t(nparts));
           for (int p = 0; p < nparts; ++p)
-            bulk_g2s(ring + p * bytes, pm.of(c_first + p) + (size_t)cs * kBM, bytes, fix_bar);
+            bulk_g2s(ring + p * bytes, pm.of(c_first + p) + part_chunk(ch0 * 16, 0), bytes, fix_bar);
         }
         mbar_wait(fix_bar, fix_phase);
         fix_phase ^= 1;
-        // item = (token column, 8 consecutive weight rows); 4 items per thread per
-        // batch, residual loads of the batch issued before its stores
-        for (int it0 = et; it0 < nc * 16; it0 += 4 * kEpiThreads) {
-          float4 res[4][2];
-          if (a.epi == EPI_RESID) {
+        for (int ch = ch0; ch < ch0 + nch; ++ch) {
+          float v[16];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int it = it0 + j * kEpiThreads;
-              const int col = it >> 4, g = it & 15;
-              if (it < nc * 16 && m0 + g * 8 < a.N) {
-                const float4* y = reinterpret_cast<const float4*>(out_f32(a, m0 + g * 8, row0 + cs + col));
-                res[j][0] = __ldcg(y);
-                res[j][1] = __ldcg(y + 1);
-              }
-            }
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int p = 0; p < nparts; ++p) {
+            const float* src = reinterpret_cast<const float*>(ring + p * bytes) + part_chunk((ch - ch0) * 16, e.q);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += src[i * 32 + e.lane];
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int it = it0 + j * kEpiThreads;
-            if (it >= nc * 16) break;
-            const int col = it >> 4, g = it & 15;
-            float s[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) s[e] = 0.f;
-            for (int p = 0; p < nparts; ++p) {
-              float x[8];
-              load8(reinterpret_cast<const float*>(ring + p * bytes) + col * kBM + g * 8, x);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) s[e] += x[e];
-            }
-            emit8(a, m0 + g * 8, row0 + cs + col, s, res[j]);
-          }
+          emit_chunk(a, tmO, e, m0 + e.q * 32, row0 + ch * 16, min(16, ncols - ch * 16), v);
         }
         named_bar_sync(1, kEpiThreads);  // every read of this round is done before the next copy lands
         if (et == 0) fence_proxy_async_smem();
       }
     } else {
-      // work item = (row pair, token column); 8 items per thread in flight per round trip.
-      const int n_items = 64 * ncols;
-      for (int base = et; base < n_items; base += 8 * kEpiThreads) {
-        float2 sum[8];
+      for (int ch = 0; ch < nchunks; ++ch) {
+        float v[16];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) sum[j] = make_float2(0.f, 0.f);
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
         for (int cc = c_first; cc <= c_last; ++cc) {
-          const float* p = pm.of(cc);
-          float2 ld[8];
+          const float* src = pm.of(cc) + part_chunk(ch * 16, e.q);
+          float x[16];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ld[j] = make_float2(0.f, 0.f);
+          for (int i = 0; i < 16; ++i) x[i] = __ldcg(src + i * 32 + e.lane);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int it = base + j * kEpiThreads;
-            if (it < n_items) ld[j] = __ldcg(reinterpret_cast<const float2*>(p + (size_t)(it >> 6) * kBM + 2 * (it & 63)));
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            sum[j].x += ld[j].x;
-            sum[j].y += ld[j].y;
-          }
+          for (int i = 0; i < 16; ++i) v[i] += x[i];
         }
-        if (a.epi == EPI_RESID && a.vec) {  // residual loads of the round first, then the stores
-          float2 y[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int it = base + j * kEpiThreads, n = m0 + 2 * (it & 63);
-            y[j] = (it < n_items && n + 1 < a.N) ? __ldcg(reinterpret_cast<const float2*>(out_f32(a, n, row0 + (it >> 6))))
-                                                 : make_float2(0.f, 0.f);
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int it = base + j * kEpiThreads, n = m0 + 2 * (it & 63);
-            if (it < n_items && n + 1 < a.N)
-              *reinterpret_cast<float2*>(out_f32(a, n, row0 + (it >> 6))) =
-                  make_float2(y[j].x + sum[j].x, y[j].y + sum[j].y);
-            else if (it < n_items)
-              emit_pair(a, n, row0 + (it >> 6), sum[j].x, sum[j].y);
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int it = base + j * kEpiThreads;
-            if (it < n_items) emit_pair(a, m0 + 2 * (it & 63), row0 + (it >> 6), sum[j].x, sum[j].y);
-          }
-        }
+        emit_chunk(a, tmO, e, m0 + e.q * 32, row0 + ch * 16, min(16, ncols - ch * 16), v);
       }
     }
     if (et == 0) *counter = 0;
@@ -413,14 +435,14 @@ CB_DEVICE void epi_fixup(const GemmArgs& a, int* counter, const PartMap& pm, int
 template <int TN>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   const GemmArgs a) {
+                   const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
   using Cfg = GemmCfg<TN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
-  float* tbuf_all = reinterpret_cast<float*>(smem + Cfg::kRingBytes);
+  uint8_t* epi_smem = smem + Cfg::kRingBytes;  // 4 x kEpiWarpBytes
   // Two stage rings with a shared index: weights and activations, each with
   // its own full/empty barriers, so the weight ring fills before the
   // activations of the previous kernel exist.
@@ -447,6 +469,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
     const int tile = c / csplit, r = c % csplit;
     ubeg = tile * sk.kb + (r * sk.kb) / csplit;
     uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
+  } else if (a.whole_tiles) {
+    const int tiles = sk.units / sk.kb;
+    ubeg = int((long long)c * tiles / sk.grid) * sk.kb;
+    uend = int((long long)(c + 1) * tiles / sk.grid) * sk.kb;
   } else {
     ubeg = sk.u0(c);
     uend = sk.u0(c + 1);
@@ -566,7 +592,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 64;  // 0..127
-    float* tb = tbuf_all + q * (16 * kTbRow);
+    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t fix_phase = 0;
@@ -588,7 +614,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       // partials are column-major [col][128 rows]: slot 0 = the CTA's first segment
       float* part = csplit > 1 ? reinterpret_cast<float*>(sW)  // cluster mode: partial stays in smem
                                : a.ws + ((size_t)c * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TN);
-      if (!(a.dbg & 2)) epi_drain(a, t_addr, mt * kBM, row0, ncols, whole, part, tb, q, lane);
+      if (!(a.dbg & 2)) epi_drain(a, &tmO, e, t_addr, mt * kBM, row0, ncols, whole, part, csplit > 1);
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       acc ^= 1;
@@ -596,11 +622,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (tr) tr[1] = globaltimer_ns();
       if (!whole && csplit == 1) {
         const PartMap pm{a.ws, sk, tile, 1, 0, TN};
-        epi_fixup(a, &a.counters[tile], pm, sk.cta_of(tile * sk.kb), sk.cta_of(tile * sk.kb + sk.kb - 1), mt * kBM,
-                  row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes), fix_bar, fix_phase, bcast, et, tr);
+        epi_fixup(a, &tmO, e, &a.counters[tile], pm, sk.cta_of(tile * sk.kb), sk.cta_of(tile * sk.kb + sk.kb - 1),
+                  mt * kBM, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes), fix_bar, fix_phase, bcast, et,
+                  tr);
       }
       u += kb1 - kb0;
     }
+    e.drain();
     if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
   }
   if (csplit > 1) {
@@ -617,62 +645,30 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     cluster_sync_all();
     if (epi_warp) {
-      const int et = threadIdx.x - 64;
+      // CTA `rank` reduces its 128/csplit rows (qpr warp quarters) over the S
+      // partials in fixed rank order; the 4 epilogue warps split the quarters
+      // and the 16-column chunks, and emit like a whole tile.
       const uint32_t rank = cluster_ctarank();
-      const int rows_per = kBM / csplit;
-      const int row_base = int(rank) * rows_per;
+      const int w = warp - 2;
+      const int qpr = 4 / csplit;  // quarters per rank (csplit is 2 or 4)
+      const int qq = int(rank) * qpr + (w % qpr);
+      EpiWarp e(epi_smem + w * kEpiWarpBytes, qq, lane);
       const int row0 = a.row_off + tt * TN;
       const uint32_t base = smem_u32(sW);
-      if (a.vec) {
-        // item = (token column, 8 consecutive rows of this rank's share); 4 items
-        // per thread per batch, residual loads of a batch before its stores
-        const int gpr = rows_per / 8, n_items = gpr * ncols_tile;
-        for (int it0 = et; it0 < n_items; it0 += 4 * kEpiThreads) {
-          float4 res[4][2];
-          if (a.epi == EPI_RESID) {
+      const int nchunks = (ncols_tile + 15) >> 4;
+      for (int ch = w / qpr; ch < nchunks; ch += 4 / qpr) {
+        float v[16];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int it = it0 + j * kEpiThreads;
-              const int n0 = mt * kBM + row_base + 8 * (it % gpr);
-              if (it < n_items && n0 < a.N) {
-                const float4* y = reinterpret_cast<const float4*>(out_f32(a, n0, row0 + it / gpr));
-                res[j][0] = __ldcg(y);
-                res[j][1] = __ldcg(y + 1);
-              }
-            }
-          }
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        const uint32_t off = base + uint32_t(part_chunk(ch * 16, qq) * 4 + lane * 4);
+        for (int src = 0; src < csplit; ++src) {
+          const uint32_t ra = dsmem_map(off, uint32_t(src));
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int it = it0 + j * kEpiThreads;
-            if (it >= n_items) break;
-            const int col = it / gpr, row = row_base + 8 * (it % gpr);
-            const uint32_t off = base + uint32_t((col * kBM + row) * 4);
-            float s8[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) s8[e] = 0.f;
-            for (int src = 0; src < csplit; ++src) {
-              const uint32_t ra = dsmem_map(off, uint32_t(src));
-              const float4 x0 = dsmem_ld_f4(ra), x1 = dsmem_ld_f4(ra + 16);
-              s8[0] += x0.x; s8[1] += x0.y; s8[2] += x0.z; s8[3] += x0.w;
-              s8[4] += x1.x; s8[5] += x1.y; s8[6] += x1.z; s8[7] += x1.w;
-            }
-            emit8(a, mt * kBM + row, row0 + col, s8, res[j]);
-          }
+          for (int i = 0; i < 16; ++i) v[i] += dsmem_ld_f32(ra + uint32_t(i * 128));
         }
-      } else {
-        const int pairs = rows_per / 2;
-        for (int it = et; it < pairs * ncols_tile; it += kEpiThreads) {
-          const int col = it / pairs, row = row_base + 2 * (it % pairs);
-          const uint32_t off = base + uint32_t((col * kBM + row) * 4);
-          float2 sum = make_float2(0.f, 0.f);
-          for (int src = 0; src < csplit; ++src) {
-            const float2 v = dsmem_ld_f2(dsmem_map(off, uint32_t(src)));
-            sum.x += v.x;
-            sum.y += v.y;
-          }
-          emit_pair(a, mt * kBM + row, row0 + col, sum.x, sum.y);
-        }
+        emit_chunk(a, &tmO, e, mt * kBM + qq * 32, row0 + ch * 16, min(16, ncols_tile - ch * 16), v);
       }
+      e.drain();
     }
     cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
@@ -693,14 +689,14 @@ __global__ void __launch_bounds__(kThreads1, 1)
 template <int TNP>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                    const GemmArgs a) {
+                    const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
   using Cfg = PairCfg<TNP>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
-  float* tbuf_all = reinterpret_cast<float*>(smem + Cfg::kRingBytes);
+  uint8_t* epi_smem = smem + Cfg::kRingBytes;  // 4 x kEpiWarpBytes
   uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + kTbufBytes);  // leader: weights landed
   uint64_t* xfull_bar = wfull_bar + S;   // leader: both CTAs' tokens landed
   uint64_t* empty_bar = xfull_bar + S;   // each CTA: stage consumed
@@ -717,7 +713,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
   const int pair = blockIdx.x >> 1;
   const int n_tt = a.n_ttiles;
   const StreamK sk{a.units, int(gridDim.x) >> 1, a.kblocks};
-  const int ubeg = sk.u0(pair), uend = sk.u0(pair + 1);
+  const int ptiles = sk.units / sk.kb;
+  const int ubeg = a.whole_tiles ? int((long long)pair * ptiles / sk.grid) * sk.kb : sk.u0(pair);
+  const int uend = a.whole_tiles ? int((long long)(pair + 1) * ptiles / sk.grid) * sk.kb : sk.u0(pair + 1);
   const int c = blockIdx.x;
 
   pdl_trigger();
@@ -821,7 +819,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
-    float* tb = tbuf_all + q * (16 * kTbRow);
+    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
     const uint32_t tempty_leader0 = dsmem_map(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = dsmem_map(smem_u32(&tempty_bar[1]), 0);
     int acc = 0;
@@ -844,7 +842,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (tr) tr[0] = globaltimer_ns() | (whole ? (1ull << 62) : 0);
       const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TNP);
       float* part = a.ws + ((size_t)blockIdx.x * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TNP);
-      epi_drain(a, t_addr, m0, row0, ncols, whole, part, tb, q, lane);
+      epi_drain(a, &tmO, e, t_addr, m0, row0, ncols, whole, part, false);
       tc_fence_before();
       mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
@@ -852,12 +850,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (tr) tr[1] = globaltimer_ns();
       if (!whole) {
         const PartMap pm{a.ws, sk, tile, 2, int(rank), TNP};
-        epi_fixup(a, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
+        epi_fixup(a, &tmO, e, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
                   sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes),
                   fix_bar, fix_phase, bcast, et, tr);
       }
       u += kb1 - kb0;
     }
+    e.drain();
     if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
   }
   tc_fence_before();
@@ -890,6 +889,22 @@ int make_kmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+int make_out_map(CUtensorMap* map, const void* out, int epi, uint64_t rows, uint64_t cols, uint64_t ldo) {
+  if (!load_encode_fn()) return -1;
+  const bool f32 = epi == EPI_F32 || epi == EPI_RESID;
+  const uint32_t esz = f32 ? 4 : 2;
+  const uint32_t box_c = epi == EPI_SWIGLU ? 16 : 32;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo * esz) % 16 || cols % box_c) return -3;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ldo * esz};
+  cuuint32_t box[2] = {box_c, 16};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(out), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
@@ -939,12 +954,14 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
     p.tn = 256;
     p.box_rows = p.tn / 2;
     const long long ptiles = (long long)((N + 2 * kBM - 1) / (2 * kBM)) * ((kind_T + p.tn - 1) / p.tn);
-    if (ptiles <= num_sms / 2 && kb < 128) p.max_parts = 1;
+    if (ptiles <= num_sms / 2 && kb < 128) p.max_parts = 1;  // QKV: one wave of whole tiles
+    if (ptiles > num_sms / 2) p.whole = 1;                   // gate/up, lm_head: whole tiles beat stream-K fixups
     return p;
   }
   p.pair = 0;
   p.tn = gemm_pick_tn(T);
-  if (tiles <= num_sms) p.max_parts = 1;  // QKV: one wave of whole tiles
+  if (tiles <= num_sms) p.max_parts = 1;             // QKV: one wave of whole tiles
+  if (tiles * 2 >= (long long)num_sms * 3) p.whole = 1;  // lm_head (>= 1.5 waves): whole tiles
   p.box_rows = p.tn;
   return p;
 }
@@ -959,8 +976,8 @@ static int vec_ok(const GemmArgs& a) {
 }
 
 template <int TN>
-static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, const GemmPlan& plan,
-                             int num_sms, cudaStream_t st) {
+static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& o, GemmArgs a,
+                             const GemmPlan& plan, int num_sms, cudaStream_t st) {
   using Cfg = GemmCfg<TN>;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -980,20 +997,21 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, GemmArg
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;
   a.units = int(tiles * a.kblocks);
+  a.whole_tiles = plan.whole;
   if (plan.csplit > 1)
     return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
-                              Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, a);
+                              Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, o, a);
   // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
   long long ctas = num_sms;
   if (ctas > a.units) ctas = a.units;
   const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
   if (mp > 0 && ctas > tiles * mp) ctas = tiles * mp;
-  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, a);
+  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, o, a);
 }
 
 template <int TNP>
-static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, GemmArgs a, const GemmPlan& plan,
-                               int num_sms, cudaStream_t st) {
+static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& o, GemmArgs a,
+                               const GemmPlan& plan, int num_sms, cudaStream_t st) {
   using Cfg = PairCfg<TNP>;
   static bool attr_set[64] = {};
   int dev = 0;
@@ -1010,28 +1028,40 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, GemmA
   a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.units = int(tiles * a.kblocks);
+  a.whole_tiles = plan.whole;
   long long pairs = num_sms / 2;
   if (pairs > a.units) pairs = a.units;
   const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
   if (mp > 0 && pairs > tiles * mp) pairs = tiles * mp;
   return launch_pdl_cluster(gemm_tc2_kernel<TNP>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes, st,
-                            2u, w, x, a);
+                            2u, w, x, o, a);
 }
 
-cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
-                        int num_sms, cudaStream_t st) {
-  if (a.T <= 0 || a.N <= 0) return cudaSuccess;
+cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a_in, const GemmPlan& plan,
+                        int num_sms, cudaStream_t st, const CUtensorMap* out_map) {
+  if (a_in.T <= 0 || a_in.N <= 0) return cudaSuccess;
+  GemmArgs a = a_in;
+  CUtensorMap o;
+  // TMA stores measured: a win for the fp32 outputs (residual reduce-add,
+  // logits), neutral for bf16, 3x slower for the 32-byte SwiGLU boxes
+  if (out_map && (a.epi == EPI_RESID || a.epi == EPI_F32)) {
+    o = *out_map;
+    a.tma = 1;
+  } else {
+    std::memset(&o, 0, sizeof(o));
+    a.tma = 0;
+  }
   if (plan.pair) {
-    if (plan.tn == 128) return launch_pair<128>(w, x, a, plan, num_sms, st);
-    if (plan.tn == 256) return launch_pair<256>(w, x, a, plan, num_sms, st);
+    if (plan.tn == 128) return launch_pair<128>(w, x, o, a, plan, num_sms, st);
+    if (plan.tn == 256) return launch_pair<256>(w, x, o, a, plan, num_sms, st);
     return cudaErrorInvalidValue;
   }
   switch (plan.tn) {
-    case 16: return launch_tn<16>(w, x, a, plan, num_sms, st);
-    case 32: return launch_tn<32>(w, x, a, plan, num_sms, st);
-    case 64: return launch_tn<64>(w, x, a, plan, num_sms, st);
-    case 128: return launch_tn<128>(w, x, a, plan, num_sms, st);
-    case 256: return launch_tn<256>(w, x, a, plan, num_sms, st);
+    case 16: return launch_tn<16>(w, x, o, a, plan, num_sms, st);
+    case 32: return launch_tn<32>(w, x, o, a, plan, num_sms, st);
+    case 64: return launch_tn<64>(w, x, o, a, plan, num_sms, st);
+    case 128: return launch_tn<128>(w, x, o, a, plan, num_sms, st);
+    case 256: return launch_tn<256>(w, x, o, a, plan, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -32,6 +32,8 @@ struct GemmArgs {
   int w_tiled;        // 1 = weight stored tile-major [N/128][K/64][128][64] (each TMA box contiguous)
   unsigned long long* trace;  // experiments only: per-CTA event timestamps (globaltimer ns) when non-null
   int vec;            // set by the launcher: 16-byte vector epilogue stores are legal for out/N/ldo
+  int tma;            // set by the launcher: an output tensor map was passed (TMA-store epilogue)
+  int whole_tiles;    // set from the plan: CTA (pair) ranges rounded to whole tiles
   int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
@@ -49,12 +51,19 @@ struct GemmPlan {
   int box_rows;  // activation tensor-map box height this plan needs (pair: tn / 2)
   int csplit;    // cluster split-K size (1, 2, 4, 8)
   int max_parts; // stream-K: max CTAs (pairs) sharing a tile (0 = no cap; 1 = one tile per CTA, no fixups)
+  int whole;     // 1 = persistent over whole tiles (contiguous tile ranges per CTA / pair, no fixups)
 };
 // kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
 // micro-batches compute exactly what the unreplicated pass would.
 GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T = 0);
+// out_map: TMA map of the output (make_out_map) or null -> register-store epilogue
 cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a, const GemmPlan& plan,
-                        int num_sms, cudaStream_t st);
+                        int num_sms, cudaStream_t st, const CUtensorMap* out_map = nullptr);
+// Output tensor map for the TMA-store epilogue: `out` is [rows][ldo] (bf16, or fp32
+// for EPI_F32 / EPI_RESID) holding `cols` output columns (N, or N/2 for SwiGLU);
+// box = one epilogue warp chunk (16 tokens x 32 weight rows).  Returns 0 when the
+// shape allows it (16-byte aligned base and pitch, cols a multiple of the box).
+int make_out_map(CUtensorMap* map, const void* out, int epi, uint64_t rows, uint64_t cols, uint64_t ldo);
 size_t gemm_ws_floats(int num_sms);
 constexpr int kGemmMaxTiles = 1 << 16;
 

@@ -25,9 +25,11 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/cocob200.h"
@@ -122,6 +124,8 @@ struct Workspace {
   size_t attn_ws_floats = 0;
   float2* rope = nullptr;
   CUtensorMap map_h[kTnCount], map_hl[kTnCount], map_att[kTnCount], map_act[kTnCount];
+  // TMA-store epilogue maps by (output base, epi, cols, ldo, rows), built on first use
+  std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, CUtensorMap> out_maps;
 };
 
 struct Route {
@@ -415,8 +419,23 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
   const double out_n = epi == cb::EPI_SWIGLU ? N / 2.0 : double(N);
   const double bytes = double(N) * K * 2 + double(T) * K * 2 + double(T) * out_n * out_b +
                        (epi == cb::EPI_RESID ? double(T) * N * 4 : 0.0);
+  // output map for the TMA-store epilogue (rows = the buffer's rows: a store box
+  // never crosses the launch's last token row, partial chunks use register stores)
+  const uint64_t ocols = epi == cb::EPI_SWIGLU ? uint64_t(N) / 2 : uint64_t(N);
+  const uint64_t orows = out == ws.logits ? uint64_t(m->d.max_slots) : uint64_t(m->d.max_tokens);
+  const auto key = std::make_tuple(static_cast<const void*>(out), epi, ocols, uint64_t(ldo), orows);
+  const CUtensorMap* om = nullptr;
+  static const bool no_tma_store = std::getenv("COCOB200_NO_TMA_STORE") != nullptr;  // A/B experiments
+  auto it = no_tma_store ? ws.out_maps.end() : ws.out_maps.find(key);
+  if (it != ws.out_maps.end()) {
+    om = &it->second;
+  } else {
+    CUtensorMap mo;
+    if (!no_tma_store && cb::make_out_map(&mo, out, epi, orows, ocols, uint64_t(ldo)) == 0)
+      om = &(ws.out_maps[key] = mo);
+  }
   ProfScope ps(m, dev, CB_KCLASS_GEMM, dc.compute, bytes, 2.0 * N * K * T);
-  CB_CUDA(cb::gemm_launch(w, xmaps[box_index(plan.box_rows)], a, plan, dc.num_sms, dc.compute));
+  CB_CUDA(cb::gemm_launch(w, xmaps[box_index(plan.box_rows)], a, plan, dc.num_sms, dc.compute, om));
   return CB_OK;
 }
 

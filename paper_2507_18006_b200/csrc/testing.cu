@@ -77,7 +77,10 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
-  return finish(cb::gemm_launch(mw, mx, a, plan, ws->sms, 0));
+  CUtensorMap mo;
+  const uint64_t ocols = epi == cb::EPI_SWIGLU ? uint64_t(N) / 2 : uint64_t(N);
+  const bool tma = cb::make_out_map(&mo, out, epi, uint64_t(row_off + T), ocols, uint64_t(ldo)) == 0;
+  return finish(cb::gemm_launch(mw, mx, a, plan, ws->sms, 0, tma ? &mo : nullptr));
 }
 
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
@@ -102,6 +105,8 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   } else if (max_parts == 99) {
     plan.max_parts = 0;  // experiments: force stream-K
   }
+  if (dbg_bits & 512) plan.whole = 1, plan.max_parts = 0, plan.csplit = plan.pair ? 1 : plan.csplit;  // whole tiles
+  if (dbg_bits & 1024) plan.whole = 0;                                                          // stream-K
   CUtensorMap mw, mx;
   if ((r = gemm_setup(w, x, x_rows, N, K, plan, &mw, &mx))) return r;
   const bool tiled = (dbg_bits & 4) != 0;  // w holds the tile-major layout
@@ -129,13 +134,17 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
     cudaMemset(trace, 0, 148 * 512 * 8);
     a.trace = trace;
   }
-  a.dbg = dbg_bits & ~(4 | 8);  // experiments: knob + 1000 * dbg bits (4 = tile-major weight)
-  for (int i = 0; i < 3; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0);
+  a.dbg = dbg_bits & ~(4 | 8 | 256 | 512 | 1024);  // experiments: knob + 1000 * dbg bits (4 = tile-major weight, 256 = no TMA store)
+  CUtensorMap mo;
+  const uint64_t ocols = epi == cb::EPI_SWIGLU ? uint64_t(N) / 2 : uint64_t(N);
+  const CUtensorMap* pmo =
+      (!(dbg_bits & 256) && cb::make_out_map(&mo, out, epi, uint64_t(T), ocols, uint64_t(ldo)) == 0) ? &mo : nullptr;
+  for (int i = 0; i < 3; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0, pmo);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
-  for (int i = 0; i < iters; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0);
+  for (int i = 0; i < iters; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0, pmo);
   cudaEventRecord(e1, 0);
   if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
   float ms = 0;
@@ -143,7 +152,7 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   *ms_per_launch = ms / iters;
   if (a.trace) {
     cudaMemset(trace, 0, 148 * 512 * 8);
-    cb::gemm_launch(mws[iters % mws.size()], mx, a, plan, ws->sms, 0);
+    cb::gemm_launch(mws[iters % mws.size()], mx, a, plan, ws->sms, 0, pmo);
     cudaDeviceSynchronize();
     cudaMemcpy(g_trace, trace, sizeof(g_trace), cudaMemcpyDeviceToHost);
   }

@@ -1,3 +1,3 @@
-timeout 120 python scripts/gemm_trace.py 12288 4096 256 0 6 0 > gpurun_out/trace11.txt 2>&1
-timeout 120 python scripts/gemm_trace.py 22016 4096 256 0 6 3 >> gpurun_out/trace11.txt 2>&1
-timeout 120 python scripts/gemm_trace.py 4096 4096 256 0 3 2 >> gpurun_out/trace11.txt 2>&1
+for i in 1 2; do
+for B in 64 256; do timeout 300 python scripts/step_profile.py $B 5 2>&1 | head -1; COCOB200_NO_TMA_STORE=1 timeout 300 python scripts/step_profile.py $B 5 2>&1 | head -1; done
+done > gpurun_out/ab_tma.txt

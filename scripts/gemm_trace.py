@@ -65,3 +65,6 @@ for c in (0, 1, 2, 75, 147):
         dec = flags[c, 132 + 4 * sg]
         print(f"     seg {sg}: {'whole' if fl & 1 else 'part '} tfull {ev[0]:.2f} drained {ev[1]:.2f} "
               f"decision {ev[2]:.2f}{' FINISHER' if dec & 2 else ''}{' ring-idle' if dec & 1 else ''} done {ev[3]:.2f}")
+        fx = rel[c, 130 + 4 * sg + 220: 130 + 4 * sg + 226]
+        if not np.all(np.isnan(fx)):
+            print("       fixup rounds (copy landed, summed):", " ".join(f"{v:.2f}" for v in fx if not np.isnan(v)))
