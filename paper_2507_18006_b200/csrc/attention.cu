@@ -31,14 +31,17 @@ static constexpr int kUnroll = 4;
 // byte is fetched once for the whole head group.
 template <int HD, int U>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-    attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq) {
+    attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq, int head_major) {
   pdl_trigger();
   pdl_wait();
   constexpr int G = HD / 8;               // lanes per group
   constexpr int P = 32 / G;               // groups per warp
   constexpr int NG = kAttnWarps * P;      // groups per CTA
-  const int row = a.row_off + blockIdx.x;
-  const int hk = blockIdx.y;
+  // head-major grids launch the kv heads of one row back to back, so the CTAs
+  // running together read the whole contiguous [k | v] rows of their positions
+  const int rl = head_major ? blockIdx.y : blockIdx.x;
+  const int row = a.row_off + rl;
+  const int hk = head_major ? blockIdx.x : blockIdx.y;
   const int split = blockIdx.z;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lg = lane % G, pg = lane / G;
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
     } else {
       // partial state: [(row_local * H + qh) * nsplit + split] -> (m, l, acc[HD])
-      const size_t idx = ((size_t)blockIdx.x * a.H + qh) * nsplit + split;
+      const size_t idx = ((size_t)rl * a.H + qh) * nsplit + split;
       float* st = a.ws + idx * (HD + 2);
       if (lg == 0) {
         st[0] = M;
@@ -253,7 +256,11 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
     while (nsplit > 1 && (size_t)a.T * a.H * nsplit * (HD + 2) > a.ws_floats) --nsplit;
   }
   const int chunk = (a.max_len + nsplit - 1) / nsplit;
-  dim3 grid(a.T, a.Hkv, nsplit);
+  static const int head_major = [] {
+    const char* e = getenv("CB_ATTN_HEAD_MAJOR");
+    return e ? atoi(e) : 1;
+  }();
+  const dim3 grid = head_major ? dim3(a.Hkv, a.T, nsplit) : dim3(a.T, a.Hkv, nsplit);
   // positions in flight per lane group: 4 when there are enough CTAs to fill
   // the GPU (measured best for decode batches), 8 for few long rows
   static const int forced = [] {
@@ -262,8 +269,8 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
   }();
   const long long total = ctas * nsplit;
   const int u = forced ? forced : (gq == 1 && total >= 8LL * num_sms ? 4 : 8);
-  cudaError_t e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq)
-                         : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq);
+  cudaError_t e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major)
+                         : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major);
   if (e != cudaSuccess || nsplit == 1) return e;
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);
 }
