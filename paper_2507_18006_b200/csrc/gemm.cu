@@ -32,6 +32,7 @@
 //
 // Stand-in replaced: reference `_kernels._work_units` (`_kernels.py:17-38`) and
 // the per-module GEMM FLOPs of `ModuleCatalog.from_model` (`domain.py:241-264`).
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -62,8 +63,8 @@ struct RingCfg {
   // ring | transpose buffers | barriers
   static constexpr size_t kSmemBytes = size_t(kRingBytes) + kTbufBytes + 1024 /*align slack*/ + 1024 /*barriers*/;
 };
-template <int TN>
-struct GemmCfg : RingCfg<kBM * kBK * 2, TN * kBK * 2> {
+template <int TN, int KD = 1>
+struct GemmCfg : RingCfg<kBM * kBK * 2 * KD, TN * kBK * 2 * KD> {
   static constexpr uint32_t kTmemCols = (2 * TN <= 32)    ? 32
                                         : (2 * TN <= 64)  ? 64
                                         : (2 * TN <= 128) ? 128
@@ -432,11 +433,14 @@ CB_DEVICE void epi_fixup(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, 
 }
 
 // ------------------------------------------------------------------ 1-CTA kernel
-template <int TN>
+// KD = k-blocks per stage: 2 -> one 3-D TMA box per operand and 8 MMAs per
+// stage issue, halving the per-k-block cost of the MMA warp (waits, commits,
+// descriptor moves) that bounds small-T decode GEMMs.
+template <int TN, int KD>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
-  using Cfg = GemmCfg<TN>;
+  using Cfg = GemmCfg<TN, KD>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -513,7 +517,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
         const int mt = tile / n_ttiles;
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         mbar_arrive_expect_tx(&full_bar[stage], Cfg::kWBytes);
-        if (a.w_tiled)
+        if (KD > 1)
+          tma_load_3d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, 0, mt * kBM, kb * KD, pol_w);
+        else if (a.w_tiled)
           tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, 0, (mt * sk.kb + kb) * kBM, pol_w);
         else
           tma_load_2d(&tmW, &full_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt * kBM, pol_w);
@@ -534,7 +540,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
         const int tt = tile % n_ttiles;
         mbar_wait(&xempty_bar[stage], phase ^ 1);
         mbar_arrive_expect_tx(&xfull_bar[stage], Cfg::kXBytes);
-        tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
+        if (KD > 1)
+          tma_load_3d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, 0, a.row_off + tt * TN, kb * KD, pol_x);
+        else
+          tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -572,7 +581,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
           // descriptor start address += stage offset (>> 4 encoded, stays inside its 14-bit field)
           const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
           const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
-          umma_kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage]);
+          if (KD > 1)  // second k-block: 128 weight rows / TN token rows x 128 B further
+            umma_2kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage],
+                               uint32_t(kBM * kBK * 2) >> 4, uint32_t(TN * kBK * 2) >> 4);
+          else
+            umma_kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage]);
         }
         if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -908,6 +921,20 @@ int make_out_map(CUtensorMap* map, const void* out, int epi, uint64_t rows, uint
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+int make_kmajor_map3(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
+                     uint32_t box_rows, uint32_t kd) {
+  if (!load_encode_fn()) return -1;
+  if (k % (uint64_t(kBK) * kd)) return -3;
+  cuuint64_t dims[3] = {uint64_t(kBK), rows, k / kBK};
+  cuuint64_t strides[2] = {row_stride_elems * 2, uint64_t(kBK) * 2};
+  cuuint32_t box[3] = {uint32_t(kBK), box_rows, kd};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
 int gemm_pick_tn(int T) {
   if (T <= 16) return 16;
   if (T <= 32) return 32;
@@ -940,11 +967,19 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   if (kind_T < T) kind_T = T;
   const int kb = (K + kBK - 1) / kBK;
   const long long tiles = (N + kBM - 1) / kBM;  // 128-row weight tiles
+  // 2 k-blocks per stage (3-D TMA boxes) for the 1-CTA kernel up to 128 rows
+  static const int kd_env = [] {
+    const char* e = getenv("COCOB200_KD");
+    return e ? atoi(e) : 2;
+  }();
+  const int kd2 = (kd_env == 2 && K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // whole-pass rows: replica-invariant
+  p.kd = 1;
   if (kind_T <= 256 && tiles * 10 < (long long)num_sms * 6) {
     // few wide-K tiles (O / down projections): 1-CTA kernel, cluster split-K
     // (DSMEM reduction) -- measured fastest up to 256 rows
     p.pair = 0;
     p.tn = gemm_pick_tn(T);
+    p.kd = kd2;
     p.box_rows = p.tn;
     while (p.csplit < 4 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
     return p;
@@ -960,6 +995,7 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   }
   p.pair = 0;
   p.tn = gemm_pick_tn(T);
+  p.kd = kd2;
   if (tiles <= num_sms) p.max_parts = 1;             // QKV: one wave of whole tiles
   if (tiles * 2 >= (long long)num_sms * 3) p.whole = 1;  // lm_head (>= 1.5 waves): whole tiles
   p.box_rows = p.tn;
@@ -975,38 +1011,38 @@ static int vec_ok(const GemmArgs& a) {
   return (a.ldo % 4 == 0) ? 1 : 0;
 }
 
-template <int TN>
+template <int TN, int KD>
 static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& o, GemmArgs a,
                              const GemmPlan& plan, int num_sms, cudaStream_t st) {
-  using Cfg = GemmCfg<TN>;
+  using Cfg = GemmCfg<TN, KD>;
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<TN, KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Cfg::kSmemBytes));
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(gemm_tc_kernel<TN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(gemm_tc_kernel<TN, KD>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) cudaGetLastError();
     attr_set[dev & 63] = true;
   }
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
-  a.kblocks = (a.K + kBK - 1) / kBK;
+  a.kblocks = (a.K + kBK * KD - 1) / (kBK * KD);
   a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;
   a.units = int(tiles * a.kblocks);
   a.whole_tiles = plan.whole;
   if (plan.csplit > 1)
-    return launch_pdl_cluster(gemm_tc_kernel<TN>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
+    return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
                               Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, o, a);
   // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
   long long ctas = num_sms;
   if (ctas > a.units) ctas = a.units;
   const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
   if (mp > 0 && ctas > tiles * mp) ctas = tiles * mp;
-  return launch_pdl(gemm_tc_kernel<TN>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, o, a);
+  return launch_pdl(gemm_tc_kernel<TN, KD>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, o, a);
 }
 
 template <int TNP>
@@ -1056,12 +1092,21 @@ cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmAr
     if (plan.tn == 256) return launch_pair<256>(w, x, o, a, plan, num_sms, st);
     return cudaErrorInvalidValue;
   }
+  if (plan.kd == 2) {
+    switch (plan.tn) {
+      case 16: return launch_tn<16, 2>(w, x, o, a, plan, num_sms, st);
+      case 32: return launch_tn<32, 2>(w, x, o, a, plan, num_sms, st);
+      case 64: return launch_tn<64, 2>(w, x, o, a, plan, num_sms, st);
+      case 128: return launch_tn<128, 2>(w, x, o, a, plan, num_sms, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (plan.tn) {
-    case 16: return launch_tn<16>(w, x, o, a, plan, num_sms, st);
-    case 32: return launch_tn<32>(w, x, o, a, plan, num_sms, st);
-    case 64: return launch_tn<64>(w, x, o, a, plan, num_sms, st);
-    case 128: return launch_tn<128>(w, x, o, a, plan, num_sms, st);
-    case 256: return launch_tn<256>(w, x, o, a, plan, num_sms, st);
+    case 16: return launch_tn<16, 1>(w, x, o, a, plan, num_sms, st);
+    case 32: return launch_tn<32, 1>(w, x, o, a, plan, num_sms, st);
+    case 64: return launch_tn<64, 1>(w, x, o, a, plan, num_sms, st);
+    case 128: return launch_tn<128, 1>(w, x, o, a, plan, num_sms, st);
+    case 256: return launch_tn<256, 1>(w, x, o, a, plan, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

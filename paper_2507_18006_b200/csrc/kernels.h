@@ -41,6 +41,9 @@ struct GemmArgs {
 
 int make_kmajor_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
                     uint32_t box_rows);
+// 3-D view (64, rows, k / 64) of the same operand: one box = box_rows x (kd x 64) in kd SW128 sub-tiles
+int make_kmajor_map3(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint64_t row_stride_elems,
+                     uint32_t box_rows, uint32_t kd);
 // TN bucket of a 1-CTA launch (16..256).
 int gemm_pick_tn(int T);
 // Launches with more rows than this use the CTA-pair kernel (tunable for experiments).
@@ -52,6 +55,7 @@ struct GemmPlan {
   int csplit;    // cluster split-K size (1, 2, 4, 8)
   int max_parts; // stream-K: max CTAs (pairs) sharing a tile (0 = no cap; 1 = one tile per CTA, no fixups)
   int whole;     // 1 = persistent over whole tiles (contiguous tile ranges per CTA / pair, no fixups)
+  int kd;        // k-blocks (64 wide) per pipeline stage: 2 = 3-D TMA maps (make_kmajor_map3), 1-CTA kernel only
 };
 // kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
 // micro-batches compute exactly what the unreplicated pass would.

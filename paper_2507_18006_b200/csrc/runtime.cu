@@ -71,6 +71,14 @@ struct DeviceCtx {
 // activation tensor maps per box height (GEMM plans need 8..256-row boxes)
 constexpr int kTnCount = 6;
 constexpr int kTns[kTnCount] = {8, 16, 32, 64, 128, 256};
+// A GEMM operand's TMA views: 2-D (64-wide k-blocks) and, when K allows, the
+// 3-D view the 2-k-block-per-stage 1-CTA kernel loads with one box.
+struct OpMap {
+  CUtensorMap m2;
+  CUtensorMap m3;
+  bool has3 = false;
+};
+
 int box_index(int rows) {
   for (int i = 0; i < kTnCount; ++i)
     if (kTns[i] == rows) return i;
@@ -88,7 +96,7 @@ namespace {
 struct LayerCopy {
   int dev = -1;
   uint8_t* block = nullptr;
-  CUtensorMap m_qkv, m_o, m_gu, m_d;
+  OpMap m_qkv, m_o, m_gu, m_d;
 };
 
 // A sub-module moved off its layer by MigrateSubModule (ops.py:230-251): its
@@ -123,7 +131,7 @@ struct Workspace {
   float* attn_ws = nullptr;
   size_t attn_ws_floats = 0;
   float2* rope = nullptr;
-  CUtensorMap map_h[kTnCount], map_hl[kTnCount], map_att[kTnCount], map_act[kTnCount];
+  OpMap map_h[kTnCount], map_hl[kTnCount], map_att[kTnCount], map_act[kTnCount];
   // TMA-store epilogue maps by (output base, epi, cols, ldo, rows), built on first use
   std::map<std::tuple<const void*, int, uint64_t, uint64_t, uint64_t>, CUtensorMap> out_maps;
 };
@@ -164,7 +172,7 @@ struct cb_model {
   size_t kv_block_bytes = 0;
   std::vector<LayerState> layers;
   uint16_t *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
-  CUtensorMap m_head;
+  OpMap m_head;
   bool head_loaded = false;
   std::map<int, Workspace> ws;
   std::vector<int> slot_len;
@@ -287,9 +295,10 @@ int check_dev(cb_model* m, int dev) {
   return CB_OK;
 }
 
-int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t box_rows) {
-  int r = cb::make_kmajor_map(map, base, rows, k, k, box_rows);
+int make_map(OpMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  int r = cb::make_kmajor_map(&map->m2, base, rows, k, k, box_rows);
   if (r != 0) return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  map->has3 = box_rows <= 128 && k % 128 == 0 && cb::make_kmajor_map3(&map->m3, base, rows, k, k, box_rows, 2) == 0;
   return CB_OK;
 }
 
@@ -400,11 +409,13 @@ int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t
   return CB_OK;
 }
 
-int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, int N, int K, int T, int row_off,
-         int epi, void* out, long long ldo) {
+int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K, int T, int row_off, int epi,
+         void* out, long long ldo) {
   DeviceCtx& dc = devctx(m, dev);
   Workspace& ws = m->ws[dev];
-  const cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms, m->cur_T);
+  cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms, m->cur_T);
+  const OpMap& xm = xmaps[box_index(plan.box_rows)];
+  if (plan.kd == 2 && !(w.has3 && xm.has3)) plan.kd = 1;
   cb::GemmArgs a{};
   a.N = N;
   a.K = K;
@@ -435,7 +446,8 @@ int gemm(cb_model* m, int dev, const CUtensorMap& w, const CUtensorMap* xmaps, i
       om = &(ws.out_maps[key] = mo);
   }
   ProfScope ps(m, dev, CB_KCLASS_GEMM, dc.compute, bytes, 2.0 * N * K * T);
-  CB_CUDA(cb::gemm_launch(w, xmaps[box_index(plan.box_rows)], a, plan, dc.num_sms, dc.compute, om));
+  CB_CUDA(cb::gemm_launch(plan.kd == 2 ? w.m3 : w.m2, plan.kd == 2 ? xm.m3 : xm.m2, a, plan, dc.num_sms, dc.compute,
+                          om));
   return CB_OK;
 }
 
@@ -547,11 +559,11 @@ int hop_cols(cb_model* m, int src, int dst, const uint16_t* sbase, uint16_t* dba
   return CB_OK;
 }
 
-int proj_gemm(cb_model* m, const ProjView& v, const CUtensorMap* xmaps, int T, int r0, int epi, void* out,
+int proj_gemm(cb_model* m, const ProjView& v, const OpMap* xmaps, int T, int r0, int epi, void* out,
               long long ldo) {
-  CUtensorMap wm;
+  OpMap wm;
   CB_TRY(use(devctx(m, v.dev)));
-  if (cb::make_kmajor_map(&wm, v.base, uint64_t(v.rows), uint64_t(v.k), v.row_stride, 128) != 0)
+  if (cb::make_kmajor_map(&wm.m2, v.base, uint64_t(v.rows), uint64_t(v.k), v.row_stride, 128) != 0)
     return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed for a migrated projection");
   return gemm(m, v.dev, wm, xmaps, v.rows, v.k, T, r0, epi, out, ldo);
 }
@@ -645,7 +657,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
 // fp32 residual rows too for the += epilogues (O, down), and the output rows
 // hop back -- the "module on another device" of PAPER.md:182-189.
 int remote_resid_proj(cb_model* m, const ProjView& v, int dev, const uint16_t* in_local, size_t in_row_bytes,
-                      uint16_t* in_remote, const CUtensorMap* xmaps_remote, int T, int r0) {
+                      uint16_t* in_remote, const OpMap* xmaps_remote, int T, int r0) {
   const size_t x_row = size_t(m->d.d_model) * 4;
   CB_TRY(hop_rows(m, dev, v.dev, in_local, in_remote, in_row_bytes, r0, T));
   CB_TRY(hop_rows(m, dev, v.dev, m->ws[dev].x, m->ws[v.dev].x, x_row, r0, T));
@@ -861,7 +873,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
     CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
   }
-  const CUtensorMap* xm = hw.map_h;
+  const OpMap* xm = hw.map_h;
   if (prefill) {
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.d_model * 4);
     CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * T, hw.hl, bs, d.d_model, hc.compute));

@@ -50,6 +50,11 @@ int finish(cudaError_t e) {
 
 int gemm_setup(const void* w, const void* x, int64_t x_rows, int N, int K, const cb::GemmPlan& plan,
                CUtensorMap* mw, CUtensorMap* mx) {
+  if (plan.kd == 2) {  // 3-D views for the 2-k-block-per-stage kernel
+    if (cb::make_kmajor_map3(mw, w, N, K, K, 128, 2) != 0) return CB_ECUDA;
+    if (cb::make_kmajor_map3(mx, x, x_rows, K, K, plan.box_rows, 2) != 0) return CB_ECUDA;
+    return CB_OK;
+  }
   if (cb::make_kmajor_map(mw, w, N, K, K, 128) != 0) return CB_ECUDA;
   if (cb::make_kmajor_map(mx, x, x_rows, K, K, plan.box_rows) != 0) return CB_ECUDA;
   return CB_OK;
@@ -105,6 +110,7 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   } else if (max_parts == 99) {
     plan.max_parts = 0;  // experiments: force stream-K
   }
+  if (dbg_bits & 4) plan.kd = 1;  // tile-major weight experiment uses 2-D maps
   if (dbg_bits & 512) plan.whole = 1, plan.max_parts = 0, plan.csplit = plan.pair ? 1 : plan.csplit;  // whole tiles
   if (dbg_bits & 1024) plan.whole = 0;                                                          // stream-K
   CUtensorMap mw, mx;
@@ -113,8 +119,9 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   std::vector<CUtensorMap> mws(std::max(1, g_wcopies));
   for (size_t i = 0; i < mws.size(); ++i) {
     const void* wi = static_cast<const uint8_t*>(w) + i * g_wcopy_stride;
-    int e = tiled ? cb::make_kmajor_map(&mws[i], wi, uint64_t(N) * (K / 64), 64, 64, 128)
-                  : cb::make_kmajor_map(&mws[i], wi, N, K, K, 128);
+    int e = tiled           ? cb::make_kmajor_map(&mws[i], wi, uint64_t(N) * (K / 64), 64, 64, 128)
+            : plan.kd == 2 ? cb::make_kmajor_map3(&mws[i], wi, N, K, K, 128, 2)
+                           : cb::make_kmajor_map(&mws[i], wi, N, K, K, 128);
     if (e != 0) return CB_ECUDA;
   }
   cb::GemmArgs a{};
@@ -312,15 +319,6 @@ int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V) {
 // L2, large ones stream from HBM: the per-SM and chip-wide TMA fill rates the
 // GEMM kernels are bounded by.
 namespace {
-__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int c1,
-                                            int c2, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(cb::smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(cb::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
-      : "memory");
-}
-
 // warp w (< nw) streams its own S-stage ring; kd > 1 = 3-D boxes of kd k-slices
 template <int S>
 __global__ void __launch_bounds__(128, 1) tma_probe_kernel(const __grid_constant__ CUtensorMap tm, int rows,
@@ -377,7 +375,7 @@ __global__ void __launch_bounds__(128, 1) tma_probe_kernel(const __grid_constant
     if (kd == 1)
       cb::tma_load_2d(&tm, &bar[s], ring + s * box_bytes, 0, b * box_rows, pol);
     else
-      tma_load_3d(&tm, &bar[s], ring + s * box_bytes, 0, b * box_rows, 0, pol);
+      cb::tma_load_3d(&tm, &bar[s], ring + s * box_bytes, 0, b * box_rows, 0, pol);
   };
   for (; next < S && next < iters; ++next) issue(next);
   for (int i = 0; i < iters; ++i) {
