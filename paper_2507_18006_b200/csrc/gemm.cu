@@ -51,6 +51,7 @@ static constexpr int kChunkBytes = 16 * 32 * 4;  // one epilogue warp chunk: 16 
 static constexpr int kEpiWarpBytes = 16 * kTbRow * 4 + 2 * kChunkBytes;
 static constexpr int kTbufBytes = 4 * kEpiWarpBytes;
 static constexpr int kMaxStages = 16;
+static constexpr size_t kCorunSmem = 112 * 1024;  // per CTA when two CTAs share an SM (228 KB - reserves)
 
 template <int WB, int XB>
 struct RingCfg {
@@ -437,20 +438,23 @@ CB_DEVICE void epi_fixup(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, 
 // stage issue, halving the per-k-block cost of the MMA warp (waits, commits,
 // descriptor moves) that bounds small-T decode GEMMs.
 template <int TN, int KD>
-__global__ void __launch_bounds__(kThreads1, 1)
+__global__ void __launch_bounds__(kThreads1, TN <= 128 ? 2 : 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
   using Cfg = GemmCfg<TN, KD>;
-  constexpr int S = Cfg::kStages;
+  // ring depth chosen at launch (<= Cfg::kStages): a shallow ring lets two CTAs
+  // -- this kernel's and the next kernel's (PDL) -- share an SM
+  const int S = a.stages;
+  const int ring_bytes = S * Cfg::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
-  uint8_t* epi_smem = smem + Cfg::kRingBytes;  // 4 x kEpiWarpBytes
+  uint8_t* epi_smem = smem + ring_bytes;  // 4 x kEpiWarpBytes
   // Two stage rings with a shared index: weights and activations, each with
   // its own full/empty barriers, so the weight ring fills before the
   // activations of the previous kernel exist.
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + kTbufBytes);  // weights landed
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + ring_bytes + kTbufBytes);  // weights landed
   uint64_t* empty_bar = full_bar + S;                                                     // weights consumed
   uint64_t* xfull_bar = empty_bar + S;                                                    // activations landed
   uint64_t* xempty_bar = xfull_bar + S;                                                   // activations consumed
@@ -636,8 +640,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (!whole && csplit == 1) {
         const PartMap pm{a.ws, sk, tile, 1, 0, TN};
         epi_fixup(a, &tmO, e, &a.counters[tile], pm, sk.cta_of(tile * sk.kb), sk.cta_of(tile * sk.kb + sk.kb - 1),
-                  mt * kBM, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes), fix_bar, fix_phase, bcast, et,
-                  tr);
+                  mt * kBM, row0, ncols, last_seg, smem, uint32_t(ring_bytes), fix_bar, fix_phase, bcast, et, tr);
       }
       u += kb1 - kb0;
     }
@@ -972,7 +975,16 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
     const char* e = getenv("COCOB200_KD");
     return e ? atoi(e) : 2;
   }();
-  const int kd2 = (kd_env == 2 && K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // whole-pass rows: replica-invariant
+  // co-resident CTAs (PDL overlap of consecutive GEMMs on one SM) measured
+  // 15-30% slower in the decode step: the shallow ring starves the weight
+  // stream.  Off unless COCOB200_CORUN=1.
+  static const int corun_env = [] {
+    const char* e = getenv("COCOB200_CORUN");
+    return e ? atoi(e) : 0;
+  }();
+  p.corun = (corun_env && kind_T <= 128) ? 1 : 0;
+  // (co-resident CTAs need a small ring: one 64-wide k-block per stage then)
+  const int kd2 = (kd_env == 2 && !p.corun && K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // replica-invariant
   p.kd = 1;
   if (kind_T <= 256 && tiles * 10 < (long long)num_sms * 6) {
     // few wide-K tiles (O / down projections): 1-CTA kernel, cluster split-K
@@ -1029,6 +1041,16 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK * KD - 1) / (kBK * KD);
+  // two co-resident CTAs per SM (<= ~113 KB each) when the plan asks for it
+  int stages = Cfg::kStages;
+  if (plan.corun) {
+    const int fit = int((kCorunSmem - kTbufBytes - 2048) / Cfg::kStageBytes);
+    stages = fit < stages ? fit : stages;
+    if (stages < 2) stages = 2;
+  }
+  if (plan.csplit > 1 && stages * Cfg::kStageBytes < TN * kBM * 4) stages = Cfg::kStages;  // smem holds the partial
+  a.stages = stages;
+  const size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + 1024;
   a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;
@@ -1036,13 +1058,13 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   a.whole_tiles = plan.whole;
   if (plan.csplit > 1)
     return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
-                              Cfg::kSmemBytes, st, unsigned(plan.csplit), w, x, o, a);
+                              smem_bytes, st, unsigned(plan.csplit), w, x, o, a);
   // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
   long long ctas = num_sms;
   if (ctas > a.units) ctas = a.units;
   const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
   if (mp > 0 && ctas > tiles * mp) ctas = tiles * mp;
-  return launch_pdl(gemm_tc_kernel<TN, KD>, dim3(unsigned(ctas)), dim3(kThreads1), Cfg::kSmemBytes, st, w, x, o, a);
+  return launch_pdl(gemm_tc_kernel<TN, KD>, dim3(unsigned(ctas)), dim3(kThreads1), smem_bytes, st, w, x, o, a);
 }
 
 template <int TNP>
