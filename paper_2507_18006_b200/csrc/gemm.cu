@@ -438,7 +438,7 @@ CB_DEVICE void epi_fixup(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, 
 // stage issue, halving the per-k-block cost of the MMA warp (waits, commits,
 // descriptor moves) that bounds small-T decode GEMMs.
 template <int TN, int KD>
-__global__ void __launch_bounds__(kThreads1, TN <= 128 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
   using Cfg = GemmCfg<TN, KD>;
