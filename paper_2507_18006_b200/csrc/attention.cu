@@ -219,6 +219,232 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// attn2: same CTA = (kv head, row, context split) grid, re-mapped for decode:
+//  * every lane group (hd/8 lanes, 16 bytes of a K/V row each) owns whole
+//    positions and computes ALL gq q-heads of the KV group against them, so a
+//    K/V byte is read once per KV head for MHA and GQA alike (the old mapping
+//    re-read the context per q-head group under GQA);
+//  * the fused decode path keeps the row's own (rotated) k / v in registers and
+//    substitutes them at position `cur` inside the loop -- same arithmetic
+//    order as reading them back, but without the append -> __syncthreads ->
+//    reload round trip before the first K/V load;
+//  * groups merge by shuffles inside a warp, then across the 4 warps in smem.
+template <int HD, int GQ, int U>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attn2_kernel(const AttnArgs a, int nsplit, int chunk) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int G = HD / 8;           // lanes per group
+  constexpr int P = 32 / G;           // groups per warp
+  constexpr int NG = kAttnWarps * P;  // groups per CTA
+  extern __shared__ float sm2[];      // [kAttnWarps][GQ][G][10]
+  const int hk = blockIdx.x, rl = blockIdx.y, split = blockIdx.z;
+  const int row = a.row_off + rl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lg = lane % G, pg = lane / G;
+  const int grp = warp * P + pg;
+  const int slot = a.row_slot[row];
+  const int len = a.row_pos[row] + 1;
+  const int cur = len - 1;
+  const int p_begin = split * chunk;
+  const int p_end = min(len, p_begin + chunk);
+  const float qscale = a.scale * 1.4426950408889634f;
+  const size_t kvd = size_t(a.Hkv) * HD;
+  const size_t pos_stride = 2 * kvd;
+  const uint16_t* kbase = a.kv + (size_t)slot * a.max_ctx * pos_stride + (size_t)hk * HD + lg * 8;
+  const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
+  const uint16_t* qrow = a.qkv + row * qkv_ld;
+  const bool fused = a.rope != nullptr;
+  const int hl = lg % (G / 2);
+  const bool first_half = lg < G / 2;
+  const float2* rp = fused ? a.rope + (size_t)cur * (HD / 2) + hl * 8 : nullptr;
+
+  // rotate-half RoPE of 8 consecutive dims held by this lane (partner G/2 lanes away), bf16-rounded
+  auto rope8 = [&](float (&x)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float other = __shfl_xor_sync(0xffffffffu, x[i], G / 2);
+      const float2 cs = rp[i];
+      const float r = first_half ? x[i] * cs.x - other * cs.y : x[i] * cs.x + other * cs.y;
+      x[i] = bf16_to_f(f_to_bf16(r));
+    }
+  };
+  auto load8 = [&](const uint16_t* src, float (&x)[8]) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src);
+    x[0] = bf16_lo(v.x); x[1] = bf16_hi(v.x); x[2] = bf16_lo(v.y); x[3] = bf16_hi(v.y);
+    x[4] = bf16_lo(v.z); x[5] = bf16_hi(v.z); x[6] = bf16_lo(v.w); x[7] = bf16_hi(v.w);
+  };
+
+  float q[GQ][8];
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+    load8(qrow + (size_t)(hk * GQ + h) * HD + lg * 8, q[h]);
+    if (fused) rope8(q[h]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[h][i] *= qscale;
+  }
+  // fused decode: this row's own k (rotated) and v, substituted at position cur
+  uint4 kc = make_uint4(0, 0, 0, 0), vc = make_uint4(0, 0, 0, 0);
+  const bool have_cur = fused && p_begin <= cur && cur < p_end;
+  if (have_cur) {
+    float k8[8];
+    load8(qrow + (size_t)(a.H + hk) * HD + lg * 8, k8);
+    rope8(k8);
+    kc.x = pack_bf16x2(k8[0], k8[1]); kc.y = pack_bf16x2(k8[2], k8[3]);
+    kc.z = pack_bf16x2(k8[4], k8[5]); kc.w = pack_bf16x2(k8[6], k8[7]);
+    vc = *reinterpret_cast<const uint4*>(qrow + (size_t)(a.H + a.Hkv + hk) * HD + lg * 8);
+    if (grp == 0) {  // append (rotated k, raw v) to the cache for the next steps
+      uint16_t* kcp = const_cast<uint16_t*>(kbase) + (size_t)cur * pos_stride;
+      *reinterpret_cast<uint4*>(kcp) = kc;
+      *reinterpret_cast<uint4*>(kcp + kvd) = vc;
+    }
+  }
+
+  float m[GQ], l[GQ], acc[GQ][8];
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[h][i] = 0.f;
+  }
+  // warp-uniform trip count: a warp's groups start at grp = warp*P .. warp*P+P-1
+  const int wbase = p_begin + warp * P;
+  for (int pb = wbase; pb < p_end; pb += NG * U) {
+    uint4 kk[U], vv[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int pos = pb + pg + u * NG;
+      ok[u] = pos < p_end;
+      if (ok[u] && fused && pos == cur) {
+        kk[u] = kc;
+        vv[u] = vc;
+      } else if (ok[u]) {
+        const uint16_t* kp = kbase + (size_t)pos * pos_stride;
+        kk[u] = *reinterpret_cast<const uint4*>(kp);
+        vv[u] = *reinterpret_cast<const uint4*>(kp + kvd);
+      } else {
+        kk[u] = make_uint4(0, 0, 0, 0);
+        vv[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    float kf[U][8];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      kf[u][0] = bf16_lo(kk[u].x); kf[u][1] = bf16_hi(kk[u].x); kf[u][2] = bf16_lo(kk[u].y);
+      kf[u][3] = bf16_hi(kk[u].y); kf[u][4] = bf16_lo(kk[u].z); kf[u][5] = bf16_hi(kk[u].z);
+      kf[u][6] = bf16_lo(kk[u].w); kf[u][7] = bf16_hi(kk[u].w);
+    }
+#pragma unroll
+    for (int h = 0; h < GQ; ++h) {
+      float s[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        s[u] = q[h][0] * kf[u][0] + q[h][1] * kf[u][1] + q[h][2] * kf[u][2] + q[h][3] * kf[u][3] +
+               q[h][4] * kf[u][4] + q[h][5] * kf[u][5] + q[h][6] * kf[u][6] + q[h][7] * kf[u][7];
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+        for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+      float mx = m[h];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) s[u] = -INFINITY;
+        mx = fmaxf(mx, s[u]);
+      }
+      if (mx != -INFINITY) {
+        const float cf = exp2f(m[h] - mx);
+        l[h] *= cf;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[h][i] *= cf;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const float pr = exp2f(s[u] - mx);
+          l[h] += pr;
+          acc[h][0] += pr * bf16_lo(vv[u].x);
+          acc[h][1] += pr * bf16_hi(vv[u].x);
+          acc[h][2] += pr * bf16_lo(vv[u].y);
+          acc[h][3] += pr * bf16_hi(vv[u].y);
+          acc[h][4] += pr * bf16_lo(vv[u].z);
+          acc[h][5] += pr * bf16_hi(vv[u].z);
+          acc[h][6] += pr * bf16_lo(vv[u].w);
+          acc[h][7] += pr * bf16_hi(vv[u].w);
+        }
+        m[h] = mx;
+      }
+    }
+  }
+  // merge the P groups of a warp (lanes lg, lg+G, ...) with shuffles
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m[h], o);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l[h], o);
+      const float M = fmaxf(m[h], m2);
+      const float c1 = (m[h] == -INFINITY) ? 0.f : exp2f(m[h] - M);
+      const float c2 = (m2 == -INFINITY) ? 0.f : exp2f(m2 - M);
+      l[h] = l[h] * c1 + l2 * c2;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, acc[h][i], o);
+        acc[h][i] = acc[h][i] * c1 + a2 * c2;
+      }
+      m[h] = M;
+    }
+  }
+  if (pg == 0) {
+#pragma unroll
+    for (int h = 0; h < GQ; ++h) {
+      float* st = sm2 + ((warp * GQ + h) * G + lg) * 10;
+      st[0] = m[h];
+      st[1] = l[h];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) st[2 + i] = acc[h][i];
+    }
+  }
+  __syncthreads();
+  // warp w finalises heads h = w, w + 4, ... over the 4 warps' states (lanes < G)
+  if (pg == 0) {
+    for (int h = warp; h < GQ; h += kAttnWarps) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int f = 0; f < kAttnWarps; ++f) M = fmaxf(M, sm2[((f * GQ + h) * G + lg) * 10]);
+      float L = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int f = 0; f < kAttnWarps; ++f) {
+        const float* stt = sm2 + ((f * GQ + h) * G + lg) * 10;
+        const float cw = (stt[0] == -INFINITY) ? 0.f : exp2f(stt[0] - M);
+        L += stt[1] * cw;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += stt[2 + i] * cw;
+      }
+      const int qh = hk * GQ + h;
+      if (nsplit == 1) {
+        const float inv = 1.f / L;
+        uint4 ov;
+        ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
+        ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
+        ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
+        ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
+        *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
+      } else {
+        const size_t idx = ((size_t)rl * a.H + qh) * nsplit + split;
+        float* st = a.ws + idx * (HD + 2);
+        if (lg == 0) {
+          st[0] = M;
+          st[1] = L;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st[2 + lg * 8 + i] = o[i];
+      }
+    }
+  }
+}
+
 template <int HD>
 __global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
   pdl_trigger();
@@ -269,8 +495,27 @@ static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st)
   }();
   const long long total = ctas * nsplit;
   const int u = forced ? forced : (gq == 1 && total >= 8LL * num_sms ? 4 : 8);
-  cudaError_t e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major)
-                         : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major);
+  static const int v2 = [] {
+    const char* e = getenv("CB_ATTN_V1");
+    return e ? 0 : 1;
+  }();
+  cudaError_t e;
+  if (v2) {
+    const dim3 g2(a.Hkv, a.T, nsplit);
+    const size_t sm = size_t(kAttnWarps) * gq * (HD / 8) * 10 * sizeof(float);
+    switch (gq) {
+      case 1: e = u == 8 ? launch_pdl(attn2_kernel<HD, 1, 8>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk)
+                         : launch_pdl(attn2_kernel<HD, 1, 4>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk);
+        break;
+      case 2: e = launch_pdl(attn2_kernel<HD, 2, 4>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk); break;
+      case 4: e = launch_pdl(attn2_kernel<HD, 4, 4>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk); break;
+      case 8: e = launch_pdl(attn2_kernel<HD, 8, 2>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk); break;
+      default: e = cudaErrorInvalidValue;
+    }
+  } else {
+    e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major)
+               : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major);
+  }
   if (e != cudaSuccess || nsplit == 1) return e;
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);
 }
