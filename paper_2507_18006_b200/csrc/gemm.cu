@@ -66,11 +66,14 @@ struct RingCfg {
 };
 template <int TN, int KD = 1>
 struct GemmCfg : RingCfg<kBM * kBK * 2 * KD, TN * kBK * 2 * KD> {
-  static constexpr uint32_t kTmemCols = (2 * TN <= 32)    ? 32
-                                        : (2 * TN <= 64)  ? 64
-                                        : (2 * TN <= 128) ? 128
-                                        : (2 * TN <= 256) ? 256
-                                                          : 512;
+  // accumulators: [0, 2TN) double buffer for whole tiles, then (TN <= 128) two
+  // retained partial tiles for cluster stream-K: [2TN, 3TN) first, [3TN, 4TN) last
+  static constexpr uint32_t kAccCols = TN <= 128 ? 4 * TN : 2 * TN;
+  static constexpr uint32_t kTmemCols = (kAccCols <= 32)    ? 32
+                                        : (kAccCols <= 64)  ? 64
+                                        : (kAccCols <= 128) ? 128
+                                        : (kAccCols <= 256) ? 256
+                                                            : 512;
 };
 template <int TNP>
 struct PairCfg : RingCfg<kBM * kBK * 2, (TNP / 2) * kBK * 2> {
@@ -461,7 +464,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
   uint64_t* tfull_bar = xempty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* fix_bar = tempty_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
+  uint64_t* pfull_bar = fix_bar + 1;  // cluster stream-K: retained partial [first, last] complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull_bar + 2);
   int* bcast = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -472,8 +476,22 @@ __global__ void __launch_bounds__(kThreads1, 1)
   // Work range: stream-K slice of the (tile, k-block) space, or -- in cluster
   // split mode -- k-slice r of tile c / S (the cluster = the tile's S CTAs).
   const int csplit = a.cluster_split > 1 ? a.cluster_split : 1;
+  // Cluster stream-K (cstream = cs > 1): cluster g owns whole tiles [T0, T1);
+  // its units are split evenly over its cs CTAs, so a split tile is only ever
+  // shared by CTAs of one cluster and is reduced through DSMEM (no fixup in
+  // global memory).  A CTA keeps its first / last partial tile in TMEM.
+  const int cs = a.cstream > 1 ? a.cstream : 1;
+  int cl_u0 = 0, cl_units = 0;
   int ubeg, uend;
-  if (csplit > 1) {
+  if (cs > 1) {
+    const int tiles = sk.units / sk.kb;
+    const int nc = int(gridDim.x) / cs, g = c / cs, r = c % cs;
+    const int t0 = int((long long)g * tiles / nc), t1 = int((long long)(g + 1) * tiles / nc);
+    cl_u0 = t0 * sk.kb;
+    cl_units = (t1 - t0) * sk.kb;
+    ubeg = cl_u0 + int((long long)r * cl_units / cs);
+    uend = cl_u0 + int((long long)(r + 1) * cl_units / cs);
+  } else if (csplit > 1) {
     const int tile = c / csplit, r = c % csplit;
     ubeg = tile * sk.kb + (r * sk.kb) / csplit;
     uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
@@ -502,6 +520,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
       mbar_init(&tempty_bar[i], kEpiThreads);
     }
     mbar_init(fix_bar, 1);
+    mbar_init(&pfull_bar[0], 1);
+    mbar_init(&pfull_bar[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -566,9 +586,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
     for (int u = ubeg; u < uend;) {
       const int kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
-      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      // cluster stream-K: a partial tile accumulates into its retained buffer
+      const bool keep = cs > 1 && !(kb0 == 0 && kb1 == sk.kb);
+      const int pslot = (u == ubeg) ? 0 : 1;
+      if (!keep) mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + uint32_t(acc * TN);
+      const uint32_t d_tmem = tmem_base + uint32_t(keep ? (2 + pslot) * TN : acc * TN);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         mbar_wait(&xfull_bar[stage], phase);
@@ -595,6 +618,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
       __syncwarp();
+      if (keep) {
+        umma_commit_elect(&pfull_bar[pslot]);
+        u += kb1 - kb0;
+        continue;
+      }
       if (a.dbg & 1) {
         if (lane == 0) mbar_arrive(&tfull_bar[acc]);
       } else {
@@ -622,6 +650,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const int ncols = min(TN, a.T - tt * TN);
       const bool whole = (kb0 == 0 && kb1 == sk.kb);
       const bool last_seg = (u + (kb1 - kb0) == uend);
+      if (cs > 1 && !whole) {  // retained in TMEM, reduced through DSMEM after the loop
+        u += kb1 - kb0;
+        continue;
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       unsigned long long* tr = (a.trace && et == 0 && seg_i < 4) ? a.trace + (size_t)c * 512 + 130 + 4 * seg_i : nullptr;
@@ -645,7 +677,71 @@ __global__ void __launch_bounds__(kThreads1, 1)
       u += kb1 - kb0;
     }
     e.drain();
+    if (cs > 1) {
+      // retained partials -> this CTA's (idle) stage ring, chunk-major, slot 0 =
+      // first segment.  Slot 1 first: its commit retires every MMA of the CTA, so
+      // no MMA still reads the ring when slot 0 is written over it.
+      for (int slot = 1; slot >= 0; --slot) {
+        const int u = slot == 0 ? ubeg : (uend - 1);
+        if (ubeg >= uend || (slot == 1 && u / sk.kb == ubeg / sk.kb)) continue;  // single segment: slot 0 only
+        const int kb0 = slot == 0 ? ubeg % sk.kb : 0;
+        const int kb1 = slot == 0 ? min(sk.kb, kb0 + (uend - ubeg)) : (uend - 1) % sk.kb + 1;
+        if (kb0 == 0 && kb1 == sk.kb) continue;  // whole: emitted in the loop
+        mbar_wait(&pfull_bar[slot], 0);
+        tc_fence_after();
+        const int tt = (u / sk.kb) % n_ttiles;
+        const int ncols = min(TN, a.T - tt * TN);
+        const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t((2 + slot) * TN);
+        float* part = reinterpret_cast<float*>(smem) + slot * (TN * kBM);
+        for (int c0 = 0; c0 < ncols; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(t_addr + uint32_t(c0), r);
+          tmem_ld_wait();
+          float* pc = part + part_chunk(c0, q);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pc[i * 32 + lane] = __uint_as_float(r[i]);
+        }
+      }
+    }
     if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
+  }
+  if (cs > 1) {
+    // every CTA of the cluster deposited its partials; the CTA holding a split
+    // tile's first k-block sums the parts (rank order) through DSMEM and emits
+    cluster_sync_all();
+    if (warp >= 2 && warp < 6) {
+      const int q = warp & 3;
+      EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
+      const int r_me = c % cs;
+      const uint32_t base = smem_u32(smem);
+      auto rank_of = [&](int uu) { return int(((long long)(uu - cl_u0 + 1) * cs - 1) / cl_units); };
+      auto beg_of = [&](int rr) { return cl_u0 + int((long long)rr * cl_units / cs); };
+      for (int tile = ubeg / sk.kb; ubeg < uend && tile <= (uend - 1) / sk.kb; ++tile) {
+        const int ra = rank_of(tile * sk.kb), rb = rank_of(tile * sk.kb + sk.kb - 1);
+        if (ra != r_me || ra == rb) continue;  // not the head of a split tile
+        const int mt = tile / n_ttiles, tt = tile % n_ttiles;
+        const int row0 = a.row_off + tt * TN;
+        const int ncols = min(TN, a.T - tt * TN);
+        for (int ch = 0; ch < (ncols + 15) / 16; ++ch) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int rr = ra; rr <= rb; ++rr) {
+            const int slot = (beg_of(rr) / sk.kb == tile) ? 0 : 1;
+            const uint32_t off = base + uint32_t((slot * (TN * kBM) + part_chunk(ch * 16, q) + lane) * 4);
+            const uint32_t ra_addr = dsmem_map(off, uint32_t(rr));
+            float x[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[i] = dsmem_ld_f32(ra_addr + uint32_t(i * 128));
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += x[i];
+          }
+          emit_chunk(a, &tmO, e, mt * kBM + q * 32, row0 + ch * 16, min(16, ncols - ch * 16), v);
+        }
+      }
+      e.drain();
+    }
+    cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
   if (csplit > 1) {
     // Cluster split-K: every CTA of the cluster holds a partial [TN][128] in
@@ -946,6 +1042,36 @@ int gemm_pick_tn(int T) {
   return 256;
 }
 
+// How many clusters of `cs` 1-CTA-kernel CTAs can be resident at once (one CTA
+// per SM; GPCs are not multiples of every cluster size).  Cached per device.
+static int cluster_capacity(int cs, int num_sms) {
+  static int cache[64][9] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& slot = cache[dev & 63][cs & 7];
+  if (slot) return slot;
+  using Cfg = GemmCfg<64, 2>;
+  cudaFuncSetAttribute(gemm_tc_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmemBytes));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(unsigned(cs));
+  cfg.blockDim = dim3(unsigned(kThreads1));
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(cs);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<64, 2>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms / cs;
+  }
+  slot = n;
+  return n;
+}
+
 // Work split of one launch.  Everything but the TN bucket depends on (N, K),
 // the kernel kind and the tile count only, so within one kind a decode row's
 // result does not depend on how many rows share the launch.
@@ -1011,6 +1137,36 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   if (tiles <= num_sms) p.max_parts = 1;             // QKV: one wave of whole tiles
   if (tiles * 2 >= (long long)num_sms * 3) p.whole = 1;  // lm_head (>= 1.5 waves): whole tiles
   p.box_rows = p.tn;
+  // Cluster stream-K when it balances better than the options above: units
+  // (stages) per CTA of the most loaded CTA, a global stream-K split charged a
+  // fixup of ~a third of a tile.  Correct (tested) but measured 5-15% slower
+  // than the plans above on the 7B decode shapes (co-resident cluster counts),
+  // so it is opt-in: COCOB200_CSTREAM=1.
+  static const int cstream_env = [] {
+    const char* e = getenv("COCOB200_CSTREAM");
+    return e ? atoi(e) : 0;
+  }();
+  const long long units_tile = (K + kBK * p.kd - 1) / (kBK * p.kd);
+  long long best = p.max_parts == 1 ? units_tile
+                   : p.whole        ? (tiles + num_sms - 1) / num_sms * units_tile
+                                    : (tiles * units_tile + num_sms - 1) / num_sms + units_tile / 3;
+  if (cstream_env && T <= 128) {
+    for (int cs = 2; cs <= 4; ++cs) {
+      const long long nc = std::min<long long>(cluster_capacity(cs, num_sms), tiles);
+      if (nc < 1) continue;
+      const long long tpc = (tiles + nc - 1) / nc;
+      const long long per = (tpc * units_tile + cs - 1) / cs + 1;  // +1: the DSMEM reduction
+      if (per < best) {
+        best = per;
+        p.cstream = cs;
+        p.nclusters = int(nc);
+      }
+    }
+    if (p.cstream > 1) {
+      p.max_parts = 0;
+      p.whole = 0;
+    }
+  }
   return p;
 }
 
@@ -1059,6 +1215,10 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   if (plan.csplit > 1)
     return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
                               smem_bytes, st, unsigned(plan.csplit), w, x, o, a);
+  a.cstream = plan.cstream;
+  if (plan.cstream > 1)
+    return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(plan.nclusters * plan.cstream)),
+                              dim3(kThreads1), smem_bytes, st, unsigned(plan.cstream), w, x, o, a);
   // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
   long long ctas = num_sms;
   if (ctas > a.units) ctas = a.units;

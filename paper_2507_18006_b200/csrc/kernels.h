@@ -35,6 +35,7 @@ struct GemmArgs {
   int tma;            // set by the launcher: an output tensor map was passed (TMA-store epilogue)
   int whole_tiles;    // set from the plan: CTA (pair) ranges rounded to whole tiles
   int stages;         // set by the launcher: pipeline ring depth (1-CTA kernel)
+  int cstream;        // set from the plan: cluster stream-K cluster size (> 1)
   int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
@@ -58,6 +59,8 @@ struct GemmPlan {
   int whole;     // 1 = persistent over whole tiles (contiguous tile ranges per CTA / pair, no fixups)
   int kd;        // k-blocks (64 wide) per pipeline stage: 2 = 3-D TMA maps (make_kmajor_map3), 1-CTA kernel only
   int corun;     // 1 = shallow ring so two CTAs (this kernel's and the next one's) share an SM
+  int cstream;   // > 1: cluster stream-K, clusters of cstream CTAs each owning whole tiles (DSMEM reduce)
+  int nclusters; // cluster stream-K: number of clusters
 };
 // kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
 // micro-batches compute exactly what the unreplicated pass would.
