@@ -31,6 +31,9 @@ int cbt_attention_bench(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, 
                         const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,
                         int32_t max_len, int32_t iters, float* ms_per_launch);
 int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
+/* causal tensor-core prefill attention: blocks_dev = int4 (row, rows <= 64, slot, first position) per block */
+int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
+                          int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx);
 /* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
                    void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch);

@@ -107,6 +107,10 @@ cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
 
 // act = bf16(silu(gate) * act) over rows [row_off, row_off + T) of [rows][d_ff] buffers (d_ff % 8 == 0)
 cudaError_t swiglu_launch(const uint16_t* gate, uint16_t* act, int T, int d_ff, int row_off, cudaStream_t st);
+// Causal prefill attention on the tensor cores: blocks[i] = (first row relative to
+// a.row_off, rows (<= 64), slot, first position) of one sequence; q already rotated
+// and the block's K/V already in the cache (rope_kv_launch).  Grid (blocks, H).
+cudaError_t prefill_attention_launch(const AttnArgs& a, const int4* blocks, int nblocks, cudaStream_t st);
 // dst[i, :] = src[idx[i], :] (bf16 rows; prefill keeps only each sequence's last row)
 cudaError_t gather_rows_launch(const uint16_t* src, const int32_t* idx, uint16_t* dst, int n, int d,
                                cudaStream_t st);

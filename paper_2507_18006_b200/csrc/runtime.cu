@@ -181,6 +181,8 @@ struct cb_model {
   std::vector<std::vector<Route>> last_routing;
   int cur_phase = 0;  // CB_PHASE_* of the pass in flight
   int cur_T = 0;  // rows of the pass in flight: per-step meta = [tokens | slot | pos] x T, then gather x bs
+  int cur_bs = 0;  // sequences of the pass in flight
+  std::vector<int> seq_blk;  // prefill: first q-block of each sequence (+ total), blocks follow the gather list
   Prof prof;
 };
 
@@ -314,7 +316,7 @@ int ensure_ws(cb_model* m, int dev) {
   CB_TRY(dev_alloc(dc, (void**)&w.qkv, T * m->qkv_n * 2));
   CB_TRY(dev_alloc(dc, (void**)&w.att, T * m->q_n * 2));
   CB_TRY(dev_alloc(dc, (void**)&w.act, T * d.d_ff * 2));
-  CB_TRY(dev_alloc(dc, (void**)&w.meta, (3 * T + d.max_slots) * 4));
+  CB_TRY(dev_alloc(dc, (void**)&w.meta, (3 * T + d.max_slots + 4 + 4 * (T / 64 + d.max_slots)) * 4));
   CB_TRY(dev_alloc(dc, (void**)&w.next, size_t(d.max_slots) * 4));
   const size_t gws = cb::gemm_ws_floats(dc.num_sms);
   CB_TRY(dev_alloc(dc, (void**)&w.gemm_ws, gws * 4));
@@ -614,6 +616,35 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
     CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
                                d.max_ctx, ac.compute));
   }
+  static const bool pf_rows = std::getenv("COCOB200_PREFILL_ROWS") != nullptr;  // A/B: row-parallel prefill
+  if (!fused && !pf_rows) {
+    // prefill: causal tensor-core attention over the segment's sequences' 64-row blocks
+    const int b0 = m->seq_blk[s.s0], b1 = m->seq_blk[s.s1];
+    const int4* blocks = reinterpret_cast<const int4*>(wa.meta + ((3 * m->cur_T + m->cur_bs + 3) & ~3)) + b0;
+    cb::AttnArgs pa{};
+    pa.qkv = wa.qkv;
+    pa.kv = kv;
+    pa.out = wa.att;
+    pa.T = T;
+    pa.row_off = 0;  // block rows are absolute pass rows
+    pa.H = d.n_heads;
+    pa.Hkv = d.n_kv_heads;
+    pa.hd = m->hd;
+    pa.max_ctx = d.max_ctx;
+    pa.scale = 1.0f / std::sqrt(float(m->hd));
+    double flops = 0;  // QK^T + PV over the causal prefix of every row
+    for (int r = s.r0; r < s.r1; ++r) flops += 4.0 * (row_pos[r] + 1) * m->q_n;
+    ProfScope ps(m, ad, CB_KCLASS_ATTENTION, ac.compute, double(T) * m->q_n * 4, flops);
+    CB_CUDA(cb::prefill_attention_launch(pa, blocks, b1 - b0, ac.compute));
+    if (ad != dev) {
+      CB_TRY(depend(dc, ac));
+      CB_TRY(use(dc));
+      CB_CUDA(cudaMemcpyPeerAsync(reinterpret_cast<uint8_t*>(ws.att) + s.r0 * att_row, dc.ordinal,
+                                  reinterpret_cast<uint8_t*>(wa.att) + s.r0 * att_row, ac.ordinal, T * att_row,
+                                  dc.compute));
+    }
+    return CB_OK;
+  }
   int max_len = 0;
   double kv_tokens = 0;
   for (int r = s.r0; r < s.r1; ++r) {
@@ -818,6 +849,25 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       meta[2 * T + r] = pos;
     }
   for (int i = 0; i < bs; ++i) meta[3 * T + i] = seq_row[i + 1] - 1;
+  // prefill: 64-row query blocks of every sequence for the tensor-core attention
+  m->cur_bs = bs;
+  m->seq_blk.assign(bs + 1, 0);
+  int nblk = 0;
+  const int blk_off = (3 * T + bs + 3) & ~3;  // int4-aligned
+  if (prefill) {
+    int32_t* blk = meta + blk_off;
+    for (int i = 0; i < bs; ++i) {
+      m->seq_blk[i] = nblk;
+      const int len = seq_row[i + 1] - seq_row[i];
+      for (int b0 = 0; b0 < len; b0 += 64, ++nblk) {
+        blk[4 * nblk + 0] = seq_row[i] + b0;
+        blk[4 * nblk + 1] = std::min(64, len - b0);
+        blk[4 * nblk + 2] = slots[i];
+        blk[4 * nblk + 3] = b0;
+      }
+    }
+    m->seq_blk[bs] = nblk;
+  }
 
   // participating devices
   std::vector<int> devs{m->home};
@@ -832,7 +882,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   DeviceCtx& hc = devctx(m, m->home);
   CB_TRY(use(hc));
   CB_CUDA(cudaEventRecord(hc.t0, hc.compute));
-  const size_t meta_bytes = (3 * size_t(T) + bs) * 4;  // exactly what this pass needs
+  const size_t meta_bytes = (size_t(blk_off) + 4 * size_t(nblk)) * 4;  // exactly what this pass needs
   for (int dv : devs) {
     CB_TRY(ensure_ws(m, dv));
     DeviceCtx& dc = devctx(m, dv);
@@ -1193,7 +1243,8 @@ int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home, cb_
   m->layers.resize(d.n_layers);
   m->slot_len.assign(d.max_slots, 0);
   cudaSetDevice(rt->devs[home].ordinal);
-  if (cudaMallocHost(&m->pin_meta, (3 * size_t(d.max_tokens) + d.max_slots) * 4) != cudaSuccess ||
+  if (cudaMallocHost(&m->pin_meta, (3 * size_t(d.max_tokens) + d.max_slots + 4 +
+                                    4 * (size_t(d.max_tokens) / 64 + d.max_slots)) * 4) != cudaSuccess ||
       cudaMallocHost(&m->pin_next, size_t(d.max_slots) * 4) != cudaSuccess) {
     delete m;
     return fail(CB_ECUDA, "pinned host allocation failed");

@@ -512,3 +512,21 @@ extern "C" int cbt_mma_probe(int32_t N, int32_t n, int32_t grid, int32_t kstep, 
   *cyc_per_mma = s / grid / n;
   return CB_OK;
 }
+
+// causal prefill attention: rows [0, T) of qkv hold consecutive prompts; blocks_dev
+// = int4 (row, rows, slot, first position) per 64-row block; K/V already in kv.
+extern "C" int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
+                                     int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd,
+                                     int32_t max_ctx) {
+  cb::AttnArgs a{};
+  a.qkv = qkv;
+  a.kv = kv;
+  a.out = out;
+  a.T = T;
+  a.H = H;
+  a.Hkv = Hkv;
+  a.hd = hd;
+  a.max_ctx = max_ctx;
+  a.scale = 1.0f / std::sqrt(float(hd));
+  return finish(cb::prefill_attention_launch(a, reinterpret_cast<const int4*>(blocks_dev), nblocks, 0));
+}

@@ -1,4 +1,2 @@
-timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_model_gpu.py -q -x 2>&1 | tail -15 > gpurun_out/kt11.txt
-timeout 300 python scripts/gemm_perf.py 0 8,64,128 --real-epi > gpurun_out/perf_cs.txt 2>&1
-COCOB200_CSTREAM=0 timeout 300 python scripts/gemm_perf.py 0 8,64,128 --real-epi > gpurun_out/perf_nocs.txt 2>&1
-for i in 1 2; do for B in 64 128; do timeout 300 python scripts/step_profile.py $B 20 2>&1 | head -1 | sed "s/^/cs   /"; COCOB200_CSTREAM=0 timeout 300 python scripts/step_profile.py $B 20 2>&1 | head -1 | sed "s/^/nocs /"; done; done > gpurun_out/step_cs.txt
+timeout 600 python -m pytest tests/test_model_gpu.py tests/test_kernels_gpu.py -q -x 2>&1 | tail -15 > gpurun_out/kt13.txt
+for L in 128 512 2048; do timeout 300 python scripts/prefill_profile.py $((8192/L)) $L; done > gpurun_out/prefill2.txt 2>&1
