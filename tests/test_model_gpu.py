@@ -362,3 +362,22 @@ def test_kv_offload_to_host_and_back_matches_oracle(runtime, confident):
         assert np.array_equal(nxt, ref.argmax(-1)), step
         assert np.abs(lg - ref).max() <= LOGIT_TOL
     ex.close()
+
+
+def test_ragged_long_prompts_prefill_matches_oracle(runtime, confident):
+    """Ragged prompts longer than one 64-row prefill block (1 .. 150 tokens) in
+    one pass, layer 2 replicated (prompts split across the two replicas): the
+    tensor-core causal prefill attention + decode continue to match the fp32
+    oracle (tokens equal, logits within 2e-2)."""
+    rng = np.random.default_rng(5)
+    lens = [150, 1, 64, 65, 130, 7]
+    prompts = [rng.integers(0, TINY.vocab, L).astype(np.int32) for L in lens]
+    ex = Executor(runtime, _tiny_cfg(max_ctx=192, max_tokens=512))
+    ex.load_model(confident, device_of_layer=0)
+    cat, cl = _catalog_cluster()
+    ex.apply(O.ReplicateLayer(2, 1), cat, cl)
+    got, logits = _greedy_gpu(ex, prompts, 6)
+    ref, ref_logits = greedy_generate(OracleModel(TINY, confident, 192), prompts, 6, replicas={1: 2})
+    assert np.array_equal(got, ref)
+    assert max(np.abs(a - b).max() for a, b in zip(logits, ref_logits)) <= LOGIT_TOL
+    ex.close()
