@@ -271,7 +271,7 @@ def run_single(args) -> None:
     for sb in sorted(sweep):
         s_slots = all_slots[:sb]
         s_next = all_next[:sb]
-        for _ in range(2):
+        for _ in range(max(3, args.warmup)):
             s_next, _, _ = ex.decode(s_slots, s_next)
         ms = []
         for _ in range(args.sweep_steps):

@@ -34,6 +34,53 @@ cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x,
   return launch_pdl(embed_kernel, dim3((T + 3) / 4), dim3(128), 0, st, table, tokens, x, T, d, row_off);
 }
 
+// Embedding + the producer half of the fused RMSNorm of layer 0: besides x,
+// h = bf16(x * gamma) and ssq[t][g] = sum of x^2 over features 32g..32g+31
+// (the QKV GEMM scales its outputs by rsqrt(mean(x^2) + eps); kernels.h GemmArgs).
+__global__ void embed_norm_kernel(const uint16_t* __restrict__ table, const int32_t* __restrict__ tokens,
+                                  float* __restrict__ x, const uint16_t* __restrict__ gamma, uint16_t* __restrict__ h,
+                                  float* __restrict__ ssq, int T, int d, int row_off) {
+  pdl_trigger();
+  pdl_wait();
+  const int warps = blockDim.x >> 5;
+  const int t = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const size_t row = size_t(row_off + t);
+  const uint4* src = reinterpret_cast<const uint4*>(table + (size_t)tokens[t] * d);
+  const uint4* g8 = reinterpret_cast<const uint4*>(gamma);
+  float4* dst = reinterpret_cast<float4*>(x + row * d);
+  uint4* hd = reinterpret_cast<uint4*>(h + row * d);
+  const int np = d >> 5;
+  for (int i = lane; i < d / 8; i += 32) {  // d % 256 == 0: every lane of the warp is active
+    const uint4 v = __ldg(src + i), g = __ldg(g8 + i);
+    const float e[8] = {bf16_lo(v.x), bf16_hi(v.x), bf16_lo(v.y), bf16_hi(v.y),
+                        bf16_lo(v.z), bf16_hi(v.z), bf16_lo(v.w), bf16_hi(v.w)};
+    dst[2 * i] = make_float4(e[0], e[1], e[2], e[3]);
+    dst[2 * i + 1] = make_float4(e[4], e[5], e[6], e[7]);
+    uint4 o;
+    o.x = pack_bf16x2(e[0] * bf16_lo(g.x), e[1] * bf16_hi(g.x));
+    o.y = pack_bf16x2(e[2] * bf16_lo(g.y), e[3] * bf16_hi(g.y));
+    o.z = pack_bf16x2(e[4] * bf16_lo(g.z), e[5] * bf16_hi(g.z));
+    o.w = pack_bf16x2(e[6] * bf16_lo(g.w), e[7] * bf16_hi(g.w));
+    hd[i] = o;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += e[k] * e[k];
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if ((lane & 3) == 0) ssq[row * np + (i >> 2)] = s;
+  }
+}
+
+cudaError_t embed_norm_launch(const uint16_t* table, const int32_t* tokens, float* x, const uint16_t* gamma,
+                              uint16_t* h, float* ssq, int T, int d, int row_off, cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  if (d % 256 != 0) return cudaErrorInvalidValue;
+  return launch_pdl(embed_norm_kernel, dim3((T + 3) / 4), dim3(128), 0, st, table, tokens, x, gamma, h, ssq, T, d,
+                    row_off);
+}
+
 // ---------------------------------------------------------------- SwiGLU combine
 // act[r] = bf16(silu(gate[r]) * up[r]) in place over act, rows [row_off, row_off + T):
 // the gate/up pair of a layer whose FFN_PROJ_GATE / FFN_PROJ_UP was migrated

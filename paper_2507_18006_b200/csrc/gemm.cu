@@ -51,6 +51,11 @@ static constexpr int kChunkBytes = 16 * 32 * 4;  // one epilogue warp chunk: 16 
 static constexpr int kEpiWarpBytes = 16 * kTbRow * 4 + 2 * kChunkBytes;
 static constexpr int kTbufBytes = 4 * kEpiWarpBytes;
 static constexpr int kMaxStages = 16;
+// after the transpose buffers: mbarriers (first 1 KB), then the fused-RMSNorm
+// row-scale table (256 fp32, one per token row of the CTA's token tile)
+static constexpr int kBarBytes = 2048;
+static constexpr int kRtabOff = 1024;
+static constexpr int kMaxNormRows = 256;
 static constexpr size_t kCorunSmem = 112 * 1024;  // per CTA when two CTAs share an SM (228 KB - reserves)
 
 template <int WB, int XB>
@@ -58,11 +63,11 @@ struct RingCfg {
   static constexpr int kWBytes = WB;
   static constexpr int kXBytes = XB;
   static constexpr int kStageBytes = WB + XB;
-  static constexpr int kStagesRaw = int((kSmemBudget - 2048 - kTbufBytes) / kStageBytes);
+  static constexpr int kStagesRaw = int((kSmemBudget - 1024 - kBarBytes - kTbufBytes) / kStageBytes);
   static constexpr int kStages = kStagesRaw > kMaxStages ? kMaxStages : kStagesRaw;
   static constexpr int kRingBytes = kStages * kStageBytes;
   // ring | transpose buffers | barriers
-  static constexpr size_t kSmemBytes = size_t(kRingBytes) + kTbufBytes + 1024 /*align slack*/ + 1024 /*barriers*/;
+  static constexpr size_t kSmemBytes = size_t(kRingBytes) + kTbufBytes + 1024 /*align slack*/ + kBarBytes;
 };
 template <int TN, int KD = 1>
 struct GemmCfg : RingCfg<kBM * kBK * 2 * KD, TN * kBK * 2 * KD> {
@@ -200,16 +205,27 @@ CB_DEVICE void load8(const float* src, float (&s)[8]) {
 // One warp's 32 weight rows (lane = row) x 16 token columns, transposed through
 // the warp's smem buffer so every lane stores whole 16-byte runs of one token
 // row: 2 store instructions per chunk instead of 16 scalar ones.
+// Residual rows of one warp chunk in the fp32 store mapping: lane -> (token
+// p*4 + lane/8, 4 features at (lane%8)*4).
+CB_DEVICE void load_res(const GemmArgs& a, int nw0, int row, int nc, int lane, float4 (&res)[4]) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
+    res[p] = (i < nc && nw0 + f0 < a.N) ? __ldcg(reinterpret_cast<const float4*>(out_f32(a, nw0 + f0, row + i)))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 CB_DEVICE void emit_warp_vec(const GemmArgs& a, float* tb, int nw0, int row, int nc, const float (&v)[16],
-                             int lane) {
-  // fp32 outputs: lane -> (token p*4 + lane/8, 4 rows at (lane%8)*4); residual loads issued first
+                             int lane, const float4* res_pre = nullptr, const uint2* g_pre = nullptr) {
+  // fp32 outputs: residual loads issued first (or prefetched by the caller)
   float4 res[4];
   if (a.epi == EPI_RESID) {
+    if (res_pre) {
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
-      res[p] = (i < nc && nw0 + f0 < a.N) ? __ldcg(reinterpret_cast<const float4*>(out_f32(a, nw0 + f0, row + i)))
-                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int p = 0; p < 4; ++p) res[p] = res_pre[p];
+    } else {
+      load_res(a, nw0, row, nc, lane, res);
     }
   }
 #pragma unroll
@@ -236,13 +252,35 @@ CB_DEVICE void emit_warp_vec(const GemmArgs& a, float* tb, int nw0, int row, int
       }
     }
   } else {
+    float ss[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       const int i = p * 4 + (lane >> 3), f0 = (lane & 7) * 4;
+      ss[p] = 0.f;
       if (i < nc && nw0 + f0 < a.N) {
         float4 x = *reinterpret_cast<const float4*>(tb + i * kTbRow + f0);
         if (a.epi == EPI_RESID) x = make_float4(res[p].x + x.x, res[p].y + x.y, res[p].z + x.z, res[p].w + x.w);
         *reinterpret_cast<float4*>(out_f32(a, nw0 + f0, row + i)) = x;
+        if (a.h_out) {  // fused RMSNorm producer: h' = bf16(x * gamma), partial sum of squares
+          const uint2 g = g_pre ? *g_pre : *reinterpret_cast<const uint2*>(a.gamma_next + nw0 + f0);
+          uint2 h;
+          h.x = pack_bf16x2(x.x * bf16_lo(g.x), x.y * bf16_hi(g.x));
+          h.y = pack_bf16x2(x.z * bf16_lo(g.y), x.w * bf16_hi(g.y));
+          *reinterpret_cast<uint2*>(a.h_out + (size_t)(row + i) * a.ldo + nw0 + f0) = h;
+          ss[p] = x.x * x.x + x.y * x.y + x.z * x.z + x.w * x.w;
+        }
+      }
+    }
+    if (a.h_out) {
+      // the 8 lanes of token i hold its 32 features: xor tree (fixed order)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        float t = ss[p];
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        const int i = p * 4 + (lane >> 3);
+        if ((lane & 7) == 0 && i < nc) a.ssq_out[(size_t)(row + i) * a.ssq_np + (nw0 >> 5)] = t;
       }
     }
   }
@@ -255,8 +293,9 @@ struct EpiWarp {
   uint8_t* st;  // 2 x kChunkBytes staging for TMA stores / bulk partial stores
   int sb;       // staging chunk to use next
   int q, lane;
-  CB_DEVICE EpiWarp(uint8_t* base, int q_, int lane_)
-      : tb(reinterpret_cast<float*>(base)), st(base + 16 * kTbRow * 4), sb(0), q(q_), lane(lane_) {}
+  const float* rt;  // fused RMSNorm consumer: per-row scale table (index row - row_off), else null
+  CB_DEVICE EpiWarp(uint8_t* base, int q_, int lane_, const float* rt_)
+      : tb(reinterpret_cast<float*>(base)), st(base + 16 * kTbRow * 4), sb(0), q(q_), lane(lane_), rt(rt_) {}
   // a staging chunk whose previous TMA store has finished reading it
   CB_DEVICE uint8_t* next_stage() {
     uint8_t* p = st + sb * kChunkBytes;
@@ -271,14 +310,65 @@ struct EpiWarp {
   }
 };
 
+// Fused RMSNorm consumer: the epilogue warps turn the producer's per-row
+// partial sums of squares into row scales rsqrt(mean(x^2) + eps), once per CTA
+// (after griddepcontrol.wait: the partials belong to the previous kernel).
+// Same summation order in every kernel, so a row's scale is bit-identical
+// whichever kernel / plan consumes it.
+CB_DEVICE const float* build_row_scales(const GemmArgs& a, uint8_t* bar_base, int et) {
+  if (!a.ssq_in) return nullptr;
+  float* rt = reinterpret_cast<float*>(bar_base + kRtabOff);
+  const float inv_d = 1.0f / float(a.norm_d);
+  const int w = et >> 5, l = et & 31, nv = a.ssq_np >> 2;
+  // warp w: rows 64i + 16w + j (j < 16) -- 16 independent 16-byte loads in
+  // flight per lane, lanes stride a row's partials, fixed xor-tree reduction
+  for (int t0 = 16 * w; t0 < a.T; t0 += 64) {
+    float s[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) s[j] = 0.f;
+    for (int k = l; k - l < nv; k += 32) {  // one 16-byte load per row in flight at once
+      float4 x[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        x[j] = (t0 + j < a.T && k < nv)
+                   ? __ldcg(reinterpret_cast<const float4*>(a.ssq_in + (size_t)(a.row_off + t0 + j) * a.ssq_np) + k)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) s[j] += (x[j].x + x[j].y) + (x[j].z + x[j].w);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+    }
+    if (l < 16 && t0 + l < a.T) {
+      float v = s[0];
+#pragma unroll
+      for (int j = 1; j < 16; ++j) v = (l == j) ? s[j] : v;
+      rt[t0 + l] = rsqrtf(v * inv_d + a.norm_eps);
+    }
+  }
+  named_bar_sync(1, kEpiThreads);
+  return rt;
+}
+
+// the table build_row_scales filled (reduction passes after the main epilogue)
+CB_DEVICE const float* row_scales(const GemmArgs& a, uint8_t* bar_base) {
+  return a.ssq_in ? reinterpret_cast<const float*>(bar_base + kRtabOff) : nullptr;
+}
+
 // One warp chunk of output: weight rows nw0..nw0+31 (lane = row) x tokens
 // row..row+nc-1 (register i = token).  Full chunks go through smem and one TMA
 // store (EPI_RESID: TMA reduce-add = the fp32 residual +=) issued by lane 0 --
 // the LSU never sees the output; a partial chunk (token tail) uses 16-byte
 // register stores (or scalar ones for unaligned shapes).
 CB_DEVICE void emit_chunk(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, int nw0, int row, int nc,
-                          const float (&v)[16]) {
-  if (a.tma && nc == 16) {
+                          const float (&v_in)[16], const float4* res_pre = nullptr,
+                          const uint2* g_pre = nullptr) {
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = e.rt ? v_in[i] * e.rt[row - a.row_off + i] : v_in[i];
+  if (a.tma && nc == 16 && !a.h_out) {
     uint8_t* stg = e.next_stage();
     if (a.epi == EPI_SWIGLU) {
 #pragma unroll
@@ -306,7 +396,7 @@ CB_DEVICE void emit_chunk(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e,
     return;
   }
   if (a.vec)
-    emit_warp_vec(a, e.tb, nw0, row, nc, v, e.lane);
+    emit_warp_vec(a, e.tb, nw0, row, nc, v, e.lane, res_pre, g_pre);
   else
     emit16(a, nw0 + e.lane, row, nc, v);
 }
@@ -504,6 +594,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
     uend = sk.u0(c + 1);
   }
 
+  float4 rp[4][4];  // epilogue warps, cluster split-K fused-norm producer: prefetched residual chunks
+  uint2 gp = make_uint2(0u, 0u);  // ... and this lane's 4 gamma values
+
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
   if (a.trace && threadIdx.x == 0) a.trace[(size_t)c * 512] = globaltimer_ns();
   if (warp == 0 && lane == 0) {
@@ -635,9 +728,25 @@ __global__ void __launch_bounds__(kThreads1, 1)
   } else {
     // ---------------------------------------------------------- epilogue
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
+    if (csplit > 1 && a.epi == EPI_RESID && a.h_out) {
+      // register-path residual epilogue of cluster split-K (fused-norm
+      // producer): the residual of this warp's first 4 reduction chunks is
+      // loaded now, while the main loop runs, and kept 4 chunks ahead later
+      const int w = warp - 2, qpr = 4 / csplit, cstep = 4 / qpr;
+      const int tile = c / csplit, mt = tile / n_ttiles, tt = tile % n_ttiles;
+      const int qq = int(cluster_ctarank()) * qpr + (w % qpr);
+      const int ncols_tile = min(TN, a.T - tt * TN), nchunks = (ncols_tile + 15) >> 4;
+      gp = __ldg(reinterpret_cast<const uint2*>(a.gamma_next + mt * kBM + qq * 32 + (lane & 7) * 4));
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const int ch = w / qpr + g * cstep;
+        if (ch < nchunks)
+          load_res(a, mt * kBM + qq * 32, a.row_off + tt * TN + ch * 16, min(16, ncols_tile - ch * 16), lane, rp[g]);
+      }
+    }
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int et = threadIdx.x - 64;  // 0..127
-    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
+    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane, build_row_scales(a, smem + ring_bytes + kTbufBytes, et));
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t fix_phase = 0;
@@ -711,7 +820,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     cluster_sync_all();
     if (warp >= 2 && warp < 6) {
       const int q = warp & 3;
-      EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
+      EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane, row_scales(a, smem + ring_bytes + kTbufBytes));
       const int r_me = c % cs;
       const uint32_t base = smem_u32(smem);
       auto rank_of = [&](int uu) { return int(((long long)(uu - cl_u0 + 1) * cs - 1) / cl_units); };
@@ -755,20 +864,23 @@ __global__ void __launch_bounds__(kThreads1, 1)
       float* part = reinterpret_cast<float*>(sW);
       for (int i = threadIdx.x - 64; i < TN * kBM; i += kEpiThreads) part[i] = 0.f;
     }
+    // CTA `rank` reduces its 128/csplit rows (qpr warp quarters) over the S
+    // partials in fixed rank order; the 4 epilogue warps split the quarters
+    // and the 16-column chunks, and emit like a whole tile.
+    const uint32_t rank = cluster_ctarank();
+    const int w = warp - 2;
+    const int qpr = 4 / csplit;  // quarters per rank (csplit is 2 or 4)
+    const int qq = int(rank) * qpr + (w % qpr);
+    const int row0 = a.row_off + tt * TN;
+    const int nchunks = (ncols_tile + 15) >> 4;
+    const int cstep = 4 / qpr;
+    const int nw0 = mt * kBM + qq * 32;
+    const bool pre = epi_warp && a.epi == EPI_RESID && a.h_out != nullptr;  // rp holds the residual (see above)
     cluster_sync_all();
     if (epi_warp) {
-      // CTA `rank` reduces its 128/csplit rows (qpr warp quarters) over the S
-      // partials in fixed rank order; the 4 epilogue warps split the quarters
-      // and the 16-column chunks, and emit like a whole tile.
-      const uint32_t rank = cluster_ctarank();
-      const int w = warp - 2;
-      const int qpr = 4 / csplit;  // quarters per rank (csplit is 2 or 4)
-      const int qq = int(rank) * qpr + (w % qpr);
-      EpiWarp e(epi_smem + w * kEpiWarpBytes, qq, lane);
-      const int row0 = a.row_off + tt * TN;
+      EpiWarp e(epi_smem + w * kEpiWarpBytes, qq, lane, row_scales(a, smem + ring_bytes + kTbufBytes));
       const uint32_t base = smem_u32(sW);
-      const int nchunks = (ncols_tile + 15) >> 4;
-      for (int ch = w / qpr; ch < nchunks; ch += 4 / qpr) {
+      for (int ch = w / qpr; ch < nchunks; ch += cstep) {
         float v[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = 0.f;
@@ -778,7 +890,16 @@ __global__ void __launch_bounds__(kThreads1, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) v[i] += dsmem_ld_f32(ra + uint32_t(i * 128));
         }
-        emit_chunk(a, &tmO, e, mt * kBM + qq * 32, row0 + ch * 16, min(16, ncols_tile - ch * 16), v);
+        emit_chunk(a, &tmO, e, nw0, row0 + ch * 16, min(16, ncols_tile - ch * 16), v, pre ? rp[0] : nullptr,
+                   pre ? &gp : nullptr);
+        if (pre) {
+#pragma unroll
+          for (int g = 0; g < 3; ++g)
+#pragma unroll
+            for (int p = 0; p < 4; ++p) rp[g][p] = rp[g + 1][p];
+          const int chn = ch + 4 * cstep;
+          if (chn < nchunks) load_res(a, nw0, row0 + chn * 16, min(16, ncols_tile - chn * 16), lane, rp[3]);
+        }
       }
       e.drain();
     }
@@ -931,7 +1052,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
-    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane);
+    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane, build_row_scales(a, smem + Cfg::kRingBytes + kTbufBytes, et));
     const uint32_t tempty_leader0 = dsmem_map(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = dsmem_map(smem_u32(&tempty_bar[1]), 0);
     int acc = 0;
@@ -1200,13 +1321,13 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   // two co-resident CTAs per SM (<= ~113 KB each) when the plan asks for it
   int stages = Cfg::kStages;
   if (plan.corun) {
-    const int fit = int((kCorunSmem - kTbufBytes - 2048) / Cfg::kStageBytes);
+    const int fit = int((kCorunSmem - kTbufBytes - 1024 - kBarBytes) / Cfg::kStageBytes);
     stages = fit < stages ? fit : stages;
     if (stages < 2) stages = 2;
   }
   if (plan.csplit > 1 && stages * Cfg::kStageBytes < TN * kBM * 4) stages = Cfg::kStages;  // smem holds the partial
   a.stages = stages;
-  const size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + 1024;
+  const size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + kBarBytes;
   a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;
@@ -1259,10 +1380,19 @@ cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmAr
                         int num_sms, cudaStream_t st, const CUtensorMap* out_map) {
   if (a_in.T <= 0 || a_in.N <= 0) return cudaSuccess;
   GemmArgs a = a_in;
+  // fused RMSNorm: the row-scale table holds one token tile; the producer needs
+  // the vector epilogue (whole 32-feature groups per warp, x in registers)
+  if (a.ssq_in && (a.T > kMaxNormRows || a.ssq_np <= 0 || (a.ssq_np & 3) || a.norm_d <= 0))
+    return cudaErrorInvalidValue;
+  if (a.h_out && (a.epi != EPI_RESID || !a.gamma_next || !a.ssq_out || (a.N & 31) || a.ssq_np != a.N / 32 ||
+                  !vec_ok(a) || (reinterpret_cast<uintptr_t>(a.h_out) & 7) ||
+                  (reinterpret_cast<uintptr_t>(a.gamma_next) & 7)))
+    return cudaErrorInvalidValue;
   CUtensorMap o;
   // TMA stores measured: a win for the fp32 outputs (residual reduce-add,
-  // logits), neutral for bf16, 3x slower for the 32-byte SwiGLU boxes
-  if (out_map && (a.epi == EPI_RESID || a.epi == EPI_F32)) {
+  // logits), neutral for bf16, 3x slower for the 32-byte SwiGLU boxes.  The
+  // fused-norm producer needs x_new in registers: no reduce-add.
+  if (out_map && (a.epi == EPI_F32 || (a.epi == EPI_RESID && !a.h_out))) {
     o = *out_map;
     a.tma = 1;
   } else {

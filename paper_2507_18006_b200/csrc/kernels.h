@@ -37,6 +37,19 @@ struct GemmArgs {
   int stages;         // set by the launcher: pipeline ring depth (1-CTA kernel)
   int cstream;        // set from the plan: cluster stream-K cluster size (> 1)
   int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
+  // Fused RMSNorm (decode passes, T <= 256; SURVEY.md §8(a) rmsnorm):
+  //  consumer (ssq_in != null): X rows are h' = bf16(x * gamma); output row t is
+  //    scaled by rsqrt(sum_k ssq_in[t][k] / norm_d + norm_eps) before the epilogue op;
+  //  producer (EPI_RESID, h_out != null): besides x += proj it writes
+  //    h_out = bf16(x * gamma_next) and ssq_out[t][n / 32] = sum over the 32
+  //    features n..n+31 of x^2 (fixed order: deterministic).
+  const float* ssq_in;
+  uint16_t* h_out;
+  const uint16_t* gamma_next;
+  float* ssq_out;
+  int ssq_np;  // partials per row (= d / 32)
+  int norm_d;
+  float norm_eps;
   // filled by the launcher
   int n_mtiles, n_ttiles, kblocks, units;
 };
@@ -80,6 +93,10 @@ constexpr int kGemmMaxTiles = 1 << 16;
 // x[row_off + t, :] = fp32(table[tokens[t], :])
 cudaError_t embed_launch(const uint16_t* table, const int32_t* tokens, float* x, int T, int d, int row_off,
                          cudaStream_t st);
+// embed_launch + fused-RMSNorm producer outputs: h = bf16(x * gamma), ssq[t][g] =
+// sum of x^2 over features 32g..32g+31 (d % 256 == 0)
+cudaError_t embed_norm_launch(const uint16_t* table, const int32_t* tokens, float* x, const uint16_t* gamma,
+                              uint16_t* h, float* ssq, int T, int d, int row_off, cudaStream_t st);
 // y = bf16(x * rsqrt(mean(x^2) + eps) * gamma) for rows [row_off, row_off + T)
 cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, int T, int d, float eps,
                            int row_off, cudaStream_t st);

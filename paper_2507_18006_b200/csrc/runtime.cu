@@ -123,6 +123,7 @@ struct Workspace {
   float* x = nullptr;
   uint16_t *h = nullptr, *hl = nullptr, *qkv = nullptr, *att = nullptr, *act = nullptr;
   uint16_t* gbuf = nullptr;  // [max_tokens][d_ff] gate output when gate / up run as separate GEMMs
+  float* ssq = nullptr;      // fused RMSNorm: [max_tokens][d_model / 32] partial sums of x^2 of the rows in h
   float* logits = nullptr;
   int32_t* meta = nullptr;  // [tokens | row_slot | row_pos | gather]
   int32_t* next = nullptr;
@@ -180,6 +181,7 @@ struct cb_model {
   int32_t* pin_next = nullptr;
   std::vector<std::vector<Route>> last_routing;
   int cur_phase = 0;  // CB_PHASE_* of the pass in flight
+  bool fuse_norm = false;  // this pass folds RMSNorm into the GEMM epilogues (decode, T <= 256)
   int cur_T = 0;  // rows of the pass in flight: per-step meta = [tokens | slot | pos] x T, then gather x bs
   int cur_bs = 0;  // sequences of the pass in flight
   std::vector<int> seq_blk;  // prefill: first q-block of each sequence (+ total), blocks follow the gather list
@@ -312,6 +314,7 @@ int ensure_ws(cb_model* m, int dev) {
   const size_t T = d.max_tokens;
   CB_TRY(dev_alloc(dc, (void**)&w.x, T * d.d_model * 4));
   CB_TRY(dev_alloc(dc, (void**)&w.h, T * d.d_model * 2));
+  CB_TRY(dev_alloc(dc, (void**)&w.ssq, T * (d.d_model / 32) * 4));
   CB_TRY(dev_alloc(dc, (void**)&w.hl, size_t(d.max_slots) * d.d_model * 2));
   CB_TRY(dev_alloc(dc, (void**)&w.qkv, T * m->qkv_n * 2));
   CB_TRY(dev_alloc(dc, (void**)&w.att, T * m->q_n * 2));
@@ -411,8 +414,16 @@ int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t
   return CB_OK;
 }
 
+// Fused RMSNorm hooks of one GEMM (kernels.h GemmArgs): consume = X rows are
+// h' = bf16(x * gamma), outputs scaled by the rows' rsqrt(mean(x^2) + eps);
+// gamma_next != null = EPI_RESID producer of h' / ssq for the next norm.
+struct NormIO {
+  bool consume = false;
+  const uint16_t* gamma_next = nullptr;
+};
+
 int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K, int T, int row_off, int epi,
-         void* out, long long ldo) {
+         void* out, long long ldo, const NormIO& nio = NormIO{}) {
   DeviceCtx& dc = devctx(m, dev);
   Workspace& ws = m->ws[dev];
   cb::GemmPlan plan = cb::gemm_plan(N, K, T, dc.num_sms, m->cur_T);
@@ -428,6 +439,17 @@ int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K,
   a.out = out;
   a.ws = ws.gemm_ws;
   a.counters = ws.gemm_cnt;
+  if (nio.consume || nio.gamma_next) {
+    a.ssq_np = m->d.d_model / 32;
+    a.norm_d = m->d.d_model;
+    a.norm_eps = m->d.norm_eps;
+  }
+  if (nio.consume) a.ssq_in = ws.ssq;
+  if (nio.gamma_next) {
+    a.h_out = ws.h;
+    a.gamma_next = nio.gamma_next;
+    a.ssq_out = ws.ssq;
+  }
   const double out_b = (epi == cb::EPI_F32 || epi == cb::EPI_RESID) ? 4.0 : 2.0;
   const double out_n = epi == cb::EPI_SWIGLU ? N / 2.0 : double(N);
   const double bytes = double(N) * K * 2 + double(T) * K * 2 + double(T) * out_n * out_b +
@@ -468,6 +490,14 @@ int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& t
       CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].x + size_t(a) * m->d.d_model, dd.ordinal,
                                   m->ws[os.dev].x + size_t(a) * m->d.d_model, sd.ordinal,
                                   size_t(b - a) * row_bytes, dd.compute));
+      if (m->fuse_norm) {  // the next layer's normalised input rows and their sums of squares travel too
+        const size_t np = size_t(m->d.d_model / 32);
+        CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].h + size_t(a) * m->d.d_model, dd.ordinal,
+                                    m->ws[os.dev].h + size_t(a) * m->d.d_model, sd.ordinal,
+                                    size_t(b - a) * m->d.d_model * 2, dd.compute));
+        CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].ssq + size_t(a) * np, dd.ordinal, m->ws[os.dev].ssq + size_t(a) * np,
+                                    sd.ordinal, size_t(b - a) * np * 4, dd.compute));
+      }
     }
   return CB_OK;
 }
@@ -789,8 +819,10 @@ int run_layer_overridden(cb_model* m, LayerState& L, const Seg& s, const std::ve
   return CB_OK;
 }
 
+// gamma_next: the norm that follows this layer (next layer's attention norm,
+// or the final norm), readable from s.dev -- used when the pass fuses RMSNorm.
 int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
-                      const std::vector<int>& row_pos) {
+                      const std::vector<int>& row_pos, const uint16_t* gamma_next) {
   if (L.proj_ov) return run_layer_overridden(m, L, s, seq_slot, row_pos);
   const cb_model_desc& d = m->d;
   const LayerCopy& W = L.reps[s.rep];
@@ -802,6 +834,22 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
   const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
   const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
+  if (m->fuse_norm) {
+    // RMSNorm folded into the GEMMs: the residual projections emit h' = bf16(x * gamma)
+    // plus per-row sums of squares, the next projection scales its outputs by rsqrt(mean + eps)
+    NormIO cons;
+    cons.consume = true;
+    NormIO prod_fn, prod_next;
+    prod_fn.gamma_next = fn;
+    prod_next.gamma_next = gamma_next;
+    CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n, cons));
+    CB_TRY(attention_part(m, L, s, seq_slot, row_pos));
+    CB_TRY(use(dc));
+    CB_TRY(gemm(m, dev, W.m_o, ws.map_att, d.d_model, m->q_n, T, s.r0, cb::EPI_RESID, ws.x, d.d_model, prod_fn));
+    CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff, cons));
+    CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model, prod_next));
+    return CB_OK;
+  }
   {
     ProfScope ps(m, dev, CB_KCLASS_ELEMWISE, dc.compute, norm_bytes);
     CB_CUDA(cb::rmsnorm_launch(ws.x, an, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
@@ -817,6 +865,16 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff));
   CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
   return CB_OK;
+}
+
+// A norm vector (attention norm of layer li, or the final norm for li == n_layers)
+// that kernels on logical device dev can read: a copy on the same physical GPU.
+const uint16_t* norm_gamma_for(cb_model* m, int li, int dev) {
+  const int ord = devctx(m, dev).ordinal;
+  if (li >= m->d.n_layers) return devctx(m, m->home).ordinal == ord ? m->final_norm : nullptr;
+  for (const LayerCopy& c : m->layers[li].reps)
+    if (devctx(m, c.dev).ordinal == ord) return reinterpret_cast<const uint16_t*>(c.block + m->off_an);
+  return nullptr;
 }
 
 std::vector<int> split_batch_vec(int bs, int p) {
@@ -891,10 +949,30 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     CB_CUDA(cudaMemcpyAsync(m->ws[dv].meta, meta, meta_bytes, cudaMemcpyHostToDevice, dc.compute));
   }
   Workspace& hw = m->ws[m->home];
+  // Fused RMSNorm: decode passes whose rows fit one GEMM token tile, plain
+  // layers (no migrated projections), every norm vector readable where its
+  // producer runs.  Prefill keeps the separate norm kernels (compute-bound GEMMs).
+  static const bool no_fuse = std::getenv("COCOB200_NO_FUSED_NORM") != nullptr;  // A/B experiments
+  m->fuse_norm = !no_fuse && !prefill && T <= 256 && d.d_model % 256 == 0;
+  std::vector<std::vector<const uint16_t*>> gamma_next(d.n_layers);
+  const uint16_t* g_embed = m->fuse_norm ? norm_gamma_for(m, 0, m->home) : nullptr;
+  if (m->fuse_norm && !g_embed) m->fuse_norm = false;
+  for (int li = 0; li < d.n_layers && m->fuse_norm; ++li) {
+    const LayerState& L = m->layers[li];
+    if (L.proj_ov) m->fuse_norm = false;
+    for (const LayerCopy& c : L.reps) {
+      const uint16_t* g = norm_gamma_for(m, li + 1, c.dev);
+      if (!g) m->fuse_norm = false;
+      gamma_next[li].push_back(g);
+    }
+  }
   CB_TRY(use(hc));
   {
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
-    CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
+    if (m->fuse_norm)
+      CB_CUDA(cb::embed_norm_launch(m->embed, hw.meta, hw.x, g_embed, hw.h, hw.ssq, T, d.d_model, 0, hc.compute));
+    else
+      CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
   }
 
   std::vector<Seg> layout{{m->home, 0, 0, T, 0, bs}};
@@ -911,7 +989,8 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       s0 += shares[j];
     }
     CB_TRY(reshard(m, layout, segs));
-    for (const Seg& s : segs) CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos));
+    for (const Seg& s : segs)
+      CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos, m->fuse_norm ? gamma_next[li][s.rep] : nullptr));
     layout = segs;
   }
   std::vector<Seg> home_layout{{m->home, 0, 0, T, 0, bs}};
@@ -919,7 +998,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   // every device's trailing work joins the home stream
   for (int dv : devs) CB_TRY(depend(hc, devctx(m, dv)));
   CB_TRY(use(hc));
-  {
+  if (!m->fuse_norm) {  // fused: the last layer's down projection already wrote h' for the final norm
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
     CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
   }
@@ -929,7 +1008,9 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * T, hw.hl, bs, d.d_model, hc.compute));
     xm = hw.map_hl;
   }
-  CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab));
+  NormIO head_norm;
+  head_norm.consume = m->fuse_norm;
+  CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab, head_norm));
   {
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.vocab * 4);
     CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));

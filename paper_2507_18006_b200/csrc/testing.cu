@@ -48,6 +48,26 @@ int finish(cudaError_t e) {
   return cudaDeviceSynchronize() == cudaSuccess ? CB_OK : CB_ECUDA;
 }
 
+// fused-RMSNorm fields applied to every cbt_gemm / cbt_gemm_bench launch (cbt_gemm_set_norm)
+struct NormFields {
+  const float* ssq_in = nullptr;
+  uint16_t* h_out = nullptr;
+  const uint16_t* gamma_next = nullptr;
+  float* ssq_out = nullptr;
+  int np = 0, d = 0;
+  float eps = 0.f;
+} g_norm;
+
+void apply_norm(cb::GemmArgs& a) {
+  a.ssq_in = g_norm.ssq_in;
+  a.h_out = g_norm.h_out;
+  a.gamma_next = g_norm.gamma_next;
+  a.ssq_out = g_norm.ssq_out;
+  a.ssq_np = g_norm.np;
+  a.norm_d = g_norm.d;
+  a.norm_eps = g_norm.eps;
+}
+
 int gemm_setup(const void* w, const void* x, int64_t x_rows, int N, int K, const cb::GemmPlan& plan,
                CUtensorMap* mw, CUtensorMap* mx) {
   if (plan.kd == 2) {  // 3-D views for the 2-k-block-per-stage kernel
@@ -82,6 +102,7 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
+  apply_norm(a);
   CUtensorMap mo;
   const uint64_t ocols = epi == cb::EPI_SWIGLU ? uint64_t(N) / 2 : uint64_t(N);
   const bool tma = cb::make_out_map(&mo, out, epi, uint64_t(row_off + T), ocols, uint64_t(ldo)) == 0;
@@ -135,6 +156,7 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
   a.max_parts = (max_parts > 0 && max_parts < 100) ? max_parts : 0;
+  apply_norm(a);
   static unsigned long long* trace = nullptr;
   if (dbg_bits & 8) {  // experiments: per-CTA timeline of the last launch -> g_trace
     if (!trace) cudaMalloc(&trace, 148 * 512 * 8);
@@ -437,6 +459,18 @@ extern "C" int cbt_tma_probe(const void* buf, int64_t rows, int32_t box_rows, in
 extern "C" int cbt_gemm_trace(unsigned long long* out, int32_t n) {
   if (n > 148 * 512) n = 148 * 512;
   std::memcpy(out, g_trace, size_t(n) * 8);
+  return CB_OK;
+}
+
+extern "C" int cbt_gemm_set_norm(const float* ssq_in, uint16_t* h_out, const uint16_t* gamma_next, float* ssq_out,
+                                 int32_t np, int32_t d, float eps) {
+  g_norm.ssq_in = ssq_in;
+  g_norm.h_out = h_out;
+  g_norm.gamma_next = gamma_next;
+  g_norm.ssq_out = ssq_out;
+  g_norm.np = np;
+  g_norm.d = d;
+  g_norm.eps = eps;
   return CB_OK;
 }
 

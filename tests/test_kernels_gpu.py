@@ -114,6 +114,88 @@ def test_gemm_deterministic_and_row_split_invariant(lib, cuda, N, K):
     assert torch.equal(a, c)
 
 
+def _set_norm(lib, ssq_in=None, h_out=None, gamma=None, ssq_out=None, d=0, eps=1e-5):
+    P = lambda t: None if t is None else t.data_ptr()
+    assert lib.cbt_gemm_set_norm(P(ssq_in), P(h_out), P(gamma), P(ssq_out), d // 32, d, C.c_float(eps)) == 0
+
+
+@pytest.mark.parametrize("epi,N,K,T,row_off", [(0, 12288, 4096, 64, 0), (0, 384, 256, 1, 3), (3, 22016, 4096, 256, 0),
+                                               (3, 640, 512, 37, 2), (1, 32000, 4096, 128, 0), (1, 256, 256, 200, 0),
+                                               (0, 12288, 4096, 256, 0)])
+def test_gemm_fused_norm_consumer(lib, cuda, epi, N, K, T, row_off):
+    """Fused RMSNorm, consumer side: X rows are h' = bf16(x * gamma), the
+    epilogue scales each token row by rsqrt(sum(ssq partials) / d + eps) before
+    its op (bf16 store, SwiGLU, fp32 logits) == GEMM of RMSNorm(x) (fp64 ref)."""
+    torch = cuda
+    rows = T + row_off
+    x = torch.randn(rows, K, dtype=torch.float32) * 2
+    gamma = (torch.rand(K) * 0.5 + 0.75).to(torch.bfloat16)
+    hp = (x * gamma.float()).to(torch.bfloat16)
+    ssq = (x * x).view(rows, K // 32, 32).sum(-1).contiguous()
+    w = _bf16(torch, (N, K), 0.03, 21)
+    ocols = N // 2 if epi == 3 else N
+    odt = torch.float32 if epi == 1 else torch.bfloat16
+    out = torch.zeros(rows, ocols, dtype=odt, device="cuda")
+    ssq_d = ssq.cuda()
+    _set_norm(lib, ssq_in=ssq_d, d=K)
+    try:
+        _gemm(lib, torch, w.cuda(), hp.cuda(), T, row_off, epi, out, ocols)
+    finally:
+        _set_norm(lib)
+    xd = x.double()[row_off:]
+    hn = xd / torch.sqrt((xd * xd).mean(-1, keepdim=True) + 1e-5) * gamma.double()
+    y = hn @ w.double().T
+    if epi == 3:
+        g, u = y[:, 0::2], y[:, 1::2]
+        y = g / (1 + torch.exp(-g)) * u
+    got = out[row_off:].double().cpu()
+    err = (got - y).abs().max().item()
+    assert err <= 1.5e-2 * y.abs().max().item() + 1e-3, err
+    if row_off:
+        assert out[:row_off].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("N,K,T", [(4096, 4096, 64), (4096, 11008, 256), (4096, 4096, 1), (4096, 4096, 130),
+                                   (512, 256, 19)])
+def test_gemm_fused_norm_producer(lib, cuda, N, K, T):
+    """Fused RMSNorm, producer side (residual epilogue): x += proj as before,
+    plus h' = bf16(x_new * gamma) bit-exactly and per-32-feature sums of x_new^2."""
+    torch = cuda
+    w = _bf16(torch, (N, K), 0.03, 22).cuda()
+    a = _bf16(torch, (T, K), 1.0, 23).cuda()
+    base = torch.randn(T, N, dtype=torch.float32, device="cuda")
+    x = base.clone()
+    gamma = (torch.rand(N) * 0.5 + 0.75).to(torch.bfloat16).cuda()
+    h = torch.zeros(T, N, dtype=torch.bfloat16, device="cuda")
+    ssq = torch.zeros(T, N // 32, dtype=torch.float32, device="cuda")
+    _set_norm(lib, h_out=h, gamma=gamma, ssq_out=ssq, d=N)
+    try:
+        _gemm(lib, torch, w, a, T, 0, 2, x, N)
+    finally:
+        _set_norm(lib)
+    ref = base.double().cpu() + a.double().cpu() @ w.double().cpu().T
+    assert (x.double().cpu() - ref).abs().max().item() < 2e-6 * K ** 0.5 * ref.abs().max().item() + 1e-4
+    assert torch.equal(h, (x * gamma.float()).to(torch.bfloat16))
+    ssq_ref = (x.double() ** 2).view(T, N // 32, 32).sum(-1)
+    assert torch.allclose(ssq.double(), ssq_ref, rtol=1e-5, atol=1e-5)
+
+
+def test_gemm_fused_norm_rejects_multi_tile(lib, cuda):
+    """The row-scale table holds one token tile: T > 256 with ssq_in is refused."""
+    torch = cuda
+    K, N, T = 256, 256, 300
+    ssq = torch.ones(T, K // 32, device="cuda")
+    w = _bf16(torch, (N, K), 0.03, 24).cuda()
+    x = _bf16(torch, (T, K), 1.0, 25).cuda()
+    out = torch.zeros(T, N, dtype=torch.bfloat16, device="cuda")
+    _set_norm(lib, ssq_in=ssq, d=K)
+    try:
+        st = lib.cbt_gemm(_ptr(w), _ptr(x), T, N, K, T, 0, 0, _ptr(out), N)
+    finally:
+        _set_norm(lib)
+    assert st != 0
+
+
 def test_rmsnorm(lib, cuda):
     torch = cuda
     T, d = 37, 4096
