@@ -34,6 +34,9 @@
 // the per-module GEMM FLOPs of `ModuleCatalog.from_model` (`domain.py:241-264`).
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -48,7 +51,9 @@ static constexpr size_t kSmemBudget = 224 * 1024;  // of the 227 KB opt-in maxim
 static constexpr int kTbRow = 36;  // transpose buffer row stride (floats): 32 + 4 pad -> conflict-free 16-byte reads
 static constexpr int kChunkBytes = 16 * 32 * 4;  // one epilogue warp chunk: 16 tokens x 32 weight rows, fp32
 // per epilogue warp: padded transpose buffer (register-store path) + 2 TMA staging chunks
-static constexpr int kEpiWarpBytes = 16 * kTbRow * 4 + 2 * kChunkBytes;
+// (staging first and the per-warp block a multiple of 1 KB: the swizzled
+// staging boxes of the token-major epilogue need 512-byte alignment)
+static constexpr int kEpiWarpBytes = ((2 * kChunkBytes + 16 * kTbRow * 4) + 1023) / 1024 * 1024;
 static constexpr int kTbufBytes = 4 * kEpiWarpBytes;
 static constexpr int kMaxStages = 16;
 // after the transpose buffers: mbarriers (first 1 KB), then the fused-RMSNorm
@@ -295,7 +300,7 @@ struct EpiWarp {
   int q, lane;
   const float* rt;  // fused RMSNorm consumer: per-row scale table (index row - row_off), else null
   CB_DEVICE EpiWarp(uint8_t* base, int q_, int lane_, const float* rt_)
-      : tb(reinterpret_cast<float*>(base)), st(base + 16 * kTbRow * 4), sb(0), q(q_), lane(lane_), rt(rt_) {}
+      : tb(reinterpret_cast<float*>(base + 2 * kChunkBytes)), st(base), sb(0), q(q_), lane(lane_), rt(rt_) {}
   // a staging chunk whose previous TMA store has finished reading it
   CB_DEVICE uint8_t* next_stage() {
     uint8_t* p = st + sb * kChunkBytes;
@@ -304,11 +309,21 @@ struct EpiWarp {
     sb ^= 1;
     return p;
   }
+  // 3-deep staging ring over the whole per-warp block (token-major epilogue:
+  // the transpose buffer is unused there)
+  CB_DEVICE uint8_t* next_stage3() {
+    uint8_t* p = st + sb * kChunkBytes;
+    if (lane == 0) bulk_wait_read<2>();
+    __syncwarp();
+    sb = sb == 2 ? 0 : sb + 1;
+    return p;
+  }
   CB_DEVICE void drain() {
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
   }
 };
+static_assert(3 * kChunkBytes <= kEpiWarpBytes, "token-major staging ring");
 
 // Fused RMSNorm consumer: the epilogue warps turn the producer's per-row
 // partial sums of squares into row scales rsqrt(mean(x^2) + eps), once per CTA
@@ -429,6 +444,7 @@ CB_DEVICE void epi_drain(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, 
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    if (a.dbg & 16) continue;  // experiments: TMEM loads only
     if (whole) {
       emit_chunk(a, tmO, e, m0 + e.q * 32, row0 + c0, min(16, ncols - c0), v);
     } else if (part_in_smem) {
@@ -911,6 +927,145 @@ __global__ void __launch_bounds__(kThreads1, 1)
   if (warp == 1) tmem_dealloc<Cfg::kTmemCols>(tmem_base);
 }
 
+// Token-major accumulator (swapped CTA-pair kernel): TMEM lane = token, column
+// = weight row, so each lane owns one output row and stores 32 consecutive
+// outputs per TMEM load -- no smem transpose, no shuffles.  The 4 epilogue
+// warps of a CTA cover its 128 tokens; a tile's 256 weight rows are 8 loads.
+// Swizzled staging row for a TMA store of a token-major box (SW64 / SW32 --
+// the store's swizzle mode): 16-byte chunk c of box row r.  The XOR spreads the
+// 8 lanes of a quarter-warp over 8 different 16-byte bank groups.
+template <int RB, int M>
+CB_DEVICE uint4* stg_chunk(uint8_t* stg, int r, int c) {
+  const uint32_t o = uint32_t(r * RB + c * 16);
+  return reinterpret_cast<uint4*>(stg + (o ^ (((o >> 7) & M) << 4)));
+}
+
+CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, uint32_t t_addr, int n_base,
+                             int nw, int row0, int tok0, int ncols) {
+  const int tok = tok0 + e.lane;  // tok0: first token of this warp
+  const bool ok = tok < ncols;
+  // full 32-token groups go out through swizzled staging + one TMA store per
+  // box (the token-major map: 64-byte rows, 32 rows); a partial group and the
+  // fused-norm producer store from registers
+  const bool use_tma = a.tma && tok0 + 32 <= ncols && !(a.epi == EPI_RESID && a.h_out);
+  const int row = row0 + tok;
+  const float* rt = e.rt;
+  const float sc = (rt && ok) ? rt[row - a.row_off] : 1.0f;
+  for (int c0 = 0; c0 < nw; c0 += 32) {
+    const int n0 = n_base + c0;
+    if (n0 >= a.N) break;  // N % 32 == 0 (launcher)
+    float4 res[8];
+    if (!use_tma && a.epi == EPI_RESID && ok) {  // residual loads in flight during the TMEM load
+#pragma unroll
+      for (int j = 0; j < 8; ++j) res[j] = __ldcg(reinterpret_cast<const float4*>(out_f32(a, n0 + 4 * j, row)));
+    }
+    uint32_t r[32];
+    tmem_ld32(t_addr + uint32_t(c0), r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = rt ? __uint_as_float(r[i]) * sc : __uint_as_float(r[i]);
+    if (use_tma) {
+      if (a.epi == EPI_F32 || a.epi == EPI_RESID) {  // two 16-feature boxes (64-byte fp32 rows)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint8_t* stg = e.next_stage3();
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            *stg_chunk<64, 3>(stg, e.lane, c) =
+                make_uint4(__float_as_uint(v[16 * h + 4 * c]), __float_as_uint(v[16 * h + 4 * c + 1]),
+                           __float_as_uint(v[16 * h + 4 * c + 2]), __float_as_uint(v[16 * h + 4 * c + 3]));
+          if (!(a.dbg & 64)) fence_proxy_async_smem();
+          __syncwarp();
+          if (e.lane == 0 && !(a.dbg & 32)) {
+            if (a.epi == EPI_RESID)
+              tma_reduce_add_2d(tmO, stg, n0 + 16 * h, row0 + tok0);
+            else
+              tma_store_2d(tmO, stg, n0 + 16 * h, row0 + tok0);
+            bulk_commit();
+          }
+        }
+      } else if (a.epi == EPI_BF16) {  // one box: 32 bf16 = 64-byte rows
+        uint8_t* stg = e.next_stage3();
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          *stg_chunk<64, 3>(stg, e.lane, c) =
+              make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                         pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+        if (!(a.dbg & 64)) fence_proxy_async_smem();
+        __syncwarp();
+        if (e.lane == 0 && !(a.dbg & 32)) {
+          tma_store_2d(tmO, stg, n0, row0 + tok0);
+          bulk_commit();
+        }
+      } else {  // SwiGLU: 16 bf16 outputs = 32-byte rows
+        uint8_t* stg = e.next_stage3();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float* g = v + 16 * c;
+          *stg_chunk<32, 1>(stg, e.lane, c) = make_uint4(
+              pack_bf16x2(silu_mul(g[0], g[1]), silu_mul(g[2], g[3])),
+              pack_bf16x2(silu_mul(g[4], g[5]), silu_mul(g[6], g[7])),
+              pack_bf16x2(silu_mul(g[8], g[9]), silu_mul(g[10], g[11])),
+              pack_bf16x2(silu_mul(g[12], g[13]), silu_mul(g[14], g[15])));
+        }
+        if (!(a.dbg & 64)) fence_proxy_async_smem();
+        __syncwarp();
+        if (e.lane == 0 && !(a.dbg & 32)) {
+          tma_store_2d(tmO, stg, n0 >> 1, row0 + tok0);
+          bulk_commit();
+        }
+      }
+      continue;
+    }
+    if (!ok) continue;
+    const size_t base = (size_t)row * a.ldo;
+    if (a.epi == EPI_BF16) {
+      uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.out) + base + n0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        o[j] = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]), pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                          pack_bf16x2(v[8 * j + 4], v[8 * j + 5]), pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+    } else if (a.epi == EPI_SWIGLU) {  // rows interleave gate / up: 16 outputs
+      uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.out) + base + (n0 >> 1));
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float* g = v + 16 * j;
+        o[j] = make_uint4(pack_bf16x2(silu_mul(g[0], g[1]), silu_mul(g[2], g[3])),
+                          pack_bf16x2(silu_mul(g[4], g[5]), silu_mul(g[6], g[7])),
+                          pack_bf16x2(silu_mul(g[8], g[9]), silu_mul(g[10], g[11])),
+                          pack_bf16x2(silu_mul(g[12], g[13]), silu_mul(g[14], g[15])));
+      }
+    } else {
+      float4* o = reinterpret_cast<float4*>(out_f32(a, n0, row));
+      float4 x[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        x[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        if (a.epi == EPI_RESID)
+          x[j] = make_float4(res[j].x + x[j].x, res[j].y + x[j].y, res[j].z + x[j].z, res[j].w + x[j].w);
+        o[j] = x[j];
+      }
+      if (a.epi == EPI_RESID && a.h_out) {  // fused-norm producer: h' and this 32-feature group's sum of squares
+        const uint4* gm = reinterpret_cast<const uint4*>(a.gamma_next + n0);
+        uint4* h = reinterpret_cast<uint4*>(a.h_out + base + n0);
+        float ss = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 g = __ldg(gm + j);
+          const float4 p = x[2 * j], q = x[2 * j + 1];
+          h[j] = make_uint4(pack_bf16x2(p.x * bf16_lo(g.x), p.y * bf16_hi(g.x)),
+                            pack_bf16x2(p.z * bf16_lo(g.y), p.w * bf16_hi(g.y)),
+                            pack_bf16x2(q.x * bf16_lo(g.z), q.y * bf16_hi(g.z)),
+                            pack_bf16x2(q.z * bf16_lo(g.w), q.w * bf16_hi(g.w)));
+          ss += (p.x * p.x + p.y * p.y + p.z * p.z + p.w * p.w) + (q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+        }
+        a.ssq_out[(size_t)row * a.ssq_np + (n0 >> 5)] = ss;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ CTA-pair kernel
 // One MMA computes a 256 (weight rows) x TNP (tokens) tile across the two SMs of
 // a cluster pair; each CTA stages its own 128 weight rows and TNP/2 token rows
@@ -919,7 +1074,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
 // (L2 traffic 3x the weight bytes); the pair kernel once per 256 rows.  Same
 // stream-K split (over pairs) and fixup as the 1-CTA kernel; each CTA finishes
 // its own 128-row half.
-template <int TNP>
+//
+// SWAP (TNP = 256, whole tiles only): the MMA operands trade places -- A = the
+// 256 token rows (128 per CTA), B = the 256 weight rows (128 per CTA), the
+// same smem tiles and TMA loads -- so the accumulator is token-major and the
+// epilogue stores rows straight from TMEM (epi_drain_tok).  The transposing
+// epilogue of the weight-major layout was 20% of a T = 256 launch.
+template <int TNP, bool SWAP>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
@@ -984,6 +1145,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
         const int mt = (u / sk.kb) / n_tt, kb = u % sk.kb;
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 66 + (u - ubeg)] = globaltimer_ns();
+        if (SWAP) {  // nw / 2 weight rows per CTA (box height of the launcher's map)
+          if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2);
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK,
+                           mt * a.nw + int(rank) * (a.nw >> 1), pol_w);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+          continue;
+        }
         if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], 2 * Cfg::kWBytes);
         const int mt128 = mt * 2 + int(rank);
         if (a.w_tiled)
@@ -1013,7 +1181,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer (leader, converged warp)
     if (leader) {
-      constexpr uint32_t idesc = make_idesc_bf16(2 * kBM, TNP);
+      // token-major: M = 256 tokens (A = activations), N = nw weight rows (B)
+      const uint32_t idesc = SWAP ? make_idesc_bf16(TNP, uint32_t(a.nw)) : make_idesc_bf16(2 * kBM, TNP);
       const uint64_t dw0 = make_sw128_desc(smem_u32(sW));
       const uint64_t dx0 = make_sw128_desc(smem_u32(sX));
       int stage = 0;
@@ -1036,7 +1205,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
           __syncwarp();
           const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
           const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
-          umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+          if (SWAP)
+            umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+          else
+            umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
@@ -1075,13 +1247,19 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (tr) tr[0] = globaltimer_ns() | (whole ? (1ull << 62) : 0);
       const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * TNP);
       float* part = a.ws + ((size_t)blockIdx.x * 2 + (u == ubeg ? 0 : 1)) * (size_t)(kBM * TNP);
-      epi_drain(a, &tmO, e, t_addr, m0, row0, ncols, whole, part, false);
+      if (SWAP) {
+        if (!whole) __trap();  // the launcher only swaps whole-tile plans
+        if (!(a.dbg & 2))
+          epi_drain_tok(a, &tmO, e, t_addr, mt * a.nw, a.nw, row0, int(rank) * kBM + q * 32, ncols);
+      } else if (!(a.dbg & 2)) {
+        epi_drain(a, &tmO, e, t_addr, m0, row0, ncols, whole, part, false);
+      }
       tc_fence_before();
       mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if (tr) tr[1] = globaltimer_ns();
-      if (!whole) {
+      if (!SWAP && !whole) {
         const PartMap pm{a.ws, sk, tile, 2, int(rank), TNP};
         epi_fixup(a, &tmO, e, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
                   sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes),
@@ -1138,6 +1316,25 @@ int make_out_map(CUtensorMap* map, const void* out, int epi, uint64_t rows, uint
   CUresult r = g_encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                         const_cast<void*>(out), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+// Token-major output boxes of the swapped pair kernel: 64-byte rows (16 fp32 /
+// 32 bf16; SwiGLU 16 bf16 = 32 bytes) x 32 tokens, swizzled like the staging.
+static int make_out_map_tok(CUtensorMap* map, const void* out, int epi, uint64_t rows, uint64_t cols, uint64_t ldo) {
+  if (!load_encode_fn()) return -1;
+  const bool f32 = epi == EPI_F32 || epi == EPI_RESID;
+  const uint32_t esz = f32 ? 4 : 2;
+  const uint32_t box_c = epi == EPI_SWIGLU ? 16 : 64 / esz;
+  if ((reinterpret_cast<uintptr_t>(out) & 15) || (ldo * esz) % 16 || cols % box_c) return -3;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ldo * esz};
+  cuuint32_t box[2] = {box_c, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                        const_cast<void*>(out), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        epi == EPI_SWIGLU ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
@@ -1247,9 +1444,29 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
     p.pair = 1;
     p.tn = 256;
     p.box_rows = p.tn / 2;
-    const long long ptiles = (long long)((N + 2 * kBM - 1) / (2 * kBM)) * ((kind_T + p.tn - 1) / p.tn);
+    const long long n_tt = (kind_T + p.tn - 1) / p.tn;
+    const long long ptiles = (long long)((N + 2 * kBM - 1) / (2 * kBM)) * n_tt;
     if (ptiles <= num_sms / 2 && kb < 128) p.max_parts = 1;  // QKV: one wave of whole tiles
     if (ptiles > num_sms / 2) p.whole = 1;                   // gate/up, lm_head: whole tiles beat stream-K fixups
+    // Token-major kernel: whole tiles of nw weight rows, nw picked so the
+    // waves of pair tiles fit the SMs -- per-SM work of a wave ~ nw, so the
+    // cost is waves * nw (12288 rows: 64 tiles of 192 = one wave on 74 pairs
+    // instead of 48 tiles of 256 on 48 pairs); ties keep the larger tile.
+    static const bool no_swap = std::getenv("COCOB200_NO_SWAP") != nullptr;  // A/B experiments
+    if (!no_swap && N % 32 == 0) {
+      const long long pairs = num_sms / 2;
+      long long best = -1;
+      for (int nw = 256; nw >= 128; nw -= 32) {
+        const long long t = (N + nw - 1) / nw * n_tt;
+        const long long cost = (t + pairs - 1) / pairs * nw;
+        if (best < 0 || cost < best) {
+          best = cost;
+          p.nw = nw;
+        }
+      }
+      p.whole = 1;
+      p.max_parts = 0;
+    }
     return p;
   }
   p.pair = 0;
@@ -1356,15 +1573,66 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Cfg::kSmemBytes));
+    if (e == cudaSuccess && TNP == 2 * kBM)
+      e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(Cfg::kSmemBytes));
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
   a.n_ttiles = (a.T + TNP - 1) / TNP;
-  a.n_mtiles = (a.N + 2 * kBM - 1) / (2 * kBM);
   a.kblocks = (a.K + kBK - 1) / kBK;
   a.vec = vec_ok(a);
+  // Token-major kernel (plan.nw): whole tiles of nw weight rows; the weight
+  // map with nw / 2-row boxes and the token-major output map are built here
+  // and cached (the runtime's weight and output buffers are long-lived).
+  if (TNP == 2 * kBM && plan.nw > 0 && a.w_base && !a.w_tiled && a.N % 32 == 0 && a.vec) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, long long, long long, long long, int>, CUtensorMap> wcache;
+    static std::map<std::tuple<const void*, int, long long, long long, int>, CUtensorMap> ocache;
+    CUtensorMap wt;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      const auto key = std::make_tuple(a.w_base, (long long)a.N, (long long)a.K, a.w_stride, plan.nw);
+      auto it = wcache.find(key);
+      if (it == wcache.end()) {
+        CUtensorMap m;
+        if (make_kmajor_map(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride), uint32_t(plan.nw / 2)))
+          return cudaErrorInvalidValue;
+        it = wcache.emplace(key, m).first;
+      }
+      wt = it->second;
+    }
+    a.nw = plan.nw;
+    a.n_mtiles = (a.N + a.nw - 1) / a.nw;
+    const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
+    a.units = int(tiles * a.kblocks);
+    a.whole_tiles = 1;
+    const long long pairs = std::min<long long>(num_sms / 2, tiles);
+    CUtensorMap ot;
+    std::memset(&ot, 0, sizeof(ot));
+    a.tma = 0;
+    static const bool no_tma = std::getenv("COCOB200_NO_TMA_STORE") != nullptr;  // A/B experiments
+    if (a.out_rows > 0 && !no_tma) {
+      const long long cols = a.epi == EPI_SWIGLU ? a.N / 2 : a.N;
+      const auto key = std::make_tuple(static_cast<const void*>(a.out), a.epi, a.out_rows, a.ldo, int(cols));
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = ocache.find(key);
+      if (it == ocache.end()) {
+        CUtensorMap m;
+        if (make_out_map_tok(&m, a.out, a.epi, uint64_t(a.out_rows), uint64_t(cols), uint64_t(a.ldo)) == 0)
+          it = ocache.emplace(key, m).first;
+      }
+      if (it != ocache.end()) {
+        ot = it->second;
+        a.tma = 1;
+      }
+    }
+    return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes,
+                              st, 2u, wt, x, ot, a);
+  }
+  a.n_mtiles = (a.N + 2 * kBM - 1) / (2 * kBM);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.units = int(tiles * a.kblocks);
   a.whole_tiles = plan.whole;
@@ -1372,8 +1640,8 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
   if (pairs > a.units) pairs = a.units;
   const int mp = a.max_parts > 0 ? a.max_parts : plan.max_parts;
   if (mp > 0 && pairs > tiles * mp) pairs = tiles * mp;
-  return launch_pdl_cluster(gemm_tc2_kernel<TNP>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes, st,
-                            2u, w, x, o, a);
+  return launch_pdl_cluster(gemm_tc2_kernel<TNP, false>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes,
+                            st, 2u, w, x, o, a);
 }
 
 cudaError_t gemm_launch(const CUtensorMap& w, const CUtensorMap& x, const GemmArgs& a_in, const GemmPlan& plan,

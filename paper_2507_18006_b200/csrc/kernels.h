@@ -48,6 +48,10 @@ struct GemmArgs {
   const uint16_t* gamma_next;
   float* ssq_out;
   int ssq_np;  // partials per row (= d / 32)
+  long long out_rows;  // rows of the output tensor (TMA-store maps); 0 = unknown (register stores)
+  const void* w_base;  // weight base / row stride (elements): token-major plans build their own weight map
+  long long w_stride;
+  int nw;              // set by the launcher: weight rows per pair tile of the token-major kernel
   int norm_d;
   float norm_eps;
   // filled by the launcher
@@ -74,6 +78,7 @@ struct GemmPlan {
   int corun;     // 1 = shallow ring so two CTAs (this kernel's and the next one's) share an SM
   int cstream;   // > 1: cluster stream-K, clusters of cstream CTAs each owning whole tiles (DSMEM reduce)
   int nclusters; // cluster stream-K: number of clusters
+  int nw;        // > 0: token-major CTA-pair kernel, whole tiles of nw weight rows (32..256, multiple of 32)
 };
 // kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
 // micro-batches compute exactly what the unreplicated pass would.

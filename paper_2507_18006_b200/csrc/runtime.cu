@@ -77,6 +77,8 @@ struct OpMap {
   CUtensorMap m2;
   CUtensorMap m3;
   bool has3 = false;
+  const void* base = nullptr;  // operand base / row stride (elements): the GEMM launcher builds
+  uint64_t stride = 0;         // the token-major kernel's weight boxes from these
 };
 
 int box_index(int rows) {
@@ -300,6 +302,8 @@ int check_dev(cb_model* m, int dev) {
 }
 
 int make_map(OpMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  map->base = base;
+  map->stride = k;
   int r = cb::make_kmajor_map(&map->m2, base, rows, k, k, box_rows);
   if (r != 0) return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   map->has3 = box_rows <= 128 && k % 128 == 0 && cb::make_kmajor_map3(&map->m3, base, rows, k, k, box_rows, 2) == 0;
@@ -437,6 +441,9 @@ int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K,
   a.epi = epi;
   a.ldo = ldo;
   a.out = out;
+  a.out_rows = out == ws.logits ? m->d.max_slots : m->d.max_tokens;
+  a.w_base = w.base;
+  a.w_stride = (long long)w.stride;
   a.ws = ws.gemm_ws;
   a.counters = ws.gemm_cnt;
   if (nio.consume || nio.gamma_next) {
@@ -597,6 +604,8 @@ int proj_gemm(cb_model* m, const ProjView& v, const OpMap* xmaps, int T, int r0,
   CB_TRY(use(devctx(m, v.dev)));
   if (cb::make_kmajor_map(&wm.m2, v.base, uint64_t(v.rows), uint64_t(v.k), v.row_stride, 128) != 0)
     return fail(CB_ECUDA, "cuTensorMapEncodeTiled failed for a migrated projection");
+  wm.base = v.base;
+  wm.stride = v.row_stride;
   return gemm(m, v.dev, wm, xmaps, v.rows, v.k, T, r0, epi, out, ldo);
 }
 

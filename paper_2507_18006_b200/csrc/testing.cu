@@ -99,6 +99,9 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   a.row_off = row_off;
   a.epi = epi;
   a.ldo = ldo;
+  a.out_rows = row_off + T;
+  a.w_base = w;
+  a.w_stride = K;
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
@@ -152,6 +155,9 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   a.T = T;
   a.epi = epi;
   a.ldo = ldo;
+  a.out_rows = T;
+  a.w_base = tiled ? nullptr : w;  // (weight copies: the token-major map follows the first copy)
+  a.w_stride = K;
   a.out = out;
   a.ws = ws->gemm_ws;
   a.counters = ws->cnt;
@@ -168,12 +174,18 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   const uint64_t ocols = epi == cb::EPI_SWIGLU ? uint64_t(N) / 2 : uint64_t(N);
   const CUtensorMap* pmo =
       (!(dbg_bits & 256) && cb::make_out_map(&mo, out, epi, uint64_t(T), ocols, uint64_t(ldo)) == 0) ? &mo : nullptr;
-  for (int i = 0; i < 3; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0, pmo);
+  // launch with weight copy i (the token-major plan builds its weight map from w_base)
+  auto launch = [&](int i) {
+    const size_t ci = size_t(i) % mws.size();
+    if (!tiled) a.w_base = static_cast<const uint8_t*>(w) + ci * g_wcopy_stride;
+    return cb::gemm_launch(mws[ci], mx, a, plan, ws->sms, 0, pmo);
+  };
+  for (int i = 0; i < 3; ++i) launch(i);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, 0);
-  for (int i = 0; i < iters; ++i) cb::gemm_launch(mws[i % mws.size()], mx, a, plan, ws->sms, 0, pmo);
+  for (int i = 0; i < iters; ++i) launch(i);
   cudaEventRecord(e1, 0);
   if (cudaEventSynchronize(e1) != cudaSuccess) return CB_ECUDA;
   float ms = 0;
@@ -181,7 +193,7 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   *ms_per_launch = ms / iters;
   if (a.trace) {
     cudaMemset(trace, 0, 148 * 512 * 8);
-    cb::gemm_launch(mws[iters % mws.size()], mx, a, plan, ws->sms, 0, pmo);
+    launch(iters);
     cudaDeviceSynchronize();
     cudaMemcpy(g_trace, trace, sizeof(g_trace), cudaMemcpyDeviceToHost);
   }
