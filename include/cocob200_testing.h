@@ -39,6 +39,8 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
                    void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch);
 /* cbt_gemm_bench rotates over n weight copies stride_bytes apart (weights larger than L2, as in a step) */
 int cbt_gemm_set_wcopies(int32_t n, int64_t stride_bytes);
+/* host milliseconds the runtime spent enqueuing its last forward pass (launch-overhead experiments) */
+double cbt_last_enqueue_ms(void);
 /* Fused-RMSNorm fields (GemmArgs ssq_in / h_out / gamma_next / ssq_out) for
  * every following cbt_gemm / cbt_gemm_bench launch; all null = plain GEMM. */
 int cbt_gemm_set_norm(const float* ssq_in, uint16_t* h_out, const uint16_t* gamma_next, float* ssq_out, int32_t np,

@@ -128,6 +128,7 @@ _SIGS = {
     "cbt_gemm_trace": (C.c_int, [_P, C.c_int32]),
     "cbt_mma_probe": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "cbt_gemm_set_wcopies": (C.c_int, [C.c_int32, C.c_int64]),
+    "cbt_last_enqueue_ms": (C.c_double, []),
     "cbt_gemm_set_norm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float]),
     "cbt_tma_probe": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_int32, _F32P]),

@@ -23,6 +23,7 @@
 // peer-to-peer copy of exactly ModuleCatalog.decoder_layer_mb bytes (MHA).
 // KV per (layer, device): [slot][max_ctx][2][Hkv hd] bf16.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -894,8 +895,11 @@ std::vector<int> split_batch_vec(int bs, int p) {
 }
 
 // One pass over a group of sequences whose rows fit max_tokens.
+double g_last_enqueue_ms = 0.0;  // experiments: host time to enqueue the last pass (cbt_last_enqueue_ms)
+
 int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_t* tokens, const int32_t* lens,
               int32_t* next_out, float* logits_out, float* ms_out) {
+  const auto enq0 = std::chrono::steady_clock::now();
   const cb_model_desc& d = m->d;
   const bool prefill = phase == CB_PHASE_PREFILL;
   std::vector<int> seq_row(bs + 1, 0);
@@ -1025,6 +1029,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
   }
   CB_CUDA(cudaEventRecord(hc.t1, hc.compute));
+  g_last_enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - enq0).count();
   CB_CUDA(cudaMemcpyAsync(m->pin_next, hw.next, size_t(bs) * 4, cudaMemcpyDeviceToHost, hc.compute));
   if (logits_out)
     CB_CUDA(cudaMemcpyAsync(logits_out, hw.logits, size_t(bs) * d.vocab * 4, cudaMemcpyDeviceToHost, hc.compute));
@@ -1800,5 +1805,8 @@ int cb_evict_replica(cb_model* m, int32_t layer, int32_t dev, cb_op_stats* st) {
   drop_kv_if_unused(m, L, dev);
   return CB_OK;
 }
+
+// experiments: host milliseconds spent enqueuing the last forward pass
+double cbt_last_enqueue_ms() { return g_last_enqueue_ms; }
 
 }  // extern "C"

@@ -125,6 +125,10 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   // 1..99 cap the stream-K parts per tile
   if (max_parts == 201 || max_parts == 202) {
     plan = cb::GemmPlan{max_parts == 201 ? 256 : 128, 1, max_parts == 201 ? 128 : 64, 1, 0};
+  } else if (max_parts > 300 && max_parts <= 308) {  // token-major pair kernel, nw = 32 * (knob - 300)
+    plan = cb::GemmPlan{256, 1, 128, 1, 0};
+    plan.whole = 1;
+    plan.nw = 32 * (max_parts - 300);
   } else if (max_parts == 203 && plan.pair) {
     plan = cb::GemmPlan{cb::gemm_pick_tn(T), 0, cb::gemm_pick_tn(T), 1, 0};
   } else if (max_parts < 0) {  // 1-CTA kernel with cluster split -max_parts

@@ -23,13 +23,17 @@ slots = np.arange(B, dtype=np.int32)
 nxt, _, _ = ex.prefill(slots, rng.integers(0, 32000, B * 128).astype(np.int32), np.full(B, 128, np.int32))
 for _ in range(3):
     nxt, _, ms = ex.decode(slots, nxt)
-ms_all = []
+ms_all, enq = [], []
+from paper_2507_18006_b200 import _lib
+lib = _lib.load()
 torch.cuda.profiler.start()
 for _ in range(STEPS):
     nxt, _, ms = ex.decode(slots, nxt)
     ms_all.append(ms)
+    enq.append(lib.cbt_last_enqueue_ms())
 torch.cuda.profiler.stop()
-print(f"B={B}: decode step device ms {np.mean(ms_all):.3f} ({B / np.mean(ms_all) * 1e3:.0f} tok/s)")
+print(f"B={B}: decode step device ms {np.mean(ms_all):.3f} ({B / np.mean(ms_all) * 1e3:.0f} tok/s)"
+      f"  host enqueue ms {np.mean(enq):.3f}")
 ex.profile(True)
 for _ in range(3):
     nxt, _, ms = ex.decode(slots, nxt)
