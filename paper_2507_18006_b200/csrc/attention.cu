@@ -234,6 +234,20 @@ template <int HD, int GQ, int U>
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attn2_kernel(const AttnArgs a, int nsplit, int chunk) {
   pdl_trigger();
+  if (a.prefetch_pos > 0) {
+    // The cached K/V before the newest position were written by earlier steps
+    // (and the row metadata by the step's H2D copy): pull this CTA's share of
+    // them towards L2 while the kernel producing q (the QKV GEMM) finishes.
+    // 4 threads per position: K and V rows of this kv head, 2 x 128 B lines each.
+    const int row = a.row_off + int(blockIdx.y);
+    const int cur = a.row_pos[row];
+    const int p0 = int(blockIdx.z) * chunk, p1 = min(cur, p0 + min(chunk, a.prefetch_pos));
+    const size_t kvd = size_t(a.Hkv) * HD, pos_stride = 2 * kvd;
+    const uint16_t* kb = a.kv + (size_t)a.row_slot[row] * a.max_ctx * pos_stride + (size_t)blockIdx.x * HD;
+    const int part = threadIdx.x & 3;
+    for (int p = p0 + int(threadIdx.x >> 2); p < p1; p += int(blockDim.x >> 2))
+      prefetch_l2(kb + (size_t)p * pos_stride + (part >> 1) * kvd + (part & 1) * 64);
+  }
   pdl_wait();
   constexpr int G = HD / 8;           // lanes per group
   constexpr int P = 32 / G;           // groups per warp
@@ -465,7 +479,14 @@ __global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
 }
 
 template <int HD>
-static cudaError_t attention_hd(const AttnArgs& a, int num_sms, cudaStream_t st) {
+static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t st) {
+  // positions per CTA warmed into L2 before the PDL wait (0 = none)
+  static const int prefetch_pos = [] {
+    const char* e = getenv("CB_ATTN_PREFETCH_POS");
+    return e ? atoi(e) : 64;
+  }();
+  AttnArgs a = a_in;
+  a.prefetch_pos = prefetch_pos;
   const int gq = a.H / a.Hkv;
   constexpr int NG = kAttnWarps * (32 / (HD / 8));
   if (gq < 1 || NG % gq != 0) return cudaErrorInvalidValue;

@@ -893,7 +893,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     const int nw0 = mt * kBM + qq * 32;
     const bool pre = epi_warp && a.epi == EPI_RESID && a.h_out != nullptr;  // rp holds the residual (see above)
     cluster_sync_all();
-    if (epi_warp) {
+    if (epi_warp && !(a.dbg & 128)) {  // dbg 128 (experiments): skip the reduction
       EpiWarp e(epi_smem + w * kEpiWarpBytes, qq, lane, row_scales(a, smem + ring_bytes + kTbufBytes));
       const uint32_t base = smem_u32(sW);
       for (int ch = w / qpr; ch < nchunks; ch += cstep) {

@@ -124,6 +124,7 @@ struct AttnArgs {
   const float2* rope;  // non-null: fused decode path (RoPE of q/k + KV append inside the kernel)
   int T, row_off, H, Hkv, hd, max_ctx, max_len;
   float scale;  // 1/sqrt(hd)
+  int prefetch_pos;  // set by the launcher: cached positions per CTA prefetched to L2 before the PDL wait
 };
 cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
 

@@ -118,8 +118,9 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
   int r = ws_for_current(&ws);
   if (r) return r;
   cb::GemmPlan plan = cb::gemm_plan(N, K, T, ws->sms);
-  const int dbg_bits = max_parts / 1000;
-  max_parts %= 1000;
+  // knob + sign * 1000 * dbg bits (negative knobs keep their sign: -4 - 8000)
+  const int dbg_bits = (max_parts < 0 ? -max_parts : max_parts) / 1000;
+  max_parts = max_parts < 0 ? -((-max_parts) % 1000) : max_parts % 1000;
   // experiment knobs: 201 / 202 force the CTA-pair kernel (256 / 128-token
   // tiles), 203 forces the 1-CTA kernel, < 0 forces cluster split -max_parts,
   // 1..99 cap the stream-K parts per tile
@@ -129,6 +130,10 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
     plan = cb::GemmPlan{256, 1, 128, 1, 0};
     plan.whole = 1;
     plan.nw = 32 * (max_parts - 300);
+  } else if (max_parts > 400 && max_parts <= 408) {  // 1-CTA kernel, 128-token tiles, cluster split (knob - 400)
+    plan = cb::GemmPlan{128, 0, 128, max_parts - 400, 0};
+  } else if (max_parts > 410 && max_parts <= 418) {  // 1-CTA kernel, 64-token tiles, cluster split (knob - 410)
+    plan = cb::GemmPlan{64, 0, 64, max_parts - 410, 0};
   } else if (max_parts == 203 && plan.pair) {
     plan = cb::GemmPlan{cb::gemm_pick_tn(T), 0, cb::gemm_pick_tn(T), 1, 0};
   } else if (max_parts < 0) {  // 1-CTA kernel with cluster split -max_parts

@@ -20,7 +20,7 @@ OC = N // 2 if EPI == 3 else N
 out = torch.zeros(T, OC, device='cuda', dtype=torch.float32 if EPI in (1, 2) else torch.bfloat16)
 ms = C.c_float()
 assert lib.cbt_gemm_bench(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()), T, N, K, T, EPI,
-                          C.c_void_p(out.data_ptr()), OC, 20, mode + 8000, C.byref(ms)) == 0
+                          C.c_void_p(out.data_ptr()), OC, 20, mode + 8000 if mode >= 0 else mode - 8000, C.byref(ms)) == 0
 tr = np.zeros(148 * 512, dtype=np.uint64)
 lib.cbt_gemm_trace(tr.ctypes.data_as(C.c_void_p), tr.size)
 tr = tr.reshape(148, 512)
@@ -57,6 +57,9 @@ for c in (0, 1, 2, 75, 147):
           f"{np.nanmedian(iss[:nk]-mma[:nk])*1000:.0f} ns, issued->next W-landed {np.nanmedian(wl[1:nk]-iss[:nk-1])*1000:.0f} ns")
     print(f"     S={S}: landed -> stage free median {np.median(lt)*1000:.0f} ns; "
           f"load issued -> landed median {np.median(land)*1000:.0f} ns")
+    if not np.isnan(rel[c, 140]):
+        print(f"     cluster split-K: reduce start {rel[c,140]:.2f} reduce+emit done {rel[c,141]:.2f}; chunks (loaded, emitted):",
+              " ".join(f"({rel[c,142+2*k]:.2f},{rel[c,143+2*k]:.2f})" for k in range(4)))
     for sg in range(4):
         ev = rel[c, 130 + 4 * sg: 134 + 4 * sg]
         if np.isnan(ev[0]):
