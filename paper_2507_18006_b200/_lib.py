@@ -9,9 +9,10 @@ CB_ENOREPLICA -> MissingReplicaError, everything else -> RuntimeError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libcocob200.so"
+LIB_PATH = Path(os.environ.get("COCOB200_LIB") or Path(__file__).resolve().parent / "libcocob200.so")  # override: A/B experiments
 
 CB_OK = 0
 CB_EINVAL = -1
