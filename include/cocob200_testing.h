@@ -35,6 +35,9 @@ int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
 int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
                           int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx);
 /* wall-clock of `iters` back-to-back GEMM launches measured with CUDA events, ms per launch */
+// gemm_plan's choice for an (N, K, T) launch (host only): out[11] = tn, pair, box_rows, csplit,
+// max_parts, whole, kd, corun, cstream, nclusters, nw.
+int cbt_gemm_plan(int32_t N, int32_t K, int32_t T, int32_t num_sms, int32_t kind_T, int32_t* out);
 int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K, int32_t T, int32_t epi,
                    void* out, int64_t ldo, int32_t iters, int32_t max_parts, float* ms_per_launch);
 /* cbt_gemm_bench rotates over n weight copies stride_bytes apart (weights larger than L2, as in a step) */
