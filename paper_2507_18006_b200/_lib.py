@@ -114,6 +114,7 @@ _SIGS = {
     "cb_profile_read": (C.c_int, [_P, C.c_int32, C.POINTER(KStat)]),
     # kernel-level test entry points (include/cocob200_testing.h)
     "cbt_gemm": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64]),
+    "cbt_gemm_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "cbt_gemm_bench": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64,
                                  C.c_int32, C.c_int32, _F32P]),
     "cbt_rmsnorm": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_float]),
