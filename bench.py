@@ -419,7 +419,10 @@ def run_replicas(args, rank: int, world: int, dist) -> None:
     if rank == 0 and world >= 2 and not same_gpu:
         ex.close()
         rt.close()
-        mig = measure_nvlink_migration()
+        try:
+            mig = measure_nvlink_migration()
+        except Exception as e:  # the throughput line must still print (the migration is a side measurement)
+            mig = {"error": f"{type(e).__name__}: {e}"[:300]}
     dist.barrier()
     if rank != 0:
         return
