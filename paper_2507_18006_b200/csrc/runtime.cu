@@ -1575,8 +1575,26 @@ int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const 
     if (phase == CB_PHASE_PREFILL && len != 0) return fail(CB_EINVAL, "prefill into a non-empty slot");
     if (phase == CB_PHASE_DECODE && len == 0) return fail(CB_EINVAL, "decode on an empty slot");
   }
-  if (phase == CB_PHASE_DECODE) return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out);
+  // token ids index the embedding table on the device: reject out-of-range ids
+  // before any launch (an out-of-bounds gather would poison the context)
+  auto bad_tokens = [&](long long n) {
+    for (long long t = 0; t < n; ++t)
+      if (tokens[t] < 0 || tokens[t] >= m->d.vocab) return true;
+    return false;
+  };
+  if (phase == CB_PHASE_DECODE) {
+    if (bad_tokens(bs)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
+    return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out);
+  }
   if (!prompt_lens) return fail(CB_EINVAL, "prefill needs prompt_lens");
+  {
+    long long total = 0;
+    for (int t = 0; t < bs; ++t) {
+      if (prompt_lens[t] < 1 || prompt_lens[t] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
+      total += prompt_lens[t];
+    }
+    if (bad_tokens(total)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
+  }
   // prefill: group sequences so each pass fits max_tokens rows
   int i = 0, tok_off = 0;
   while (i < bs) {

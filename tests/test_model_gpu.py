@@ -381,3 +381,39 @@ def test_ragged_long_prompts_prefill_matches_oracle(runtime, confident):
     assert np.array_equal(got, ref)
     assert max(np.abs(a - b).max() for a, b in zip(logits, ref_logits)) <= LOGIT_TOL
     ex.close()
+
+
+def test_invalid_step_inputs_rejected_before_any_launch(runtime, confident):
+    """Bad batches fail with OpError (CB_EINVAL) before a kernel runs, and the
+    executor keeps serving: its next steps equal a fresh executor's (whose
+    tokens the config-1 tests pin to the oracle)."""
+    ex = _executor(runtime, confident)
+    rng = np.random.default_rng(5)
+    prompts = [rng.integers(0, TINY.vocab, 8).astype(np.int32) for _ in range(4)]
+    slots = np.arange(4, dtype=np.int32)
+    lens = np.full(4, 8, np.int32)
+    bad = np.concatenate(prompts)
+    bad[5] = TINY.vocab  # one past the embedding table
+    with pytest.raises(O.OpError):
+        ex.prefill(slots, bad, lens)
+    bad[5] = -1
+    with pytest.raises(O.OpError):
+        ex.prefill(slots, bad, lens)
+    with pytest.raises(O.OpError):  # duplicate slot
+        ex.prefill(np.array([0, 0, 1, 2], np.int32), np.concatenate(prompts), lens)
+    with pytest.raises(O.OpError):  # decode on empty slots
+        ex.decode(slots, np.zeros(4, np.int32))
+    nxt, _, _ = ex.prefill(slots, np.concatenate(prompts), lens)
+    with pytest.raises(O.OpError):  # prefill into live slots
+        ex.prefill(slots, np.concatenate(prompts), lens)
+    with pytest.raises(O.OpError):
+        ex.decode(slots, np.full(4, TINY.vocab + 3, np.int32))
+    # the model state is intact: greedy decode continues exactly like a fresh run
+    fresh = _executor(runtime, confident)
+    want, _ = _greedy_gpu(fresh, prompts, 4)
+    got = [nxt]
+    for _ in range(3):
+        got.append(ex.decode(slots, got[-1])[0])
+    assert np.array_equal(np.stack(got, 1), want)
+    ex.close()
+    fresh.close()
