@@ -417,3 +417,44 @@ def test_invalid_step_inputs_rejected_before_any_launch(runtime, confident):
     assert np.array_equal(np.stack(got, 1), want)
     ex.close()
     fresh.close()
+
+
+@pytest.mark.parametrize("B", [8, 160])
+def test_llama7b_shape_layers_match_oracle(runtime, B):
+    """Full Llama-2-7B geometry (d 4096, d_ff 11008, 32 heads, vocab 32000) --
+    the kernels and plans the bench runs, incl. the CTA-pair kernels above 128
+    rows -- for 2 decoder layers, layer 2 replicated on a second logical device:
+    teacher-forced logits vs the fp32 oracle within the north star's 2e-2
+    max-abs, greedy tokens identical wherever the oracle's top-2 margin exceeds
+    twice that."""
+    from oracle.cpu_llama import LlamaConfig
+
+    cfg7 = LlamaConfig(2, 4096, 11008, 32, 32, 32000)
+    w = init_weights(cfg7, seed=3)
+    L, steps = 4, 3
+    ex = Executor(runtime, ExecutorConfig(n_layers=2, d_model=4096, d_ff=11008, n_heads=32, vocab=32000,
+                                          max_slots=B, max_ctx=16, max_tokens=max(B * L, 256)))
+    ex.load_model(w, device_of_layer=0)
+    cat = D.ModuleCatalog.from_model(D.ModelSpec(2, 4096, 11008, 32))
+    ex.apply(O.ReplicateLayer(2, 1), cat, D.ClusterSpec.b200(2))
+    oracle = OracleModel(cfg7, w, max_ctx=16)
+    rng = np.random.default_rng(9)
+    prompts = [rng.integers(0, 32000, L).astype(np.int32) for _ in range(B)]
+    slots = np.arange(B, dtype=np.int32)
+    _, lg, _ = ex.prefill(slots, np.concatenate(prompts), np.full(B, L, np.int32), True)
+    ref = oracle.forward(list(range(B)), np.concatenate(prompts), [L] * B)
+    worst, checked = 0.0, 0
+    for step in range(steps):
+        worst = max(worst, float(np.abs(lg - ref).max()))
+        srt = np.sort(ref, axis=1)
+        sure = (srt[:, -1] - srt[:, -2]) > 2 * LOGIT_TOL
+        assert np.array_equal(lg.argmax(1)[sure], ref.argmax(1)[sure])
+        checked += int(sure.sum())
+        inp = ref.argmax(1).astype(np.int32)  # teacher forcing: both sides consume the oracle's tokens
+        if step + 1 < steps:
+            _, lg, _ = ex.decode(slots, inp, True)
+            ref = oracle.forward(list(range(B)), inp, None)
+    print(f"7B shape B={B}: max |logit - oracle| = {worst:.4g} over {steps} steps, {checked} confident decisions")
+    assert worst <= LOGIT_TOL, worst
+    assert checked >= steps * B // 2
+    ex.close()
