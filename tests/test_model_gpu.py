@@ -419,24 +419,28 @@ def test_invalid_step_inputs_rejected_before_any_launch(runtime, confident):
     fresh.close()
 
 
-@pytest.mark.parametrize("B", [8, 160])
-def test_llama7b_shape_layers_match_oracle(runtime, B):
-    """Full Llama-2-7B geometry (d 4096, d_ff 11008, 32 heads, vocab 32000) --
-    the kernels and plans the bench runs, incl. the CTA-pair kernels above 128
-    rows -- for 2 decoder layers, layer 2 replicated on a second logical device:
-    teacher-forced logits vs the fp32 oracle within the north star's 2e-2
-    max-abs, greedy tokens identical wherever the oracle's top-2 margin exceeds
-    twice that."""
+@pytest.mark.parametrize("shape,B", [("7b", 8), ("7b", 160), ("13b", 6), ("70b-gqa", 4)])
+def test_llama2_geometries_match_oracle(runtime, shape, B):
+    """Full Llama-2 geometries (7B: d 4096, d_ff 11008, 32 heads; 13B: d 5120,
+    d_ff 13824, 40 heads; 70B: d 8192, d_ff 28672, 64 q / 8 kv heads; vocab
+    32000) -- the kernels and plans the bench and configs 4 / 5 run, incl. the
+    CTA-pair kernels above 128 rows -- for 2 (7B) or 1 decoder layers, the last
+    layer replicated on a second logical device: teacher-forced logits vs the
+    fp32 oracle within the north star's 2e-2 max-abs, greedy tokens identical
+    wherever the oracle's top-2 margin exceeds twice that."""
     from oracle.cpu_llama import LlamaConfig
 
-    cfg7 = LlamaConfig(2, 4096, 11008, 32, 32, 32000)
+    n_l, d, ff, H, Hkv = {"7b": (2, 4096, 11008, 32, 32), "13b": (1, 5120, 13824, 40, 40),
+                          "70b-gqa": (1, 8192, 28672, 64, 8)}[shape]
+    cfg7 = LlamaConfig(n_l, d, ff, H, Hkv, 32000)
     w = init_weights(cfg7, seed=3)
     L, steps = 4, 3
-    ex = Executor(runtime, ExecutorConfig(n_layers=2, d_model=4096, d_ff=11008, n_heads=32, vocab=32000,
+    ex = Executor(runtime, ExecutorConfig(n_layers=n_l, d_model=d, d_ff=ff, n_heads=H,
+                                          n_kv_heads=None if Hkv == H else Hkv, vocab=32000,
                                           max_slots=B, max_ctx=16, max_tokens=max(B * L, 256)))
     ex.load_model(w, device_of_layer=0)
-    cat = D.ModuleCatalog.from_model(D.ModelSpec(2, 4096, 11008, 32))
-    ex.apply(O.ReplicateLayer(2, 1), cat, D.ClusterSpec.b200(2))
+    cat = D.ModuleCatalog.from_model(D.ModelSpec(n_l, d, ff, H))
+    ex.apply(O.ReplicateLayer(n_l, 1), cat, D.ClusterSpec.b200(2))
     oracle = OracleModel(cfg7, w, max_ctx=16)
     rng = np.random.default_rng(9)
     prompts = [rng.integers(0, 32000, L).astype(np.int32) for _ in range(B)]
@@ -454,7 +458,7 @@ def test_llama7b_shape_layers_match_oracle(runtime, B):
         if step + 1 < steps:
             _, lg, _ = ex.decode(slots, inp, True)
             ref = oracle.forward(list(range(B)), inp, None)
-    print(f"7B shape B={B}: max |logit - oracle| = {worst:.4g} over {steps} steps, {checked} confident decisions")
+    print(f"{shape} shape B={B}: max |logit - oracle| = {worst:.4g} over {steps} steps, {checked} confident decisions")
     assert worst <= LOGIT_TOL, worst
     assert checked >= steps * B // 2
     ex.close()
