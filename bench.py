@@ -484,7 +484,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--batch", type=int, default=256, help="sequences per GPU (headline; BASELINE config 2 lists 1..256)")
-    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",") if x], default=[64, 128],
+    ap.add_argument("--sweep", type=lambda s: [int(x) for x in s.split(",") if x], default=[1, 16, 64, 128],
                     help="other batch sizes timed on the same instance")
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--prompt", type=int, default=128)
