@@ -342,6 +342,44 @@ CB_DEVICE void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* sme
       "l"(cache_policy)
       : "memory");
 }
+// 3-D tile load (kd k-blocks in one box) whose completion bytes land on the pair leader's barrier
+CB_DEVICE void tma_load_3d_pair(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int c1, int c2,
+                                uint64_t cache_policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2),
+      "l"(cache_policy)
+      : "memory");
+}
+// CTA-pair version of umma_2kblock_elect: 8 x (M x N x 16) cta_group::2 MMAs over a
+// 2-k-block stage (the second k-block's operands a_step / b_step further, >> 4
+// encoded) and one commit multicast to the stage barrier of both CTAs.
+CB_DEVICE void umma_2kblock_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate, uint64_t* bar, uint32_t a_step, uint32_t b_step) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7, as, bs;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "cvt.u64.u32 as, %7;\n\tcvt.u64.u32 bs, %8;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 a4, %1, as;\n\tadd.s64 a5, a4, 2;\n\tadd.s64 a6, a4, 4;\n\tadd.s64 a7, a4, 6;\n\t"
+      "add.s64 b4, %2, bs;\n\tadd.s64 b5, b4, 2;\n\tadd.s64 b6, b4, 4;\n\tadd.s64 b7, b4, 6;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, 1;\n\t"
+      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t}" ::"r"(
+          d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)), "h"(uint16_t(3)), "r"(a_step),
+      "r"(b_step)
+      : "memory");
+}
 CB_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }

@@ -85,8 +85,8 @@ struct GemmCfg : RingCfg<kBM * kBK * 2 * KD, TN * kBK * 2 * KD> {
                                         : (kAccCols <= 256) ? 256
                                                             : 512;
 };
-template <int TNP>
-struct PairCfg : RingCfg<kBM * kBK * 2, (TNP / 2) * kBK * 2> {
+template <int TNP, int KD = 1>
+struct PairCfg : RingCfg<kBM * kBK * 2 * KD, (TNP / 2) * kBK * 2 * KD> {
   static constexpr uint32_t kTmemCols = 2 * TNP <= 256 ? 256 : 512;
 };
 
@@ -1080,11 +1080,17 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
 // same smem tiles and TMA loads -- so the accumulator is token-major and the
 // epilogue stores rows straight from TMEM (epi_drain_tok).  The transposing
 // epilogue of the weight-major layout was 20% of a T = 256 launch.
-template <int TNP, bool SWAP>
+//
+// KD = 2 (token-major plans, K % 128 == 0): a stage holds two k-blocks loaded as
+// one 3-D TMA box per operand -- a thread issues one box per ~400 clk whatever
+// its size up to 32 KB (TMA probe), so 16 KB boxes capped each producer at
+// ~41 B/clk/SM, below the MMA rate.
+template <int TNP, bool SWAP, int KD = 1>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
-  using Cfg = PairCfg<TNP>;
+  static_assert(KD == 1 || SWAP, "2-k-block stages: token-major kernel only");
+  using Cfg = PairCfg<TNP, KD>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1146,9 +1152,13 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 66 + (u - ubeg)] = globaltimer_ns();
         if (SWAP) {  // nw / 2 weight rows per CTA (box height of the launcher's map)
-          if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2);
-          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK,
-                           mt * a.nw + int(rank) * (a.nw >> 1), pol_w);
+          if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2 * KD);
+          if (KD > 1)
+            tma_load_3d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, 0,
+                             mt * a.nw + int(rank) * (a.nw >> 1), kb * KD, pol_w);
+          else
+            tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK,
+                             mt * a.nw + int(rank) * (a.nw >> 1), pol_w);
           if (++stage == S) { stage = 0; phase ^= 1; }
           continue;
         }
@@ -1173,8 +1183,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * Cfg::kXBytes);
-        tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
-                         a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
+        if (KD > 1)
+          tma_load_3d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, 0,
+                           a.row_off + tt * TNP + int(rank) * (TNP / 2), kb * KD, pol_x);
+        else
+          tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
+                           a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -1205,7 +1219,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
           __syncwarp();
           const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
           const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
-          if (SWAP)
+          if (SWAP && KD > 1)  // second k-block: 128 token rows / nw / 2 weight rows x 128 B further
+            umma_2kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage],
+                                    uint32_t((TNP / 2) * kBK * 2) >> 4, uint32_t(a.nw >> 1) * (kBK * 2) >> 4);
+          else if (SWAP)
             umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           else
             umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
@@ -1466,6 +1483,14 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
       }
       p.whole = 1;
       p.max_parts = 0;
+      // 2 k-blocks per stage (3-D boxes, half the TMA issues per byte): correct
+      // (tested) but measured 5-15% slower at T = 192..8192 -- the 3-stage ring
+      // of 64 KB stages pipelines worse -- so opt-in: COCOB200_PAIR_KD=2
+      static const int pair_kd_env = [] {
+        const char* e = std::getenv("COCOB200_PAIR_KD");
+        return e ? std::atoi(e) : 1;
+      }();
+      if (pair_kd_env == 2 && K % (2 * kBK) == 0) p.kd = 2;
     }
     return p;
   }
@@ -1569,6 +1594,7 @@ template <int TNP>
 static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& o, GemmArgs a,
                                const GemmPlan& plan, int num_sms, cudaStream_t st) {
   using Cfg = PairCfg<TNP>;
+  using Cfg2 = PairCfg<TNP, 2>;
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1578,6 +1604,9 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     if (e == cudaSuccess && TNP == 2 * kBM)
       e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(Cfg::kSmemBytes));
+    if (e == cudaSuccess && TNP == 2 * kBM)
+      e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(Cfg2::kSmemBytes));
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
@@ -1589,21 +1618,26 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
   // and cached (the runtime's weight and output buffers are long-lived).
   if (TNP == 2 * kBM && plan.nw > 0 && a.w_base && !a.w_tiled && a.N % 32 == 0 && a.vec) {
     static std::mutex mu;
-    static std::map<std::tuple<const void*, long long, long long, long long, int>, CUtensorMap> wcache;
+    static std::map<std::tuple<const void*, long long, long long, long long, int, int>, CUtensorMap> wcache;
     static std::map<std::tuple<const void*, int, long long, long long, int>, CUtensorMap> ocache;
+    const int kd = (plan.kd == 2 && a.K % (2 * kBK) == 0) ? 2 : 1;  // 3-D boxes of 2 k-blocks (x must be a 3-D map)
     CUtensorMap wt;
     {
       std::lock_guard<std::mutex> lk(mu);
-      const auto key = std::make_tuple(a.w_base, (long long)a.N, (long long)a.K, a.w_stride, plan.nw);
+      const auto key = std::make_tuple(a.w_base, (long long)a.N, (long long)a.K, a.w_stride, plan.nw, kd);
       auto it = wcache.find(key);
       if (it == wcache.end()) {
         CUtensorMap m;
-        if (make_kmajor_map(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride), uint32_t(plan.nw / 2)))
-          return cudaErrorInvalidValue;
+        const int e = kd == 2 ? make_kmajor_map3(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride),
+                                                 uint32_t(plan.nw / 2), 2)
+                              : make_kmajor_map(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride),
+                                                uint32_t(plan.nw / 2));
+        if (e) return cudaErrorInvalidValue;
         it = wcache.emplace(key, m).first;
       }
       wt = it->second;
     }
+    if (kd == 2) a.kblocks = a.K / (2 * kBK);
     a.nw = plan.nw;
     a.n_mtiles = (a.N + a.nw - 1) / a.nw;
     const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
@@ -1629,6 +1663,9 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
         a.tma = 1;
       }
     }
+    if (kd == 2)
+      return launch_pdl_cluster(gemm_tc2_kernel<TNP, true, 2>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
+                                Cfg2::kSmemBytes, st, 2u, wt, x, ot, a);
     return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes,
                               st, 2u, wt, x, ot, a);
   }
