@@ -333,7 +333,8 @@ def test_gemm_pair_kernel_row_count_invariant(lib, cuda, N, K):
 
 def test_gemm_optional_plans_subprocess():
     """The opt-in GEMM plans (cluster stream-K with DSMEM reduction, 1 k-block
-    stages, co-resident shallow rings) stay correct: same shapes through a fresh
+    stages, co-resident shallow rings, 2-k-block stages of the token-major pair
+    kernel) stay correct: same shapes through a fresh
     process with each switch flipped (plans are chosen once per process)."""
     import os
     import subprocess
@@ -347,7 +348,8 @@ from paper_2507_18006_b200 import _lib
 lib = _lib.load()
 P = lambda t: C.c_void_p(t.data_ptr())
 g = torch.Generator().manual_seed(0)
-for N, K, T, epi in [(12288, 4096, 64, 1), (22016, 4096, 16, 1), (4096, 4096, 100, 2), (2048, 1024, 7, 1)]:
+for N, K, T, epi in [(12288, 4096, 64, 1), (22016, 4096, 16, 1), (4096, 4096, 100, 2), (2048, 1024, 7, 1),
+                     (12288, 4096, 256, 1), (32000, 4096, 300, 1)]:
     w = (torch.randn(N, K, generator=g) * 0.02).to(torch.bfloat16).cuda()
     x = torch.randn(T, K, generator=g).to(torch.bfloat16).cuda()
     base = torch.randn(T, N, generator=g).cuda() if epi == 2 else torch.zeros(T, N).cuda()
@@ -359,7 +361,7 @@ for N, K, T, epi in [(12288, 4096, 64, 1), (22016, 4096, 16, 1), (4096, 4096, 10
 print("ok")
 '''
     from conftest import ROOT
-    for env in ({"COCOB200_CSTREAM": "1"}, {"COCOB200_KD": "1"}, {"COCOB200_CORUN": "1"}):
+    for env in ({"COCOB200_CSTREAM": "1"}, {"COCOB200_KD": "1"}, {"COCOB200_CORUN": "1"}, {"COCOB200_PAIR_KD": "2"}):
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT,
                              env={**os.environ, **env})
         assert out.returncode == 0 and "ok" in out.stdout, (env, out.stderr[-2000:])
