@@ -16,7 +16,7 @@ for region_mb in ([int(a) for a in sys.argv[1].split(',')] if len(sys.argv) > 1 
         iters = 3000 if region_mb <= 64 else 400
         iters = max(200, iters // kd)
         ms = C.c_float()
-        st = lib.cbt_tma_probe(C.c_void_p(big.data_ptr()), rows, box, stages, grid, iters, kd, nw, C.byref(ms))
+        st = lib.cbt_tma_probe(C.c_void_p(big.data_ptr()), rows, box, stages, grid, iters, kd, nw, 0, C.byref(ms))
         assert st == 0, (st, box, kd, stages, nw)
         tb = grid * nw * iters * box * 128 * kd / (ms.value * 1e-3) / 1e12
         print(f"region {region_mb:5d}MB box {box:3d}x{kd}x128B ({box*kd*128//1024:3d}KB) stages {stages:2d} warps {nw} "
