@@ -125,6 +125,15 @@ class Executor:
         """Load bf16 (uint16) weights; the first copy of a layer is its original."""
         arrs = {k: np.ascontiguousarray(getattr(w, k), dtype=np.uint16) for k in
                 ("attn_norm", "wq", "wk", "wv", "wo", "ffn_norm", "w_gate", "w_up", "w_down")}
+        c = self.cfg
+        hd = c.d_model // c.n_heads
+        kvd = (c.n_kv_heads or c.n_heads) * hd
+        want = {"attn_norm": (c.d_model,), "wq": (c.n_heads * hd, c.d_model), "wk": (kvd, c.d_model),
+                "wv": (kvd, c.d_model), "wo": (c.d_model, c.n_heads * hd), "ffn_norm": (c.d_model,),
+                "w_gate": (c.d_ff, c.d_model), "w_up": (c.d_ff, c.d_model), "w_down": (c.d_model, c.d_ff)}
+        for k, shape in want.items():  # the C side reads exactly these extents from the host pointers
+            if arrs[k].shape != shape:
+                raise O.OpError(f"layer {layer} {k}: shape {arrs[k].shape}, expected {shape} (PyTorch [out, in])")
         lw = _lib.LayerWeights(*[a.ctypes.data for a in arrs.values()])
         _lib.check(self.lib.cb_layer_load(self.handle, layer, device, C.byref(lw)), "cb_layer_load")
         self._rows[layer - 1] = (Replica(device, True),)
@@ -135,6 +144,11 @@ class Executor:
 
     def load_head(self, embed: np.ndarray, final_norm: np.ndarray, lm_head: np.ndarray) -> None:
         e, f, h = (np.ascontiguousarray(a, dtype=np.uint16) for a in (embed, final_norm, lm_head))
+        c = self.cfg
+        for name, a, shape in (("embed", e, (c.vocab, c.d_model)), ("final_norm", f, (c.d_model,)),
+                               ("lm_head", h, (c.vocab, c.d_model))):
+            if a.shape != shape:
+                raise O.OpError(f"{name}: shape {a.shape}, expected {shape}")
         _lib.check(self.lib.cb_head_load(self.handle, e.ctypes.data, f.ctypes.data, h.ctypes.data), "cb_head_load")
 
     def init_head_random(self, std: float = 0.02) -> None:

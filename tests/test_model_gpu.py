@@ -408,6 +408,9 @@ def test_invalid_step_inputs_rejected_before_any_launch(runtime, confident):
         ex.prefill(slots, np.concatenate(prompts), lens)
     with pytest.raises(O.OpError):
         ex.decode(slots, np.full(4, TINY.vocab + 3, np.int32))
+    import dataclasses
+    with pytest.raises(O.OpError):  # weights in the wrong layout are refused before the C side reads them
+        ex.load_layer(1, 0, dataclasses.replace(confident.layers[0], w_down=confident.layers[0].w_down.T))
     # the model state is intact: greedy decode continues exactly like a fresh run
     fresh = _executor(runtime, confident)
     want, _ = _greedy_gpu(fresh, prompts, 4)
