@@ -1081,10 +1081,9 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
 // epilogue stores rows straight from TMEM (epi_drain_tok).  The transposing
 // epilogue of the weight-major layout was 20% of a T = 256 launch.
 //
-// KD = 2 (token-major plans, K % 128 == 0): a stage holds two k-blocks loaded as
-// one 3-D TMA box per operand -- a thread issues one box per ~400 clk whatever
-// its size up to 32 KB (TMA probe), so 16 KB boxes capped each producer at
-// ~41 B/clk/SM, below the MMA rate.
+// KD = 2 (opt-in, token-major plans, K % 128 == 0): a stage holds two k-blocks
+// loaded as one 3-D TMA box per operand (half the TMA issues); measured slower
+// than KD = 1 -- 64 KB stages leave a 3-deep ring.
 template <int TNP, bool SWAP, int KD = 1>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
