@@ -324,6 +324,8 @@ struct EpiWarp {
   }
 };
 static_assert(3 * kChunkBytes <= kEpiWarpBytes, "token-major staging ring");
+static constexpr int kTokEpiWarpBytes = 3 * kChunkBytes;  // token-major kernel: the staging ring only
+static constexpr size_t kMaxDynSmem = 227 * 1024;         // sm_100 opt-in maximum per CTA
 
 // Fused RMSNorm consumer: the epilogue warps turn the producer's per-row
 // partial sums of squares into row scales rsqrt(mean(x^2) + eps), once per CTA
@@ -1090,13 +1092,22 @@ __global__ void __launch_bounds__(kThreads1, 1)
                     const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
   static_assert(KD == 1 || SWAP, "2-k-block stages: token-major kernel only");
   using Cfg = PairCfg<TNP, KD>;
-  constexpr int S = Cfg::kStages;
+  // Token-major (SWAP, KD 1) launches size the ring at run time: weight stages
+  // of exactly nw / 2 rows and 6 KB epilogue blocks (the token-major epilogue
+  // only stages TMA stores) leave room for a deeper ring (launch_pair)
+  constexpr bool kRt = SWAP && KD == 1;
+  const int S = kRt ? a.stages : Cfg::kStages;
+  const int WBYTES = kRt ? (a.nw >> 1) * kBK * 2 : Cfg::kWBytes;
+  constexpr int XBYTES = Cfg::kXBytes;
+  const int ring_bytes = S * (WBYTES + XBYTES);
+  const int tbuf_bytes = kRt ? 4 * kTokEpiWarpBytes : kTbufBytes;
+  const int epi_stride = kRt ? kTokEpiWarpBytes : kEpiWarpBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
-  uint8_t* sX = smem + S * Cfg::kWBytes;
-  uint8_t* epi_smem = smem + Cfg::kRingBytes;  // 4 x kEpiWarpBytes
-  uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + Cfg::kRingBytes + kTbufBytes);  // leader: weights landed
+  uint8_t* sX = smem + S * WBYTES;
+  uint8_t* epi_smem = smem + ring_bytes;  // 4 x epi_stride
+  uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + ring_bytes + tbuf_bytes);  // leader: weights landed
   uint64_t* xfull_bar = wfull_bar + S;   // leader: both CTAs' tokens landed
   uint64_t* empty_bar = xfull_bar + S;   // each CTA: stage consumed
   uint64_t* tfull_bar = empty_bar + S;   // each CTA: accumulator ready
@@ -1153,20 +1164,20 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (SWAP) {  // nw / 2 weight rows per CTA (box height of the launcher's map)
           if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2 * KD);
           if (KD > 1)
-            tma_load_3d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, 0,
+            tma_load_3d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, 0,
                              mt * a.nw + int(rank) * (a.nw >> 1), kb * KD, pol_w);
           else
-            tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK,
+            tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, kb * kBK,
                              mt * a.nw + int(rank) * (a.nw >> 1), pol_w);
           if (++stage == S) { stage = 0; phase ^= 1; }
           continue;
         }
-        if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], 2 * Cfg::kWBytes);
+        if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], 2 * WBYTES);
         const int mt128 = mt * 2 + int(rank);
         if (a.w_tiled)
-          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, 0, (mt128 * sk.kb + kb) * kBM, pol_w);
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, 0, (mt128 * sk.kb + kb) * kBM, pol_w);
         else
-          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * Cfg::kWBytes, kb * kBK, mt128 * kBM, pol_w);
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, kb * kBK, mt128 * kBM, pol_w);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
     }
@@ -1181,12 +1192,12 @@ __global__ void __launch_bounds__(kThreads1, 1)
         const int tt = (u / sk.kb) % n_tt, kb = u % sk.kb;
         mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
-        if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * Cfg::kXBytes);
+        if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * XBYTES);
         if (KD > 1)
-          tma_load_3d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, 0,
+          tma_load_3d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, 0,
                            a.row_off + tt * TNP + int(rank) * (TNP / 2), kb * KD, pol_x);
         else
-          tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK,
+          tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, kb * kBK,
                            a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
@@ -1216,8 +1227,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
           tc_fence_after();
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 2 + i] = globaltimer_ns();
           __syncwarp();
-          const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
-          const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
+          const uint64_t dw = dw0 + uint64_t((stage * WBYTES) >> 4);
+          const uint64_t dx = dx0 + uint64_t((stage * XBYTES) >> 4);
           if (SWAP && KD > 1)  // second k-block: 128 token rows / nw / 2 weight rows x 128 B further
             umma_2kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage],
                                     uint32_t((TNP / 2) * kBK * 2) >> 4, uint32_t(a.nw >> 1) * (kBK * 2) >> 4);
@@ -1240,7 +1251,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
     pdl_wait();  // outputs / residual / stream-K workspace belong to the previous kernel until now
     const int q = warp & 3;
     const int et = threadIdx.x - 64;  // 0..127
-    EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane, build_row_scales(a, smem + Cfg::kRingBytes + kTbufBytes, et));
+    EpiWarp e(epi_smem + q * epi_stride, q, lane, build_row_scales(a, smem + ring_bytes + tbuf_bytes, et));
     const uint32_t tempty_leader0 = dsmem_map(smem_u32(&tempty_bar[0]), 0);
     const uint32_t tempty_leader1 = dsmem_map(smem_u32(&tempty_bar[1]), 0);
     int acc = 0;
@@ -1278,7 +1289,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       if (!SWAP && !whole) {
         const PartMap pm{a.ws, sk, tile, 2, int(rank), TNP};
         epi_fixup(a, &tmO, e, &a.counters[2 * tile + int(rank)], pm, sk.cta_of(tile * sk.kb),
-                  sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(Cfg::kRingBytes),
+                  sk.cta_of(tile * sk.kb + sk.kb - 1), m0, row0, ncols, last_seg, smem, uint32_t(ring_bytes),
                   fix_bar, fix_phase, bcast, et, tr);
       }
       u += kb1 - kb0;
@@ -1600,9 +1611,9 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
   if (!attr_set[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(Cfg::kSmemBytes));
-    if (e == cudaSuccess && TNP == 2 * kBM)
+    if (e == cudaSuccess && TNP == 2 * kBM)  // runtime-sized ring: up to the opt-in maximum
       e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(Cfg::kSmemBytes));
+                               int(kMaxDynSmem));
     if (e == cudaSuccess && TNP == 2 * kBM)
       e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(Cfg2::kSmemBytes));
@@ -1665,8 +1676,20 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     if (kd == 2)
       return launch_pdl_cluster(gemm_tc2_kernel<TNP, true, 2>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
                                 Cfg2::kSmemBytes, st, 2u, wt, x, ot, a);
-    return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1), Cfg::kSmemBytes,
-                              st, 2u, wt, x, ot, a);
+    // ring of exactly-sized stages (nw / 2 weight rows + TNP / 2 token rows per
+    // k-block) in whatever the 6 KB-per-warp epilogue and the barriers leave
+    static const size_t budget = [] {
+      const char* e = std::getenv("COCOB200_PAIR_SMEM_KB");  // A/B experiments: the old 224 KB budget
+      return e ? size_t(std::atoi(e)) * 1024 : kMaxDynSmem;
+    }();
+    const size_t stage_bytes = size_t(plan.nw / 2) * kBK * 2 + Cfg::kXBytes;
+    const size_t fixed = size_t(4) * kTokEpiWarpBytes + 1024 + kBarBytes;
+    int stages = int((budget - fixed) / stage_bytes);
+    if (stages > kMaxStages) stages = kMaxStages;
+    if (stages < 2) return cudaErrorInvalidValue;
+    a.stages = stages;
+    return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
+                              size_t(stages) * stage_bytes + fixed, st, 2u, wt, x, ot, a);
   }
   a.n_mtiles = (a.N + 2 * kBM - 1) / (2 * kBM);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
