@@ -1467,6 +1467,9 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
     while (p.csplit < 4 && tiles * p.csplit * 2 <= num_sms && p.csplit * 2 <= kb) p.csplit *= 2;
     return p;
   }
+  // (token-major pairs also win for QKV / gate/up alone from ~80 rows -- 5-11%
+  // in gemm_perf -- but made the B=96/128 decode step 3-5% slower: the 1-CTA
+  // QKV plan leaves 52 SMs free for the attention CTAs that start under PDL)
   if (kind_T > kPairMinT) {
     p.pair = 1;
     p.tn = 256;

@@ -49,7 +49,7 @@ def test_gemm_bf16_out(lib, cuda, N, K, T):
 @pytest.mark.parametrize("N,K,T,row_off", [(4096, 4096, 64, 0), (12288, 4096, 16, 3), (4096, 11008, 64, 0),
                                            (22016, 4096, 8, 0), (1024, 4096, 1, 5), (12288, 4096, 200, 0),
                                            (32000, 4096, 128, 2), (4096, 11008, 256, 0), (22016, 4096, 1000, 0),
-                                           (4096, 4096, 2100, 7)])
+                                           (4096, 4096, 2100, 7), (12288, 4096, 100, 0), (22016, 4096, 77, 3)])
 def test_gemm_f32_7b_shapes(lib, cuda, N, K, T, row_off):
     """7B projection shapes (QKV / O / down / gate+up): stream-K splits across SMs."""
     torch = cuda

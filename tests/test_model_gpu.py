@@ -422,7 +422,7 @@ def test_invalid_step_inputs_rejected_before_any_launch(runtime, confident):
     fresh.close()
 
 
-@pytest.mark.parametrize("shape,B", [("7b", 8), ("7b", 160), ("13b", 6), ("70b-gqa", 4)])
+@pytest.mark.parametrize("shape,B", [("7b", 8), ("7b", 96), ("7b", 160), ("13b", 6), ("70b-gqa", 4)])
 def test_llama2_geometries_match_oracle(runtime, shape, B):
     """Full Llama-2 geometries (7B: d 4096, d_ff 11008, 32 heads; 13B: d 5120,
     d_ff 13824, 40 heads; 70B: d 8192, d_ff 28672, 64 q / 8 kv heads; vocab
