@@ -5,8 +5,11 @@ sys.path.insert(0, '.')
 from paper_2507_18006_b200 import _lib
 lib = _lib.load()
 P = lambda t: C.c_void_p(t.data_ptr())
-for (T, H, Hkv, ctx) in [(64, 32, 32, 150), (64, 32, 32, 512), (128, 32, 32, 256), (256, 32, 32, 300),
-                         (16, 32, 32, 2048), (1, 32, 32, 4096), (64, 64, 8, 512)]:
+SHAPES = [(64, 32, 32, 150), (64, 32, 32, 512), (128, 32, 32, 256), (256, 32, 32, 300),
+          (16, 32, 32, 2048), (1, 32, 32, 4096), (64, 64, 8, 512)]
+if len(sys.argv) > 1:  # T:ctx,T:ctx,... (MHA 32 heads)
+    SHAPES = [(int(a), 32, 32, int(b)) for a, b in (x.split(':') for x in sys.argv[1].split(','))]
+for (T, H, Hkv, ctx) in SHAPES:
     hd = 128
     qkv = torch.randn(T, (H + 2 * Hkv) * hd, device='cuda').to(torch.bfloat16)
     kv = torch.randn(T, ctx + 2, 2, Hkv * hd, device='cuda').to(torch.bfloat16)
