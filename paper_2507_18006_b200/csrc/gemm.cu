@@ -555,21 +555,23 @@ __global__ void __launch_bounds__(kThreads1, 1)
   using Cfg = GemmCfg<TN, KD>;
   // ring depth chosen at launch (<= Cfg::kStages): a shallow ring lets two CTAs
   // -- this kernel's and the next kernel's (PDL) -- share an SM
-  const int S = a.stages;
-  const int ring_bytes = S * Cfg::kStageBytes;
+  const int S = a.stages;                            // weight ring depth
+  const int SX = a.xstages > 0 ? a.xstages : S;      // activation ring depth
+  const int ring_bytes = S * Cfg::kWBytes + SX * Cfg::kXBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sW = smem;
   uint8_t* sX = smem + S * Cfg::kWBytes;
   uint8_t* epi_smem = smem + ring_bytes;  // 4 x kEpiWarpBytes
-  // Two stage rings with a shared index: weights and activations, each with
-  // its own full/empty barriers, so the weight ring fills before the
-  // activations of the previous kernel exist.
+  // Two stage rings, weights and activations, each with its own depth and
+  // full/empty barriers: the weight ring fills before the activations of the
+  // previous kernel exist, and streams from HBM (~1.1 us away) while the
+  // activations come from L2, so the weight ring gets the deeper share.
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + ring_bytes + kTbufBytes);  // weights landed
   uint64_t* empty_bar = full_bar + S;                                                     // weights consumed
   uint64_t* xfull_bar = empty_bar + S;                                                    // activations landed
-  uint64_t* xempty_bar = xfull_bar + S;                                                   // activations consumed
-  uint64_t* tfull_bar = xempty_bar + S;
+  uint64_t* xempty_bar = xfull_bar + SX;                                                  // activations consumed
+  uint64_t* tfull_bar = xempty_bar + SX;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* fix_bar = tempty_bar + 2;
   uint64_t* pfull_bar = fix_bar + 1;  // cluster stream-K: retained partial [first, last] complete
@@ -623,6 +625,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
     for (int i = 0; i < S; ++i) {
       mbar_init(&full_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < SX; ++i) {
       mbar_init(&xfull_bar[i], 1);
       mbar_init(&xempty_bar[i], 1);
     }
@@ -679,7 +683,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           tma_load_3d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, 0, a.row_off + tt * TN, kb * KD, pol_x);
         else
           tma_load_2d(&tmX, &xfull_bar[stage], sX + stage * Cfg::kXBytes, kb * kBK, a.row_off + tt * TN, pol_x);
-        if (++stage == S) { stage = 0; phase ^= 1; }
+        if (++stage == SX) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -690,8 +694,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
     constexpr uint32_t idesc = make_idesc_bf16(kBM, TN);
     const uint64_t dw0 = make_sw128_desc(smem_u32(sW));
     const uint64_t dx0 = make_sw128_desc(smem_u32(sX));
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, xstage = 0;
+    uint32_t phase = 0, xphase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = ubeg; u < uend;) {
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const uint32_t d_tmem = tmem_base + uint32_t(keep ? (2 + pslot) * TN : acc * TN);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
-        mbar_wait(&xfull_bar[stage], phase);
+        mbar_wait(&xfull_bar[xstage], xphase);
         tc_fence_after();
         const int i = u + (kb - kb0) - ubeg;
         if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 2 + i] = globaltimer_ns();
@@ -713,20 +717,21 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (a.dbg & 1) {  // experiments: no MMAs, release the stage at once
           if (lane == 0) {
             mbar_arrive(&empty_bar[stage]);
-            mbar_arrive(&xempty_bar[stage]);
+            mbar_arrive(&xempty_bar[xstage]);
           }
         } else {
           // descriptor start address += stage offset (>> 4 encoded, stays inside its 14-bit field)
           const uint64_t dw = dw0 + uint64_t((stage * Cfg::kWBytes) >> 4);
-          const uint64_t dx = dx0 + uint64_t((stage * Cfg::kXBytes) >> 4);
+          const uint64_t dx = dx0 + uint64_t((xstage * Cfg::kXBytes) >> 4);
           if (KD > 1)  // second k-block: 128 weight rows / TN token rows x 128 B further
-            umma_2kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage],
+            umma_2kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage],
                                uint32_t(kBM * kBK * 2) >> 4, uint32_t(TN * kBK * 2) >> 4);
           else
-            umma_kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[stage]);
+            umma_kblock_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage]);
         }
         if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
         if (++stage == S) { stage = 0; phase ^= 1; }
+        if (++xstage == SX) { xstage = 0; xphase ^= 1; }
       }
       __syncwarp();
       if (keep) {
@@ -1564,7 +1569,7 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   cudaGetDevice(&dev);
   if (!attr_set[dev & 63]) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<TN, KD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(Cfg::kSmemBytes));
+                                         int(kMaxDynSmem));
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(gemm_tc_kernel<TN, KD>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) cudaGetLastError();
@@ -1582,7 +1587,30 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   }
   if (plan.csplit > 1 && stages * Cfg::kStageBytes < TN * kBM * 4) stages = Cfg::kStages;  // smem holds the partial
   a.stages = stages;
-  const size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + kBarBytes;
+  a.xstages = 0;
+  size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + kBarBytes;
+  // Decoupled depths: activations (L2, re-read by every tile) need a short
+  // ring; the rest of the 227 KB goes to the weight ring (HBM, ~1.1 us away).
+  static const int xs_env = [] {
+    const char* e = std::getenv("COCOB200_XSTAGES");  // 0 = one shared depth (A/B experiments)
+    return e ? std::atoi(e) : -1;
+  }();
+  // Measured: a win for 128-row token tiles (2-k-block stages: -1% per B=128
+  // step); tiles <= 64 rows starve on 2-3 activation stages (consumed in ~0.2
+  // us each), and the T=256 split-K launches, faster alone, made the B=256
+  // step no faster -- both keep one shared depth.
+  const int xs = xs_env >= 0 ? xs_env : (TN == 128 && KD == 2 ? 2 : 0);
+  if (!plan.corun && xs > 0) {
+    const size_t fixed = size_t(kTbufBytes) + 1024 + kBarBytes;
+    int ws = int((kMaxDynSmem - fixed - size_t(xs) * Cfg::kXBytes) / Cfg::kWBytes);
+    if (ws > kMaxStages) ws = kMaxStages;
+    const size_t ring = size_t(ws) * Cfg::kWBytes + size_t(xs) * Cfg::kXBytes;
+    if (ws >= 2 && (plan.csplit <= 1 || ring >= size_t(TN) * kBM * 4)) {
+      a.stages = ws;
+      a.xstages = xs;
+      smem_bytes = ring + fixed;
+    }
+  }
   a.vec = vec_ok(a);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
   a.cluster_split = plan.csplit;

@@ -34,7 +34,8 @@ struct GemmArgs {
   int vec;            // set by the launcher: 16-byte vector epilogue stores are legal for out/N/ldo
   int tma;            // set by the launcher: an output tensor map was passed (TMA-store epilogue)
   int whole_tiles;    // set from the plan: CTA (pair) ranges rounded to whole tiles
-  int stages;         // set by the launcher: pipeline ring depth (1-CTA kernel)
+  int stages;         // set by the launcher: pipeline ring depth (1-CTA kernel: the weight ring)
+  int xstages;        // set by the launcher: activation ring depth (1-CTA kernel; 0 = stages)
   int cstream;        // set from the plan: cluster stream-K cluster size (> 1)
   int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
   // Fused RMSNorm (decode passes, T <= 256; SURVEY.md §8(a) rmsnorm):
