@@ -334,7 +334,7 @@ def test_gemm_pair_kernel_row_count_invariant(lib, cuda, N, K):
 def test_gemm_optional_plans_subprocess():
     """The opt-in GEMM plans (cluster stream-K with DSMEM reduction, 1 k-block
     stages, co-resident shallow rings, 2-k-block stages of the token-major pair
-    kernel) stay correct: same shapes through a fresh
+    kernel, decoupled / shared activation ring depths) stay correct: same shapes through a fresh
     process with each switch flipped (plans are chosen once per process)."""
     import os
     import subprocess
@@ -361,7 +361,8 @@ for N, K, T, epi in [(12288, 4096, 64, 1), (22016, 4096, 16, 1), (4096, 4096, 10
 print("ok")
 '''
     from conftest import ROOT
-    for env in ({"COCOB200_CSTREAM": "1"}, {"COCOB200_KD": "1"}, {"COCOB200_CORUN": "1"}, {"COCOB200_PAIR_KD": "2"}):
+    for env in ({"COCOB200_CSTREAM": "1"}, {"COCOB200_KD": "1"}, {"COCOB200_CORUN": "1"}, {"COCOB200_PAIR_KD": "2"},
+                {"COCOB200_XSTAGES": "3"}, {"COCOB200_XSTAGES": "0"}):
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT,
                              env={**os.environ, **env})
         assert out.returncode == 0 and "ok" in out.stdout, (env, out.stderr[-2000:])
