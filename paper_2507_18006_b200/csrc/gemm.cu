@@ -1100,11 +1100,15 @@ __global__ void __launch_bounds__(kThreads1, 1)
   // Token-major (SWAP, KD 1) launches size the ring at run time: weight stages
   // of exactly nw / 2 rows and 6 KB epilogue blocks (the token-major epilogue
   // only stages TMA stores) leave room for a deeper ring (launch_pair)
+  // ... and may give the weight ring (HBM) and the token ring (L2) their own
+  // depths (a.xstages > 0), each with its own stage-release barrier
   constexpr bool kRt = SWAP && KD == 1;
   const int S = kRt ? a.stages : Cfg::kStages;
+  const bool dec = kRt && a.xstages > 0;
+  const int SX = dec ? a.xstages : S;
   const int WBYTES = kRt ? (a.nw >> 1) * kBK * 2 : Cfg::kWBytes;
   constexpr int XBYTES = Cfg::kXBytes;
-  const int ring_bytes = S * (WBYTES + XBYTES);
+  const int ring_bytes = S * WBYTES + SX * XBYTES;
   const int tbuf_bytes = kRt ? 4 * kTokEpiWarpBytes : kTbufBytes;
   const int epi_stride = kRt ? kTokEpiWarpBytes : kEpiWarpBytes;
   extern __shared__ uint8_t smem_raw[];
@@ -1114,8 +1118,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
   uint8_t* epi_smem = smem + ring_bytes;  // 4 x epi_stride
   uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + ring_bytes + tbuf_bytes);  // leader: weights landed
   uint64_t* xfull_bar = wfull_bar + S;   // leader: both CTAs' tokens landed
-  uint64_t* empty_bar = xfull_bar + S;   // each CTA: stage consumed
-  uint64_t* tfull_bar = empty_bar + S;   // each CTA: accumulator ready
+  uint64_t* empty_bar = xfull_bar + SX;  // each CTA: (weight) stage consumed
+  uint64_t* xempty_bar = dec ? empty_bar + S : empty_bar;  // each CTA: token stage consumed (decoupled rings)
+  uint64_t* tfull_bar = empty_bar + S + (dec ? SX : 0);  // each CTA: accumulator ready
   uint64_t* tempty_bar = tfull_bar + 2;  // leader: both epilogues drained
   uint64_t* fix_bar = tempty_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
@@ -1140,8 +1145,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
     tma_prefetch_desc(&tmX);
     for (int i = 0; i < S; ++i) {
       mbar_init(&wfull_bar[i], 1);
-      mbar_init(&xfull_bar[i], 1);
       mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < SX; ++i) {
+      mbar_init(&xfull_bar[i], 1);
+      if (dec) mbar_init(&xempty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -1195,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
         const int tt = (u / sk.kb) % n_tt, kb = u % sk.kb;
-        mbar_wait(&empty_bar[stage], phase ^ 1);
+        mbar_wait(&xempty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * XBYTES);
         if (KD > 1)
@@ -1204,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
         else
           tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, kb * kBK,
                            a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
-        if (++stage == S) { stage = 0; phase ^= 1; }
+        if (++stage == SX) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
@@ -1214,8 +1222,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const uint32_t idesc = SWAP ? make_idesc_bf16(TNP, uint32_t(a.nw)) : make_idesc_bf16(2 * kBM, TNP);
       const uint64_t dw0 = make_sw128_desc(smem_u32(sW));
       const uint64_t dx0 = make_sw128_desc(smem_u32(sX));
-      int stage = 0;
-      uint32_t phase = 0;
+      int stage = 0, xstage = 0;
+      uint32_t phase = 0, xphase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int u = ubeg; u < uend;) {
@@ -1228,21 +1236,24 @@ __global__ void __launch_bounds__(kThreads1, 1)
           const int i = u + (kb - kb0) - ubeg;
           mbar_wait(&wfull_bar[stage], phase);
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 214 + i] = globaltimer_ns();
-          mbar_wait(&xfull_bar[stage], phase);
+          mbar_wait(&xfull_bar[xstage], xphase);
           tc_fence_after();
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 2 + i] = globaltimer_ns();
           __syncwarp();
           const uint64_t dw = dw0 + uint64_t((stage * WBYTES) >> 4);
-          const uint64_t dx = dx0 + uint64_t((stage * XBYTES) >> 4);
+          const uint64_t dx = dx0 + uint64_t((xstage * XBYTES) >> 4);
           if (SWAP && KD > 1)  // second k-block: 128 token rows / nw / 2 weight rows x 128 B further
             umma_2kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage],
                                     uint32_t((TNP / 2) * kBK * 2) >> 4, uint32_t(a.nw >> 1) * (kBK * 2) >> 4);
+          else if (SWAP && dec)
+            umma_kblock_pair2_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage]);
           else if (SWAP)
             umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           else
             umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
           if (++stage == S) { stage = 0; phase ^= 1; }
+          if (++xstage == SX) { xstage = 0; xphase ^= 1; }
         }
         __syncwarp();
         umma_commit_pair_elect(&tfull_bar[acc]);
@@ -1713,14 +1724,31 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
       const char* e = std::getenv("COCOB200_PAIR_SMEM_KB");  // A/B experiments: the old 224 KB budget
       return e ? size_t(std::atoi(e)) * 1024 : kMaxDynSmem;
     }();
-    const size_t stage_bytes = size_t(plan.nw / 2) * kBK * 2 + Cfg::kXBytes;
+    const size_t wbytes = size_t(plan.nw / 2) * kBK * 2;
+    const size_t stage_bytes = wbytes + Cfg::kXBytes;
     const size_t fixed = size_t(4) * kTokEpiWarpBytes + 1024 + kBarBytes;
     int stages = int((budget - fixed) / stage_bytes);
     if (stages > kMaxStages) stages = kMaxStages;
     if (stages < 2) return cudaErrorInvalidValue;
     a.stages = stages;
-    return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
-                              size_t(stages) * stage_bytes + fixed, st, 2u, wt, x, ot, a);
+    a.xstages = 0;
+    size_t smem = size_t(stages) * stage_bytes + fixed;
+    // decoupled depths: a short token ring (L2), the rest to weights (HBM)
+    static const int pxs = [] {
+      const char* e = std::getenv("COCOB200_PAIR_XSTAGES");  // 0 = one shared depth
+      return e ? std::atoi(e) : 0;
+    }();
+    if (pxs > 0) {
+      int ws = int((budget - fixed - size_t(pxs) * Cfg::kXBytes) / wbytes);
+      if (ws > kMaxStages) ws = kMaxStages;
+      if (ws >= 2) {
+        a.stages = ws;
+        a.xstages = pxs;
+        smem = size_t(ws) * wbytes + size_t(pxs) * Cfg::kXBytes + fixed;
+      }
+    }
+    return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1), smem, st, 2u,
+                              wt, x, ot, a);
   }
   a.n_mtiles = (a.N + 2 * kBM - 1) / (2 * kBM);
   const long long tiles = (long long)a.n_mtiles * a.n_ttiles;

@@ -362,7 +362,7 @@ print("ok")
 '''
     from conftest import ROOT
     for env in ({"COCOB200_CSTREAM": "1"}, {"COCOB200_KD": "1"}, {"COCOB200_CORUN": "1"}, {"COCOB200_PAIR_KD": "2"},
-                {"COCOB200_XSTAGES": "3"}, {"COCOB200_XSTAGES": "0"}):
+                {"COCOB200_XSTAGES": "3"}, {"COCOB200_XSTAGES": "0"}, {"COCOB200_PAIR_XSTAGES": "3"}):
         out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT,
                              env={**os.environ, **env})
         assert out.returncode == 0 and "ok" in out.stdout, (env, out.stderr[-2000:])
