@@ -155,7 +155,10 @@ int cb_get_placement(cb_model* m, int64_t* layer_ptr, int32_t* replica_dev, int3
  * (contiguous ranges in replica order), activations move between devices at
  * placement changes, and KV rows follow their sequence's replica.
  * Outputs: greedy next token per sequence, optional fp32 logits [bs][vocab],
- * device time of the pass. */
+ * device time of the pass.  CB_EINVAL before any launch for: slots out of range
+ * or repeated, token ids outside [0, vocab), prompt lengths outside
+ * [1, max_ctx], prefill into a live slot, decode on an empty one, a sequence
+ * reaching max_ctx. */
 int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const int32_t* tokens,
             const int32_t* prompt_lens, int32_t* next_tokens_out, float* logits_out, float* device_ms_out);
 int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots);
