@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define CB_ABI_VERSION 1
+#define CB_ABI_VERSION 2
 
 #define CB_OK 0
 #define CB_EINVAL (-1)
@@ -93,13 +93,30 @@ typedef struct {
   const uint16_t* w_down;    /* [d, d_ff] */
 } cb_layer_weights;
 
-/* Data movement of one scaling op, measured with CUDA events on the copy stream. */
+/* Data movement of one scaling op, measured with CUDA events: the transfer on
+ * the destination's copy stream(s) and the commit's KV catch-up on the new KV
+ * device's compute stream. */
 typedef struct {
-  uint64_t weight_bytes; /* bytes of module weights moved */
-  uint64_t kv_bytes;     /* bytes of KV moved */
-  float device_ms;       /* first copy start -> last copy end */
+  uint64_t weight_bytes;    /* bytes of module weights moved */
+  uint64_t kv_bytes;        /* bytes of KV moved (pre-copy + catch-up) */
+  float device_ms;          /* copy_ms + catchup_ms */
   uint64_t shortfall_bytes; /* set on CB_ENOMEM */
+  float copy_ms;            /* transfer start -> end (serving continues meanwhile) */
+  float catchup_ms;         /* commit: KV appended since the pre-copy (or all of it for evict) */
+  uint64_t catchup_bytes;
+  int32_t done;             /* every copy of the op has finished */
+  int32_t committed;        /* the placement switched */
 } cb_op_stats;
+
+/* What the executor really holds on one logical device (bytes). */
+typedef struct {
+  uint64_t weight_bytes;    /* layer blocks, migrated sub-modules, embedding / lm_head */
+  uint64_t kv_bytes;        /* KV blocks */
+  uint64_t workspace_bytes; /* activations, GEMM / attention workspaces */
+  uint64_t reserved_bytes;  /* held by issued, uncommitted scaling ops (included above) */
+  uint64_t free_bytes;      /* allocatable now: cudaMemGetInfo + the pool's cached free memory */
+  uint64_t total_bytes;
+} cb_mem_stats;
 
 /* ---- library ---------------------------------------------------------- */
 int cb_abi_version(void);
@@ -182,6 +199,43 @@ int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, 
 /* EvictReplica (ops.py:253-258): drop a non-original copy; KV rows it held move
  * back to the original first. */
 int cb_evict_replica(cb_model* m, int32_t layer, int32_t device, cb_op_stats* st);
+/* The four functions above are the synchronous forms (issue + commit + wait)
+ * for callers between steps.  The serving path uses the asynchronous forms:
+ *
+ * Asynchronous, serving-concurrent scaling ops -- the reference's transition
+ * (_Transition / _controller_tick / _commit_transitions, sim.py:396-403,
+ * 812-841, 614-622; "the old placement keeps serving until the switch",
+ * SPEC.md:531).  cb_issue_* validates (CB_EINVAL / CB_ENOREPLICA / CB_ESTATE
+ * before anything moves), RESERVES the destination memory (CB_ENOMEM with the
+ * shortfall, nothing reserved), enqueues the transfer on the destination's copy
+ * streams and returns at once with an op id.  cb_step keeps running on the
+ * pre-op placement meanwhile.  KV the op moves is pre-copied at issue and only
+ * the tokens appended since are copied at the commit.  At most one uncommitted
+ * op per layer (CB_ESTATE).  cb_commit switches the placement of one op
+ * (op_id >= 0) or of every pending op in issue order (op_id = -1) at the step
+ * boundary it is called at, without host synchronisation (the next step's
+ * kernels are stream-ordered after the transfer).  cb_op_abort releases the
+ * reservations of uncommitted ops (op_id = -1: all, newest first): a decision
+ * whose k-th op fails leaves the executor exactly as before (batch_apply's
+ * transactionality, ops.py:263-296). */
+int cb_issue_replicate_layer(cb_model* m, int32_t layer, int32_t dst, int64_t* op_id, uint64_t* shortfall_bytes);
+int cb_issue_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, int64_t* op_id,
+                           uint64_t* shortfall_bytes);
+int cb_issue_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, int64_t* op_id,
+                               uint64_t* shortfall_bytes);
+int cb_issue_evict_replica(cb_model* m, int32_t layer, int32_t device, int64_t* op_id);
+int cb_op_poll(cb_model* m, int64_t op_id, int32_t* done); /* non-blocking */
+int cb_op_wait(cb_model* m, int64_t op_id, cb_op_stats* st); /* blocks until the op's copies finished */
+int cb_commit(cb_model* m, int64_t op_id, int32_t* n_committed);
+int cb_op_abort(cb_model* m, int64_t op_id);
+int cb_pending_ops(cb_model* m, int32_t* n);
+/* Per-device memory the executor holds (the controller's usage view,
+ * PressureView / _usage_by_device, sim.py:507-525). */
+int cb_mem_usage(cb_model* m, int32_t device, cb_mem_stats* out);
+/* Transfer engine of the scaling ops: 0 = one cudaMemcpyPeerAsync, 1 = chunks
+ * alternating over two copy lanes (default, 64 MB chunks), 2 = SM kernel pushing
+ * 16-byte stores from the source GPU.  chunk_bytes 0 keeps the current chunk. */
+int cb_set_copy_mode(cb_runtime* rt, int32_t mode, uint64_t chunk_bytes);
 
 /* Phase-3 KV offload (autoscaler.py:568-583 PerformanceReduction): move the
  * layer's KV blocks to (to_host=1) or back from (0) mapped pinned host memory.

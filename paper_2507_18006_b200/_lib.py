@@ -69,7 +69,17 @@ class OpStats(C.Structure):
         ("kv_bytes", C.c_uint64),
         ("device_ms", C.c_float),
         ("shortfall_bytes", C.c_uint64),
+        ("copy_ms", C.c_float),
+        ("catchup_ms", C.c_float),
+        ("catchup_bytes", C.c_uint64),
+        ("done", C.c_int32),
+        ("committed", C.c_int32),
     ]
+
+
+class MemStats(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "weight_bytes", "kv_bytes", "workspace_bytes", "reserved_bytes", "free_bytes", "total_bytes")]
 
 
 class KStat(C.Structure):
@@ -108,6 +118,17 @@ _SIGS = {
     "cb_migrate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_migrate_submodule": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_evict_replica": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
+    "cb_issue_replicate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P, C.POINTER(C.c_uint64)]),
+    "cb_issue_migrate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P, C.POINTER(C.c_uint64)]),
+    "cb_issue_migrate_submodule": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P, C.POINTER(C.c_uint64)]),
+    "cb_issue_evict_replica": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
+    "cb_op_poll": (C.c_int, [_P, C.c_int64, _I32P]),
+    "cb_op_wait": (C.c_int, [_P, C.c_int64, C.POINTER(OpStats)]),
+    "cb_commit": (C.c_int, [_P, C.c_int64, _I32P]),
+    "cb_op_abort": (C.c_int, [_P, C.c_int64]),
+    "cb_pending_ops": (C.c_int, [_P, _I32P]),
+    "cb_mem_usage": (C.c_int, [_P, C.c_int32, C.POINTER(MemStats)]),
+    "cb_set_copy_mode": (C.c_int, [_P, C.c_int32, C.c_uint64]),
     "cb_kv_offload": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(OpStats)]),
     "cb_kv_offloaded": (C.c_int, [_P, C.c_int32, _I32P]),
     "cb_profile": (C.c_int, [_P, C.c_int32]),

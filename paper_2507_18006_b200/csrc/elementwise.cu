@@ -359,4 +359,27 @@ cudaError_t copy_segments_launch(const CopySeg* segs_dev, int nseg, cudaStream_t
   return cudaGetLastError();
 }
 
+__global__ void __launch_bounds__(512) copy_bulk_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                          size_t n16) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                d = __ldcs(src + i + 3 * stride);
+    __stcs(dst + i, a);
+    __stcs(dst + i + stride, b);
+    __stcs(dst + i + 2 * stride, c);
+    __stcs(dst + i + 3 * stride, d);
+  }
+  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+}
+
+cudaError_t copy_bulk_launch(void* dst, const void* src, size_t bytes, int num_sms, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  const size_t n16 = bytes / 16;
+  const int ctas = int(std::min<size_t>(size_t(num_sms) * 2, (n16 + 511) / 512));
+  copy_bulk_kernel<<<ctas, 512, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16);
+  return cudaGetLastError();
+}
+
 }  // namespace cb

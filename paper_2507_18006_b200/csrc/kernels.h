@@ -150,5 +150,8 @@ struct CopySeg {
   unsigned long long bytes;
 };
 cudaError_t copy_segments_launch(const CopySeg* segs_dev, int nseg, cudaStream_t st);
+// Contiguous copy by the SMs of the launching GPU (dst and/or src may be peer
+// memory): 16-byte vectors, 4 in flight per thread.  bytes % 16 == 0, 16-byte aligned.
+cudaError_t copy_bulk_launch(void* dst, const void* src, size_t bytes, int num_sms, cudaStream_t st);
 
 }  // namespace cb

@@ -58,15 +58,24 @@ int fail(int code, const std::string& msg) {
     if (_r != CB_OK) return _r; \
   } while (0)
 
+// Device memory categories (cb_mem_usage): what the executor really holds per
+// logical device, for the controller's pressure view (autoscaler PressureView).
+enum MemCat { MEM_WS = 0, MEM_WEIGHTS = 1, MEM_KV = 2, MEM_CATS = 3 };
+
 struct DeviceCtx {
   int id = 0;
   int ordinal = 0;
   int num_sms = 148;
   cudaStream_t compute = nullptr;
-  cudaStream_t copy = nullptr;
+  cudaStream_t copy = nullptr;   // scaling-op transfers (main lane)
+  cudaStream_t copy2 = nullptr;  // second copy lane: chunks of large transfers alternate between the two
+  cudaStream_t alloc = nullptr;  // always idle: synchronous pool allocations never wait on a running copy
   std::vector<cudaEvent_t> ev_pool;  // dependency events (no timing)
   size_t ev_next = 0;
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing events
+  std::map<void*, std::pair<size_t, int>> allocs;  // live allocations: bytes, MemCat
+  size_t mem[MEM_CATS] = {0, 0, 0};
+  size_t reserved = 0;  // bytes held by pending (uncommitted) scaling ops
 };
 
 // activation tensor maps per box height (GEMM plans need 8..256-row boxes)
@@ -92,6 +101,8 @@ int box_index(int rows) {
 
 struct cb_runtime {
   std::vector<DeviceCtx> devs;
+  int copy_mode = 1;                  // transfer engine (cb_set_copy_mode)
+  size_t copy_chunk = size_t(64) << 20;
 };
 
 namespace {
@@ -119,6 +130,31 @@ struct LayerState {
   ModCopy mod[kModKinds];           // projection / self-attention overrides
   bool proj_ov = false;             // any entry of mod[] in use
   std::map<int, bool> kv_host;      // device -> its KV block lives in mapped pinned host memory (offloaded)
+  int n_pending = 0;                // uncommitted scaling ops on this layer: any number of
+  bool pending_excl = false;        // replications, or exactly one other op (exclusive)
+  std::vector<int> pending_rep_dst; // destinations of the pending replications
+};
+
+// An issued, not yet committed scaling op (A17: the reference's _Transition,
+// sim.py:396-403).  Destination memory is reserved at issue (sim.py:812-841);
+// the transfer runs on the destination's copy streams while the executor keeps
+// serving on the pre-op placement; the commit switches at a step boundary
+// (sim.py:614-622) after a catch-up copy of the KV appended since.
+enum OpKind { OPK_REPLICATE = 0, OPK_MIGRATE = 1, OPK_PROJ = 2, OPK_KV = 3, OPK_EVICT = 4 };
+struct PendingOp {
+  int64_t id = 0;
+  int kind = 0, layer = 0, dst = -1, with_kv = 0, mod_kind = -1;
+  LayerCopy copy;  // replicate / migrate: the reserved destination block
+  ModCopy mod;     // projection: the reserved destination buffer
+  int kv_from = -1, kv_to = -1;  // KV transfer of the slots kv_from holds (pre-copied at issue when safe)
+  bool kv_new = false;           // this op allocated kv_to's block (abort releases it)
+  std::vector<int> snap_len, snap_epoch;  // per slot: prefix pre-copied at issue (-1 = none)
+  int copy_dev = -1;             // device whose copy stream carries the transfer
+  cudaEvent_t e0 = nullptr, e1 = nullptr;  // transfer start / end (copy stream)
+  cudaEvent_t c0 = nullptr, c1 = nullptr;  // commit catch-up start / end (kv_to's compute stream)
+  uint64_t weight_bytes = 0, kv_bytes = 0, catchup_bytes = 0;
+  size_t reserved = 0;           // bytes reserved on dst (released from the pending count at commit / abort)
+  bool committed = false;
 };
 
 struct Workspace {
@@ -189,6 +225,9 @@ struct cb_model {
   int cur_bs = 0;  // sequences of the pass in flight
   std::vector<int> seq_blk;  // prefill: first q-block of each sequence (+ total), blocks follow the gather list
   Prof prof;
+  std::vector<uint32_t> slot_epoch;  // bumped on release: a pre-copied KV prefix of an older occupant is stale
+  std::map<int64_t, PendingOp> ops;  // issued scaling ops (pending, then committed records)
+  int64_t next_op = 1;
 };
 
 namespace {
@@ -266,11 +305,17 @@ void prof_resolve(cb_model* m) {
 // release threshold: a migrated / evicted layer block returns to the pool and
 // the next replication reuses it without cudaMalloc / cudaFree (which unmap and
 // synchronise the device -- hundreds of ms per op for 0.6 GB blocks).
-int dev_alloc(const DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullptr) {
+//  - synchronous allocations (workspaces, loads) go through the device's idle
+//    `alloc` stream, so they never wait on a scaling op's running copy;
+//  - a scaling op's reservation is allocated on the destination's copy stream
+//    without any host synchronisation (`st`): the op's copies run on that
+//    stream and the commit orders the compute streams after them.
+int dev_alloc(DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullptr, int cat = MEM_WS,
+              cudaStream_t st = nullptr) {
   CB_TRY(use(d));
   *p = nullptr;
-  cudaError_t e = cudaMallocAsync(p, bytes, d.copy);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(d.copy);  // usable from every stream from here on
+  cudaError_t e = cudaMallocAsync(p, bytes, st ? st : d.alloc);
+  if (e == cudaSuccess && !st) e = cudaStreamSynchronize(d.alloc);  // usable from every stream from here on
   if (e != cudaSuccess) {
     cudaGetLastError();
     size_t free_b = 0, total_b = 0;
@@ -280,15 +325,38 @@ int dev_alloc(const DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = 
     return fail(CB_ENOMEM, "device " + std::to_string(d.id) + " lacks memory for " + std::to_string(bytes) +
                                " bytes (" + cudaGetErrorString(e) + ")");
   }
+  d.allocs[*p] = {bytes, cat};
+  d.mem[cat] += bytes;
   return CB_OK;
 }
 
+// `dst_stream` (on dst) waits for everything issued so far on `src_stream` (on src)
+int join(DeviceCtx& dst, cudaStream_t dst_stream, DeviceCtx& src, cudaStream_t src_stream) {
+  if (dst_stream == src_stream) return CB_OK;
+  CB_TRY(use(src));
+  cudaEvent_t ev = src.ev_pool[src.ev_next++ % src.ev_pool.size()];
+  CB_CUDA(cudaEventRecord(ev, src_stream));
+  CB_TRY(use(dst));
+  CB_CUDA(cudaStreamWaitEvent(dst_stream, ev, 0));
+  return CB_OK;
+}
+
+// Stream-ordered free, no host synchronisation: the owning device's compute
+// stream first joins every stream of every logical device (any of them may
+// still read the buffer: peer row pulls, KV moves, op copies), then returns the
+// buffer to the pool.
 void dev_free(cb_model* m, int dev, void* p) {
   if (!p) return;
-  const DeviceCtx& d = devctx(m, dev);
+  DeviceCtx& d = devctx(m, dev);
+  for (auto& o : m->rt->devs)
+    for (cudaStream_t s : {o.compute, o.copy, o.copy2}) join(d, d.compute, o, s);
   cudaSetDevice(d.ordinal);
-  cudaStreamSynchronize(d.compute);  // no kernel of this device may still read the block
-  cudaFreeAsync(p, d.copy);
+  cudaFreeAsync(p, d.compute);
+  auto it = d.allocs.find(p);
+  if (it != d.allocs.end()) {
+    d.mem[it->second.second] -= it->second.first;
+    d.allocs.erase(it);
+  }
 }
 
 int check_layer(cb_model* m, int layer) {
@@ -314,7 +382,7 @@ int make_map(OpMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t b
 int ensure_ws(cb_model* m, int dev) {
   Workspace& w = m->ws[dev];
   if (w.ready) return CB_OK;
-  const DeviceCtx& dc = devctx(m, dev);
+  DeviceCtx& dc = devctx(m, dev);
   const cb_model_desc& d = m->d;
   const size_t T = d.max_tokens;
   CB_TRY(dev_alloc(dc, (void**)&w.x, T * d.d_model * 4));
@@ -365,11 +433,16 @@ int make_layer_maps(cb_model* m, LayerCopy& c) {
   return CB_OK;
 }
 
-int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr) {
+// st != null: stream-ordered reservation for a scaling op (no host sync);
+// *created tells the caller whether this call allocated the block.
+int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr, cudaStream_t st = nullptr,
+              bool* created = nullptr) {
+  if (created) *created = false;
   if (L.kv.count(dev)) return CB_OK;
   void* p = nullptr;
-  CB_TRY(dev_alloc(devctx(m, dev), &p, m->kv_block_bytes, shortfall));
+  CB_TRY(dev_alloc(devctx(m, dev), &p, m->kv_block_bytes, shortfall, MEM_KV, st));
   L.kv[dev] = static_cast<uint16_t*>(p);
+  if (created) *created = true;
   return CB_OK;
 }
 
@@ -407,16 +480,21 @@ int kv_device(const LayerState& L) { return L.kv_override >= 0 ? L.kv_override :
 size_t kv_token_bytes(cb_model* m) { return size_t(2) * m->kv_n * 2; }
 size_t kv_slot_offset(cb_model* m, int slot) { return size_t(slot) * m->d.max_ctx * m->kv_n * 2; }  // elements
 
-// copy KV prefix of `slot` from src block to dst block (pulled on dst's stream)
-int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t st, uint64_t* bytes) {
-  const int len = m->slot_len[slot];
-  if (len <= 0 || src == dst) return CB_OK;
-  const size_t nbytes = size_t(len) * kv_token_bytes(m);
-  const size_t off = kv_slot_offset(m, slot);
+// copy KV positions [p0, p1) of `slot` from src's block to dst's block
+int kv_copy(cb_model* m, LayerState& L, int slot, int src, int dst, int p0, int p1, cudaStream_t st,
+            uint64_t* bytes) {
+  if (p1 <= p0 || src == dst) return CB_OK;
+  const size_t tb = kv_token_bytes(m);
+  const size_t off = kv_slot_offset(m, slot) + size_t(p0) * tb / 2;  // elements
   // cudaMemcpyDefault: either block may be offloaded to mapped pinned host memory
-  CB_CUDA(cudaMemcpyAsync(L.kv[dst] + off, L.kv[src] + off, nbytes, cudaMemcpyDefault, st));
-  if (bytes) *bytes += nbytes;
+  CB_CUDA(cudaMemcpyAsync(L.kv[dst] + off, L.kv[src] + off, size_t(p1 - p0) * tb, cudaMemcpyDefault, st));
+  if (bytes) *bytes += size_t(p1 - p0) * tb;
   return CB_OK;
+}
+
+// copy the whole live KV prefix of `slot` (pulled on dst's stream)
+int kv_move(cb_model* m, LayerState& L, int slot, int src, int dst, cudaStream_t st, uint64_t* bytes) {
+  return kv_copy(m, L, slot, src, dst, 0, m->slot_len[slot], st, bytes);
 }
 
 // Fused RMSNorm hooks of one GEMM (kernels.h GemmArgs): consume = X rows are
@@ -1063,7 +1141,7 @@ int begin_layer_load(cb_model* m, int layer, int dev, LayerCopy& c) {
   LayerState& L = m->layers[layer - 1];
   if (!L.reps.empty()) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already loaded");
   c.dev = dev;
-  CB_TRY(dev_alloc(devctx(m, dev), (void**)&c.block, m->layer_bytes));
+  CB_TRY(dev_alloc(devctx(m, dev), (void**)&c.block, m->layer_bytes, nullptr, MEM_WEIGHTS));
   return CB_OK;
 }
 
@@ -1077,46 +1155,428 @@ int finish_layer_load(cb_model* m, int layer, LayerCopy& c) {
   return CB_OK;
 }
 
-int timed_begin(DeviceCtx& dc) {
-  CB_TRY(use(dc));
-  CB_CUDA(cudaStreamSynchronize(dc.compute));
-  CB_CUDA(cudaEventRecord(dc.t0, dc.copy));
-  return CB_OK;
-}
-int timed_end(DeviceCtx& dc, cb_op_stats* st) {
-  CB_TRY(use(dc));
-  CB_CUDA(cudaEventRecord(dc.t1, dc.copy));
-  CB_CUDA(cudaStreamSynchronize(dc.copy));
-  float ms = 0.f;
-  CB_CUDA(cudaEventElapsedTime(&ms, dc.t0, dc.t1));
-  if (st) st->device_ms = ms;
-  return CB_OK;
-}
-
-int copy_block(cb_model* m, const LayerCopy& src, LayerCopy& dst, cudaStream_t st) {
-  CB_CUDA(cudaMemcpyPeerAsync(dst.block, devctx(m, dst.dev).ordinal, src.block, devctx(m, src.dev).ordinal,
-                              m->layer_bytes, st));
-  return CB_OK;
-}
-
 void sync_all(cb_model* m) {
   for (auto& dc : m->rt->devs) {
     cudaSetDevice(dc.ordinal);
     cudaStreamSynchronize(dc.compute);
     cudaStreamSynchronize(dc.copy);
+    cudaStreamSynchronize(dc.copy2);
   }
 }
 void sync_all_devices(cb_model* m) { sync_all(m); }
 
-// Phase-3 KV offload (autoscaler.py:568-583 PerformanceReduction; the
-// reference prices it as a latency multiplier, sim.py:258): the layer's KV
-// blocks move between device memory and mapped pinned host memory.  The
-// attention kernel reads an offloaded block in place through its UVA address
-// (zero-copy over PCIe / C2C), so nothing else in the executor changes.
+// ---- transfer engine of the scaling ops (NVLink 5 / NVSwitch between GPUs).
+// copy_mode 1 (default): the transfer is cut into copy_chunk pieces that
+// alternate between the destination's two copy lanes, so two copy engines move
+// it; 0: one cudaMemcpyPeerAsync; 2: an SM kernel on the SOURCE GPU pushes
+// 16-byte stores into the destination (NVLink writes need no round trip).
+// Everything ends ordered on the destination's main copy stream.
+int transfer(cb_model* m, int dst_dev, void* dst, int src_dev, const void* src, size_t bytes) {
+  DeviceCtx& dc = devctx(m, dst_dev);
+  DeviceCtx& sc = devctx(m, src_dev);
+  const cb_runtime& rt = *m->rt;
+  if (rt.copy_mode == 2 && bytes % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(src) % 16 == 0) {
+    CB_TRY(join(sc, sc.copy, dc, dc.copy));
+    CB_TRY(use(sc));
+    CB_CUDA(cb::copy_bulk_launch(dst, src, bytes, sc.num_sms, sc.copy));
+    return join(dc, dc.copy, sc, sc.copy);
+  }
+  CB_TRY(use(dc));
+  const size_t chunk = std::max<size_t>(rt.copy_chunk, 1 << 20);
+  if (rt.copy_mode == 0 || bytes <= chunk) {
+    CB_CUDA(cudaMemcpyPeerAsync(dst, dc.ordinal, src, sc.ordinal, bytes, dc.copy));
+    return CB_OK;
+  }
+  CB_TRY(join(dc, dc.copy2, dc, dc.copy));
+  CB_TRY(use(dc));
+  int lane = 0;
+  for (size_t off = 0; off < bytes; off += chunk, lane ^= 1) {
+    const size_t n = std::min(chunk, bytes - off);
+    CB_CUDA(cudaMemcpyPeerAsync(static_cast<uint8_t*>(dst) + off, dc.ordinal, static_cast<const uint8_t*>(src) + off,
+                                sc.ordinal, n, lane ? dc.copy2 : dc.copy));
+  }
+  return join(dc, dc.copy, dc, dc.copy2);
+}
+
+// ---- asynchronous scaling ops (A17) ----------------------------------------
+// A layer may carry several pending replications (a scale-up decision fans a
+// layer out to many devices) or exactly one other pending op.
+int check_idle(const LayerState& L, int layer, bool replicate = false, int dst = -1) {
+  const bool clash = replicate ? L.pending_excl || std::count(L.pending_rep_dst.begin(), L.pending_rep_dst.end(), dst)
+                               : L.n_pending > 0;
+  if (clash)
+    return fail(CB_ESTATE, "layer " + std::to_string(layer) + " has an uncommitted scaling op in the way");
+  return CB_OK;
+}
+
+PendingOp new_op(cb_model* m, int kind, int layer, int dst, int copy_dev) {
+  PendingOp op;
+  op.kind = kind;
+  op.layer = layer;
+  op.dst = dst;
+  op.copy_dev = copy_dev;
+  op.snap_len.assign(m->d.max_slots, -1);
+  op.snap_epoch.assign(m->d.max_slots, 0);
+  return op;
+}
+
+// open the transfer: ordered after every compute stream's work so far (the KV
+// prefixes it may read were written by earlier steps)
+int op_open(cb_model* m, PendingOp& op) {
+  DeviceCtx& dc = devctx(m, op.copy_dev);
+  for (auto& o : m->rt->devs) CB_TRY(join(dc, dc.copy, o, o.compute));
+  CB_TRY(use(dc));
+  CB_CUDA(cudaEventCreate(&op.e0));
+  CB_CUDA(cudaEventCreate(&op.e1));
+  CB_CUDA(cudaEventRecord(op.e0, dc.copy));
+  return CB_OK;
+}
+
+// register the op: transfer end event, layer lock, reservation count
+int op_close(cb_model* m, PendingOp& op, int64_t* id_out) {
+  DeviceCtx& dc = devctx(m, op.copy_dev);
+  CB_TRY(use(dc));
+  CB_CUDA(cudaEventRecord(op.e1, dc.copy));
+  op.id = m->next_op++;
+  LayerState& L = m->layers[op.layer - 1];
+  L.n_pending += 1;
+  if (op.kind == OPK_REPLICATE)
+    L.pending_rep_dst.push_back(op.dst);
+  else
+    L.pending_excl = true;
+  if (op.dst >= 0) devctx(m, op.dst).reserved += op.reserved;
+  m->ops[op.id] = op;
+  if (id_out) *id_out = op.id;
+  return CB_OK;
+}
+
+// Pre-copy of the live KV prefixes held by op.kv_from into op.kv_to's block,
+// on the destination's copy stream.  KV is append-only: positions below a
+// slot's length never change while its occupant lives, so the prefix stays
+// valid and the commit copies only what was appended since (a slot released
+// and refilled meanwhile has a new epoch and is copied whole).  Only used when
+// nothing else writes kv_to's block for this layer while the op is pending.
+int op_precopy_kv(cb_model* m, PendingOp& op, LayerState& L) {
+  DeviceCtx& dc = devctx(m, op.copy_dev);
+  CB_TRY(use(dc));
+  for (int slot = 0; slot < m->d.max_slots; ++slot) {
+    if (L.owner[slot] != op.kv_from || m->slot_len[slot] <= 0) continue;
+    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, 0, m->slot_len[slot], dc.copy, &op.kv_bytes));
+    op.snap_len[slot] = m->slot_len[slot];
+    op.snap_epoch[slot] = int(m->slot_epoch[slot]);
+  }
+  return CB_OK;
+}
+
+// At the commit: the rest of every slot op.kv_from still holds moves to
+// op.kv_to on kv_to's compute stream (stream-ordered before the next step).
+int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
+  DeviceCtx& tc = devctx(m, op.kv_to);
+  DeviceCtx& fc = devctx(m, op.kv_from);
+  CB_TRY(join(tc, tc.compute, fc, fc.compute));
+  CB_TRY(use(tc));
+  CB_CUDA(cudaEventCreate(&op.c0));
+  CB_CUDA(cudaEventCreate(&op.c1));
+  CB_CUDA(cudaEventRecord(op.c0, tc.compute));
+  for (int slot = 0; slot < m->d.max_slots; ++slot) {
+    if (L.owner[slot] != op.kv_from) continue;
+    const int len = m->slot_len[slot];
+    const bool fresh = op.snap_len[slot] >= 0 && op.snap_epoch[slot] == int(m->slot_epoch[slot]);
+    const int have = fresh ? std::min(op.snap_len[slot], len) : 0;
+    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, tc.compute, &op.catchup_bytes));
+    L.owner[slot] = op.kv_to;
+  }
+  CB_CUDA(cudaEventRecord(op.c1, tc.compute));
+  return CB_OK;
+}
+
+void op_unlock(LayerState& L, const PendingOp& op) {
+  L.n_pending -= 1;
+  if (op.kind == OPK_REPLICATE) {
+    auto it = std::find(L.pending_rep_dst.begin(), L.pending_rep_dst.end(), op.dst);
+    if (it != L.pending_rep_dst.end()) L.pending_rep_dst.erase(it);
+  } else {
+    L.pending_excl = false;
+  }
+}
+
+// release what an op reserved but never committed
+void op_release_reservation(cb_model* m, PendingOp& op) {
+  LayerState& L = m->layers[op.layer - 1];
+  if (op.copy.block) dev_free(m, op.copy.dev, op.copy.block);
+  if (op.mod.buf) dev_free(m, op.mod.dev, op.mod.buf);
+  op.copy.block = nullptr;
+  op.mod.buf = nullptr;
+  if (op.kv_new && op.kv_to >= 0) {
+    auto it = L.kv.find(op.kv_to);
+    if (it != L.kv.end()) {
+      dev_free(m, op.kv_to, it->second);
+      L.kv.erase(it);
+    }
+  }
+}
+
+// ReplicateLayer (ops.py:199-211): reserve + copy the layer block original -> dst.
+int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) {
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dst));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  CB_TRY(check_idle(L, layer, true, dst));
+  for (auto& c : L.reps)
+    if (c.dev == dst)
+      return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
+  if (L.kv_override >= 0 || L.proj_ov) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
+  DeviceCtx& dc = devctx(m, dst);
+  PendingOp op = new_op(m, OPK_REPLICATE, layer, dst, dst);
+  op.copy.dev = dst;
+  int r = dev_alloc(dc, (void**)&op.copy.block, m->layer_bytes, shortfall, MEM_WEIGHTS, dc.copy);
+  if (r == CB_OK) {
+    r = ensure_kv(m, L, dst, shortfall, dc.copy, &op.kv_new);
+    op.kv_to = dst;  // (no KV moves at issue: rows move with split_batch once serving)
+  }
+  if (r == CB_OK) r = ensure_ws(m, dst);
+  if (r != CB_OK) {
+    const std::string err = g_err;
+    op_release_reservation(m, op);
+    return fail(r, err);
+  }
+  op.reserved = m->layer_bytes + (op.kv_new ? m->kv_block_bytes : 0);
+  CB_TRY(op_open(m, op));
+  CB_TRY(transfer(m, dst, op.copy.block, L.reps[0].dev, L.reps[0].block, m->layer_bytes));
+  op.weight_bytes = m->layer_bytes;
+  return op_close(m, op, id);
+}
+
+// MigrateLayer (ops.py:213-228): reserve + copy the original to dst; with_kv
+// pre-copies the KV the layer's KV device holds (replica-held rows stay).
+int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uint64_t* shortfall) {
+  CB_TRY(check_layer(m, layer));
+  CB_TRY(check_dev(m, dst));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  CB_TRY(check_idle(L, layer));
+  const int src = L.reps[0].dev;
+  if (dst == src) return fail(CB_EINVAL, "layer original already on device " + std::to_string(dst));
+  for (auto& c : L.reps)
+    if (c.dev == dst) return fail(CB_EINVAL, "layer already has a copy on device " + std::to_string(dst));
+  if (!with_kv && L.reps.size() > 1) return fail(CB_EINVAL, "cannot detach KV from a replicated layer");
+  DeviceCtx& dc = devctx(m, dst);
+  PendingOp op = new_op(m, OPK_MIGRATE, layer, dst, dst);
+  op.with_kv = with_kv;
+  op.copy.dev = dst;
+  op.kv_from = kv_device(L);
+  int r = dev_alloc(dc, (void**)&op.copy.block, m->layer_bytes, shortfall, MEM_WEIGHTS, dc.copy);
+  if (r == CB_OK && with_kv && op.kv_from != dst) {
+    op.kv_to = dst;
+    r = ensure_kv(m, L, dst, shortfall, dc.copy, &op.kv_new);
+  }
+  if (r == CB_OK) r = ensure_ws(m, dst);
+  if (r != CB_OK) {
+    const std::string err = g_err;
+    op_release_reservation(m, op);
+    return fail(r, err);
+  }
+  op.reserved = m->layer_bytes + (op.kv_new ? m->kv_block_bytes : 0);
+  CB_TRY(op_open(m, op));
+  CB_TRY(transfer(m, dst, op.copy.block, src, L.reps[0].block, m->layer_bytes));
+  op.weight_bytes = m->layer_bytes;
+  if (op.kv_to >= 0) CB_TRY(op_precopy_kv(m, op, L));  // dst serves nothing of this layer until the commit
+  return op_close(m, op, id);
+}
+
+// MigrateSubModule of a projection / SELF_ATTENTION (ops.py:230-251): reserve +
+// copy the module's weights (canonical [out, in] layout) to dst; after the
+// commit the layer runs that projection there with activation hops
+// (run_layer_overridden).  The layer block keeps its bytes (one allocation);
+// the registry does the reference's memory accounting (domain.py:481-535).
+int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uint64_t* shortfall) {
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  CB_TRY(check_idle(L, layer));
+  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
+  const bool attn_part = kind <= CB_ATTN_PROJ_O;
+  if ((kind == CB_SELF_ATTENTION && (L.mod[0].dev >= 0 || L.mod[1].dev >= 0 || L.mod[2].dev >= 0 ||
+                                     L.mod[3].dev >= 0)) ||
+      (attn_part && L.mod[CB_SELF_ATTENTION].dev >= 0))
+    return fail(CB_EINVAL, "projection override conflicts with a self_attention override (domain.py:298-303)");
+  const uint64_t bytes = cb_module_bytes(m, kind);
+  DeviceCtx& dc = devctx(m, dst);
+  PendingOp op = new_op(m, OPK_PROJ, layer, dst, dst);
+  op.mod_kind = kind;
+  op.mod.dev = dst;
+  int r = dev_alloc(dc, (void**)&op.mod.buf, bytes, shortfall, MEM_WEIGHTS, dc.copy);
+  if (r == CB_OK) r = ensure_ws(m, dst);
+  if (r != CB_OK) {
+    const std::string err = g_err;
+    op_release_reservation(m, op);
+    return fail(r, err);
+  }
+  op.reserved = bytes;
+  CB_TRY(op_open(m, op));
+  const ModCopy& mc = L.mod[kind];
+  if (mc.dev >= 0) {  // moved once already: copy from the current override
+    CB_TRY(transfer(m, dst, op.mod.buf, mc.dev, mc.buf, bytes));
+  } else {
+    const LayerCopy& src = L.reps[0];
+    const uint8_t* from = src.block + block_offset(m, kind);
+    if (kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP) {  // every other row of the interleaved block
+      const size_t row = size_t(m->d.d_model) * 2;
+      CB_TRY(use(dc));
+      CB_CUDA(cudaMemcpy2DAsync(op.mod.buf, row, from, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
+    } else {
+      CB_TRY(transfer(m, dst, op.mod.buf, src.dev, from, bytes));
+    }
+  }
+  op.weight_bytes = bytes;
+  return op_close(m, op, id);
+}
+
+// MigrateSubModule(KV_CACHE) (ops.py:230-251): the layer's KV moves to dst
+// (pre-copied now, caught up at the commit); attention then runs there.
+int issue_kv(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) {
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  CB_TRY(check_idle(L, layer));
+  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
+  DeviceCtx& dc = devctx(m, dst);
+  PendingOp op = new_op(m, OPK_KV, layer, dst, dst);
+  op.kv_from = kv_device(L);
+  op.kv_to = dst;
+  int r = ensure_kv(m, L, dst, shortfall, dc.copy, &op.kv_new);
+  if (r == CB_OK) r = ensure_ws(m, dst);
+  if (r != CB_OK) {
+    const std::string err = g_err;
+    op_release_reservation(m, op);
+    return fail(r, err);
+  }
+  op.reserved = op.kv_new ? m->kv_block_bytes : 0;
+  CB_TRY(op_open(m, op));
+  if (op.kv_from != dst) CB_TRY(op_precopy_kv(m, op, L));  // attention stays on kv_from until the commit
+  return op_close(m, op, id);
+}
+
+// EvictReplica (ops.py:253-258).  The original keeps serving its own rows
+// while the op is pending, so the KV rows the replica holds move back at the
+// commit (on the original's compute stream, before the next step).
+int issue_evict(cb_model* m, int layer, int dev, int64_t* id) {
+  CB_TRY(check_layer(m, layer));
+  LayerState& L = m->layers[layer - 1];
+  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  CB_TRY(check_idle(L, layer));
+  if (L.reps[0].dev == dev) return fail(CB_ENOREPLICA, "cannot evict the original replica");
+  auto it = std::find_if(L.reps.begin() + 1, L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; });
+  if (it == L.reps.end())
+    return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no replica on device " + std::to_string(dev));
+  PendingOp op = new_op(m, OPK_EVICT, layer, -1, L.reps[0].dev);
+  op.kv_from = dev;
+  op.kv_to = L.reps[0].dev;
+  CB_TRY(op_open(m, op));
+  return op_close(m, op, id);
+}
+
+// Switch one op's placement at this step boundary.  No host synchronisation:
+// every compute stream orders after the op's transfer, the KV catch-up runs on
+// the new KV device's compute stream, replaced buffers are freed stream-ordered.
+int op_commit(cb_model* m, PendingOp& op) {
+  LayerState& L = m->layers[op.layer - 1];
+  for (auto& o : m->rt->devs) {
+    CB_TRY(use(o));
+    CB_CUDA(cudaStreamWaitEvent(o.compute, op.e1, 0));
+  }
+  switch (op.kind) {
+    case OPK_REPLICATE:
+      CB_TRY(make_layer_maps(m, op.copy));
+      L.reps.push_back(op.copy);
+      break;
+    case OPK_MIGRATE: {
+      const int kv_src = op.kv_from;
+      if (op.kv_to >= 0) CB_TRY(op_catchup_kv(m, op, L));
+      CB_TRY(make_layer_maps(m, op.copy));
+      const LayerCopy old = L.reps[0];
+      L.reps[0] = op.copy;
+      dev_free(m, old.dev, old.block);
+      L.kv_override = op.with_kv ? -1 : kv_src;  // without KV it stays resident where it was (domain.py:445-451)
+      for (int dv : std::vector<int>{old.dev, kv_src}) drop_kv_if_unused(m, L, dv);
+      break;
+    }
+    case OPK_PROJ: {
+      const ModCopy old = L.mod[op.mod_kind];
+      L.mod[op.mod_kind] = op.mod;
+      if (old.dev >= 0) dev_free(m, old.dev, old.buf);
+      L.proj_ov = false;
+      for (const ModCopy& x : L.mod)
+        if (x.dev >= 0) L.proj_ov = true;
+      break;
+    }
+    case OPK_KV:
+      if (op.kv_from != op.kv_to) CB_TRY(op_catchup_kv(m, op, L));
+      L.kv_override = op.kv_to;
+      drop_kv_if_unused(m, L, op.kv_from);
+      break;
+    case OPK_EVICT: {
+      CB_TRY(op_catchup_kv(m, op, L));
+      auto it = std::find_if(L.reps.begin() + 1, L.reps.end(), [&](const LayerCopy& c) { return c.dev == op.kv_from; });
+      dev_free(m, it->dev, it->block);
+      L.reps.erase(it);
+      drop_kv_if_unused(m, L, op.kv_from);
+      break;
+    }
+  }
+  op.copy.block = nullptr;  // owned by the layer now
+  op.mod.buf = nullptr;
+  op_unlock(L, op);
+  if (op.dst >= 0) devctx(m, op.dst).reserved -= op.reserved;
+  op.committed = true;
+  return CB_OK;
+}
+
+int op_abort(cb_model* m, PendingOp& op) {
+  op_release_reservation(m, op);
+  op_unlock(m->layers[op.layer - 1], op);
+  if (op.dst >= 0) devctx(m, op.dst).reserved -= op.reserved;
+  return CB_OK;
+}
+
+void op_destroy_events(PendingOp& op) {
+  for (cudaEvent_t e : {op.e0, op.e1, op.c0, op.c1})
+    if (e) cudaEventDestroy(e);
+}
+
+int op_stats(cb_model* m, PendingOp& op, cb_op_stats* st, bool wait) {
+  if (wait) {
+    CB_TRY(use(devctx(m, op.copy_dev)));
+    CB_CUDA(cudaEventSynchronize(op.e1));
+    if (op.c1) CB_CUDA(cudaEventSynchronize(op.c1));
+  }
+  if (!st) return CB_OK;
+  *st = cb_op_stats{};
+  st->weight_bytes = op.weight_bytes;
+  st->kv_bytes = op.kv_bytes + op.catchup_bytes;
+  st->catchup_bytes = op.catchup_bytes;
+  st->committed = op.committed ? 1 : 0;
+  float ms = 0.f;
+  st->done = cudaEventQuery(op.e1) == cudaSuccess && (!op.c1 || cudaEventQuery(op.c1) == cudaSuccess);
+  cudaGetLastError();
+  if (st->done) {
+    CB_CUDA(cudaEventElapsedTime(&ms, op.e0, op.e1));
+    st->copy_ms = ms;
+    if (op.c1) {
+      float cm = 0.f;
+      CB_CUDA(cudaEventElapsedTime(&cm, op.c0, op.c1));
+      st->catchup_ms = cm;
+    }
+    st->device_ms = st->copy_ms + st->catchup_ms;
+  }
+  return CB_OK;
+}
+
 int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  sync_all(m);
+  CB_TRY(check_idle(L, layer));
+  sync_all(m);  // Phase-3 relief (rare): a blocking move keeps the host-memory swap simple
   uint64_t moved = 0;
   float ms = 0.f;
   for (auto& kv : L.kv) {
@@ -1130,13 +1590,14 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
       CB_CUDA(cudaHostAlloc((void**)&nb, m->kv_block_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
     } else {
       uint64_t shortfall = 0;
-      int r = dev_alloc(dc, (void**)&nb, m->kv_block_bytes, &shortfall);
+      int r = dev_alloc(dc, (void**)&nb, m->kv_block_bytes, &shortfall, MEM_KV);
       if (r != CB_OK) {
         if (st) st->shortfall_bytes = shortfall;
         return r;
       }
     }
-    CB_TRY(timed_begin(dc));
+    CB_TRY(use(dc));
+    CB_CUDA(cudaEventRecord(dc.t0, dc.copy));
     for (int slot = 0; slot < m->d.max_slots; ++slot) {
       if (L.owner[slot] != dev || m->slot_len[slot] <= 0) continue;
       const size_t nbytes = size_t(m->slot_len[slot]) * kv_token_bytes(m);
@@ -1144,9 +1605,11 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
       CB_CUDA(cudaMemcpyAsync(nb + off, kv.second + off, nbytes, cudaMemcpyDefault, dc.copy));
       moved += nbytes;
     }
-    cb_op_stats one{};
-    CB_TRY(timed_end(dc, &one));
-    ms += one.device_ms;
+    CB_CUDA(cudaEventRecord(dc.t1, dc.copy));
+    CB_CUDA(cudaStreamSynchronize(dc.copy));
+    float one = 0.f;
+    CB_CUDA(cudaEventElapsedTime(&one, dc.t0, dc.t1));
+    ms += one;
     uint16_t* old = kv.second;
     free_kv_block(m, L, dev, old);
     kv.second = nb;
@@ -1156,57 +1619,6 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
     st->kv_bytes = moved;
     st->device_ms = ms;
   }
-  return CB_OK;
-}
-
-// MigrateSubModule of a projection / SELF_ATTENTION (ops.py:230-251): copy the
-// module's weights (canonical [out, in] layout) to `dst`; the layer's kernels
-// then run that projection there with activation hops (run_layer_overridden).
-// The layer block keeps its bytes (it is one allocation); the registry does
-// the reference's memory accounting (device_usage, domain.py:481-535).
-int migrate_projection(cb_model* m, int layer, int kind, int dst, cb_op_stats* st) {
-  LayerState& L = m->layers[layer - 1];
-  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
-  const bool attn_part = kind <= CB_ATTN_PROJ_O;
-  if ((kind == CB_SELF_ATTENTION && (L.mod[0].dev >= 0 || L.mod[1].dev >= 0 || L.mod[2].dev >= 0 ||
-                                     L.mod[3].dev >= 0)) ||
-      (attn_part && L.mod[CB_SELF_ATTENTION].dev >= 0))
-    return fail(CB_EINVAL, "projection override conflicts with a self_attention override (domain.py:298-303)");
-  const uint64_t bytes = cb_module_bytes(m, kind);
-  ModCopy& mc = L.mod[kind];
-  ModCopy nc;
-  nc.dev = dst;
-  uint64_t shortfall = 0;
-  int r = dev_alloc(devctx(m, dst), (void**)&nc.buf, bytes, &shortfall);
-  if (r != CB_OK) {
-    if (st) st->shortfall_bytes = shortfall;
-    return r;
-  }
-  CB_TRY(ensure_ws(m, dst));
-  sync_all(m);
-  DeviceCtx& dc = devctx(m, dst);
-  CB_TRY(timed_begin(dc));
-  CB_TRY(use(dc));
-  if (mc.dev >= 0) {  // already moved once: copy from the current override
-    CB_CUDA(cudaMemcpyPeerAsync(nc.buf, dc.ordinal, mc.buf, devctx(m, mc.dev).ordinal, bytes, dc.copy));
-  } else {
-    const LayerCopy& src = L.reps[0];
-    const uint8_t* from = src.block + block_offset(m, kind);
-    if (kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP) {  // every other row of the interleaved block
-      const size_t row = size_t(m->d.d_model) * 2;
-      CB_CUDA(cudaMemcpy2DAsync(nc.buf, row, from, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
-    } else {
-      CB_CUDA(cudaMemcpyPeerAsync(nc.buf, dc.ordinal, from, devctx(m, src.dev).ordinal, bytes, dc.copy));
-    }
-  }
-  CB_TRY(timed_end(dc, st));
-  if (st) st->weight_bytes = bytes;
-  if (mc.dev >= 0) dev_free(m, mc.dev, mc.buf);
-  mc = nc;
-  L.proj_ov = false;
-  for (const ModCopy& x : L.mod)
-    if (x.dev >= 0) L.proj_ov = true;
   return CB_OK;
 }
 
@@ -1251,6 +1663,8 @@ int cb_runtime_create(int32_t n_devices, const int32_t* ordinals, cb_runtime** o
     CB_CUDA(cudaDeviceGetAttribute(&dc.num_sms, cudaDevAttrMultiProcessorCount, dc.ordinal));
     CB_CUDA(cudaStreamCreateWithFlags(&dc.compute, cudaStreamNonBlocking));
     CB_CUDA(cudaStreamCreateWithFlags(&dc.copy, cudaStreamNonBlocking));
+    CB_CUDA(cudaStreamCreateWithFlags(&dc.copy2, cudaStreamNonBlocking));
+    CB_CUDA(cudaStreamCreateWithFlags(&dc.alloc, cudaStreamNonBlocking));
     dc.ev_pool.resize(1024);
     for (auto& e : dc.ev_pool) CB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CB_CUDA(cudaEventCreate(&dc.t0));
@@ -1288,6 +1702,7 @@ int cb_runtime_destroy(cb_runtime* rt) {
     cudaSetDevice(dc.ordinal);
     cudaStreamSynchronize(dc.compute);
     cudaStreamSynchronize(dc.copy);
+    cudaStreamSynchronize(dc.copy2);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dc.ordinal) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     for (auto e : dc.ev_pool) cudaEventDestroy(e);
@@ -1295,6 +1710,8 @@ int cb_runtime_destroy(cb_runtime* rt) {
     cudaEventDestroy(dc.t1);
     cudaStreamDestroy(dc.compute);
     cudaStreamDestroy(dc.copy);
+    cudaStreamDestroy(dc.copy2);
+    cudaStreamDestroy(dc.alloc);
   }
   delete rt;
   return CB_OK;
@@ -1337,6 +1754,7 @@ int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home, cb_
   m->kv_block_bytes = size_t(d.max_slots) * d.max_ctx * kv_token_bytes(m);
   m->layers.resize(d.n_layers);
   m->slot_len.assign(d.max_slots, 0);
+  m->slot_epoch.assign(d.max_slots, 0);
   cudaSetDevice(rt->devs[home].ordinal);
   if (cudaMallocHost(&m->pin_meta, (3 * size_t(d.max_tokens) + d.max_slots + 4 +
                                     4 * (size_t(d.max_tokens) / 64 + d.max_slots)) * 4) != cudaSuccess ||
@@ -1355,6 +1773,12 @@ int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home, cb_
 
 int cb_model_destroy(cb_model* m) {
   if (!m) return CB_OK;
+  sync_all(m);
+  for (auto& kv : m->ops) {
+    if (!kv.second.committed) op_abort(m, kv.second);
+    op_destroy_events(kv.second);
+  }
+  m->ops.clear();
   sync_all(m);
   for (auto& L : m->layers) {
     for (auto& c : L.reps) dev_free(m, c.dev, c.block);
@@ -1436,12 +1860,12 @@ int cb_layer_init_random(cb_model* m, int32_t layer, int32_t dev, uint64_t seed,
 
 int cb_head_load(cb_model* m, const uint16_t* embed, const uint16_t* final_norm, const uint16_t* lm_head) {
   if (!m || !embed || !final_norm || !lm_head) return fail(CB_EINVAL, "null argument");
-  const DeviceCtx& dc = devctx(m, m->home);
+  DeviceCtx& dc = devctx(m, m->home);
   const size_t ve = size_t(m->d.vocab) * m->d.d_model * 2;
   if (!m->embed) {
-    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve));
-    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve));
-    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2));
+    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve, nullptr, MEM_WEIGHTS));
+    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve, nullptr, MEM_WEIGHTS));
+    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2, nullptr, MEM_WEIGHTS));
   }
   CB_TRY(use(dc));
   CB_CUDA(cudaMemcpy(m->embed, embed, ve, cudaMemcpyHostToDevice));
@@ -1457,9 +1881,9 @@ int cb_head_init_random(cb_model* m, uint64_t seed, float std) {
   DeviceCtx& dc = devctx(m, m->home);
   const size_t ve = size_t(m->d.vocab) * m->d.d_model;
   if (!m->embed) {
-    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve * 2));
-    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve * 2));
-    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2));
+    CB_TRY(dev_alloc(dc, (void**)&m->embed, ve * 2, nullptr, MEM_WEIGHTS));
+    CB_TRY(dev_alloc(dc, (void**)&m->lm_head, ve * 2, nullptr, MEM_WEIGHTS));
+    CB_TRY(dev_alloc(dc, (void**)&m->final_norm, size_t(m->d.d_model) * 2, nullptr, MEM_WEIGHTS));
   }
   CB_TRY(use(dc));
   CB_CUDA(cb::init_uniform_launch(m->embed, ve, seed * 31 + 1, 1.0f, 0.f, dc.compute));
@@ -1617,6 +2041,7 @@ int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots) {
   for (int i = 0; i < n; ++i) {
     if (slots[i] < 0 || slots[i] >= m->d.max_slots) return fail(CB_EINVAL, "slot out of range");
     m->slot_len[slots[i]] = 0;
+    m->slot_epoch[slots[i]] += 1;
     for (auto& L : m->layers)
       if (!L.owner.empty()) L.owner[slots[i]] = -1;
   }
@@ -1671,157 +2096,169 @@ int cb_profile_read(cb_model* m, int32_t kclass, cb_kstat* out) {
   return CB_OK;
 }
 
-int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st) {
-  if (!m) return fail(CB_EINVAL, "null model");
-  if (st) *st = cb_op_stats{};
+// ---- scaling ops: asynchronous issue / poll / wait / commit / abort (A17)
+int cb_issue_replicate_layer(cb_model* m, int32_t layer, int32_t dst, int64_t* op_id, uint64_t* shortfall) {
+  if (!m || !op_id) return fail(CB_EINVAL, "null argument");
+  if (shortfall) *shortfall = 0;
+  return issue_replicate(m, layer, dst, op_id, shortfall);
+}
+
+int cb_issue_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, int64_t* op_id,
+                           uint64_t* shortfall) {
+  if (!m || !op_id) return fail(CB_EINVAL, "null argument");
+  if (shortfall) *shortfall = 0;
+  return issue_migrate(m, layer, dst, with_kv, op_id, shortfall);
+}
+
+int cb_issue_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, int64_t* op_id,
+                               uint64_t* shortfall) {
+  if (!m || !op_id) return fail(CB_EINVAL, "null argument");
+  if (shortfall) *shortfall = 0;
   CB_TRY(check_layer(m, layer));
   CB_TRY(check_dev(m, dst));
-  LayerState& L = m->layers[layer - 1];
-  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  for (auto& c : L.reps)
-    if (c.dev == dst) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
-  if (L.kv_override >= 0 || L.proj_ov) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
-  LayerCopy c;
-  c.dev = dst;
-  uint64_t shortfall = 0;
-  int r = dev_alloc(devctx(m, dst), (void**)&c.block, m->layer_bytes, &shortfall);
-  if (r == CB_OK) r = ensure_kv(m, L, dst, &shortfall);
+  if (kind == CB_DECODER_LAYER) return fail(CB_EINVAL, "whole layers move via MigrateLayer");
+  if (kind < 0 || kind > CB_KV_CACHE) return fail(CB_EINVAL, "unknown module kind");
+  if (kind == CB_KV_CACHE) return issue_kv(m, layer, dst, op_id, shortfall);
+  return issue_projection(m, layer, kind, dst, op_id, shortfall);
+}
+
+int cb_issue_evict_replica(cb_model* m, int32_t layer, int32_t device, int64_t* op_id) {
+  if (!m || !op_id) return fail(CB_EINVAL, "null argument");
+  return issue_evict(m, layer, device, op_id);
+}
+
+int cb_op_poll(cb_model* m, int64_t op_id, int32_t* done) {
+  if (!m || !done) return fail(CB_EINVAL, "null argument");
+  auto it = m->ops.find(op_id);
+  if (it == m->ops.end()) return fail(CB_EINVAL, "unknown op id " + std::to_string(op_id));
+  cb_op_stats st{};
+  CB_TRY(op_stats(m, it->second, &st, false));
+  *done = st.done;
+  return CB_OK;
+}
+
+int cb_op_wait(cb_model* m, int64_t op_id, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  auto it = m->ops.find(op_id);
+  if (it == m->ops.end()) return fail(CB_EINVAL, "unknown op id " + std::to_string(op_id));
+  return op_stats(m, it->second, st, true);
+}
+
+int cb_commit(cb_model* m, int64_t op_id, int32_t* n_committed) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  int n = 0;
+  for (auto& kv : m->ops) {  // issue order
+    PendingOp& op = kv.second;
+    if (op.committed || (op_id >= 0 && kv.first != op_id)) continue;
+    CB_TRY(op_commit(m, op));
+    ++n;
+  }
+  if (op_id >= 0 && n == 0) return fail(CB_EINVAL, "op " + std::to_string(op_id) + " is not pending");
+  if (n_committed) *n_committed = n;
+  return CB_OK;
+}
+
+int cb_op_abort(cb_model* m, int64_t op_id) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  std::vector<int64_t> ids;
+  for (auto& kv : m->ops)
+    if (!kv.second.committed && (op_id < 0 || kv.first == op_id)) ids.push_back(kv.first);
+  if (op_id >= 0 && ids.empty()) return fail(CB_EINVAL, "op " + std::to_string(op_id) + " is not pending");
+  for (auto it = ids.rbegin(); it != ids.rend(); ++it) {  // newest first
+    PendingOp& op = m->ops[*it];
+    CB_TRY(op_abort(m, op));
+    op_destroy_events(op);
+    m->ops.erase(*it);
+  }
+  return CB_OK;
+}
+
+int cb_pending_ops(cb_model* m, int32_t* n) {
+  if (!m || !n) return fail(CB_EINVAL, "null argument");
+  *n = 0;
+  for (auto& kv : m->ops) *n += kv.second.committed ? 0 : 1;
+  return CB_OK;
+}
+
+int cb_mem_usage(cb_model* m, int32_t device, cb_mem_stats* out) {
+  if (!m || !out) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_dev(m, device));
+  DeviceCtx& dc = devctx(m, device);
+  *out = cb_mem_stats{};
+  out->workspace_bytes = dc.mem[MEM_WS];
+  out->weight_bytes = dc.mem[MEM_WEIGHTS];
+  out->kv_bytes = dc.mem[MEM_KV];
+  out->reserved_bytes = dc.reserved;
+  CB_TRY(use(dc));
+  size_t f = 0, t = 0;
+  CB_CUDA(cudaMemGetInfo(&f, &t));
+  cudaMemPool_t pool;
+  CB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dc.ordinal));
+  uint64_t res = 0, used = 0;
+  CB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res));
+  CB_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  // pool memory freed back to the pool (not to the driver) is still allocatable
+  out->free_bytes = f + (res > used ? res - used : 0);
+  out->total_bytes = t;
+  return CB_OK;
+}
+
+int cb_set_copy_mode(cb_runtime* rt, int32_t mode, uint64_t chunk_bytes) {
+  if (!rt || mode < 0 || mode > 2) return fail(CB_EINVAL, "copy mode must be 0 (one copy engine), 1 (two lanes) or 2 (SM push)");
+  rt->copy_mode = mode;
+  if (chunk_bytes) rt->copy_chunk = chunk_bytes;
+  return CB_OK;
+}
+
+// ---- synchronous forms: issue + commit at once, then wait (data movement of
+// ops.apply, ops.py:173-260, for callers between steps)
+static int run_now(cb_model* m, int r, int64_t id, uint64_t shortfall, cb_op_stats* st) {
   if (r != CB_OK) {
-    if (c.block) dev_free(m, dst, c.block);
     if (st) st->shortfall_bytes = shortfall;
     return r;
   }
-  CB_TRY(ensure_ws(m, dst));
-  sync_all(m);
-  DeviceCtx& dc = devctx(m, dst);
-  CB_TRY(timed_begin(dc));
-  CB_TRY(copy_block(m, L.reps[0], c, dc.copy));
-  CB_TRY(timed_end(dc, st));
-  if (st) st->weight_bytes = m->layer_bytes;
-  CB_TRY(make_layer_maps(m, c));
-  L.reps.push_back(c);
+  auto it = m->ops.find(id);
+  if (it == m->ops.end()) return fail(CB_ESTATE, "internal: issued op not registered");
+  CB_TRY(op_commit(m, it->second));
+  CB_TRY(op_stats(m, it->second, st, true));
+  op_destroy_events(m->ops[id]);
+  m->ops.erase(id);
   return CB_OK;
+}
+
+int cb_replicate_layer(cb_model* m, int32_t layer, int32_t dst, cb_op_stats* st) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (st) *st = cb_op_stats{};
+  int64_t id = 0;
+  uint64_t sf = 0;
+  const int r = issue_replicate(m, layer, dst, &id, &sf);  // (issue before reading id)
+  return run_now(m, r, id, sf, st);
 }
 
 int cb_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, cb_op_stats* st) {
   if (!m) return fail(CB_EINVAL, "null model");
   if (st) *st = cb_op_stats{};
-  CB_TRY(check_layer(m, layer));
-  CB_TRY(check_dev(m, dst));
-  LayerState& L = m->layers[layer - 1];
-  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  const int src = L.reps[0].dev;
-  if (dst == src) return fail(CB_EINVAL, "layer original already on device " + std::to_string(dst));
-  for (auto& c : L.reps)
-    if (c.dev == dst) return fail(CB_EINVAL, "layer already has a copy on device " + std::to_string(dst));
-  if (!with_kv && L.reps.size() > 1) return fail(CB_EINVAL, "cannot detach KV from a replicated layer");
-  const int kv_src = kv_device(L);
-  LayerCopy c;
-  c.dev = dst;
-  uint64_t shortfall = 0;
-  int r = dev_alloc(devctx(m, dst), (void**)&c.block, m->layer_bytes, &shortfall);
-  if (r == CB_OK && with_kv) r = ensure_kv(m, L, dst, &shortfall);
-  if (r != CB_OK) {
-    if (c.block) dev_free(m, dst, c.block);
-    if (st) st->shortfall_bytes = shortfall;
-    return r;
-  }
-  CB_TRY(ensure_ws(m, dst));
-  sync_all(m);
-  DeviceCtx& dc = devctx(m, dst);
-  CB_TRY(timed_begin(dc));
-  CB_TRY(copy_block(m, L.reps[0], c, dc.copy));
-  uint64_t kvb = 0;
-  if (with_kv) {
-    for (int slot = 0; slot < m->d.max_slots; ++slot) {
-      // KV held by the layer's KV device follows the layer; replica-held rows stay
-      if (L.owner[slot] == kv_src) {
-        CB_TRY(kv_move(m, L, slot, kv_src, dst, dc.copy, &kvb));
-        L.owner[slot] = dst;
-      }
-    }
-  }
-  CB_TRY(timed_end(dc, st));
-  if (st) {
-    st->weight_bytes = m->layer_bytes;
-    st->kv_bytes = kvb;
-  }
-  CB_TRY(make_layer_maps(m, c));
-  LayerCopy old = L.reps[0];
-  L.reps[0] = c;
-  dev_free(m, old.dev, old.block);
-  if (with_kv) {
-    L.kv_override = -1;
-  } else {
-    L.kv_override = kv_src;  // KV stays resident where it was (domain.py:445-451)
-  }
-  for (int dv : std::vector<int>{old.dev, kv_src}) drop_kv_if_unused(m, L, dv);
-  return CB_OK;
+  int64_t id = 0;
+  uint64_t sf = 0;
+  const int r = issue_migrate(m, layer, dst, with_kv, &id, &sf);
+  return run_now(m, r, id, sf, st);
 }
 
 int cb_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, cb_op_stats* st) {
   if (!m) return fail(CB_EINVAL, "null model");
   if (st) *st = cb_op_stats{};
-  CB_TRY(check_layer(m, layer));
-  CB_TRY(check_dev(m, dst));
-  if (kind == CB_DECODER_LAYER) return fail(CB_EINVAL, "whole layers move via MigrateLayer");
-  if (kind < 0 || kind > CB_KV_CACHE) return fail(CB_EINVAL, "unknown module kind");
-  if (kind != CB_KV_CACHE) return migrate_projection(m, layer, kind, dst, st);
-  LayerState& L = m->layers[layer - 1];
-  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
-  uint64_t shortfall = 0;
-  int r = ensure_kv(m, L, dst, &shortfall);
-  if (r != CB_OK) {
-    if (st) st->shortfall_bytes = shortfall;
-    return r;
-  }
-  CB_TRY(ensure_ws(m, dst));
-  const int old_kv = kv_device(L);
-  sync_all(m);
-  DeviceCtx& dc = devctx(m, dst);
-  CB_TRY(timed_begin(dc));
-  uint64_t kvb = 0;
-  for (int slot = 0; slot < m->d.max_slots; ++slot) {
-    const int o = L.owner[slot];
-    if (o >= 0 && o != dst) {
-      CB_TRY(kv_move(m, L, slot, o, dst, dc.copy, &kvb));
-      L.owner[slot] = dst;
-    }
-  }
-  CB_TRY(timed_end(dc, st));
-  if (st) st->kv_bytes = kvb;
-  L.kv_override = dst;
-  drop_kv_if_unused(m, L, old_kv);
-  return CB_OK;
+  int64_t id = 0;
+  uint64_t sf = 0;
+  const int r = cb_issue_migrate_submodule(m, layer, kind, dst, &id, &sf);
+  return run_now(m, r, id, sf, st);
 }
 
 int cb_evict_replica(cb_model* m, int32_t layer, int32_t dev, cb_op_stats* st) {
   if (!m) return fail(CB_EINVAL, "null model");
   if (st) *st = cb_op_stats{};
-  CB_TRY(check_layer(m, layer));
-  LayerState& L = m->layers[layer - 1];
-  if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  if (L.reps[0].dev == dev) return fail(CB_ENOREPLICA, "cannot evict the original replica");
-  auto it = std::find_if(L.reps.begin() + 1, L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; });
-  if (it == L.reps.end())
-    return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no replica on device " + std::to_string(dev));
-  const int orig = L.reps[0].dev;
-  sync_all(m);
-  DeviceCtx& oc = devctx(m, orig);
-  CB_TRY(timed_begin(oc));
-  uint64_t kvb = 0;
-  for (int slot = 0; slot < m->d.max_slots; ++slot)
-    if (L.owner[slot] == dev) {
-      CB_TRY(kv_move(m, L, slot, dev, orig, oc.copy, &kvb));
-      L.owner[slot] = orig;
-    }
-  CB_TRY(timed_end(oc, st));
-  if (st) st->kv_bytes = kvb;
-  dev_free(m, dev, it->block);
-  L.reps.erase(it);
-  drop_kv_if_unused(m, L, dev);
-  return CB_OK;
+  int64_t id = 0;
+  const int r = issue_evict(m, layer, dev, &id);
+  return run_now(m, r, id, 0, st);
 }
 
 // experiments: host milliseconds spent enqueuing the last forward pass

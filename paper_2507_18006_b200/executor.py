@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+import weakref
 from dataclasses import dataclass, field
 from typing import Mapping, Sequence
 
@@ -65,6 +66,7 @@ class Runtime:
         h = C.c_void_p()
         _lib.check(self.lib.cb_runtime_create(len(self.ordinals), arr, C.byref(h)), "cb_runtime_create")
         self.handle = h
+        self._models = weakref.WeakSet()  # executors on this runtime: closed before it
 
     @property
     def n_devices(self) -> int:
@@ -77,6 +79,8 @@ class Runtime:
 
     def close(self) -> None:
         if self.handle:
+            for ex in list(self._models):  # a model must never outlive its runtime
+                ex.close()
             self.lib.cb_runtime_destroy(self.handle)
             self.handle = None
 
@@ -89,6 +93,9 @@ class OpMeasurement:
     weight_bytes: int
     kv_bytes: int
     device_ms: float
+    copy_ms: float | None = None      # asynchronous ops: transfer (overlapped with serving)
+    catchup_ms: float | None = None   # asynchronous ops: KV appended meanwhile, copied at the commit
+    catchup_bytes: int | None = None
 
     @property
     def gbps(self) -> float:
@@ -113,10 +120,14 @@ class Executor:
         desc = cfg.desc()
         _lib.check(self.lib.cb_model_create(runtime.handle, C.byref(desc), home_device, C.byref(h)), "cb_model_create")
         self.handle = h
+        runtime._models.add(self)
         self._rows: list = [None] * cfg.n_layers  # registry rows as layers get loaded
         self._overrides: list = []
         self._slots = list(range(cfg.max_slots - 1, -1, -1))
         self.op_log: list[OpMeasurement] = []
+        self._pending: list[tuple[object, int]] = []  # issued, uncommitted ops (op, op_id)
+        self._pending_placement: PlacementState | None = None
+        self._unresolved: list[tuple[object, int]] = []  # committed ops whose timings are not read yet
         self.last_step_ms = 0.0
         self.kv_offload_fraction = 0.0
 
@@ -199,11 +210,15 @@ class Executor:
     def apply(self, op, catalog: ModuleCatalog, cluster: ClusterSpec, cost_model: O.OpCostModel = O.DEFAULT_COST_MODEL,
               extra_used_mb: Mapping[int, float] | None = None,
               kv_mb_by_layer: Mapping[int, float] | None = None) -> tuple[PlacementState, O.TransitionCost]:
-        """Registry apply (reference semantics, errors and placement) + physical move.
+        """Registry apply (reference semantics, errors and placement) + physical move,
+        synchronously (issue, commit and wait at once; use ``issue`` / ``commit``
+        to keep serving while the bytes move).
 
         Returns the new placement and a TransitionCost whose time is the
         measured copy time; the analytic cost of the reference is
         ``ops.apply(...)[1]``."""
+        if self._pending:
+            raise O.OpError("scaling ops are pending: commit() or abort() them first")
         new_p, analytic = O.apply(self.placement, op, catalog, cluster, cost_model, extra_used_mb, kv_mb_by_layer)
         st = _lib.OpStats()
         if isinstance(op, O.ReplicateLayer):
@@ -223,6 +238,96 @@ class Executor:
         m = OpMeasurement(op, st.weight_bytes, st.kv_bytes, st.device_ms)
         self.op_log.append(m)
         return new_p, O.TransitionCost(st.device_ms / 1e3, analytic.transient_memory_mb)
+
+    # ------------------------------------------------------------ asynchronous scaling ops (A17)
+    def issue(self, op, catalog: ModuleCatalog, cluster: ClusterSpec, cost_model: O.OpCostModel = O.DEFAULT_COST_MODEL,
+              extra_used_mb: Mapping[int, float] | None = None,
+              kv_mb_by_layer: Mapping[int, float] | None = None) -> int:
+        """Start a scaling op without stopping service (the reference's
+        transition, sim.py:396-403 / 812-841): the registry ``apply`` runs on the
+        placement after every op issued so far (errors as ``ops.apply``), the
+        destination memory is reserved now, the bytes move on the copy streams
+        while ``step_batch`` keeps serving the committed placement, and
+        ``commit()`` switches every issued op at a step boundary
+        (sim.py:614-622).  Returns the op id."""
+        base = self._pending_placement if self._pending else self.placement
+        new_p, _ = O.apply(base, op, catalog, cluster, cost_model, extra_used_mb, kv_mb_by_layer)
+        oid, sf = C.c_int64(), C.c_uint64()
+        if isinstance(op, O.ReplicateLayer):
+            rc = self.lib.cb_issue_replicate_layer(self.handle, op.layer, op.dst_device, C.byref(oid), C.byref(sf))
+        elif isinstance(op, O.MigrateLayer):
+            rc = self.lib.cb_issue_migrate_layer(self.handle, op.layer, op.dst_device, int(op.with_kv), C.byref(oid),
+                                                 C.byref(sf))
+        elif isinstance(op, O.MigrateSubModule):
+            rc = self.lib.cb_issue_migrate_submodule(self.handle, op.layer, _lib.KIND_IDS[op.kind.value],
+                                                     op.dst_device, C.byref(oid), C.byref(sf))
+        elif isinstance(op, O.EvictReplica):
+            rc = self.lib.cb_issue_evict_replica(self.handle, op.layer, op.device, C.byref(oid))
+        else:
+            raise O.OpError(f"unknown op {op!r}")
+        _lib.check(rc, "issue " + type(op).__name__, sf.value)
+        self._pending.append((op, oid.value))
+        self._pending_placement = new_p
+        return oid.value
+
+    @property
+    def pending_ops(self) -> list:
+        return [op for op, _ in self._pending]
+
+    def ops_done(self) -> bool:
+        """Every issued op's transfer has finished (non-blocking)."""
+        done = C.c_int32()
+        for _, oid in self._pending:
+            _lib.check(self.lib.cb_op_poll(self.handle, oid, C.byref(done)))
+            if not done.value:
+                return False
+        return True
+
+    def commit(self) -> PlacementState:
+        """Switch every issued op at this step boundary (no host wait: the next
+        step is stream-ordered after the transfers and the KV catch-up).  The
+        measured times are read after the next step (``op_log``)."""
+        if not self._pending:
+            return self.placement
+        n = C.c_int32()
+        _lib.check(self.lib.cb_commit(self.handle, -1, C.byref(n)), "cb_commit")
+        self._set_placement(self._pending_placement)
+        self._unresolved.extend(self._pending)
+        self._pending, self._pending_placement = [], None
+        self.check_plan()
+        return self.placement
+
+    def abort(self) -> None:
+        """Release every uncommitted op's reservation; the executor is exactly as before."""
+        if self._pending:
+            _lib.check(self.lib.cb_op_abort(self.handle, -1), "cb_op_abort")
+        self._pending, self._pending_placement = [], None
+
+    def op_stats(self, op_id: int, wait: bool = True) -> dict:
+        st = _lib.OpStats()
+        if wait:
+            _lib.check(self.lib.cb_op_wait(self.handle, op_id, C.byref(st)))
+        else:
+            done = C.c_int32()
+            _lib.check(self.lib.cb_op_poll(self.handle, op_id, C.byref(done)))
+            if not done.value:
+                return {"done": False}
+            _lib.check(self.lib.cb_op_wait(self.handle, op_id, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in _lib.OpStats._fields_}
+
+    def _resolve_ops(self) -> None:
+        for op, oid in self._unresolved:
+            st = self.op_stats(oid)
+            m = OpMeasurement(op, st["weight_bytes"], st["kv_bytes"], st["device_ms"])
+            m.copy_ms, m.catchup_ms, m.catchup_bytes = st["copy_ms"], st["catchup_ms"], st["catchup_bytes"]
+            self.op_log.append(m)
+        self._unresolved = []
+
+    def mem_usage(self, device: int) -> dict:
+        """Bytes the executor holds on a logical device (+ allocatable bytes)."""
+        ms = _lib.MemStats()
+        _lib.check(self.lib.cb_mem_usage(self.handle, device, C.byref(ms)))
+        return {f: getattr(ms, f) for f, _ in _lib.MemStats._fields_}
 
     # ------------------------------------------------------------ KV slots
     def acquire_slot(self) -> int:
@@ -274,6 +379,8 @@ class Executor:
                               _lib.f32(logits) if logits is not None else None, C.byref(ms))
         _lib.check(rc, "cb_step")
         self.last_step_ms = ms.value
+        if self._unresolved:  # committed ops ran before this step: their timings are final
+            self._resolve_ops()
         return nxt, logits, ms.value
 
     def synthetic_prompt(self, req: Request) -> np.ndarray:
@@ -381,7 +488,8 @@ class Executor:
 
     def close(self) -> None:
         if getattr(self, "handle", None):
-            self.lib.cb_model_destroy(self.handle)
+            self._pending, self._pending_placement = [], None
+            self.lib.cb_model_destroy(self.handle)  # releases uncommitted reservations
             self.handle = None
 
     def __del__(self):
