@@ -130,9 +130,7 @@ struct LayerState {
   ModCopy mod[kModKinds];           // projection / self-attention overrides
   bool proj_ov = false;             // any entry of mod[] in use
   std::map<int, bool> kv_host;      // device -> its KV block lives in mapped pinned host memory (offloaded)
-  int n_pending = 0;                // uncommitted scaling ops on this layer: any number of
-  bool pending_excl = false;        // replications, or exactly one other op (exclusive)
-  std::vector<int> pending_rep_dst; // destinations of the pending replications
+  std::vector<std::pair<int, int>> pend;  // uncommitted scaling ops on this layer: (OpKind, dst or module kind)
 };
 
 // An issued, not yet committed scaling op (A17: the reference's _Transition,
@@ -1200,11 +1198,22 @@ int transfer(cb_model* m, int dst_dev, void* dst, int src_dev, const void* src, 
 }
 
 // ---- asynchronous scaling ops (A17) ----------------------------------------
-// A layer may carry several pending replications (a scale-up decision fans a
-// layer out to many devices) or exactly one other pending op.
-int check_idle(const LayerState& L, int layer, bool replicate = false, int dst = -1) {
-  const bool clash = replicate ? L.pending_excl || std::count(L.pending_rep_dst.begin(), L.pending_rep_dst.end(), dst)
-                               : L.n_pending > 0;
+// Which uncommitted ops may share a layer: a scale-up decision fans a layer out
+// to many devices (replications to distinct devices), a compute-bound
+// scale-down moves several projections of one layer (distinct, non-conflicting
+// modules) and maybe its KV; a layer migration or an eviction stands alone.
+int check_idle(const LayerState& L, int layer, int kind, int arg = -1) {
+  auto attn_part = [](int mk) { return mk <= CB_ATTN_PROJ_O; };
+  bool clash = false;
+  for (const auto& pk : L.pend) {
+    const int k = pk.first, a = pk.second;
+    if (kind == OPK_MIGRATE || kind == OPK_EVICT || k == OPK_MIGRATE || k == OPK_EVICT) clash = true;
+    else if (kind == OPK_REPLICATE) clash |= k != OPK_REPLICATE || a == arg;
+    else if (k == OPK_REPLICATE) clash = true;
+    else if (kind == OPK_KV) clash |= k == OPK_KV;
+    else if (kind == OPK_PROJ && k == OPK_PROJ)
+      clash |= a == arg || (arg == CB_SELF_ATTENTION && attn_part(a)) || (a == CB_SELF_ATTENTION && attn_part(arg));
+  }
   if (clash)
     return fail(CB_ESTATE, "layer " + std::to_string(layer) + " has an uncommitted scaling op in the way");
   return CB_OK;
@@ -1240,11 +1249,7 @@ int op_close(cb_model* m, PendingOp& op, int64_t* id_out) {
   CB_CUDA(cudaEventRecord(op.e1, dc.copy));
   op.id = m->next_op++;
   LayerState& L = m->layers[op.layer - 1];
-  L.n_pending += 1;
-  if (op.kind == OPK_REPLICATE)
-    L.pending_rep_dst.push_back(op.dst);
-  else
-    L.pending_excl = true;
+  L.pend.push_back({op.kind, op.kind == OPK_PROJ ? op.mod_kind : op.dst});
   if (op.dst >= 0) devctx(m, op.dst).reserved += op.reserved;
   m->ops[op.id] = op;
   if (id_out) *id_out = op.id;
@@ -1292,13 +1297,9 @@ int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
 }
 
 void op_unlock(LayerState& L, const PendingOp& op) {
-  L.n_pending -= 1;
-  if (op.kind == OPK_REPLICATE) {
-    auto it = std::find(L.pending_rep_dst.begin(), L.pending_rep_dst.end(), op.dst);
-    if (it != L.pending_rep_dst.end()) L.pending_rep_dst.erase(it);
-  } else {
-    L.pending_excl = false;
-  }
+  const std::pair<int, int> key{op.kind, op.kind == OPK_PROJ ? op.mod_kind : op.dst};
+  auto it = std::find(L.pend.begin(), L.pend.end(), key);
+  if (it != L.pend.end()) L.pend.erase(it);
 }
 
 // release what an op reserved but never committed
@@ -1323,7 +1324,7 @@ int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shor
   CB_TRY(check_dev(m, dst));
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer, true, dst));
+  CB_TRY(check_idle(L, layer, OPK_REPLICATE, dst));
   for (auto& c : L.reps)
     if (c.dev == dst)
       return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
@@ -1356,7 +1357,7 @@ int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uin
   CB_TRY(check_dev(m, dst));
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer));
+  CB_TRY(check_idle(L, layer, OPK_MIGRATE));
   const int src = L.reps[0].dev;
   if (dst == src) return fail(CB_EINVAL, "layer original already on device " + std::to_string(dst));
   for (auto& c : L.reps)
@@ -1394,7 +1395,7 @@ int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uin
 int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uint64_t* shortfall) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer));
+  CB_TRY(check_idle(L, layer, OPK_PROJ, kind));
   if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
   const bool attn_part = kind <= CB_ATTN_PROJ_O;
   if ((kind == CB_SELF_ATTENTION && (L.mod[0].dev >= 0 || L.mod[1].dev >= 0 || L.mod[2].dev >= 0 ||
@@ -1438,7 +1439,7 @@ int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uin
 int issue_kv(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer));
+  CB_TRY(check_idle(L, layer, OPK_KV));
   if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
   DeviceCtx& dc = devctx(m, dst);
   PendingOp op = new_op(m, OPK_KV, layer, dst, dst);
@@ -1464,7 +1465,7 @@ int issue_evict(cb_model* m, int layer, int dev, int64_t* id) {
   CB_TRY(check_layer(m, layer));
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer));
+  CB_TRY(check_idle(L, layer, OPK_EVICT));
   if (L.reps[0].dev == dev) return fail(CB_ENOREPLICA, "cannot evict the original replica");
   auto it = std::find_if(L.reps.begin() + 1, L.reps.end(), [&](const LayerCopy& c) { return c.dev == dev; });
   if (it == L.reps.end())
@@ -1575,7 +1576,7 @@ int op_stats(cb_model* m, PendingOp& op, cb_op_stats* st, bool wait) {
 int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
-  CB_TRY(check_idle(L, layer));
+  CB_TRY(check_idle(L, layer, OPK_MIGRATE));
   sync_all(m);  // Phase-3 relief (rare): a blocking move keeps the host-memory swap simple
   uint64_t moved = 0;
   float ms = 0.f;

@@ -283,10 +283,11 @@ class Executor:
                 return False
         return True
 
-    def commit(self) -> PlacementState:
+    def commit(self, wait: bool = False) -> PlacementState:
         """Switch every issued op at this step boundary (no host wait: the next
         step is stream-ordered after the transfers and the KV catch-up).  The
-        measured times are read after the next step (``op_log``)."""
+        measured times are read after the next step (``op_log``), or now with
+        ``wait`` (blocks until the copies finished)."""
         if not self._pending:
             return self.placement
         n = C.c_int32()
@@ -295,6 +296,8 @@ class Executor:
         self._unresolved.extend(self._pending)
         self._pending, self._pending_placement = [], None
         self.check_plan()
+        if wait:
+            self._resolve_ops()
         return self.placement
 
     def abort(self) -> None:

@@ -19,14 +19,27 @@ pytestmark = pytest.mark.skipif(ms is None, reason="reference modscale not impor
 
 
 class RegistryOnlyExecutor:
-    """Stand-in with the Executor's registry surface (no device)."""
+    """Stand-in with the Executor's registry / op surface (no device)."""
 
     def __init__(self, placement):
         self.placement = placement
+        self._pending, self._next = [], None
 
-    def apply(self, op, catalog, cluster, kv_mb_by_layer=None):
-        self.placement, cost = O.apply(self.placement, op, catalog, cluster, kv_mb_by_layer=kv_mb_by_layer)
-        return self.placement, cost
+    def issue(self, op, catalog, cluster, kv_mb_by_layer=None):
+        base = self._next if self._pending else self.placement
+        self._next, _ = O.apply(base, op, catalog, cluster, kv_mb_by_layer=kv_mb_by_layer)
+        self._pending.append(op)
+
+    def ops_done(self):
+        return True
+
+    def commit(self):
+        if self._pending:
+            self.placement = self._next
+        self._pending = []
+
+    def abort(self):
+        self._pending = []
 
 
 def test_placement_roundtrip():
