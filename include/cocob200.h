@@ -44,6 +44,7 @@ extern "C" {
 #define CB_ECUDA (-4)
 #define CB_ESTATE (-5)
 #define CB_ENOTSUP (-6)
+#define CB_ECOMM (-7) /* the multi-process transport failed (RuntimeError) */
 
 /* ModuleKind ids, in the reference enum's declaration order (domain.py:23-36). */
 #define CB_ATTN_PROJ_Q 0
@@ -132,6 +133,31 @@ int cb_split_batch(int32_t bs, int32_t p, int32_t* shares_out);
  * logical device gets a compute stream, a copy stream and P2P access to every
  * other physical GPU (NVLink through NVSwitch on an HGX B200). */
 int cb_runtime_create(int32_t n_devices, const int32_t* cuda_ordinals, cb_runtime** out);
+/* Multi-process (SPMD) runtime: one process per GPU, every process holding the
+ * SAME global list of logical devices; rank_of_device[i] names the process that
+ * owns device i, and the devices of my_rank live on CUDA ordinal my_ordinal.
+ * Every rank issues the same calls in the same order (loads, ops, steps, slot
+ * releases -- the reference's single-writer control plane, SPEC.md:310-311,
+ * replayed on each rank); each rank allocates and computes only for its own
+ * devices, keeps the same registry / KV-ownership bookkeeping for all of them,
+ * and hands every byte range that crosses a process boundary to `xfer`, in the
+ * same global order on every rank.  send != 0: `bytes` at dev_ptr are ready on
+ * `cuda_stream`, send them to peer_rank; send == 0: receive `bytes` from
+ * peer_rank into dev_ptr, to be consumed on `cuda_stream` (stream-ordered, no
+ * host synchronisation required).  channel 0 = per-step exchanges on compute
+ * streams (activation rows at replica-run boundaries = the reference's
+ * scatter/gather, _kernels.py:41-51; KV rows following their sequence; norm
+ * vectors at the first step), channel 1 = scaling-op transfers on copy streams
+ * (layer blocks, KV pre-copies).  A non-zero return fails the call with
+ * CB_ECOMM.  The Python host implements it with torch.distributed (NCCL over
+ * NVLink on a B200 box).  Not supported in this mode: projection / KV-cache
+ * sub-module overrides and KV offload (single-process runtime only). */
+typedef int (*cb_xfer_fn)(void* ctx, int32_t channel, int32_t send, int32_t peer_rank, void* dev_ptr,
+                          uint64_t bytes, void* cuda_stream);
+int cb_runtime_create_spmd(int32_t n_devices, const int32_t* rank_of_device, int32_t my_rank, int32_t my_ordinal,
+                           cb_xfer_fn xfer, void* xfer_ctx, cb_runtime** out);
+/* 1 if `device` is computed by this process. */
+int cb_device_is_local(cb_runtime* rt, int32_t device, int32_t* local_out);
 int cb_runtime_destroy(cb_runtime* rt);
 int cb_device_info(cb_runtime* rt, int32_t device, int32_t* num_sms, uint64_t* free_bytes,
                    uint64_t* total_bytes);
@@ -224,6 +250,12 @@ int cb_issue_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with
 int cb_issue_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, int64_t* op_id,
                                uint64_t* shortfall_bytes);
 int cb_issue_evict_replica(cb_model* m, int32_t layer, int32_t device, int64_t* op_id);
+/* SPMD runtime only: cb_issue_* reserves on the destination's rank and
+ * returns; every rank then agrees on the outcome (the host all-reduces the
+ * status) and calls cb_op_start (all succeeded: the transfer is enqueued, send
+ * on the source's rank, receive on the destination's) or cb_op_abort.  A rank
+ * whose issue failed still consumes the op id, so ids stay aligned. */
+int cb_op_start(cb_model* m, int64_t op_id);
 int cb_op_poll(cb_model* m, int64_t op_id, int32_t* done); /* non-blocking */
 int cb_op_wait(cb_model* m, int64_t op_id, cb_op_stats* st); /* blocks until the op's copies finished */
 int cb_commit(cb_model* m, int64_t op_id, int32_t* n_committed);

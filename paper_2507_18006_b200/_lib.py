@@ -21,6 +21,7 @@ CB_ENOREPLICA = -3
 CB_ECUDA = -4
 CB_ESTATE = -5
 CB_ENOTSUP = -6
+CB_ECOMM = -7
 
 PHASE_PREFILL = 0
 PHASE_DECODE = 1
@@ -89,6 +90,8 @@ class KStat(C.Structure):
 KCLASSES = ("gemm", "attention", "elementwise", "copy")
 
 _P = C.c_void_p
+# cross-process transport callback of the SPMD runtime (cb_xfer_fn)
+XFER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p)
 _I32P = C.POINTER(C.c_int32)
 _I64P = C.POINTER(C.c_int64)
 _F32P = C.POINTER(C.c_float)
@@ -98,6 +101,8 @@ _SIGS = {
     "cb_last_error": (C.c_char_p, []),
     "cb_split_batch": (C.c_int, [C.c_int32, C.c_int32, _I32P]),
     "cb_runtime_create": (C.c_int, [C.c_int32, _I32P, C.POINTER(_P)]),
+    "cb_runtime_create_spmd": (C.c_int, [C.c_int32, _I32P, C.c_int32, C.c_int32, XFER_FN, _P, C.POINTER(_P)]),
+    "cb_device_is_local": (C.c_int, [_P, C.c_int32, _I32P]),
     "cb_runtime_destroy": (C.c_int, [_P]),
     "cb_device_info": (C.c_int, [_P, C.c_int32, _I32P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "cb_model_create": (C.c_int, [_P, C.POINTER(ModelDesc), C.c_int32, C.POINTER(_P)]),
@@ -122,6 +127,7 @@ _SIGS = {
     "cb_issue_migrate_layer": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P, C.POINTER(C.c_uint64)]),
     "cb_issue_migrate_submodule": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _I64P, C.POINTER(C.c_uint64)]),
     "cb_issue_evict_replica": (C.c_int, [_P, C.c_int32, C.c_int32, _I64P]),
+    "cb_op_start": (C.c_int, [_P, C.c_int64]),
     "cb_op_poll": (C.c_int, [_P, C.c_int64, _I32P]),
     "cb_op_wait": (C.c_int, [_P, C.c_int64, C.POINTER(OpStats)]),
     "cb_commit": (C.c_int, [_P, C.c_int64, _I32P]),
@@ -189,9 +195,13 @@ def check(status: int, what: str = "", shortfall_bytes: int = 0) -> None:
     """Raise the reference-compatible exception for a CB_E* status."""
     if status == CB_OK:
         return
+    raise_status(status, f"{what}: {last_error()}" if what else last_error(), shortfall_bytes)
+
+
+def raise_status(status: int, msg: str, shortfall_bytes: int = 0) -> None:
+    """Raise the exception class of a CB_E* status with a given message."""
     from .ops import InfeasibleOpError, MissingReplicaError, OpError
 
-    msg = f"{what}: {last_error()}" if what else last_error()
     if status == CB_EINVAL:
         raise OpError(msg)
     if status == CB_ENOMEM:

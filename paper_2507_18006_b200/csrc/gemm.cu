@@ -1134,9 +1134,30 @@ __global__ void __launch_bounds__(kThreads1, 1)
   const int n_tt = a.n_ttiles;
   const StreamK sk{a.units, int(gridDim.x) >> 1, a.kblocks};
   const int ptiles = sk.units / sk.kb;
-  const int ubeg = a.whole_tiles ? int((long long)pair * ptiles / sk.grid) * sk.kb : sk.u0(pair);
-  const int uend = a.whole_tiles ? int((long long)(pair + 1) * ptiles / sk.grid) * sk.kb : sk.u0(pair + 1);
+  // Rastered whole tiles (token-major plans with several token tiles, i.e.
+  // prefill): pair p takes tiles p, p + pairs, ... of an order that walks the
+  // weight tiles inside groups of a.raster token tiles, so the tiles in flight
+  // at any moment share a few weight tiles and a few token tiles (L2-resident)
+  // instead of every pair streaming its own weight tile against all tokens.
+  const bool rast = SWAP && a.raster > 0;
+  const int n_mine = rast ? (pair < ptiles ? (ptiles - pair + sk.grid - 1) / sk.grid : 0) : 0;
+  const int ubeg = rast ? 0 : a.whole_tiles ? int((long long)pair * ptiles / sk.grid) * sk.kb : sk.u0(pair);
+  const int uend = rast ? n_mine * sk.kb
+                        : a.whole_tiles ? int((long long)(pair + 1) * ptiles / sk.grid) * sk.kb : sk.u0(pair + 1);
   const int c = blockIdx.x;
+  auto tile_of = [&](int u, int& mt_o, int& tt_o) {
+    const int t = u / sk.kb;
+    if (!rast) {
+      mt_o = t / n_tt;
+      tt_o = t % n_tt;
+      return;
+    }
+    const int g = pair + t * sk.grid, span = a.raster * a.n_mtiles;
+    const int grp = g / span, r = g - grp * span, t0 = grp * a.raster;
+    const int gw = min(a.raster, n_tt - t0);
+    mt_o = r / gw;
+    tt_o = t0 + r % gw;
+  };
 
   pdl_trigger();
   if (a.trace && threadIdx.x == 0) a.trace[(size_t)c * 512] = globaltimer_ns();
@@ -1171,7 +1192,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
-        const int mt = (u / sk.kb) / n_tt, kb = u % sk.kb;
+        int mt, tt_unused;
+        tile_of(u, mt, tt_unused);
+        const int kb = u % sk.kb;
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 66 + (u - ubeg)] = globaltimer_ns();
         if (SWAP) {  // nw / 2 weight rows per CTA (box height of the launcher's map)
@@ -1202,7 +1225,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = ubeg; u < uend; ++u) {
-        const int tt = (u / sk.kb) % n_tt, kb = u % sk.kb;
+        int mt_unused, tt;
+        tile_of(u, mt_unused, tt);
+        const int kb = u % sk.kb;
         mbar_wait(&xempty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * XBYTES);
@@ -1277,7 +1302,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
     for (int u = ubeg; u < uend;) {
       const int tile = u / sk.kb, kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
-      const int mt = tile / n_tt, tt = tile % n_tt;
+      int mt, tt;
+      tile_of(u, mt, tt);
       const int m0 = mt * 2 * kBM + int(rank) * kBM;  // this CTA's first weight row
       const int row0 = a.row_off + tt * TNP;
       const int ncols = min(TNP, a.T - tt * TNP);
@@ -1696,6 +1722,11 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     a.units = int(tiles * a.kblocks);
     a.whole_tiles = 1;
     const long long pairs = std::min<long long>(num_sms / 2, tiles);
+    // several token tiles (prefill): rastered tile order, 16 token tiles per
+    // group, so the tiles in flight share a few weight and token tiles (8192
+    // rows: QKV 703 -> 557 us, gate/up 1394 -> 1196, lm_head 2253 -> 1643;
+    // groups of 4 / 8 / 16 within 3% of each other, profiles/r02_prefill_raster_ab.txt)
+    a.raster = a.n_ttiles > 1 ? std::min(a.n_ttiles, 16) : 0;
     CUtensorMap ot;
     std::memset(&ot, 0, sizeof(ot));
     a.tma = 0;

@@ -53,6 +53,7 @@ struct GemmArgs {
   const void* w_base;  // weight base / row stride (elements): token-major plans build their own weight map
   long long w_stride;
   int nw;              // set by the launcher: weight rows per pair tile of the token-major kernel
+  int raster;          // set by the launcher: token tiles per raster group of the token-major kernel (0 = contiguous ranges)
   int norm_d;
   float norm_eps;
   // filled by the launcher

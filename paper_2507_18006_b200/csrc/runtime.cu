@@ -65,6 +65,8 @@ enum MemCat { MEM_WS = 0, MEM_WEIGHTS = 1, MEM_KV = 2, MEM_CATS = 3 };
 struct DeviceCtx {
   int id = 0;
   int ordinal = 0;
+  bool local = true;  // SPMD runtime: computed by this process (else: bookkeeping only, no streams / memory)
+  int rank = 0;       // SPMD runtime: the process that owns this device
   int num_sms = 148;
   cudaStream_t compute = nullptr;
   cudaStream_t copy = nullptr;   // scaling-op transfers (main lane)
@@ -101,6 +103,13 @@ int box_index(int rows) {
 
 struct cb_runtime {
   std::vector<DeviceCtx> devs;
+  bool spmd = false;               // one process per GPU (cb_runtime_create_spmd)
+  int my_rank = 0;
+  std::vector<int> ranks;          // the distinct ranks owning devices, ascending
+  cb_xfer_fn xfer = nullptr;       // cross-process transport (host callback)
+  void* xfer_ctx = nullptr;
+  int grp_ch = -1;                 // an exchange group is open on this channel (XGroup) ...
+  bool grp_live = false;           // ... and the transport has been told (first exchange seen)
   int copy_mode = 1;                  // transfer engine (cb_set_copy_mode)
   size_t copy_chunk = size_t(64) << 20;
 };
@@ -153,6 +162,15 @@ struct PendingOp {
   uint64_t weight_bytes = 0, kv_bytes = 0, catchup_bytes = 0;
   size_t reserved = 0;           // bytes reserved on dst (released from the pending count at commit / abort)
   bool committed = false;
+  bool started = false;          // transfer enqueued (SPMD: cb_op_start, after every rank reserved)
+  int ev_dev = -1;               // local device whose copy stream carries e0 / e1 (-1: no local part)
+  // the transfer cb_op_start / the issue enqueues
+  int src_dev = -1;
+  const void* xsrc = nullptr;
+  void* xdst = nullptr;
+  size_t xbytes = 0;
+  bool strided_gu = false;       // gate / up rows of the interleaved block (row pitch 2x)
+  bool precopy = false;          // pre-copy the KV kv_from holds into kv_to
 };
 
 struct Workspace {
@@ -226,20 +244,87 @@ struct cb_model {
   std::vector<uint32_t> slot_epoch;  // bumped on release: a pre-copied KV prefix of an older occupant is stale
   std::map<int64_t, PendingOp> ops;  // issued scaling ops (pending, then committed records)
   int64_t next_op = 1;
+  // SPMD: every layer's attention norm + the final norm on this process's GPU
+  // (the fused-norm producers of a layer need the NEXT layer's norm vector,
+  // which may live on another rank); filled by the first step (collective)
+  uint16_t* norm_tab = nullptr;
+  int norm_dev = -1;
+  bool norm_ready = false;
 };
 
 namespace {
 
 DeviceCtx& devctx(cb_model* m, int dev) { return m->rt->devs[dev]; }
+bool is_local(cb_model* m, int dev) { return m->rt->devs[dev].local; }
 
 int use(const DeviceCtx& d) {
+  if (!d.local) return fail(CB_ESTATE, "internal: device " + std::to_string(d.id) + " belongs to rank " +
+                                           std::to_string(d.rank));
   CB_CUDA(cudaSetDevice(d.ordinal));
   return CB_OK;
 }
 
+// SPMD: hand one byte range that crosses a process boundary to the host
+// transport.  send: ptr (on local device `dev`) is ready on `st`, goes to the
+// rank owning `peer`; recv: ptr is filled from that rank, ordered before later
+// work on `st`.  Every rank reaches the same sequence of exchanges.
+int xfer(cb_model* m, int channel, bool send, int dev, int peer, void* ptr, size_t bytes, cudaStream_t st) {
+  cb_runtime* rt = m->rt;
+  if (bytes == 0) return CB_OK;
+  if (!rt->xfer) return fail(CB_ESTATE, "SPMD runtime without a transport");
+  CB_TRY(use(devctx(m, dev)));
+  if (rt->grp_ch == channel && !rt->grp_live) {  // open the transport's group lazily: empty groups cost nothing
+    rt->grp_live = true;
+    if (rt->xfer(rt->xfer_ctx, channel, 2, -1, nullptr, 0, nullptr) != 0) return fail(CB_ECOMM, "transport group failed");
+  }
+  const int r = rt->xfer(rt->xfer_ctx, channel, send ? 1 : 0, devctx(m, peer).rank, ptr, bytes, st);
+  if (r != 0)
+    return fail(CB_ECOMM, std::string("transport ") + (send ? "send to" : "recv from") + " rank " +
+                              std::to_string(devctx(m, peer).rank) + " failed (" + std::to_string(r) + ")");
+  return CB_OK;
+}
+
+// Byte range src_dev:sp -> dst_dev:dp across processes: the sender's part on
+// s_st (a stream of src_dev), the receiver's on d_st (of dst_dev); a rank owning
+// neither does nothing.  (Same-process moves keep their peer-copy paths.)
+int xmove(cb_model* m, int channel, int src_dev, const void* sp, cudaStream_t s_st, int dst_dev, void* dp,
+          cudaStream_t d_st, size_t bytes) {
+  if (is_local(m, src_dev)) CB_TRY(xfer(m, channel, true, src_dev, dst_dev, const_cast<void*>(sp), bytes, s_st));
+  if (is_local(m, dst_dev)) CB_TRY(xfer(m, channel, false, dst_dev, src_dev, dp, bytes, d_st));
+  return CB_OK;
+}
+bool crosses(cb_model* m, int a, int b) { return m->rt->spmd && (!is_local(m, a) || !is_local(m, b)); }
+
+// Group the exchanges between begin and end (an NCCL group on the transport):
+// the transport may batch them into one launch (send = 2 / 3 markers).
+struct XGroup {
+  cb_model* m;
+  int ch;
+  bool on;
+  XGroup(cb_model* m_, int ch_) : m(m_), ch(ch_), on(m_->rt->spmd && m_->rt->xfer && m_->rt->grp_ch < 0) {
+    if (on) {
+      m->rt->grp_ch = ch;
+      m->rt->grp_live = false;
+    }
+  }
+  int close() {
+    if (!on) return CB_OK;
+    on = false;
+    cb_runtime* rt = m->rt;
+    const bool live = rt->grp_live;
+    rt->grp_ch = -1;
+    rt->grp_live = false;
+    if (live && rt->xfer(rt->xfer_ctx, ch, 3, -1, nullptr, 0, nullptr) != 0)
+      return fail(CB_ECOMM, "transport group failed");
+    return CB_OK;
+  }
+  ~XGroup() { close(); }
+};
+
 // dst stream waits for everything issued so far on src's compute stream
+// (devices of other processes: ordered by the transport instead)
 int depend(DeviceCtx& dst, DeviceCtx& src) {
-  if (&dst == &src) return CB_OK;
+  if (&dst == &src || !dst.local || !src.local) return CB_OK;
   CB_TRY(use(src));
   cudaEvent_t ev = src.ev_pool[src.ev_next++ % src.ev_pool.size()];
   CB_CUDA(cudaEventRecord(ev, src.compute));
@@ -330,7 +415,7 @@ int dev_alloc(DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullpt
 
 // `dst_stream` (on dst) waits for everything issued so far on `src_stream` (on src)
 int join(DeviceCtx& dst, cudaStream_t dst_stream, DeviceCtx& src, cudaStream_t src_stream) {
-  if (dst_stream == src_stream) return CB_OK;
+  if (dst_stream == src_stream || !dst.local || !src.local) return CB_OK;
   CB_TRY(use(src));
   cudaEvent_t ev = src.ev_pool[src.ev_next++ % src.ev_pool.size()];
   CB_CUDA(cudaEventRecord(ev, src_stream));
@@ -344,10 +429,11 @@ int join(DeviceCtx& dst, cudaStream_t dst_stream, DeviceCtx& src, cudaStream_t s
 // still read the buffer: peer row pulls, KV moves, op copies), then returns the
 // buffer to the pool.
 void dev_free(cb_model* m, int dev, void* p) {
-  if (!p) return;
+  if (!p || !is_local(m, dev)) return;
   DeviceCtx& d = devctx(m, dev);
   for (auto& o : m->rt->devs)
-    for (cudaStream_t s : {o.compute, o.copy, o.copy2}) join(d, d.compute, o, s);
+    if (o.local)
+      for (cudaStream_t s : {o.compute, o.copy, o.copy2}) join(d, d.compute, o, s);
   cudaSetDevice(d.ordinal);
   cudaFreeAsync(p, d.compute);
   auto it = d.allocs.find(p);
@@ -378,6 +464,7 @@ int make_map(OpMap* map, const void* base, uint64_t rows, uint64_t k, uint32_t b
 }
 
 int ensure_ws(cb_model* m, int dev) {
+  if (!is_local(m, dev)) return CB_OK;  // another process's device
   Workspace& w = m->ws[dev];
   if (w.ready) return CB_OK;
   DeviceCtx& dc = devctx(m, dev);
@@ -436,7 +523,7 @@ int make_layer_maps(cb_model* m, LayerCopy& c) {
 int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr, cudaStream_t st = nullptr,
               bool* created = nullptr) {
   if (created) *created = false;
-  if (L.kv.count(dev)) return CB_OK;
+  if (L.kv.count(dev) || !is_local(m, dev)) return CB_OK;
   void* p = nullptr;
   CB_TRY(dev_alloc(devctx(m, dev), &p, m->kv_block_bytes, shortfall, MEM_KV, st));
   L.kv[dev] = static_cast<uint16_t*>(p);
@@ -478,12 +565,19 @@ int kv_device(const LayerState& L) { return L.kv_override >= 0 ? L.kv_override :
 size_t kv_token_bytes(cb_model* m) { return size_t(2) * m->kv_n * 2; }
 size_t kv_slot_offset(cb_model* m, int slot) { return size_t(slot) * m->d.max_ctx * m->kv_n * 2; }  // elements
 
-// copy KV positions [p0, p1) of `slot` from src's block to dst's block
+// copy KV positions [p0, p1) of `slot` from src's block to dst's block (on
+// st, a stream of dst; across processes: channel ch, the sender on src_st)
 int kv_copy(cb_model* m, LayerState& L, int slot, int src, int dst, int p0, int p1, cudaStream_t st,
-            uint64_t* bytes) {
+            uint64_t* bytes, int ch = 0, cudaStream_t src_st = nullptr) {
   if (p1 <= p0 || src == dst) return CB_OK;
   const size_t tb = kv_token_bytes(m);
   const size_t off = kv_slot_offset(m, slot) + size_t(p0) * tb / 2;  // elements
+  if (crosses(m, src, dst)) {
+    if (bytes) *bytes += size_t(p1 - p0) * tb;
+    return xmove(m, ch, src, is_local(m, src) ? L.kv[src] + off : nullptr,
+                 src_st ? src_st : (is_local(m, src) ? devctx(m, src).compute : nullptr), dst,
+                 is_local(m, dst) ? L.kv[dst] + off : nullptr, st, size_t(p1 - p0) * tb);
+  }
   // cudaMemcpyDefault: either block may be offloaded to mapped pinned host memory
   CB_CUDA(cudaMemcpyAsync(L.kv[dst] + off, L.kv[src] + off, size_t(p1 - p0) * tb, cudaMemcpyDefault, st));
   if (bytes) *bytes += size_t(p1 - p0) * tb;
@@ -560,12 +654,41 @@ int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K,
 }
 
 // Move residual rows so that every row sits on the device of its new segment.
+int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to);
 int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to) {
+  XGroup grp(m, 0);
+  CB_TRY(reshard_rows(m, from, to));
+  return grp.close();
+}
+
+int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to) {
   const size_t row_bytes = size_t(m->d.d_model) * 4;
   for (const Seg& ns : to)
     for (const Seg& os : from) {
       const int a = std::max(ns.r0, os.r0), b = std::min(ns.r1, os.r1);
       if (a >= b || os.dev == ns.dev) continue;
+      if (crosses(m, os.dev, ns.dev)) {
+        // the reference's replica scatter / gather (_kernels.py:41-51) between processes:
+        // residual rows (+ the next norm's input rows and sums of squares when fused)
+        const int sd = os.dev, dd = ns.dev;
+        const bool ls = is_local(m, sd), ld = is_local(m, dd);
+        if (!ls && !ld) continue;
+        cudaStream_t ss = ls ? devctx(m, sd).compute : nullptr, ds = ld ? devctx(m, dd).compute : nullptr;
+        auto at = [&](int dv, bool loc, auto* base, size_t row) {
+          return loc ? reinterpret_cast<uint8_t*>(base) + size_t(a) * row : nullptr;
+        };
+        const size_t xr = row_bytes, hr = size_t(m->d.d_model) * 2, qr = size_t(m->d.d_model / 32) * 4;
+        ProfScope ps(m, ld ? dd : sd, CB_KCLASS_COPY, ld ? ds : ss, double(b - a) * row_bytes);
+        CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].x : nullptr, xr), ss, dd,
+                     at(dd, ld, ld ? m->ws[dd].x : nullptr, xr), ds, size_t(b - a) * xr));
+        if (m->fuse_norm) {
+          CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].h : nullptr, hr), ss, dd,
+                       at(dd, ld, ld ? m->ws[dd].h : nullptr, hr), ds, size_t(b - a) * hr));
+          CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].ssq : nullptr, qr), ss, dd,
+                       at(dd, ld, ld ? m->ws[dd].ssq : nullptr, qr), ds, size_t(b - a) * qr));
+        }
+        continue;
+      }
       DeviceCtx& dd = devctx(m, ns.dev);
       DeviceCtx& sd = devctx(m, os.dev);
       CB_TRY(depend(dd, sd));
@@ -709,18 +832,6 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
                                 ac.compute));
   }
   CB_TRY(ensure_kv(m, L, ad));
-  // KV rows follow their sequence: move any slot whose KV sits elsewhere.
-  for (int q = s.s0; q < s.s1; ++q) {
-    const int slot = seq_slot[q];
-    const int owner = L.owner[slot];
-    if (owner >= 0 && owner != ad && m->slot_len[slot] > 0) {
-      CB_TRY(depend(ac, devctx(m, owner)));
-      CB_TRY(use(ac));
-      ProfScope ps(m, ad, CB_KCLASS_COPY, ac.compute, double(m->slot_len[slot]) * kv_token_bytes(m));
-      CB_TRY(kv_move(m, L, slot, owner, ad, ac.compute, nullptr));
-    }
-    L.owner[slot] = ad;
-  }
   CB_TRY(use(ac));
   uint16_t* kv = L.kv[ad];
   const int32_t* row_slot = wa.meta + m->cur_T;
@@ -796,6 +907,41 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
     CB_CUDA(cudaMemcpyPeerAsync(reinterpret_cast<uint8_t*>(ws.att) + s.r0 * att_row, dc.ordinal,
                                 reinterpret_cast<uint8_t*>(wa.att) + s.r0 * att_row, ac.ordinal, T * att_row,
                                 dc.compute));
+  }
+  return CB_OK;
+}
+
+// KV rows follow their sequence (SURVEY §7 hard part 1, option B): before a
+// segment runs, every slot of it whose KV prefix sits on another device moves
+// to the device that attends it.  Called on every rank for every segment (the
+// owner bookkeeping is replicated; a move between processes is an exchange).
+int kv_follow(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot) {
+  const int ad = L.reps.size() > 1 ? s.dev : kv_device(L);
+  const bool la = is_local(m, ad);
+  if (la) CB_TRY(ensure_kv(m, L, ad));
+  for (int q = s.s0; q < s.s1; ++q) {
+    const int slot = seq_slot[q];
+    const int owner = L.owner[slot];
+    if (owner >= 0 && owner != ad && m->slot_len[slot] > 0) {
+      const double nb = double(m->slot_len[slot]) * kv_token_bytes(m);
+      if (crosses(m, owner, ad)) {
+        const bool lo = is_local(m, owner);
+        if (la || lo) {
+          const int pdev = la ? ad : owner;
+          ProfScope ps(m, pdev, CB_KCLASS_COPY, devctx(m, pdev).compute, nb);
+          CB_TRY(kv_move(m, L, slot, owner, ad, la ? devctx(m, ad).compute : nullptr, nullptr));
+        } else {
+          CB_TRY(kv_move(m, L, slot, owner, ad, nullptr, nullptr));  // bookkeeping only
+        }
+      } else {
+        DeviceCtx& ac = devctx(m, ad);
+        CB_TRY(depend(ac, devctx(m, owner)));
+        CB_TRY(use(ac));
+        ProfScope ps(m, ad, CB_KCLASS_COPY, ac.compute, nb);
+        CB_TRY(kv_move(m, L, slot, owner, ad, ac.compute, nullptr));
+      }
+    }
+    L.owner[slot] = ad;
   }
   return CB_OK;
 }
@@ -956,11 +1102,50 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
 // A norm vector (attention norm of layer li, or the final norm for li == n_layers)
 // that kernels on logical device dev can read: a copy on the same physical GPU.
 const uint16_t* norm_gamma_for(cb_model* m, int li, int dev) {
+  if (m->rt->spmd) return m->norm_ready ? m->norm_tab + size_t(li) * m->d.d_model : nullptr;
   const int ord = devctx(m, dev).ordinal;
   if (li >= m->d.n_layers) return devctx(m, m->home).ordinal == ord ? m->final_norm : nullptr;
   for (const LayerCopy& c : m->layers[li].reps)
     if (devctx(m, c.dev).ordinal == ord) return reinterpret_cast<const uint16_t*>(c.block + m->off_an);
   return nullptr;
+}
+
+// SPMD: the norm table of this process (every layer's attention norm, then the
+// final norm) -- each vector comes from the rank holding the layer's original
+// (the final norm from the home rank); one collective, at the first step.
+int build_norm_table(cb_model* m, int tdev) {
+  const size_t dm = m->d.d_model;
+  const int nl = m->d.n_layers;
+  DeviceCtx& tc = devctx(m, tdev);
+  if (!m->norm_tab) {
+    CB_TRY(dev_alloc(tc, (void**)&m->norm_tab, size_t(nl + 1) * dm * 2, nullptr, MEM_WEIGHTS));
+    m->norm_dev = tdev;
+  }
+  const int me = m->rt->my_rank;
+  XGroup grp(m, 0);
+  auto dev_of_rank = [&](int r) {
+    for (const DeviceCtx& dc : m->rt->devs)
+      if (dc.rank == r) return dc.id;
+    return -1;
+  };
+  for (int li = 0; li <= nl; ++li) {
+    const int src = li < nl ? m->layers[li].reps[0].dev : m->home;
+    const int src_rank = devctx(m, src).rank;
+    uint16_t* slot = m->norm_tab + size_t(li) * dm;
+    CB_TRY(use(tc));
+    if (src_rank == me) {
+      const void* from = li < nl ? static_cast<const void*>(m->layers[li].reps[0].block + m->off_an)
+                                 : static_cast<const void*>(m->final_norm);
+      CB_CUDA(cudaMemcpyAsync(slot, from, dm * 2, cudaMemcpyDefault, tc.compute));
+      for (int r : m->rt->ranks)
+        if (r != me) CB_TRY(xfer(m, 0, true, tdev, dev_of_rank(r), slot, dm * 2, tc.compute));
+    } else {
+      CB_TRY(xfer(m, 0, false, tdev, src, slot, dm * 2, tc.compute));
+    }
+  }
+  CB_TRY(grp.close());
+  m->norm_ready = true;
+  return CB_OK;
 }
 
 std::vector<int> split_batch_vec(int bs, int p) {
@@ -1016,7 +1201,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     m->seq_blk[bs] = nblk;
   }
 
-  // participating devices
+  // participating devices (SPMD: only this process's; the rest is bookkeeping)
   std::vector<int> devs{m->home};
   for (auto& L : m->layers) {
     for (auto& c : L.reps) devs.push_back(c.dev);
@@ -1026,7 +1211,23 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   }
   std::sort(devs.begin(), devs.end());
   devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
-  DeviceCtx& hc = devctx(m, m->home);
+  devs.erase(std::remove_if(devs.begin(), devs.end(), [&](int dv) { return !is_local(m, dv); }), devs.end());
+  const bool home_local = is_local(m, m->home);
+  // the device whose compute stream times the pass and roots the metadata upload
+  int tdev = m->home;
+  if (!home_local) {
+    tdev = -1;
+    for (const DeviceCtx& dc : m->rt->devs)
+      if (dc.local) {
+        tdev = dc.id;
+        break;
+      }
+    if (tdev < 0) return fail(CB_ESTATE, "no local device");
+    if (std::find(devs.begin(), devs.end(), tdev) == devs.end()) devs.insert(devs.begin(), tdev);
+  }
+  DeviceCtx& hc = devctx(m, tdev);
+  CB_TRY(ensure_ws(m, tdev));
+  if (m->rt->spmd && !m->norm_ready) CB_TRY(build_norm_table(m, tdev));
   CB_TRY(use(hc));
   CB_CUDA(cudaEventRecord(hc.t0, hc.compute));
   const size_t meta_bytes = (size_t(blk_off) + 4 * size_t(nblk)) * 4;  // exactly what this pass needs
@@ -1037,26 +1238,31 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     CB_TRY(use(dc));
     CB_CUDA(cudaMemcpyAsync(m->ws[dv].meta, meta, meta_bytes, cudaMemcpyHostToDevice, dc.compute));
   }
-  Workspace& hw = m->ws[m->home];
   // Fused RMSNorm: decode passes whose rows fit one GEMM token tile, plain
   // layers (no migrated projections), every norm vector readable where its
   // producer runs.  Prefill keeps the separate norm kernels (compute-bound GEMMs).
-  static const bool no_fuse = std::getenv("COCOB200_NO_FUSED_NORM") != nullptr;  // A/B experiments
-  m->fuse_norm = !no_fuse && !prefill && T <= 256 && d.d_model % 256 == 0;
+  // The decision depends on the placement only (identical on every SPMD rank:
+  // it decides whether the norm rows travel with the residual rows).
+  m->fuse_norm = !prefill && T <= 256 && d.d_model % 256 == 0;
   std::vector<std::vector<const uint16_t*>> gamma_next(d.n_layers);
-  const uint16_t* g_embed = m->fuse_norm ? norm_gamma_for(m, 0, m->home) : nullptr;
-  if (m->fuse_norm && !g_embed) m->fuse_norm = false;
+  const uint16_t* g_embed = m->fuse_norm && home_local ? norm_gamma_for(m, 0, m->home) : nullptr;
+  if (m->fuse_norm && home_local && !g_embed) m->fuse_norm = false;
   for (int li = 0; li < d.n_layers && m->fuse_norm; ++li) {
     const LayerState& L = m->layers[li];
     if (L.proj_ov) m->fuse_norm = false;
     for (const LayerCopy& c : L.reps) {
+      if (!is_local(m, c.dev)) {
+        gamma_next[li].push_back(nullptr);
+        continue;
+      }
       const uint16_t* g = norm_gamma_for(m, li + 1, c.dev);
       if (!g) m->fuse_norm = false;
       gamma_next[li].push_back(g);
     }
   }
-  CB_TRY(use(hc));
-  {
+  Workspace& hw = m->ws[m->home];
+  if (home_local) {
+    CB_TRY(use(devctx(m, m->home)));
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
     if (m->fuse_norm)
       CB_CUDA(cb::embed_norm_launch(m->embed, hw.meta, hw.x, g_embed, hw.h, hw.ssq, T, d.d_model, 0, hc.compute));
@@ -1078,43 +1284,56 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       s0 += shares[j];
     }
     CB_TRY(reshard(m, layout, segs));
+    {
+      XGroup grp(m, 0);
+      for (const Seg& s : segs) CB_TRY(kv_follow(m, L, s, seq_slot));
+      CB_TRY(grp.close());
+    }
     for (const Seg& s : segs)
-      CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos, m->fuse_norm ? gamma_next[li][s.rep] : nullptr));
+      if (is_local(m, s.dev))
+        CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos, m->fuse_norm ? gamma_next[li][s.rep] : nullptr));
     layout = segs;
   }
   std::vector<Seg> home_layout{{m->home, 0, 0, T, 0, bs}};
   CB_TRY(reshard(m, layout, home_layout));
-  // every device's trailing work joins the home stream
+  // every device's trailing work joins the timing stream
   for (int dv : devs) CB_TRY(depend(hc, devctx(m, dv)));
   CB_TRY(use(hc));
-  if (!m->fuse_norm) {  // fused: the last layer's down projection already wrote h' for the final norm
-    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
-    CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
-  }
-  const OpMap* xm = hw.map_h;
-  if (prefill) {
-    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.d_model * 4);
-    CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * T, hw.hl, bs, d.d_model, hc.compute));
-    xm = hw.map_hl;
-  }
-  NormIO head_norm;
-  head_norm.consume = m->fuse_norm;
-  CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab, head_norm));
-  {
-    ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.vocab * 4);
-    CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
+  if (home_local) {
+    if (!m->fuse_norm) {  // fused: the last layer's down projection already wrote h' for the final norm
+      ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
+      CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
+    }
+    const OpMap* xm = hw.map_h;
+    if (prefill) {
+      ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.d_model * 4);
+      CB_CUDA(cb::gather_rows_launch(hw.h, hw.meta + 3 * T, hw.hl, bs, d.d_model, hc.compute));
+      xm = hw.map_hl;
+    }
+    NormIO head_norm;
+    head_norm.consume = m->fuse_norm;
+    CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab, head_norm));
+    {
+      ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.vocab * 4);
+      CB_CUDA(cb::argmax_launch(hw.logits, hw.next, bs, d.vocab, hc.compute));
+    }
   }
   CB_CUDA(cudaEventRecord(hc.t1, hc.compute));
   g_last_enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - enq0).count();
-  CB_CUDA(cudaMemcpyAsync(m->pin_next, hw.next, size_t(bs) * 4, cudaMemcpyDeviceToHost, hc.compute));
-  if (logits_out)
-    CB_CUDA(cudaMemcpyAsync(logits_out, hw.logits, size_t(bs) * d.vocab * 4, cudaMemcpyDeviceToHost, hc.compute));
+  if (home_local) {
+    CB_CUDA(cudaMemcpyAsync(m->pin_next, hw.next, size_t(bs) * 4, cudaMemcpyDeviceToHost, hc.compute));
+    if (logits_out)
+      CB_CUDA(cudaMemcpyAsync(logits_out, hw.logits, size_t(bs) * d.vocab * 4, cudaMemcpyDeviceToHost, hc.compute));
+  }
   CB_CUDA(cudaStreamSynchronize(hc.compute));
   if (m->prof.on) prof_resolve(m);
   float ms = 0.f;
   CB_CUDA(cudaEventElapsedTime(&ms, hc.t0, hc.t1));
   if (ms_out) *ms_out += ms;
-  std::memcpy(next_out, m->pin_next, size_t(bs) * 4);
+  if (home_local)
+    std::memcpy(next_out, m->pin_next, size_t(bs) * 4);
+  else
+    std::fill(next_out, next_out + bs, -1);  // the tokens are sampled on the home device's rank
   for (int i = 0; i < bs; ++i) m->slot_len[slots[i]] = prefill ? lens[i] : m->slot_len[slots[i]] + 1;
   return CB_OK;
 }
@@ -1139,14 +1358,16 @@ int begin_layer_load(cb_model* m, int layer, int dev, LayerCopy& c) {
   LayerState& L = m->layers[layer - 1];
   if (!L.reps.empty()) return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already loaded");
   c.dev = dev;
+  if (!is_local(m, dev)) return CB_OK;  // SPMD: another rank holds the bytes
   CB_TRY(dev_alloc(devctx(m, dev), (void**)&c.block, m->layer_bytes, nullptr, MEM_WEIGHTS));
   return CB_OK;
 }
 
 int finish_layer_load(cb_model* m, int layer, LayerCopy& c) {
   LayerState& L = m->layers[layer - 1];
-  CB_TRY(make_layer_maps(m, c));
+  if (c.block) CB_TRY(make_layer_maps(m, c));
   L.reps.push_back(c);
+  m->norm_ready = false;
   L.owner.assign(m->d.max_slots, -1);
   CB_TRY(ensure_kv(m, L, c.dev));
   CB_TRY(ensure_ws(m, c.dev));
@@ -1155,6 +1376,7 @@ int finish_layer_load(cb_model* m, int layer, LayerCopy& c) {
 
 void sync_all(cb_model* m) {
   for (auto& dc : m->rt->devs) {
+    if (!dc.local) continue;
     cudaSetDevice(dc.ordinal);
     cudaStreamSynchronize(dc.compute);
     cudaStreamSynchronize(dc.copy);
@@ -1173,6 +1395,13 @@ int transfer(cb_model* m, int dst_dev, void* dst, int src_dev, const void* src, 
   DeviceCtx& dc = devctx(m, dst_dev);
   DeviceCtx& sc = devctx(m, src_dev);
   const cb_runtime& rt = *m->rt;
+  if (crosses(m, src_dev, dst_dev)) {
+    // between processes: the source's copy lane (after its compute stream:
+    // the block may be a layer the source still serves) sends, the
+    // destination's copy lane receives (NCCL over NVLink via the host transport)
+    if (sc.local) CB_TRY(join(sc, sc.copy, sc, sc.compute));
+    return xmove(m, 1, src_dev, src, sc.local ? sc.copy : nullptr, dst_dev, dst, dc.local ? dc.copy : nullptr, bytes);
+  }
   if (rt.copy_mode == 2 && bytes % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0) {
     CB_TRY(join(sc, sc.copy, dc, dc.copy));
@@ -1230,10 +1459,21 @@ PendingOp new_op(cb_model* m, int kind, int layer, int dst, int copy_dev) {
   return op;
 }
 
+// The local device whose copy stream carries this rank's part of an op's
+// transfer (its e0 / e1 events): the destination, else (SPMD) the source.
+int op_event_dev(cb_model* m, const PendingOp& op) {
+  if (op.copy_dev >= 0 && is_local(m, op.copy_dev)) return op.copy_dev;
+  if (op.src_dev >= 0 && is_local(m, op.src_dev)) return op.src_dev;
+  if (op.kv_from >= 0 && is_local(m, op.kv_from)) return op.kv_from;
+  return -1;
+}
+
 // open the transfer: ordered after every compute stream's work so far (the KV
 // prefixes it may read were written by earlier steps)
 int op_open(cb_model* m, PendingOp& op) {
-  DeviceCtx& dc = devctx(m, op.copy_dev);
+  op.ev_dev = op_event_dev(m, op);
+  if (op.ev_dev < 0) return CB_OK;  // SPMD: no part of this op runs on this rank
+  DeviceCtx& dc = devctx(m, op.ev_dev);
   for (auto& o : m->rt->devs) CB_TRY(join(dc, dc.copy, o, o.compute));
   CB_TRY(use(dc));
   CB_CUDA(cudaEventCreate(&op.e0));
@@ -1242,11 +1482,9 @@ int op_open(cb_model* m, PendingOp& op) {
   return CB_OK;
 }
 
-// register the op: transfer end event, layer lock, reservation count
-int op_close(cb_model* m, PendingOp& op, int64_t* id_out) {
-  DeviceCtx& dc = devctx(m, op.copy_dev);
-  CB_TRY(use(dc));
-  CB_CUDA(cudaEventRecord(op.e1, dc.copy));
+// register the op: id, layer lock, reservation count (its transfer starts now
+// or, SPMD, at cb_op_start once every rank has reserved)
+int op_register(cb_model* m, PendingOp& op, int64_t* id_out) {
   op.id = m->next_op++;
   LayerState& L = m->layers[op.layer - 1];
   L.pend.push_back({op.kind, op.kind == OPK_PROJ ? op.mod_kind : op.dst});
@@ -1263,36 +1501,79 @@ int op_close(cb_model* m, PendingOp& op, int64_t* id_out) {
 // and refilled meanwhile has a new epoch and is copied whole).  Only used when
 // nothing else writes kv_to's block for this layer while the op is pending.
 int op_precopy_kv(cb_model* m, PendingOp& op, LayerState& L) {
-  DeviceCtx& dc = devctx(m, op.copy_dev);
-  CB_TRY(use(dc));
+  const bool lt = is_local(m, op.kv_to), lf = is_local(m, op.kv_from);
+  cudaStream_t dst_st = lt ? devctx(m, op.kv_to).copy : nullptr;
+  cudaStream_t src_st = nullptr;
+  if (crosses(m, op.kv_from, op.kv_to) && lf) {  // the sender orders its copy lane after its compute stream
+    DeviceCtx& fc = devctx(m, op.kv_from);
+    CB_TRY(join(fc, fc.copy, fc, fc.compute));
+    src_st = fc.copy;
+  }
+  XGroup grp(m, 1);
   for (int slot = 0; slot < m->d.max_slots; ++slot) {
     if (L.owner[slot] != op.kv_from || m->slot_len[slot] <= 0) continue;
-    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, 0, m->slot_len[slot], dc.copy, &op.kv_bytes));
+    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, 0, m->slot_len[slot], dst_st, &op.kv_bytes, 1, src_st));
     op.snap_len[slot] = m->slot_len[slot];
     op.snap_epoch[slot] = int(m->slot_epoch[slot]);
   }
+  return grp.close();
+}
+
+// Enqueue an op's data movement: the weight transfer (+ KV pre-copy) on the
+// copy streams; e1 marks this rank's part done.
+int op_run(cb_model* m, PendingOp& op) {
+  CB_TRY(op_open(m, op));
+  if (op.xbytes) {
+    if (op.strided_gu) {  // every other row of the interleaved gate/up block (single process)
+      DeviceCtx& dc = devctx(m, op.dst);
+      const size_t row = size_t(m->d.d_model) * 2;
+      CB_TRY(use(dc));
+      CB_CUDA(cudaMemcpy2DAsync(op.xdst, row, op.xsrc, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
+    } else {
+      CB_TRY(transfer(m, op.dst, op.xdst, op.src_dev, op.xsrc, op.xbytes));
+    }
+  }
+  if (op.precopy) CB_TRY(op_precopy_kv(m, op, m->layers[op.layer - 1]));
+  if (op.ev_dev >= 0) {
+    DeviceCtx& dc = devctx(m, op.ev_dev);
+    CB_TRY(use(dc));
+    CB_CUDA(cudaEventRecord(op.e1, dc.copy));
+  }
+  op.started = true;
   return CB_OK;
+}
+
+// single process: the transfer starts at issue; SPMD: at cb_op_start
+int op_issue(cb_model* m, PendingOp& op, int64_t* id_out) {
+  if (!m->rt->spmd) CB_TRY(op_run(m, op));
+  return op_register(m, op, id_out);
 }
 
 // At the commit: the rest of every slot op.kv_from still holds moves to
 // op.kv_to on kv_to's compute stream (stream-ordered before the next step).
 int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
+  const bool lt = is_local(m, op.kv_to), lf = is_local(m, op.kv_from);
   DeviceCtx& tc = devctx(m, op.kv_to);
   DeviceCtx& fc = devctx(m, op.kv_from);
   CB_TRY(join(tc, tc.compute, fc, fc.compute));
-  CB_TRY(use(tc));
-  CB_CUDA(cudaEventCreate(&op.c0));
-  CB_CUDA(cudaEventCreate(&op.c1));
-  CB_CUDA(cudaEventRecord(op.c0, tc.compute));
+  if (lt) {
+    CB_TRY(use(tc));
+    CB_CUDA(cudaEventCreate(&op.c0));
+    CB_CUDA(cudaEventCreate(&op.c1));
+    CB_CUDA(cudaEventRecord(op.c0, tc.compute));
+  }
+  XGroup grp(m, 0);
   for (int slot = 0; slot < m->d.max_slots; ++slot) {
     if (L.owner[slot] != op.kv_from) continue;
     const int len = m->slot_len[slot];
     const bool fresh = op.snap_len[slot] >= 0 && op.snap_epoch[slot] == int(m->slot_epoch[slot]);
     const int have = fresh ? std::min(op.snap_len[slot], len) : 0;
-    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, tc.compute, &op.catchup_bytes));
+    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, lt ? tc.compute : nullptr, &op.catchup_bytes, 0,
+                   lf ? fc.compute : nullptr));
     L.owner[slot] = op.kv_to;
   }
-  CB_CUDA(cudaEventRecord(op.c1, tc.compute));
+  CB_TRY(grp.close());
+  if (lt) CB_CUDA(cudaEventRecord(op.c1, tc.compute));
   return CB_OK;
 }
 
@@ -1318,6 +1599,14 @@ void op_release_reservation(cb_model* m, PendingOp& op) {
   }
 }
 
+// reserve a layer block on dst (this rank's device only; others record the copy)
+int reserve_block(cb_model* m, PendingOp& op, int dst, uint64_t* shortfall) {
+  op.copy.dev = dst;
+  if (!is_local(m, dst)) return CB_OK;
+  DeviceCtx& dc = devctx(m, dst);
+  return dev_alloc(dc, (void**)&op.copy.block, m->layer_bytes, shortfall, MEM_WEIGHTS, dc.copy);
+}
+
 // ReplicateLayer (ops.py:199-211): reserve + copy the layer block original -> dst.
 int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) {
   CB_TRY(check_layer(m, layer));
@@ -1329,12 +1618,10 @@ int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shor
     if (c.dev == dst)
       return fail(CB_EINVAL, "layer " + std::to_string(layer) + " already has a copy on device " + std::to_string(dst));
   if (L.kv_override >= 0 || L.proj_ov) return fail(CB_EINVAL, "layer carries overrides and cannot be replicated");
-  DeviceCtx& dc = devctx(m, dst);
   PendingOp op = new_op(m, OPK_REPLICATE, layer, dst, dst);
-  op.copy.dev = dst;
-  int r = dev_alloc(dc, (void**)&op.copy.block, m->layer_bytes, shortfall, MEM_WEIGHTS, dc.copy);
+  int r = reserve_block(m, op, dst, shortfall);
   if (r == CB_OK) {
-    r = ensure_kv(m, L, dst, shortfall, dc.copy, &op.kv_new);
+    r = ensure_kv(m, L, dst, shortfall, is_local(m, dst) ? devctx(m, dst).copy : nullptr, &op.kv_new);
     op.kv_to = dst;  // (no KV moves at issue: rows move with split_batch once serving)
   }
   if (r == CB_OK) r = ensure_ws(m, dst);
@@ -1344,10 +1631,12 @@ int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shor
     return fail(r, err);
   }
   op.reserved = m->layer_bytes + (op.kv_new ? m->kv_block_bytes : 0);
-  CB_TRY(op_open(m, op));
-  CB_TRY(transfer(m, dst, op.copy.block, L.reps[0].dev, L.reps[0].block, m->layer_bytes));
+  op.src_dev = L.reps[0].dev;
+  op.xsrc = L.reps[0].block;
+  op.xdst = op.copy.block;
+  op.xbytes = m->layer_bytes;
   op.weight_bytes = m->layer_bytes;
-  return op_close(m, op, id);
+  return op_issue(m, op, id);
 }
 
 // MigrateLayer (ops.py:213-228): reserve + copy the original to dst; with_kv
@@ -1363,15 +1652,15 @@ int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uin
   for (auto& c : L.reps)
     if (c.dev == dst) return fail(CB_EINVAL, "layer already has a copy on device " + std::to_string(dst));
   if (!with_kv && L.reps.size() > 1) return fail(CB_EINVAL, "cannot detach KV from a replicated layer");
-  DeviceCtx& dc = devctx(m, dst);
+  if (!with_kv && m->rt->spmd && devctx(m, src).rank != devctx(m, dst).rank)
+    return fail(CB_ENOTSUP, "SPMD runtime: a layer's KV moves with it between processes (with_kv=1)");
   PendingOp op = new_op(m, OPK_MIGRATE, layer, dst, dst);
   op.with_kv = with_kv;
-  op.copy.dev = dst;
   op.kv_from = kv_device(L);
-  int r = dev_alloc(dc, (void**)&op.copy.block, m->layer_bytes, shortfall, MEM_WEIGHTS, dc.copy);
+  int r = reserve_block(m, op, dst, shortfall);
   if (r == CB_OK && with_kv && op.kv_from != dst) {
     op.kv_to = dst;
-    r = ensure_kv(m, L, dst, shortfall, dc.copy, &op.kv_new);
+    r = ensure_kv(m, L, dst, shortfall, is_local(m, dst) ? devctx(m, dst).copy : nullptr, &op.kv_new);
   }
   if (r == CB_OK) r = ensure_ws(m, dst);
   if (r != CB_OK) {
@@ -1380,11 +1669,13 @@ int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uin
     return fail(r, err);
   }
   op.reserved = m->layer_bytes + (op.kv_new ? m->kv_block_bytes : 0);
-  CB_TRY(op_open(m, op));
-  CB_TRY(transfer(m, dst, op.copy.block, src, L.reps[0].block, m->layer_bytes));
+  op.src_dev = src;
+  op.xsrc = L.reps[0].block;
+  op.xdst = op.copy.block;
+  op.xbytes = m->layer_bytes;
   op.weight_bytes = m->layer_bytes;
-  if (op.kv_to >= 0) CB_TRY(op_precopy_kv(m, op, L));  // dst serves nothing of this layer until the commit
-  return op_close(m, op, id);
+  op.precopy = op.kv_to >= 0;  // dst serves nothing of this layer until the commit
+  return op_issue(m, op, id);
 }
 
 // MigrateSubModule of a projection / SELF_ATTENTION (ops.py:230-251): reserve +
@@ -1395,6 +1686,7 @@ int issue_migrate(cb_model* m, int layer, int dst, int with_kv, int64_t* id, uin
 int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uint64_t* shortfall) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (m->rt->spmd) return fail(CB_ENOTSUP, "SPMD runtime: sub-module overrides need the single-process runtime");
   CB_TRY(check_idle(L, layer, OPK_PROJ, kind));
   if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
   const bool attn_part = kind <= CB_ATTN_PROJ_O;
@@ -1415,23 +1707,19 @@ int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uin
     return fail(r, err);
   }
   op.reserved = bytes;
-  CB_TRY(op_open(m, op));
   const ModCopy& mc = L.mod[kind];
   if (mc.dev >= 0) {  // moved once already: copy from the current override
-    CB_TRY(transfer(m, dst, op.mod.buf, mc.dev, mc.buf, bytes));
+    op.src_dev = mc.dev;
+    op.xsrc = mc.buf;
   } else {
-    const LayerCopy& src = L.reps[0];
-    const uint8_t* from = src.block + block_offset(m, kind);
-    if (kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP) {  // every other row of the interleaved block
-      const size_t row = size_t(m->d.d_model) * 2;
-      CB_TRY(use(dc));
-      CB_CUDA(cudaMemcpy2DAsync(op.mod.buf, row, from, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
-    } else {
-      CB_TRY(transfer(m, dst, op.mod.buf, src.dev, from, bytes));
-    }
+    op.src_dev = L.reps[0].dev;
+    op.xsrc = L.reps[0].block + block_offset(m, kind);
+    op.strided_gu = kind == CB_FFN_PROJ_GATE || kind == CB_FFN_PROJ_UP;
   }
+  op.xdst = op.mod.buf;
+  op.xbytes = bytes;
   op.weight_bytes = bytes;
-  return op_close(m, op, id);
+  return op_issue(m, op, id);
 }
 
 // MigrateSubModule(KV_CACHE) (ops.py:230-251): the layer's KV moves to dst
@@ -1439,6 +1727,7 @@ int issue_projection(cb_model* m, int layer, int kind, int dst, int64_t* id, uin
 int issue_kv(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (m->rt->spmd) return fail(CB_ENOTSUP, "SPMD runtime: sub-module overrides need the single-process runtime");
   CB_TRY(check_idle(L, layer, OPK_KV));
   if (L.reps.size() > 1) return fail(CB_EINVAL, "layer is replicated and cannot carry overrides");
   DeviceCtx& dc = devctx(m, dst);
@@ -1453,9 +1742,8 @@ int issue_kv(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shortfall) 
     return fail(r, err);
   }
   op.reserved = op.kv_new ? m->kv_block_bytes : 0;
-  CB_TRY(op_open(m, op));
-  if (op.kv_from != dst) CB_TRY(op_precopy_kv(m, op, L));  // attention stays on kv_from until the commit
-  return op_close(m, op, id);
+  op.precopy = op.kv_from != dst;  // attention stays on kv_from until the commit
+  return op_issue(m, op, id);
 }
 
 // EvictReplica (ops.py:253-258).  The original keeps serving its own rows
@@ -1473,8 +1761,7 @@ int issue_evict(cb_model* m, int layer, int dev, int64_t* id) {
   PendingOp op = new_op(m, OPK_EVICT, layer, -1, L.reps[0].dev);
   op.kv_from = dev;
   op.kv_to = L.reps[0].dev;
-  CB_TRY(op_open(m, op));
-  return op_close(m, op, id);
+  return op_issue(m, op, id);
 }
 
 // Switch one op's placement at this step boundary.  No host synchronisation:
@@ -1482,19 +1769,22 @@ int issue_evict(cb_model* m, int layer, int dev, int64_t* id) {
 // the new KV device's compute stream, replaced buffers are freed stream-ordered.
 int op_commit(cb_model* m, PendingOp& op) {
   LayerState& L = m->layers[op.layer - 1];
-  for (auto& o : m->rt->devs) {
-    CB_TRY(use(o));
-    CB_CUDA(cudaStreamWaitEvent(o.compute, op.e1, 0));
-  }
+  if (!op.started) return fail(CB_ESTATE, "op " + std::to_string(op.id) + " was never started (cb_op_start)");
+  if (op.e1)
+    for (auto& o : m->rt->devs) {
+      if (!o.local) continue;
+      CB_TRY(use(o));
+      CB_CUDA(cudaStreamWaitEvent(o.compute, op.e1, 0));
+    }
   switch (op.kind) {
     case OPK_REPLICATE:
-      CB_TRY(make_layer_maps(m, op.copy));
+      if (op.copy.block) CB_TRY(make_layer_maps(m, op.copy));
       L.reps.push_back(op.copy);
       break;
     case OPK_MIGRATE: {
       const int kv_src = op.kv_from;
       if (op.kv_to >= 0) CB_TRY(op_catchup_kv(m, op, L));
-      CB_TRY(make_layer_maps(m, op.copy));
+      if (op.copy.block) CB_TRY(make_layer_maps(m, op.copy));
       const LayerCopy old = L.reps[0];
       L.reps[0] = op.copy;
       dev_free(m, old.dev, old.block);
@@ -1547,8 +1837,8 @@ void op_destroy_events(PendingOp& op) {
 
 int op_stats(cb_model* m, PendingOp& op, cb_op_stats* st, bool wait) {
   if (wait) {
-    CB_TRY(use(devctx(m, op.copy_dev)));
-    CB_CUDA(cudaEventSynchronize(op.e1));
+    if (!op.started) return fail(CB_ESTATE, "op " + std::to_string(op.id) + " was never started (cb_op_start)");
+    if (op.e1) CB_CUDA(cudaEventSynchronize(op.e1));
     if (op.c1) CB_CUDA(cudaEventSynchronize(op.c1));
   }
   if (!st) return CB_OK;
@@ -1558,10 +1848,11 @@ int op_stats(cb_model* m, PendingOp& op, cb_op_stats* st, bool wait) {
   st->catchup_bytes = op.catchup_bytes;
   st->committed = op.committed ? 1 : 0;
   float ms = 0.f;
-  st->done = cudaEventQuery(op.e1) == cudaSuccess && (!op.c1 || cudaEventQuery(op.c1) == cudaSuccess);
+  st->done = op.started && (!op.e1 || cudaEventQuery(op.e1) == cudaSuccess) &&
+             (!op.c1 || cudaEventQuery(op.c1) == cudaSuccess);
   cudaGetLastError();
   if (st->done) {
-    CB_CUDA(cudaEventElapsedTime(&ms, op.e0, op.e1));
+    if (op.e1) CB_CUDA(cudaEventElapsedTime(&ms, op.e0, op.e1));
     st->copy_ms = ms;
     if (op.c1) {
       float cm = 0.f;
@@ -1576,6 +1867,7 @@ int op_stats(cb_model* m, PendingOp& op, cb_op_stats* st, bool wait) {
 int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
   LayerState& L = m->layers[layer - 1];
   if (L.reps.empty()) return fail(CB_ESTATE, "layer not loaded");
+  if (m->rt->spmd) return fail(CB_ENOTSUP, "SPMD runtime: KV offload needs the single-process runtime");
   CB_TRY(check_idle(L, layer, OPK_MIGRATE));
   sync_all(m);  // Phase-3 relief (rare): a blocking move keeps the host-memory swap simple
   uint64_t moved = 0;
@@ -1697,9 +1989,53 @@ int cb_runtime_create(int32_t n_devices, const int32_t* ordinals, cb_runtime** o
   return CB_OK;
 }
 
+int cb_runtime_create_spmd(int32_t n_devices, const int32_t* rank_of_device, int32_t my_rank, int32_t my_ordinal,
+                           cb_xfer_fn xfer_fn, void* xfer_ctx, cb_runtime** out) {
+  if (n_devices < 1 || !rank_of_device || !out || !xfer_fn) return fail(CB_EINVAL, "bad runtime arguments");
+  std::vector<int32_t> ords(n_devices, my_ordinal);
+  int n_local = 0;
+  for (int i = 0; i < n_devices; ++i) n_local += rank_of_device[i] == my_rank;
+  if (n_local == 0) return fail(CB_EINVAL, "rank " + std::to_string(my_rank) + " owns no device");
+  // the local devices get streams exactly as in the single-process runtime
+  std::vector<int32_t> local_ords(n_local, my_ordinal);
+  cb_runtime* base = nullptr;
+  CB_TRY(cb_runtime_create(n_local, local_ords.data(), &base));
+  auto* rt = new cb_runtime();
+  rt->spmd = true;
+  rt->my_rank = my_rank;
+  rt->xfer = xfer_fn;
+  rt->xfer_ctx = xfer_ctx;
+  rt->devs.resize(n_devices);
+  int k = 0;
+  for (int i = 0; i < n_devices; ++i) {
+    if (rank_of_device[i] == my_rank) {
+      rt->devs[i] = base->devs[k++];
+    } else {
+      rt->devs[i].local = false;
+      rt->devs[i].ordinal = -1;
+    }
+    rt->devs[i].id = i;
+    rt->devs[i].rank = rank_of_device[i];
+    rt->ranks.push_back(rank_of_device[i]);
+  }
+  std::sort(rt->ranks.begin(), rt->ranks.end());
+  rt->ranks.erase(std::unique(rt->ranks.begin(), rt->ranks.end()), rt->ranks.end());
+  base->devs.clear();  // streams / events now owned by rt
+  delete base;
+  *out = rt;
+  return CB_OK;
+}
+
+int cb_device_is_local(cb_runtime* rt, int32_t device, int32_t* local_out) {
+  if (!rt || !local_out || device < 0 || device >= int(rt->devs.size())) return fail(CB_EINVAL, "unknown device");
+  *local_out = rt->devs[device].local ? 1 : 0;
+  return CB_OK;
+}
+
 int cb_runtime_destroy(cb_runtime* rt) {
   if (!rt) return CB_OK;
   for (auto& dc : rt->devs) {
+    if (!dc.local) continue;
     cudaSetDevice(dc.ordinal);
     cudaStreamSynchronize(dc.compute);
     cudaStreamSynchronize(dc.copy);
@@ -1721,6 +2057,7 @@ int cb_runtime_destroy(cb_runtime* rt) {
 int cb_device_info(cb_runtime* rt, int32_t device, int32_t* num_sms, uint64_t* free_bytes, uint64_t* total_bytes) {
   if (!rt || device < 0 || device >= int(rt->devs.size())) return fail(CB_EINVAL, "unknown device");
   DeviceCtx& dc = rt->devs[device];
+  if (!dc.local) return fail(CB_EINVAL, "device " + std::to_string(device) + " belongs to rank " + std::to_string(dc.rank));
   CB_TRY(use(dc));
   size_t f = 0, t = 0;
   CB_CUDA(cudaMemGetInfo(&f, &t));
@@ -1756,7 +2093,11 @@ int cb_model_create(cb_runtime* rt, const cb_model_desc* desc, int32_t home, cb_
   m->layers.resize(d.n_layers);
   m->slot_len.assign(d.max_slots, 0);
   m->slot_epoch.assign(d.max_slots, 0);
-  cudaSetDevice(rt->devs[home].ordinal);
+  for (const DeviceCtx& dc : rt->devs)
+    if (dc.local) {
+      cudaSetDevice(dc.ordinal);
+      break;
+    }
   if (cudaMallocHost(&m->pin_meta, (3 * size_t(d.max_tokens) + d.max_slots + 4 +
                                     4 * (size_t(d.max_tokens) / 64 + d.max_slots)) * 4) != cudaSuccess ||
       cudaMallocHost(&m->pin_next, size_t(d.max_slots) * 4) != cudaSuccess) {
@@ -1795,7 +2136,9 @@ int cb_model_destroy(cb_model* m) {
   dev_free(m, m->home, m->embed);
   dev_free(m, m->home, m->final_norm);
   dev_free(m, m->home, m->lm_head);
+  if (m->norm_tab) dev_free(m, m->norm_dev, m->norm_tab);
   for (auto& kv : m->prof.pool) {
+    if (!is_local(m, kv.first)) continue;
     cudaSetDevice(devctx(m, kv.first).ordinal);
     for (auto e : kv.second) cudaEventDestroy(e);
   }
@@ -1826,9 +2169,12 @@ uint64_t cb_module_bytes(cb_model* m, int32_t kind) {
 }
 
 int cb_layer_load(cb_model* m, int32_t layer, int32_t dev, const cb_layer_weights* w) {
-  if (!m || !w) return fail(CB_EINVAL, "null argument");
+  if (!m) return fail(CB_EINVAL, "null argument");
+  CB_TRY(check_dev(m, dev));
+  if (!w && is_local(m, dev)) return fail(CB_EINVAL, "null weights");
   LayerCopy c;
   CB_TRY(begin_layer_load(m, layer, dev, c));
+  if (!c.block) return finish_layer_load(m, layer, c);  // SPMD: registry entry of another rank's copy
   const size_t dm = m->d.d_model, ff = m->d.d_ff;
   CB_CUDA(cudaMemcpy(c.block + m->off_qkv, w->wq, size_t(m->q_n) * dm * 2, cudaMemcpyHostToDevice));
   CB_CUDA(cudaMemcpy(c.block + m->off_qkv + size_t(m->q_n) * dm * 2, w->wk, size_t(m->kv_n) * dm * 2,
@@ -1849,6 +2195,7 @@ int cb_layer_init_random(cb_model* m, int32_t layer, int32_t dev, uint64_t seed,
   if (!m) return fail(CB_EINVAL, "null model");
   LayerCopy c;
   CB_TRY(begin_layer_load(m, layer, dev, c));
+  if (!c.block) return finish_layer_load(m, layer, c);  // SPMD: registry entry of another rank's copy
   DeviceCtx& dc = devctx(m, dev);
   const size_t mat_elems = m->off_an / 2;
   const uint64_t s = seed * 1000003ull + uint64_t(layer);
@@ -1860,7 +2207,12 @@ int cb_layer_init_random(cb_model* m, int32_t layer, int32_t dev, uint64_t seed,
 }
 
 int cb_head_load(cb_model* m, const uint16_t* embed, const uint16_t* final_norm, const uint16_t* lm_head) {
-  if (!m || !embed || !final_norm || !lm_head) return fail(CB_EINVAL, "null argument");
+  if (!m) return fail(CB_EINVAL, "null argument");
+  if (!is_local(m, m->home)) {  // SPMD: the home device's rank holds the head
+    m->head_loaded = true;
+    return CB_OK;
+  }
+  if (!embed || !final_norm || !lm_head) return fail(CB_EINVAL, "null argument");
   DeviceCtx& dc = devctx(m, m->home);
   const size_t ve = size_t(m->d.vocab) * m->d.d_model * 2;
   if (!m->embed) {
@@ -1879,6 +2231,10 @@ int cb_head_load(cb_model* m, const uint16_t* embed, const uint16_t* final_norm,
 
 int cb_head_init_random(cb_model* m, uint64_t seed, float std) {
   if (!m) return fail(CB_EINVAL, "null model");
+  if (!is_local(m, m->home)) {
+    m->head_loaded = true;
+    return CB_OK;
+  }
   DeviceCtx& dc = devctx(m, m->home);
   const size_t ve = size_t(m->d.vocab) * m->d.d_model;
   if (!m->embed) {
@@ -1913,6 +2269,7 @@ int cb_module_read(cb_model* m, int32_t layer, int32_t dev, int32_t kind, void* 
   for (auto& r : L.reps)
     if (r.dev == dev) c = &r;
   if (!c) return fail(CB_ENOREPLICA, "layer " + std::to_string(layer) + " has no copy on device " + std::to_string(dev));
+  if (!c->block) return fail(CB_EINVAL, "device " + std::to_string(dev) + " belongs to another rank");
   CB_TRY(use(devctx(m, dev)));
   sync_all(m);
   const size_t dm = m->d.d_model, ff = m->d.d_ff;
@@ -1952,6 +2309,7 @@ int cb_kv_read(cb_model* m, int32_t layer, int32_t slot, void* dst, uint64_t nby
   const uint64_t want = uint64_t(m->slot_len[slot]) * kv_token_bytes(m);
   if (owner < 0 || want == 0) return fail(CB_ESTATE, "slot holds no KV for this layer");
   if (nbytes != want) return fail(CB_EINVAL, "nbytes must be " + std::to_string(want));
+  if (!is_local(m, owner)) return fail(CB_EINVAL, "the slot's KV lives on another rank's device " + std::to_string(owner));
   sync_all(m);
   CB_TRY(use(devctx(m, owner)));
   CB_CUDA(cudaMemcpy(dst, L.kv[owner] + kv_slot_offset(m, slot), want, cudaMemcpyDefault));
@@ -2098,17 +2456,26 @@ int cb_profile_read(cb_model* m, int32_t kclass, cb_kstat* out) {
 }
 
 // ---- scaling ops: asynchronous issue / poll / wait / commit / abort (A17)
+// SPMD: a failed issue still consumes its op id (the other ranks' issue of the
+// same op may have succeeded and registered it under that id)
+static int issued(cb_model* m, int r, int64_t* op_id) {
+  if (r != CB_OK && m->rt->spmd) {
+    *op_id = m->next_op++;
+  }
+  return r;
+}
+
 int cb_issue_replicate_layer(cb_model* m, int32_t layer, int32_t dst, int64_t* op_id, uint64_t* shortfall) {
   if (!m || !op_id) return fail(CB_EINVAL, "null argument");
   if (shortfall) *shortfall = 0;
-  return issue_replicate(m, layer, dst, op_id, shortfall);
+  return issued(m, issue_replicate(m, layer, dst, op_id, shortfall), op_id);
 }
 
 int cb_issue_migrate_layer(cb_model* m, int32_t layer, int32_t dst, int32_t with_kv, int64_t* op_id,
                            uint64_t* shortfall) {
   if (!m || !op_id) return fail(CB_EINVAL, "null argument");
   if (shortfall) *shortfall = 0;
-  return issue_migrate(m, layer, dst, with_kv, op_id, shortfall);
+  return issued(m, issue_migrate(m, layer, dst, with_kv, op_id, shortfall), op_id);
 }
 
 int cb_issue_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t dst, int64_t* op_id,
@@ -2119,13 +2486,21 @@ int cb_issue_migrate_submodule(cb_model* m, int32_t layer, int32_t kind, int32_t
   CB_TRY(check_dev(m, dst));
   if (kind == CB_DECODER_LAYER) return fail(CB_EINVAL, "whole layers move via MigrateLayer");
   if (kind < 0 || kind > CB_KV_CACHE) return fail(CB_EINVAL, "unknown module kind");
-  if (kind == CB_KV_CACHE) return issue_kv(m, layer, dst, op_id, shortfall);
-  return issue_projection(m, layer, kind, dst, op_id, shortfall);
+  if (kind == CB_KV_CACHE) return issued(m, issue_kv(m, layer, dst, op_id, shortfall), op_id);
+  return issued(m, issue_projection(m, layer, kind, dst, op_id, shortfall), op_id);
 }
 
 int cb_issue_evict_replica(cb_model* m, int32_t layer, int32_t device, int64_t* op_id) {
   if (!m || !op_id) return fail(CB_EINVAL, "null argument");
-  return issue_evict(m, layer, device, op_id);
+  return issued(m, issue_evict(m, layer, device, op_id), op_id);
+}
+
+int cb_op_start(cb_model* m, int64_t op_id) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  auto it = m->ops.find(op_id);
+  if (it == m->ops.end() || it->second.committed) return fail(CB_EINVAL, "op " + std::to_string(op_id) + " is not pending");
+  if (it->second.started) return CB_OK;  // single-process ops start at issue
+  return op_run(m, it->second);
 }
 
 int cb_op_poll(cb_model* m, int64_t op_id, int32_t* done) {
@@ -2185,6 +2560,7 @@ int cb_mem_usage(cb_model* m, int32_t device, cb_mem_stats* out) {
   if (!m || !out) return fail(CB_EINVAL, "null argument");
   CB_TRY(check_dev(m, device));
   DeviceCtx& dc = devctx(m, device);
+  if (!dc.local) return fail(CB_EINVAL, "device " + std::to_string(device) + " belongs to rank " + std::to_string(dc.rank));
   *out = cb_mem_stats{};
   out->workspace_bytes = dc.mem[MEM_WS];
   out->weight_bytes = dc.mem[MEM_WEIGHTS];
@@ -2217,6 +2593,14 @@ static int run_now(cb_model* m, int r, int64_t id, uint64_t shortfall, cb_op_sta
   if (r != CB_OK) {
     if (st) st->shortfall_bytes = shortfall;
     return r;
+  }
+  if (m->rt->spmd) {  // (validation passed, the reservation is held: undo it)
+    auto it = m->ops.find(id);
+    if (it != m->ops.end()) {
+      op_abort(m, it->second);
+      m->ops.erase(it);
+    }
+    return fail(CB_ENOTSUP, "SPMD runtime: use cb_issue_* + cb_op_start + cb_commit (every rank agrees first)");
   }
   auto it = m->ops.find(id);
   if (it == m->ops.end()) return fail(CB_ESTATE, "internal: issued op not registered");

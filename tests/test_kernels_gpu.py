@@ -65,6 +65,30 @@ def test_gemm_f32_7b_shapes(lib, cuda, N, K, T, row_off):
         assert out[:row_off].abs().max().item() == 0.0  # rows before row_off untouched
 
 
+@pytest.mark.parametrize("N,K,T,row_off,epi", [(22016, 4096, 8192, 0, 1), (4096, 11008, 3000, 5, 2),
+                                               (12288, 4096, 4321, 0, 0), (4096, 4096, 1900, 3, 1)])
+def test_gemm_prefill_rastered(lib, cuda, N, K, T, row_off, epi):
+    """Prefill-size launches (token-major pair kernel, several token tiles,
+    rastered tile order incl. a ragged last group), checked on the GPU against
+    an fp32 torch matmul (TF32 off)."""
+    torch = cuda
+    torch.backends.cuda.matmul.allow_tf32 = False
+    w = _bf16(torch, (N, K), 0.02, 21).cuda()
+    x = _bf16(torch, (T + row_off, K), 1.0, 22).cuda()
+    dt = torch.bfloat16 if epi == 0 else torch.float32
+    base = torch.randn(T + row_off, N, dtype=torch.float32, device="cuda").to(dt)
+    out = base.clone()
+    _gemm(lib, torch, w, x, T, row_off, epi, out, N)
+    ref = x[row_off:].float() @ w.float().T
+    if epi == 2:
+        ref = ref + base[row_off:].float()
+    err = (out[row_off:].float() - ref).abs().max().item()
+    tol = (1e-2 if epi == 0 else 2e-5 * K ** 0.5) * ref.abs().max().item() + 1e-3
+    assert err <= tol, (err, tol)
+    if row_off:
+        assert torch.equal(out[:row_off], base[:row_off])
+
+
 @pytest.mark.parametrize("N,K,T", [(256, 512, 24), (512, 1024, 200), (4096, 4096, 256), (768, 512, 700)])
 def test_gemm_residual_epilogue(lib, cuda, N, K, T):
     """+= epilogue on the 1-CTA (T <= 128) and CTA-pair (T > 128) kernels, incl. stream-K fixups."""
