@@ -78,7 +78,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -326,17 +326,11 @@ def run_single(args) -> None:
     total_dev_s = sum(dev_ms) / 1e3
     value = batch * args.steps / total_dev_s
     e2e = batch * args.steps / sum(wall_s)
-    g = prof["gemm"]
-    a = prof["attention"]
     launches = sum(prof[k]["launches"] for k in ("gemm", "attention", "elementwise"))
-    gemm_gbs = g["bytes"] / (g["ms"] * 1e6) if g["ms"] else 0.0
-    gemm_tflops = g.get("flops", 0.0) / (g["ms"] * 1e9) if g["ms"] else 0.0
-    attn_gbs = a["bytes"] / (a["ms"] * 1e6) if a["ms"] else 0.0
     ncu = {}
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     if ncu_path.exists():
         ncu = json.loads(ncu_path.read_text())
-    step_share = {k: prof[k]["ms"] / sum(prof_ms) for k in prof}
     ctx_mid = args.prompt + args.warmup + args.steps // 2
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -354,20 +348,7 @@ def run_single(args) -> None:
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": (3 * batch + batch) * 4,
                 "d2h_bytes_per_step": batch * 4},
         "gpu_launches": launches,
-        "roofline": {"kernel": "decoder-layer GEMMs (tcgen05 gemm_tc_kernel / gemm_tc2_kernel)", "bound": "hbm",
-                     "achieved": gemm_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": gemm_gbs / peaks["hbm_gbs"], "peak_src": peaks["src"],
-                     "bytes_per_launch": g["bytes"] / max(1, g["launches"]),
-                     "ms_per_launch": g["ms"] / max(1, g["launches"]),
-                     "traffic": ncu.get("gemm_dram_bytes_per_launch"),
-                     "step_share": step_share,
-                     "attention": {"achieved": attn_gbs, "frac": attn_gbs / peaks["hbm_gbs"],
-                                   "bytes_per_launch": a["bytes"] / max(1, a["launches"])},
-                     # the same GEMM launches against the tensor pipe: at B=256 the decode
-                     # projections sit at the HBM / tensor ridge (sustained peak: timed in a long step)
-                     "tensor": {"achieved": gemm_tflops, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
-                                "frac": gemm_tflops / peaks["bf16_tflops_sustained"],
-                                "flops_per_launch": g.get("flops", 0.0) / max(1, g["launches"])}},
+        "roofline": gemm_roofline(prof, prof_ms, peaks, ncu),
         "batch_sweep": sweep_res,
         "migrate": mig,
         "serving": serving,
@@ -383,120 +364,188 @@ def run_single(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def run_replicas(args, rank: int, world: int, dist) -> None:
-    """N>1: one process per GPU, every layer replicated on every GPU (one run);
-    scatter / gather of each step through NCCL (dist.ReplicaGroup)."""
+def gemm_roofline(prof: dict, prof_ms: list, peaks: dict, ncu: dict | None = None) -> dict:
+    """Roofline of the dominant kernel class (the decode GEMMs) from one
+    profiled pass: algorithmic bytes / FLOPs per launch over the average
+    CUDA-event launch time.  The binding roof per launch is the larger of
+    bytes / HBM peak and FLOPs / tensor peak; at B=256 the 7B decode GEMMs sit
+    above the ridge (FLOP-bound)."""
+    g, a = prof["gemm"], prof["attention"]
+    n = max(1, g["launches"])
+    gbs = g["bytes"] / (g["ms"] * 1e6) if g["ms"] else 0.0
+    tfs = g.get("flops", 0.0) / (g["ms"] * 1e9) if g["ms"] else 0.0
+    t_hbm = g["bytes"] / (peaks["hbm_gbs"] * 1e9)
+    t_tc = g.get("flops", 0.0) / (peaks["bf16_tflops_sustained"] * 1e12)
+    tensor_bound = t_tc > t_hbm
+    attn_gbs = a["bytes"] / (a["ms"] * 1e6) if a["ms"] else 0.0
+    return {
+        "kernel": "decoder-layer GEMMs (tcgen05 gemm_tc_kernel / gemm_tc2_kernel)",
+        "bound": "tensor" if tensor_bound else "hbm",
+        "achieved": tfs if tensor_bound else gbs,
+        "peak": peaks["bf16_tflops_sustained"] if tensor_bound else peaks["hbm_gbs"],
+        "unit": "TFLOP/s" if tensor_bound else "GB/s",
+        "frac": (tfs / peaks["bf16_tflops_sustained"]) if tensor_bound else (gbs / peaks["hbm_gbs"]),
+        "frac_of_binding_roof": (max(t_hbm, t_tc) * 1e3) / g["ms"] if g["ms"] else 0.0,
+        "peak_src": peaks["src"],
+        "bytes_per_launch": g["bytes"] / n, "flops_per_launch": g.get("flops", 0.0) / n,
+        "ms_per_launch": g["ms"] / n,
+        "traffic": (ncu or {}).get("gemm_dram_bytes_per_launch"),
+        "step_share": {k: prof[k]["ms"] / sum(prof_ms) for k in prof} if prof_ms else None,
+        "hbm": {"achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]},
+        "tensor": {"achieved": tfs, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                   "frac": tfs / peaks["bf16_tflops_sustained"]},
+        "attention": {"achieved": attn_gbs, "unit": "GB/s", "frac": attn_gbs / peaks["hbm_gbs"],
+                      "bytes_per_launch": a["bytes"] / max(1, a["launches"])},
+    }
+
+
+def run_spmd(args, rank: int, world: int, dist) -> None:
+    """N>1 (BASELINE config 3): one process per GPU, the SPMD runtime.  The
+    model's originals live on GPU 0 (the router's home); the hot layers
+    1..k (--replicate-layers, k < 32) are replicated onto every other GPU by
+    the scaling operator (ReplicateLayer over NVLink, NCCL send/recv), so each
+    step scatters the batch rows to the replicas at the run's first layer and
+    gathers them back after its last; the cold layers and the
+    head run on GPU 0 over the whole batch.  Per-GPU batch fixed (weak
+    scaling); value = global tokens / max-over-ranks device time."""
     import torch
 
     from paper_2507_18006_b200 import _lib
-    from paper_2507_18006_b200.dist import PHASE_DECODE, PHASE_PREFILL, ReplicaGroup
-    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
+    from paper_2507_18006_b200 import domain as D
+    from paper_2507_18006_b200 import ops as O
+    from paper_2507_18006_b200.executor import ExecutorConfig
+    from paper_2507_18006_b200.spmd import SpmdExecutor, SpmdRuntime, init_spmd
 
     _lib.load()
     peaks = _peaks()
-    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"  # tests: every rank on cuda:0 (gloo collectives)
-    dev = 0 if same_gpu else rank
-    torch.cuda.set_device(dev)
-    per = args.batch
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"  # tests: every rank on cuda:0, host-staged transport
+    ordinal = 0 if same_gpu else int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(ordinal)
+    group, transport, rod = init_spmd(dist, rank, world, ordinal, "host" if same_gpu else "nccl")
+    rt = SpmdRuntime(rod, rank, ordinal, transport)
+    n_layers = LLAMA2_7B["n_layers"]
+    k = args.replicate_layers if args.replicate_layers is not None else n_layers - 4
+    k = max(1, min(k, n_layers))
+    churn_steps = args.churn_steps
+    max_ctx = args.prompt + args.warmup + 2 * args.steps + churn_steps + 16
+    # KV blocks hold max_slots x max_ctx per (layer, device): GPU 0 holds all 32
+    # layers for the whole global batch -- cap the per-GPU batch to fit
+    kv_slot = n_layers * max_ctx * 16384
+    per = min(args.batch, max(16, int(110e9 / (kv_slot * world)) // 16 * 16))
     gbatch = per * world
-    max_ctx = args.prompt + args.warmup + args.steps + 8
-    rt = Runtime([dev])
-    cfg = ExecutorConfig(**LLAMA2_7B, max_slots=per, max_ctx=max_ctx, max_tokens=max(min(per, 64) * args.prompt, 256))
-    ex = Executor(rt, cfg, home_device=0, seed=7)
+    cfg = ExecutorConfig(**LLAMA2_7B, max_slots=gbatch, max_ctx=max_ctx, max_tokens=max(gbatch, 8192))
+    ex = SpmdExecutor(rt, cfg, group, home_device=0, seed=7)
     ex.init_head_random(std=0.02)
-    for li in range(1, cfg.n_layers + 1):
+    for li in range(1, n_layers + 1):
         ex.init_layer_random(li, 0, std=0.02)
-    group = ReplicaGroup(dist, ex)
-    slots = np.arange(gbatch)
+    cat = D.ModuleCatalog.from_model(D.ModelSpec(32, 4096, 11008, 32))
+    cluster = D.ClusterSpec.b200(world)
+    t_rep = time.perf_counter()
+    for li in range(1, k + 1):
+        for dv in range(1, world):
+            ex.issue(O.ReplicateLayer(li, dv), cat, cluster)
+    ex.commit(wait=True)
+    rep_s = time.perf_counter() - t_rep
+    rep_gbps = [m.gbps for m in ex.op_log if m.gbps > 0]
     rng = np.random.default_rng(11)
-    prompts = rng.integers(0, cfg.vocab, gbatch * args.prompt).astype(np.int32) if rank == 0 else None
-    nxt, _ = group.step(PHASE_PREFILL, slots, prompts, np.full(gbatch, args.prompt) if rank == 0 else None)
+    slots = np.arange(gbatch, dtype=np.int32)
+    prompts = rng.integers(0, cfg.vocab, gbatch * args.prompt).astype(np.int32)
+    nxt, _, _ = ex.prefill(slots, prompts, np.full(gbatch, args.prompt, np.int32))
     for _ in range(args.warmup):
-        nxt, _ = group.step(PHASE_DECODE, slots, nxt)
-    dist.barrier()
+        nxt, _, _ = ex.decode(slots, nxt)
+    group.barrier()
     torch.cuda.synchronize()
     dev_ms, t0 = [], time.perf_counter()
-    with ClockSampler(rank) as clocks:
+    with ClockSampler(ordinal) as clocks:
         for _ in range(args.steps):
-            nxt, ms = group.step(PHASE_DECODE, slots, nxt)
+            nxt, _, ms = ex.decode(slots, nxt)
             dev_ms.append(ms)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
-    dist.barrier()
-    cdev = "cpu" if same_gpu else "cuda"
-    t = torch.tensor([sum(dev_ms), wall], dtype=torch.float64, device=cdev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_s, wall_s = t[0].item() / 1e3, t[1].item()
-    # kernel launches per step (one profiled local step of this rank's share, after the timed region)
+    group.barrier()
+    tot = group.allgather([int(sum(dev_ms) * 1e6), int(wall * 1e9)])
+    dev_s, wall_s = tot[:, 0].max() / 1e9, tot[:, 1].max() / 1e9
+    # per-kernel evidence: the same steps with every launch bracketed by events (rank 0 = the busiest GPU)
     ex.profile(True)
-    _, s_loc, t_loc, _, _ = group.scatter(PHASE_DECODE, slots, nxt)
-    ex.decode(s_loc, t_loc)
+    prof_ms = []
+    for _ in range(min(args.steps, 10)):
+        nxt, _, ms = ex.decode(slots, nxt)
+        prof_ms.append(ms)
     prof = ex.profile_read()
     ex.profile(False)
-    group.gather(np.zeros(len(s_loc), np.int32))
-    n = torch.tensor([sum(prof[k]["launches"] for k in ("gemm", "attention", "elementwise"))], device=cdev)
-    dist.all_reduce(n)
-    launches = int(n.item()) * args.steps
+    launches = group.allgather([sum(prof[c]["launches"] for c in ("gemm", "attention", "elementwise"))])
+    launches_per_step = int(launches[:, 0].sum()) // max(1, len(prof_ms))
+    # continuous batching after the timed region: every step 1/16 of the batch
+    # finishes and is replaced by a fresh request (prefill-only step, then the
+    # whole batch decodes) -- split_batch re-assigns sequences, their KV follows
+    moved0, bytes0 = transport.messages, transport.bytes
+    t_c, tokens_c = time.perf_counter(), 0
+    live = list(range(gbatch))
+    outs = {s: int(t) for s, t in zip(live, nxt)}
+    churn_every = max(1, gbatch // 16)
+    next_slot_gen = 0
+    for step in range(churn_steps):
+        done = live[(step * churn_every) % len(live):][:churn_every]
+        ex.release_slots(np.array(done, np.int32))
+        fresh = rng.integers(0, cfg.vocab, len(done) * args.prompt).astype(np.int32)
+        fnext, _, _ = ex.prefill(np.array(done, np.int32), fresh, np.full(len(done), args.prompt, np.int32))
+        for s_, t_ in zip(done, fnext):
+            outs[s_] = int(t_)
+        live = [s_ for s_ in live if s_ not in done] + done
+        toks = np.array([outs[s_] for s_ in live], np.int32)
+        dn, _, _ = ex.decode(np.array(live, np.int32), toks)
+        for s_, t_ in zip(live, dn):
+            outs[s_] = int(t_)
+        tokens_c += len(live) + len(done)
+        next_slot_gen += 1
+    churn_wall = time.perf_counter() - t_c
+    churn = {"steps": churn_steps, "replaced_per_step": churn_every, "tokens_per_s": tokens_c / churn_wall,
+             "transport_messages": transport.messages - moved0, "transport_bytes": transport.bytes - bytes0,
+             "what": "continuous batching: each step releases 1/16 of the batch, prefills as many fresh "
+                     "requests, then decodes the whole batch (sequences re-split; KV rows follow over NCCL)"}
+    # one more cold layer replicated to GPU 1 and evicted: a 7B layer block over NVLink (NCCL send/recv)
     mig = None
-    if rank == 0 and world >= 2 and not same_gpu:
-        ex.close()
-        rt.close()
-        try:
-            mig = measure_nvlink_migration()
-        except Exception as e:  # the throughput line must still print (the migration is a side measurement)
-            mig = {"error": f"{type(e).__name__}: {e}"[:300]}
-    dist.barrier()
-    if rank != 0:
-        return
-    value = gbatch * args.steps / dev_s
-    line = {
-        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random prompts)",
-        "config": {"workload": f"config 3: Llama-2-7B shape, every decoder layer replicated on {world} GPUs "
-                               "(one process per GPU, split_batch shares)",
-                   "batch": gbatch, "batch_per_gpu": per, "prompt_len": args.prompt,
-                   "parallelism": f"module replication x{world} (one run; NCCL scatter/gather)",
-                   "l2": "weights 13.2 GB >> 126 MB L2 per GPU: every step streams from HBM"},
-        "e2e": {"value": gbatch * args.steps / wall_s, "unit": "tokens/s",
-                "h2d_bytes_per_step": (gbatch * 3 + 3) * 8, "d2h_bytes_per_step": gbatch * 8},
-        "gpu_launches": launches,
-        "migrate": mig,
-        "clocks": clocks.summary(),
-        "peaks": peaks,
-    }
-    print(json.dumps(line), flush=True)
-
-
-def measure_nvlink_migration() -> dict:
-    """One process, GPUs 0 and 1: replicate then migrate a 7B layer block
-    (ops.apply semantics) over NVLink; device-timed copy (CUDA events on the
-    destination's copy stream)."""
-    from paper_2507_18006_b200 import domain as D
-    from paper_2507_18006_b200 import ops as O
-    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
-
-    rt = Runtime([0, 1])
-    cfg = ExecutorConfig(**{**LLAMA2_7B, "n_layers": 2}, max_slots=8, max_ctx=64, max_tokens=256)
-    ex = Executor(rt, cfg, home_device=0, seed=7)
-    ex.init_head_random(std=0.02)
-    for li in (1, 2):
-        ex.init_layer_random(li, 0, std=0.02)
-    cat = D.ModuleCatalog.from_model(D.ModelSpec(2, 4096, 11008, 32))
-    cluster = D.ClusterSpec.b200(2)
-    res = []
-    for _ in range(3):
-        ex.apply(O.ReplicateLayer(1, 1), cat, cluster)
-        res.append(ex.op_log[-1])
-        ex.apply(O.EvictReplica(1, 1), cat, cluster)
-    ex.apply(O.MigrateLayer(2, 1, with_kv=True), cat, cluster)
-    m = ex.op_log[-1]
-    best = max(res, key=lambda r: r.gbps)
+    if k < n_layers:
+        ex.apply(O.ReplicateLayer(n_layers, 1), cat, cluster)
+        m = ex.op_log[-1]
+        ex.apply(O.EvictReplica(n_layers, 1), cat, cluster)
+        g = group.allgather([int(m.weight_bytes), int(m.device_ms * 1e6)])
+        b1, ms1 = int(g[1, 0]), g[1, 1] / 1e6  # rank 1 = the receiver
+        gbps = b1 / (ms1 * 1e6) if ms1 > 0 else 0.0
+        mig = {"bytes": b1, "ms": ms1, "gbps": gbps, "frac": gbps / 900.0, "nvlink_peak_gbps_per_dir": 900.0,
+               "path": "NCCL send/recv over NVLink between the ranks' copy streams (receiver-timed)",
+               "bulk_replication": {"layers": k, "replicas_per_layer": world - 1, "wall_s": rep_s,
+                                    "median_gbps_this_rank": statistics.median(rep_gbps) if rep_gbps else None}}
+    group.barrier()
+    if rank == 0:
+        value = gbatch * args.steps / dev_s
+        ncu_path = ROOT / "profiles" / "ncu_summary.json"
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, random prompts)",
+            "config": {"workload": f"config 3: Llama-2-7B shape, hot layers 1..{k} replicated on all {world} GPUs "
+                                   f"(one process per GPU), layers {k + 1}..{n_layers} + head on GPU 0",
+                       "batch": gbatch, "batch_per_gpu": per, "prompt_len": args.prompt,
+                       "replicated_layers": k,
+                       "parallelism": f"module replication x{world} (SPMD, NCCL scatter/gather at run boundaries)",
+                       "l2": "weights 13.2 GB >> 126 MB L2 per GPU: every step streams from HBM"},
+            "latency_ms": {"p50": float(np.percentile(np.array(dev_ms), 50)),
+                           "p99": float(np.percentile(np.array(dev_ms), 99)),
+                           "what": "per-step device time on rank 0"},
+            "e2e": {"value": gbatch * args.steps / wall_s, "unit": "tokens/s",
+                    "h2d_bytes_per_step": (gbatch * 3 + gbatch) * 4, "d2h_bytes_per_step": gbatch * 4},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": gemm_roofline(prof, prof_ms, peaks,
+                                      json.loads(ncu_path.read_text()) if ncu_path.exists() else None),
+            "continuous_batching": churn,
+            "migrate": mig,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
     ex.close()
     rt.close()
-    return {"bytes": best.weight_bytes, "ms": best.device_ms, "gbps": best.gbps,
-            "migrate_layer_gbps": m.gbps, "path": "NVLink P2P (cudaMemcpyPeerAsync, GPU 0 -> GPU 1)",
-            "nvlink_peak_gbps_per_dir": 900.0, "frac": best.gbps / 900.0}
 
 
 def main() -> None:
@@ -510,7 +559,9 @@ def main() -> None:
                     help="other batch sizes timed on the same instance")
     ap.add_argument("--sweep-steps", type=int, default=10)
     ap.add_argument("--prompt", type=int, default=128)
-    ap.add_argument("--replicate-layers", type=int, default=32)
+    ap.add_argument("--replicate-layers", type=int, default=None,
+                    help="N>1: hot layers 1..k replicated on every GPU (default n_layers - 4)")
+    ap.add_argument("--churn-steps", type=int, default=12, help="N>1: continuous-batching steps after the timed region")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serve-s", type=float, default=8.0, help="serving window (0 = skip)")
     ap.add_argument("--serve-rps", type=float, default=40.0)
@@ -537,7 +588,7 @@ def main() -> None:
         elif world == 1:
             run_single(args)
         else:
-            run_replicas(args, rank, world, dist)
+            run_spmd(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()

@@ -236,7 +236,11 @@ struct cb_model {
   int32_t* pin_next = nullptr;
   std::vector<std::vector<Route>> last_routing;
   int cur_phase = 0;  // CB_PHASE_* of the pass in flight
-  bool fuse_norm = false;  // this pass folds RMSNorm into the GEMM epilogues (decode, T <= 256)
+  // Fused RMSNorm per layer boundary of the pass in flight: fin[li] = layer li's
+  // attention-norm input arrives as h' = bf16(x * gamma) + row sums of squares
+  // (produced by the previous layer's down projection, or the embedding), so
+  // its QKV GEMM applies the row scales; fin[n_layers] = the same for the head.
+  std::vector<char> fin;
   int cur_T = 0;  // rows of the pass in flight: per-step meta = [tokens | slot | pos] x T, then gather x bs
   int cur_bs = 0;  // sequences of the pass in flight
   std::vector<int> seq_blk;  // prefill: first q-block of each sequence (+ total), blocks follow the gather list
@@ -654,14 +658,15 @@ int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K,
 }
 
 // Move residual rows so that every row sits on the device of its new segment.
-int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to);
-int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to) {
+// with_norm: the next layer consumes fused-norm input (h' rows + sums of squares travel too)
+int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to, bool with_norm);
+int reshard(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to, bool with_norm) {
   XGroup grp(m, 0);
-  CB_TRY(reshard_rows(m, from, to));
+  CB_TRY(reshard_rows(m, from, to, with_norm));
   return grp.close();
 }
 
-int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to) {
+int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Seg>& to, bool with_norm) {
   const size_t row_bytes = size_t(m->d.d_model) * 4;
   for (const Seg& ns : to)
     for (const Seg& os : from) {
@@ -681,7 +686,7 @@ int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Se
         ProfScope ps(m, ld ? dd : sd, CB_KCLASS_COPY, ld ? ds : ss, double(b - a) * row_bytes);
         CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].x : nullptr, xr), ss, dd,
                      at(dd, ld, ld ? m->ws[dd].x : nullptr, xr), ds, size_t(b - a) * xr));
-        if (m->fuse_norm) {
+        if (with_norm) {
           CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].h : nullptr, hr), ss, dd,
                        at(dd, ld, ld ? m->ws[dd].h : nullptr, hr), ds, size_t(b - a) * hr));
           CB_TRY(xmove(m, 0, sd, at(sd, ls, ls ? m->ws[sd].ssq : nullptr, qr), ss, dd,
@@ -697,7 +702,7 @@ int reshard_rows(cb_model* m, const std::vector<Seg>& from, const std::vector<Se
       CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].x + size_t(a) * m->d.d_model, dd.ordinal,
                                   m->ws[os.dev].x + size_t(a) * m->d.d_model, sd.ordinal,
                                   size_t(b - a) * row_bytes, dd.compute));
-      if (m->fuse_norm) {  // the next layer's normalised input rows and their sums of squares travel too
+      if (with_norm) {  // the next layer's normalised input rows and their sums of squares travel too
         const size_t np = size_t(m->d.d_model / 32);
         CB_CUDA(cudaMemcpyPeerAsync(m->ws[ns.dev].h + size_t(a) * m->d.d_model, dd.ordinal,
                                     m->ws[os.dev].h + size_t(a) * m->d.d_model, sd.ordinal,
@@ -1053,8 +1058,11 @@ int run_layer_overridden(cb_model* m, LayerState& L, const Seg& s, const std::ve
 
 // gamma_next: the norm that follows this layer (next layer's attention norm,
 // or the final norm), readable from s.dev -- used when the pass fuses RMSNorm.
+// fused_in: this layer's input arrives fused (fin[li]; the segment has <= 256
+// rows, so the O -> gate/up norm fuses too); gamma_next != null: the next
+// consumer is fused, so the down projection emits its h' and sums of squares.
 int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot,
-                      const std::vector<int>& row_pos, const uint16_t* gamma_next) {
+                      const std::vector<int>& row_pos, bool fused_in, const uint16_t* gamma_next) {
   if (L.proj_ov) return run_layer_overridden(m, L, s, seq_slot, row_pos);
   const cb_model_desc& d = m->d;
   const LayerCopy& W = L.reps[s.rep];
@@ -1066,14 +1074,15 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
   const uint16_t* an = reinterpret_cast<const uint16_t*>(W.block + m->off_an);
   const uint16_t* fn = reinterpret_cast<const uint16_t*>(W.block + m->off_fn);
   const double norm_bytes = double(T) * d.d_model * 6 + d.d_model * 2.0;
-  if (m->fuse_norm) {
+  NormIO prod_next;
+  prod_next.gamma_next = gamma_next;
+  if (fused_in) {
     // RMSNorm folded into the GEMMs: the residual projections emit h' = bf16(x * gamma)
     // plus per-row sums of squares, the next projection scales its outputs by rsqrt(mean + eps)
     NormIO cons;
     cons.consume = true;
-    NormIO prod_fn, prod_next;
+    NormIO prod_fn;
     prod_fn.gamma_next = fn;
-    prod_next.gamma_next = gamma_next;
     CB_TRY(gemm(m, dev, W.m_qkv, ws.map_h, m->qkv_n, d.d_model, T, s.r0, cb::EPI_BF16, ws.qkv, m->qkv_n, cons));
     CB_TRY(attention_part(m, L, s, seq_slot, row_pos));
     CB_TRY(use(dc));
@@ -1095,7 +1104,7 @@ int run_layer_segment(cb_model* m, LayerState& L, const Seg& s, const std::vecto
     CB_CUDA(cb::rmsnorm_launch(ws.x, fn, ws.h, T, d.d_model, d.norm_eps, s.r0, dc.compute));
   }
   CB_TRY(gemm(m, dev, W.m_gu, ws.map_h, 2 * d.d_ff, d.d_model, T, s.r0, cb::EPI_SWIGLU, ws.act, d.d_ff));
-  CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model));
+  CB_TRY(gemm(m, dev, W.m_d, ws.map_act, d.d_model, d.d_ff, T, s.r0, cb::EPI_RESID, ws.x, d.d_model, prod_next));
   return CB_OK;
 }
 
@@ -1238,34 +1247,34 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     CB_TRY(use(dc));
     CB_CUDA(cudaMemcpyAsync(m->ws[dv].meta, meta, meta_bytes, cudaMemcpyHostToDevice, dc.compute));
   }
-  // Fused RMSNorm: decode passes whose rows fit one GEMM token tile, plain
-  // layers (no migrated projections), every norm vector readable where its
-  // producer runs.  Prefill keeps the separate norm kernels (compute-bound GEMMs).
-  // The decision depends on the placement only (identical on every SPMD rank:
-  // it decides whether the norm rows travel with the residual rows).
-  m->fuse_norm = !prefill && T <= 256 && d.d_model % 256 == 0;
-  std::vector<std::vector<const uint16_t*>> gamma_next(d.n_layers);
-  const uint16_t* g_embed = m->fuse_norm && home_local ? norm_gamma_for(m, 0, m->home) : nullptr;
-  if (m->fuse_norm && home_local && !g_embed) m->fuse_norm = false;
-  for (int li = 0; li < d.n_layers && m->fuse_norm; ++li) {
-    const LayerState& L = m->layers[li];
-    if (L.proj_ov) m->fuse_norm = false;
-    for (const LayerCopy& c : L.reps) {
-      if (!is_local(m, c.dev)) {
-        gamma_next[li].push_back(nullptr);
-        continue;
-      }
-      const uint16_t* g = norm_gamma_for(m, li + 1, c.dev);
-      if (!g) m->fuse_norm = false;
-      gamma_next[li].push_back(g);
-    }
+  // Fused RMSNorm, per layer boundary: a layer consumes fused input when every
+  // segment of it has <= 256 rows (one GEMM token tile: the row-scale table),
+  // neither it nor its producer carries migrated projections, and the norm
+  // vector is readable where the producer runs.  Prefill keeps the separate norm
+  // kernels (compute-bound GEMMs).  Decided from the placement and the batch
+  // only: identical on every SPMD rank (it decides whether h' rows travel).
+  const bool can_fuse = !prefill && d.d_model % 256 == 0;
+  m->fin.assign(d.n_layers + 1, 0);
+  for (int li = 0; li <= d.n_layers && can_fuse; ++li) {
+    const int p = li < d.n_layers ? int(m->layers[li].reps.size()) : 1;
+    const int max_share = (bs + p - 1) / p;  // decode: one row per sequence
+    bool ok = max_share <= 256;
+    if (li < d.n_layers && m->layers[li].proj_ov) ok = false;
+    if (li > 0 && m->layers[li - 1].proj_ov) ok = false;
+    // the producers (previous layer's copies, or the embedding on the home device) read the norm vector
+    if (ok && li == 0) ok = !is_local(m, m->home) || norm_gamma_for(m, 0, m->home);
+    if (ok && li > 0)
+      for (const LayerCopy& c : m->layers[li - 1].reps)
+        if (is_local(m, c.dev) && !norm_gamma_for(m, li, c.dev)) ok = false;
+    m->fin[li] = ok;
   }
   Workspace& hw = m->ws[m->home];
   if (home_local) {
     CB_TRY(use(devctx(m, m->home)));
     ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
-    if (m->fuse_norm)
-      CB_CUDA(cb::embed_norm_launch(m->embed, hw.meta, hw.x, g_embed, hw.h, hw.ssq, T, d.d_model, 0, hc.compute));
+    if (m->fin[0])
+      CB_CUDA(cb::embed_norm_launch(m->embed, hw.meta, hw.x, norm_gamma_for(m, 0, m->home), hw.h, hw.ssq, T,
+                                    d.d_model, 0, hc.compute));
     else
       CB_CUDA(cb::embed_launch(m->embed, hw.meta, hw.x, T, d.d_model, 0, hc.compute));
   }
@@ -1283,7 +1292,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       if (shares[j] > 0) segs.push_back({L.reps[j].dev, j, seq_row[s0], seq_row[s0 + shares[j]], s0, s0 + shares[j]});
       s0 += shares[j];
     }
-    CB_TRY(reshard(m, layout, segs));
+    CB_TRY(reshard(m, layout, segs, m->fin[li]));
     {
       XGroup grp(m, 0);
       for (const Seg& s : segs) CB_TRY(kv_follow(m, L, s, seq_slot));
@@ -1291,16 +1300,17 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     }
     for (const Seg& s : segs)
       if (is_local(m, s.dev))
-        CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos, m->fuse_norm ? gamma_next[li][s.rep] : nullptr));
+        CB_TRY(run_layer_segment(m, L, s, seq_slot, row_pos, m->fin[li],
+                                 m->fin[li + 1] ? norm_gamma_for(m, li + 1, s.dev) : nullptr));
     layout = segs;
   }
   std::vector<Seg> home_layout{{m->home, 0, 0, T, 0, bs}};
-  CB_TRY(reshard(m, layout, home_layout));
+  CB_TRY(reshard(m, layout, home_layout, m->fin[d.n_layers]));
   // every device's trailing work joins the timing stream
   for (int dv : devs) CB_TRY(depend(hc, devctx(m, dv)));
   CB_TRY(use(hc));
   if (home_local) {
-    if (!m->fuse_norm) {  // fused: the last layer's down projection already wrote h' for the final norm
+    if (!m->fin[d.n_layers]) {  // fused: the last layer's down projection already wrote h' for the final norm
       ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(T) * d.d_model * 6);
       CB_CUDA(cb::rmsnorm_launch(hw.x, m->final_norm, hw.h, T, d.d_model, d.norm_eps, 0, hc.compute));
     }
@@ -1311,7 +1321,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       xm = hw.map_hl;
     }
     NormIO head_norm;
-    head_norm.consume = m->fuse_norm;
+    head_norm.consume = m->fin[d.n_layers];
     CB_TRY(gemm(m, m->home, m->m_head, xm, d.vocab, d.d_model, bs, 0, cb::EPI_F32, hw.logits, d.vocab, head_norm));
     {
       ProfScope ps(m, m->home, CB_KCLASS_ELEMWISE, hc.compute, double(bs) * d.vocab * 4);

@@ -23,10 +23,13 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def test_bench_replica_ranks_world2_same_gpu():
+def test_bench_spmd_world2_same_gpu():
+    """bench.py's N>1 path (config 3, SPMD: hot layers 1..28 replicated on the
+    second rank, cold layers + head on rank 0, continuous-batching window with
+    cross-rank KV moves) with both ranks on cuda:0 (host-staged transport)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
-           "--gpus", "2", "--steps", "3", "--warmup", "1", "--batch", "8", "--prompt", "16"]
+           "--gpus", "2", "--steps", "3", "--warmup", "1", "--batch", "8", "--prompt", "16", "--churn-steps", "3"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
                          env={**os.environ, "BENCH_SAME_GPU": "1"})
     assert out.returncode == 0, out.stderr[-3000:]
@@ -34,7 +37,11 @@ def test_bench_replica_ranks_world2_same_gpu():
     assert len(lines) == 1, out.stdout[-2000:]
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["config"]["batch"] == 16 and rec["value"] > 0
+    assert rec["config"]["replicated_layers"] == 28
     assert rec["gpu_launches"] > 0 and rec["scaling"] == "weak"
+    assert rec["roofline"]["frac"] > 0 and rec["roofline"]["bound"] in ("hbm", "tensor")
+    assert rec["migrate"]["bytes"] == 404_766_720 and rec["migrate"]["gbps"] > 0
+    assert rec["continuous_batching"]["transport_messages"] > 0
 
 
 def test_replica_group_world2_gpu_executors_match_oracle():
