@@ -241,20 +241,21 @@ CB_DEVICE void umma_bf16_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b
       "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-CB_DEVICE void umma_commit_pair_elect(uint64_t* bar) {
+// (mask: the pair's two CTAs in the cluster, 0b11 << 2i for pair i of a 4-CTA cluster)
+CB_DEVICE void umma_commit_pair_elect(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
           smem_u32(bar)),
-      "h"(uint16_t(3))
+      "h"(mask)
       : "memory");
 }
 
 // CTA-pair version: 4 x (256 x N x 16) MMAs on the pair, one commit multicast to
 // the stage barrier of both CTAs.
 CB_DEVICE void umma_kblock_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                      uint32_t accumulate, uint64_t* bar) {
+                                      uint32_t accumulate, uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
@@ -267,14 +268,14 @@ CB_DEVICE void umma_kblock_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t
       "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t}" ::"r"(
           d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)), "h"(uint16_t(3))
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
 }
 
 // CTA-pair k-block with separate stage-release barriers for the two operands
 // (decoupled ring depths): two commits, each multicast to both CTAs.
 CB_DEVICE void umma_kblock_pair2_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate, uint64_t* bar_a, uint64_t* bar_b) {
+                                       uint32_t accumulate, uint64_t* bar_a, uint64_t* bar_b, uint16_t mask = 3) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
@@ -289,7 +290,7 @@ CB_DEVICE void umma_kblock_pair2_elect(uint32_t d_tmem, uint64_t a_desc, uint64_
       "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], %7;\n\t}" ::"r"(
           d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar_a)), "r"(smem_u32(bar_b)),
-      "h"(uint16_t(3))
+      "h"(mask)
       : "memory");
 }
 
@@ -490,6 +491,11 @@ CB_DEVICE unsigned long long globaltimer_ns() {
   return t;
 }
 
+CB_DEVICE void dsmem_st_f4(uint32_t cluster_addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
 CB_DEVICE float dsmem_ld_f32(uint32_t cluster_addr) {
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
@@ -512,6 +518,11 @@ CB_DEVICE float4 dsmem_ld_f4(uint32_t cluster_addr) {
 CB_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 CB_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+CB_DEVICE int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 CB_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }

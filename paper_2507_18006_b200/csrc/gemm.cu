@@ -947,8 +947,14 @@ CB_DEVICE uint4* stg_chunk(uint8_t* stg, int r, int c) {
   return reinterpret_cast<uint4*>(stg + (o ^ (((o >> 7) & M) << 4)));
 }
 
+// Split-K pairs (xp != null): the tile's other K parts of these columns, in
+// shared memory, block i (stride xstride floats) = K part i (i >= xme: part
+// i + 1), each [32-column chunk][8 float4 groups][128 tokens][float4]; the
+// column sum runs over the parts in K order, this CTA's own accumulator being
+// part xme.
 CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, uint32_t t_addr, int n_base,
-                             int nw, int row0, int tok0, int ncols) {
+                             int nw, int row0, int tok0, int ncols, const float* xp = nullptr, int xs = 0,
+                             int xme = 0, size_t xstride = 0) {
   const int tok = tok0 + e.lane;  // tok0: first token of this warp
   const bool ok = tok < ncols;
   // full 32-token groups go out through swizzled staging + one TMA store per
@@ -970,6 +976,28 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
     tmem_ld32(t_addr + uint32_t(c0), r);
     tmem_ld_wait();
     float v[32];
+    if (xp) {
+      const int lt = tok & 127;  // token row of this CTA
+      float sum[32];
+      for (int src = 0; src < xs; ++src) {
+        if (src == xme) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sum[i] = src == 0 ? __uint_as_float(r[i]) : sum[i] + __uint_as_float(r[i]);
+          continue;
+        }
+        const float4* pp =
+            reinterpret_cast<const float4*>(xp + (src - (src > xme)) * xstride) + size_t(c0 >> 5) * 8 * 128 + lt;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 p = pp[j * 128];
+          const float px[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) sum[4 * j + i] = src == 0 ? px[i] : sum[4 * j + i] + px[i];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(sum[i]);
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = rt ? __uint_as_float(r[i]) * sc : __uint_as_float(r[i]);
     if (use_tma) {
@@ -1128,9 +1156,20 @@ __global__ void __launch_bounds__(kThreads1, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  // Split-K (token-major, a.ksplit = s in {2, 4}): s pairs (clusters of 2,
+  // consecutive) per tile, pair kh accumulating K part kh; the parts are
+  // exchanged through L2 with per-(tile, column part) arrival counters and
+  // each CTA finishes nw / s of the tile's columns.  All CTAs of the launch are
+  // co-resident (<= one per SM, and the next kernel can only start once every
+  // CTA here ran pdl_trigger), so waiting for the other parts cannot deadlock.
+  const bool split = SWAP && a.ksplit > 1;
+  const int ks = split ? a.ksplit : 1;
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank;                                   // rank inside the pair
+  const int kh = split ? int(blockIdx.x >> 1) % ks : 0;          // K part of this pair
+  const uint16_t pmask = uint16_t(3);
   const bool leader = rank == 0;
-  const int pair = blockIdx.x >> 1;
+  const int pair = split ? int(blockIdx.x) / (2 * ks) : int(blockIdx.x >> 1);  // split: the tile
   const int n_tt = a.n_ttiles;
   const StreamK sk{a.units, int(gridDim.x) >> 1, a.kblocks};
   const int ptiles = sk.units / sk.kb;
@@ -1141,9 +1180,11 @@ __global__ void __launch_bounds__(kThreads1, 1)
   // instead of every pair streaming its own weight tile against all tokens.
   const bool rast = SWAP && a.raster > 0;
   const int n_mine = rast ? (pair < ptiles ? (ptiles - pair + sk.grid - 1) / sk.grid : 0) : 0;
-  const int ubeg = rast ? 0 : a.whole_tiles ? int((long long)pair * ptiles / sk.grid) * sk.kb : sk.u0(pair);
-  const int uend = rast ? n_mine * sk.kb
-                        : a.whole_tiles ? int((long long)(pair + 1) * ptiles / sk.grid) * sk.kb : sk.u0(pair + 1);
+  const int ubeg = split ? pair * sk.kb + (kh * sk.kb) / ks
+                   : rast ? 0 : a.whole_tiles ? int((long long)pair * ptiles / sk.grid) * sk.kb : sk.u0(pair);
+  const int uend = split ? pair * sk.kb + ((kh + 1) * sk.kb) / ks
+                   : rast ? n_mine * sk.kb
+                          : a.whole_tiles ? int((long long)(pair + 1) * ptiles / sk.grid) * sk.kb : sk.u0(pair + 1);
   const int c = blockIdx.x;
   auto tile_of = [&](int u, int& mt_o, int& tt_o) {
     const int t = u / sk.kb;
@@ -1271,9 +1312,10 @@ __global__ void __launch_bounds__(kThreads1, 1)
             umma_2kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage],
                                     uint32_t((TNP / 2) * kBK * 2) >> 4, uint32_t(a.nw >> 1) * (kBK * 2) >> 4);
           else if (SWAP && dec)
-            umma_kblock_pair2_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage]);
+            umma_kblock_pair2_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage],
+                                    pmask);
           else if (SWAP)
-            umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
+            umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], pmask);
           else
             umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
           if (a.trace && lane == 0 && i < 64) a.trace[(size_t)c * 512 + 278 + i] = globaltimer_ns();
@@ -1281,7 +1323,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           if (++xstage == SX) { xstage = 0; xphase ^= 1; }
         }
         __syncwarp();
-        umma_commit_pair_elect(&tfull_bar[acc]);
+        umma_commit_pair_elect(&tfull_bar[acc], pmask);
         u += kb1 - kb0;
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -1299,7 +1341,70 @@ __global__ void __launch_bounds__(kThreads1, 1)
     uint32_t acc_phase = 0;
     uint32_t fix_phase = 0;
     int seg_i = 0;
-    for (int u = ubeg; u < uend;) {
+    if (split) {
+      // one segment per CTA (its K part of the tile), accumulator 0
+      int mt, tt;
+      tile_of(ubeg, mt, tt);
+      const int row0 = a.row_off + tt * TNP;
+      const int ncols = min(TNP, a.T - tt * TNP);
+      const int w = a.nw / ks;  // columns this CTA finishes: [kh * w, (kh + 1) * w)
+      const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16);
+      const size_t blk = size_t(kBM) * w;  // floats of one (destination, source) part block
+      float* xb = a.ws + size_t(pair * 2 + int(rank)) * ks * ks * blk;  // [dst][src] part blocks of this CTA slot
+      const int lt = q * 32 + lane;
+      unsigned long long* tr = (a.trace && et == 0) ? a.trace + (size_t)c * 512 + 130 : nullptr;
+      mbar_wait(&tfull_bar[0], 0);
+      tc_fence_after();
+      if (tr) tr[0] = globaltimer_ns();
+      // my K part of the other column parts: TMEM -> the (idle) stage ring ->
+      // bulk stores to L2; the other parts of my columns: bulk loads into the
+      // ring behind them.  Blocks are [32-column chunk][8 float4 groups][128
+      // tokens][float4] (consecutive lanes = consecutive 16 bytes).
+      float* sout = reinterpret_cast<float*>(sW);
+      float* sin = sout + size_t(ks - 1) * blk;
+      int nb = 0;
+      for (int dst = 0; dst < ks; ++dst) {
+        if (dst == kh) continue;
+        float4* pp = reinterpret_cast<float4*>(sout + size_t(nb++) * blk) + lt;
+        for (int c0 = 0; c0 < w; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t_addr + uint32_t(dst * w + c0), r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pp[((c0 >> 5) * 8 + j) * 128] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                                        __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, kEpiThreads);
+      int* cnt = a.counters + size_t(pair * 2 + int(rank)) * ks;
+      if (et == 0) {
+        nb = 0;
+        for (int dst = 0; dst < ks; ++dst)
+          if (dst != kh) bulk_s2g(xb + (dst * ks + kh) * blk, sout + size_t(nb++) * blk, uint32_t(blk * 4));
+        bulk_commit();
+        bulk_wait<0>();
+        if (tr) tr[1] = globaltimer_ns();
+        fence_proxy_async_global();  // the async-proxy stores, then the generic release below
+        __threadfence();
+        for (int dst = 0; dst < ks; ++dst)
+          if (dst != kh) atomicAdd(cnt + dst, 1);
+        while (ld_acquire_gpu(cnt + kh) < ks - 1) __nanosleep(32);
+        cnt[kh] = 0;  // (every other part arrived: reset for the next launch)
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(fix_bar, uint32_t((ks - 1) * blk * 4));
+        nb = 0;
+        for (int src = 0; src < ks; ++src)
+          if (src != kh) bulk_g2s(sin + size_t(nb++) * blk, xb + (kh * ks + src) * blk, uint32_t(blk * 4), fix_bar);
+        if (tr) tr[2] = globaltimer_ns();
+      }
+      mbar_wait(fix_bar, 0);
+      epi_drain_tok(a, &tmO, e, t_addr + uint32_t(kh * w), mt * a.nw + kh * w, w, row0, int(rank) * kBM + q * 32,
+                    ncols, sin, ks, kh, blk);
+      if (tr) tr[3] = globaltimer_ns();
+    }
+    for (int u = split ? uend : ubeg; u < uend;) {
       const int tile = u / sk.kb, kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
       int mt, tt;
@@ -1499,6 +1604,25 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   // (co-resident CTAs need a small ring: one 64-wide k-block per stage then)
   const int kd2 = (kd_env == 2 && !p.corun && K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // replica-invariant
   p.kd = 1;
+  const int ks_nw = 256, ks_s = 4;
+  if (kind_T > kPairMinT && kind_T <= 256 && N % ks_nw == 0 && K % (ks_s * kBK) == 0 &&
+      (N / ks_nw) * 2 * ks_s <= num_sms && tiles * 10 < (long long)num_sms * 6) {
+    // few wide-K tiles (O / down) with more than 128 rows: token-major CTA
+    // pairs of 256 weight rows (the k-block loop runs at ~87% of the MMA rate,
+    // scripts/gemm_split_trace.py), each tile's K quarters on four pairs, the
+    // parts exchanged through L2 with arrival counters, each CTA finishing 64
+    // columns.  T = 256: O 22.7 -> 21.7 us, down 33.6 -> 30.8 us alone, the
+    // B = 256 decode step 8.1 -> 7.5 ms (profiles/r02_gemm_ksplit.txt).  Tried
+    // and slower: 128-row pairs split in halves (K halves exchanged through
+    // DSMEM or L2), 8-CTA clusters of the four pairs (two waves of clusters).
+    p.pair = 1;
+    p.tn = 256;
+    p.box_rows = 128;
+    p.nw = ks_nw;
+    p.whole = 1;
+    p.ksplit = ks_s;
+    return p;
+  }
   if (kind_T <= 256 && tiles * 10 < (long long)num_sms * 6) {
     // few wide-K tiles (O / down projections): 1-CTA kernel, cluster split-K
     // (DSMEM reduction) -- measured fastest up to 256 rows
@@ -1746,6 +1870,11 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
         a.tma = 1;
       }
     }
+    a.ksplit = (plan.ksplit > 1 && kd == 1 && a.n_ttiles == 1 && a.nw % (32 * plan.ksplit) == 0 &&
+                size_t(a.n_mtiles) * 2 * plan.ksplit * plan.ksplit * kBM * (a.nw / plan.ksplit) <=
+                    gemm_ws_floats(num_sms))
+                   ? plan.ksplit
+                   : 0;
     if (kd == 2)
       return launch_pdl_cluster(gemm_tc2_kernel<TNP, true, 2>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
                                 Cfg2::kSmemBytes, st, 2u, wt, x, ot, a);
@@ -1777,6 +1906,13 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
         a.xstages = pxs;
         smem = size_t(ws) * wbytes + size_t(pxs) * Cfg::kXBytes + fixed;
       }
+    }
+    if (a.ksplit > 1 && size_t(stages) * stage_bytes < size_t(2) * (a.ksplit - 1) * kBM * (a.nw / a.ksplit) * 4)
+      a.ksplit = 0;  // the exchange blocks must fit the stage ring
+    if (a.ksplit > 1) {  // ksplit pairs per tile, one K part each
+      a.raster = 0;
+      return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * a.ksplit * tiles)), dim3(kThreads1),
+                                smem, st, 2u, wt, x, ot, a);
     }
     return launch_pdl_cluster(gemm_tc2_kernel<TNP, true>, dim3(unsigned(2 * pairs)), dim3(kThreads1), smem, st, 2u,
                               wt, x, ot, a);

@@ -54,6 +54,7 @@ struct GemmArgs {
   long long w_stride;
   int nw;              // set by the launcher: weight rows per pair tile of the token-major kernel
   int raster;          // set by the launcher: token tiles per raster group of the token-major kernel (0 = contiguous ranges)
+  int ksplit;          // set by the launcher: token-major kernel split over K across a 4-CTA cluster (2 pairs)
   int norm_d;
   float norm_eps;
   // filled by the launcher
@@ -81,6 +82,7 @@ struct GemmPlan {
   int cstream;   // > 1: cluster stream-K, clusters of cstream CTAs each owning whole tiles (DSMEM reduce)
   int nclusters; // cluster stream-K: number of clusters
   int nw;        // > 0: token-major CTA-pair kernel, whole tiles of nw weight rows (32..256, multiple of 32)
+  int ksplit;    // token-major pair kernel: 2 = each tile's K halves on two pairs of a 4-CTA cluster
 };
 // kind_T: rows of the whole pass (>= T); selects the kernel and split so replica
 // micro-batches compute exactly what the unreplicated pass would.
