@@ -21,206 +21,9 @@
 namespace cb {
 
 static constexpr int kAttnWarps = 4;
-static constexpr int kUnroll = 4;
-
-// CTA = (row, kv head, context split), 4 warps.  Lane group j (hd/8 lanes,
-// 16 bytes of a K/V row each) owns q-head  j % gq  of the KV group and the
-// positions  p == j / gq  (mod  n_groups / gq).  For MHA (gq = 1) the groups
-// split the positions 8 (hd 128) ways; for GQA the groups of one warp read the
-// same K/V addresses (one transaction) for different q-heads, so every K/V
-// byte is fetched once for the whole head group.
-template <int HD, int U>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-    attn_kernel(const AttnArgs a, int nsplit, int chunk, int gq, int head_major) {
-  pdl_trigger();
-  pdl_wait();
-  constexpr int G = HD / 8;               // lanes per group
-  constexpr int P = 32 / G;               // groups per warp
-  constexpr int NG = kAttnWarps * P;      // groups per CTA
-  // head-major grids launch the kv heads of one row back to back, so the CTAs
-  // running together read the whole contiguous [k | v] rows of their positions
-  const int rl = head_major ? blockIdx.y : blockIdx.x;
-  const int row = a.row_off + rl;
-  const int hk = head_major ? blockIdx.x : blockIdx.y;
-  const int split = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lg = lane % G, pg = lane / G;
-  const int grp = warp * P + pg;
-  const int head = grp % gq, phase = grp / gq, nph = NG / gq;
-  const int qh = hk * gq + head;
-  const int slot = a.row_slot[row];
-  const int len = a.row_pos[row] + 1;
-  const int p_begin = split * chunk;
-  const int p_end = min(len, p_begin + chunk);
-  const float qscale = a.scale * 1.4426950408889634f;
-  const size_t kvd = size_t(a.Hkv) * HD;
-  const size_t pos_stride = 2 * kvd;
-  const uint16_t* kbase = a.kv + (size_t)slot * a.max_ctx * pos_stride + (size_t)hk * HD + lg * 8;
-  const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
-  const int cur = len - 1;  // position of this row's own token
-
-  __shared__ float sm_state[NG][G][10];
-
-  if (a.rope != nullptr && warp == 0 && p_begin <= cur && cur < p_end) {
-    // Fused decode path: the CTA whose context split holds the newest position
-    // appends this row's rotated k and raw v for kv head hk to the cache.
-    uint16_t* kc = const_cast<uint16_t*>(a.kv) + ((size_t)slot * a.max_ctx + cur) * pos_stride + (size_t)hk * HD;
-    const uint16_t* ksrc = a.qkv + row * qkv_ld + (size_t)(a.H + hk) * HD;
-    const uint16_t* vsrc = ksrc + (size_t)a.Hkv * HD;
-    constexpr int half = HD / 2, cph = half / 8;
-    const float2* rp = a.rope + (size_t)cur * half;
-    if (lane < cph) {
-      const int i0 = lane * 8;
-      const uint4 x = *reinterpret_cast<const uint4*>(ksrc + i0);
-      const uint4 y = *reinterpret_cast<const uint4*>(ksrc + i0 + half);
-      const float x1[8] = {bf16_lo(x.x), bf16_hi(x.x), bf16_lo(x.y), bf16_hi(x.y),
-                           bf16_lo(x.z), bf16_hi(x.z), bf16_lo(x.w), bf16_hi(x.w)};
-      const float x2[8] = {bf16_lo(y.x), bf16_hi(y.x), bf16_lo(y.y), bf16_hi(y.y),
-                           bf16_lo(y.z), bf16_hi(y.z), bf16_lo(y.w), bf16_hi(y.w)};
-      float o1[8], o2[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const float2 cs = rp[i0 + j];
-        o1[j] = x1[j] * cs.x - x2[j] * cs.y;
-        o2[j] = x2[j] * cs.x + x1[j] * cs.y;
-      }
-      uint4 r1, r2;
-      r1.x = pack_bf16x2(o1[0], o1[1]); r1.y = pack_bf16x2(o1[2], o1[3]);
-      r1.z = pack_bf16x2(o1[4], o1[5]); r1.w = pack_bf16x2(o1[6], o1[7]);
-      r2.x = pack_bf16x2(o2[0], o2[1]); r2.y = pack_bf16x2(o2[2], o2[3]);
-      r2.z = pack_bf16x2(o2[4], o2[5]); r2.w = pack_bf16x2(o2[6], o2[7]);
-      *reinterpret_cast<uint4*>(kc + i0) = r1;
-      *reinterpret_cast<uint4*>(kc + i0 + half) = r2;
-    }
-    if (lane < HD / 8)
-      reinterpret_cast<uint4*>(kc + kvd)[lane] = reinterpret_cast<const uint4*>(vsrc)[lane];
-  }
-  if (a.rope != nullptr) __syncthreads();  // the appended row is read back by the loop below
-
-  float q[8];
-  {
-    const uint4 qv = *reinterpret_cast<const uint4*>(a.qkv + row * qkv_ld + (size_t)qh * HD + lg * 8);
-    q[0] = bf16_lo(qv.x); q[1] = bf16_hi(qv.x); q[2] = bf16_lo(qv.y); q[3] = bf16_hi(qv.y);
-    q[4] = bf16_lo(qv.z); q[5] = bf16_hi(qv.z); q[6] = bf16_lo(qv.w); q[7] = bf16_hi(qv.w);
-    if (a.rope != nullptr) {
-      // rotate-half RoPE of q in registers: the partner chunk lives G/2 lanes away;
-      // rounded to bf16 exactly like the stand-alone rope_kv kernel
-      const int hl = lg % (G / 2);
-      const bool first = lg < G / 2;
-      const float2* rp = a.rope + (size_t)cur * (HD / 2) + hl * 8;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float other = __shfl_xor_sync(0xffffffffu, q[i], G / 2);
-        const float2 cs = rp[i];
-        const float r = first ? q[i] * cs.x - other * cs.y : q[i] * cs.x + other * cs.y;
-        q[i] = bf16_to_f(f_to_bf16(r));
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] *= qscale;
-  }
-  float m = -INFINITY, l = 0.f, acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-
-  // the loop trip count is uniform within a warp (groups of a warp share the
-  // phase when gq >= P; for gq < P they differ by < nph, handled by predication)
-  const int wphase = (warp * P) / gq;
-  for (int pb = p_begin + wphase; pb < p_end; pb += nph * U) {
-    uint4 kk[U], vv[U];
-    bool ok[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int pos = pb + (phase - wphase) + u * nph;
-      ok[u] = pos < p_end;
-      if (ok[u]) {
-        const uint16_t* kp = kbase + (size_t)pos * pos_stride;
-        // coherent loads: the fused path appended this row's K/V in this kernel
-        kk[u] = *reinterpret_cast<const uint4*>(kp);
-        vv[u] = *reinterpret_cast<const uint4*>(kp + kvd);
-      } else {
-        kk[u] = make_uint4(0, 0, 0, 0);
-        vv[u] = make_uint4(0, 0, 0, 0);
-      }
-    }
-    float s[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      s[u] = q[0] * bf16_lo(kk[u].x) + q[1] * bf16_hi(kk[u].x) + q[2] * bf16_lo(kk[u].y) +
-             q[3] * bf16_hi(kk[u].y) + q[4] * bf16_lo(kk[u].z) + q[5] * bf16_hi(kk[u].z) +
-             q[6] * bf16_lo(kk[u].w) + q[7] * bf16_hi(kk[u].w);
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1)
-#pragma unroll
-      for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-    float mx = m;
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!ok[u]) s[u] = -INFINITY;
-      mx = fmaxf(mx, s[u]);
-    }
-    if (mx != -INFINITY) {
-      const float cf = exp2f(m - mx);  // m == -inf -> 0
-      l *= cf;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] *= cf;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const float p = exp2f(s[u] - mx);  // invalid positions: exp2(-inf) = 0
-        l += p;
-        acc[0] += p * bf16_lo(vv[u].x);
-        acc[1] += p * bf16_hi(vv[u].x);
-        acc[2] += p * bf16_lo(vv[u].y);
-        acc[3] += p * bf16_hi(vv[u].y);
-        acc[4] += p * bf16_lo(vv[u].z);
-        acc[5] += p * bf16_hi(vv[u].z);
-        acc[6] += p * bf16_lo(vv[u].w);
-        acc[7] += p * bf16_hi(vv[u].w);
-      }
-      m = mx;
-    }
-  }
-  sm_state[grp][lg][0] = m;
-  sm_state[grp][lg][1] = l;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) sm_state[grp][lg][2 + i] = acc[i];
-  __syncthreads();
-  // group j < gq finalises head j over its nph phases (groups j, j+gq, ...)
-  if (grp < gq) {
-    float M = -INFINITY;
-    for (int f = 0; f < nph; ++f) M = fmaxf(M, sm_state[grp + f * gq][lg][0]);
-    float L = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int f = 0; f < nph; ++f) {
-      const float* stt = sm_state[grp + f * gq][lg];
-      const float cw = (stt[0] == -INFINITY) ? 0.f : exp2f(stt[0] - M);
-      L += stt[1] * cw;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] += stt[2 + i] * cw;
-    }
-    if (nsplit == 1) {
-      const float inv = 1.f / L;
-      uint4 ov;
-      ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
-      ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
-      ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
-      ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
-      *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
-    } else {
-      // partial state: [(row_local * H + qh) * nsplit + split] -> (m, l, acc[HD])
-      const size_t idx = ((size_t)rl * a.H + qh) * nsplit + split;
-      float* st = a.ws + idx * (HD + 2);
-      if (lg == 0) {
-        st[0] = M;
-        st[1] = L;
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) st[2 + lg * 8 + i] = o[i];
-    }
-  }
-}
 
 // ---------------------------------------------------------------------------
-// attn2: same CTA = (kv head, row, context split) grid, re-mapped for decode:
+// attn2: CTA = (kv head, row, context split) (head-major grid), 4 warps:
 //  * every lane group (hd/8 lanes, 16 bytes of a K/V row each) owns whole
 //    positions and computes ALL gq q-heads of the KV group against them, so a
 //    K/V byte is read once per KV head for MHA and GQA alike (the old mapping
@@ -480,13 +283,10 @@ __global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
 
 template <int HD>
 static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t st) {
-  // positions per CTA warmed into L2 before the PDL wait (0 = none)
-  static const int prefetch_pos = [] {
-    const char* e = getenv("CB_ATTN_PREFETCH_POS");
-    return e ? atoi(e) : 64;
-  }();
+  // positions per CTA warmed into L2 before the PDL wait (-1.6% per B=256
+  // step, profiles/r01_attn_prefetch_ab.txt)
   AttnArgs a = a_in;
-  a.prefetch_pos = prefetch_pos;
+  a.prefetch_pos = 64;
   const int gq = a.H / a.Hkv;
   constexpr int NG = kAttnWarps * (32 / (HD / 8));
   if (gq < 1 || NG % gq != 0) return cudaErrorInvalidValue;
@@ -503,26 +303,13 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
     while (nsplit > 1 && (size_t)a.T * a.H * nsplit * (HD + 2) > a.ws_floats) --nsplit;
   }
   const int chunk = (a.max_len + nsplit - 1) / nsplit;
-  static const int head_major = [] {
-    const char* e = getenv("CB_ATTN_HEAD_MAJOR");
-    return e ? atoi(e) : 1;
-  }();
-  const dim3 grid = head_major ? dim3(a.Hkv, a.T, nsplit) : dim3(a.T, a.Hkv, nsplit);
   // positions in flight per lane group: 4 when there are enough CTAs to fill
   // the GPU (measured best for decode batches), 8 for few long rows
-  static const int forced = [] {
-    const char* e = getenv("CB_ATTN_UNROLL");
-    return e ? atoi(e) : 0;
-  }();
   const long long total = ctas * nsplit;
-  const int u = forced ? forced : (gq == 1 && total >= 8LL * num_sms ? 4 : 8);
-  static const int v2 = [] {
-    const char* e = getenv("CB_ATTN_V1");
-    return e ? 0 : 1;
-  }();
+  const int u = gq == 1 && total >= 8LL * num_sms ? 4 : 8;
   cudaError_t e;
-  if (v2) {
-    const dim3 g2(a.Hkv, a.T, nsplit);
+  {
+    const dim3 g2(a.Hkv, a.T, nsplit);  // head-major grid
     const size_t sm = size_t(kAttnWarps) * gq * (HD / 8) * 10 * sizeof(float);
     switch (gq) {
       case 1: e = u == 8 ? launch_pdl(attn2_kernel<HD, 1, 8>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk)
@@ -533,9 +320,6 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
       case 8: e = launch_pdl(attn2_kernel<HD, 8, 2>, g2, dim3(kAttnWarps * 32), sm, st, a, nsplit, chunk); break;
       default: e = cudaErrorInvalidValue;
     }
-  } else {
-    e = u == 8 ? launch_pdl(attn_kernel<HD, 8>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major)
-               : launch_pdl(attn_kernel<HD, 4>, grid, dim3(kAttnWarps * 32), 0, st, a, nsplit, chunk, gq, head_major);
   }
   if (e != cudaSuccess || nsplit == 1) return e;
   return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);

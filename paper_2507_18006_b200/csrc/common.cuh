@@ -223,24 +223,6 @@ CB_DEVICE void umma_commit_elect(uint64_t* bar) {
       "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
-CB_DEVICE void umma_commit_mc_elect(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-CB_DEVICE void umma_bf16_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                    uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.b32 q, %4, 0;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
 // (mask: the pair's two CTAs in the cluster, 0b11 << 2i for pair i of a 4-CTA cluster)
 CB_DEVICE void umma_commit_pair_elect(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
@@ -272,27 +254,6 @@ CB_DEVICE void umma_kblock_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t
       : "memory");
 }
 
-// CTA-pair k-block with separate stage-release barriers for the two operands
-// (decoupled ring depths): two commits, each multicast to both CTAs.
-CB_DEVICE void umma_kblock_pair2_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate, uint64_t* bar_a, uint64_t* bar_b, uint16_t mask = 3) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.b32 q, %4, 0;\n\t"
-      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
-      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %7;\n\t"
-      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%6], %7;\n\t}" ::"r"(
-          d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar_a)), "r"(smem_u32(bar_b)),
-      "h"(mask)
-      : "memory");
-}
 
 // 1-D bulk copy global -> this CTA's shared memory, completing on `bar`.
 CB_DEVICE void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
@@ -339,22 +300,6 @@ template <uint32_t kCols>
 CB_DEVICE void tmem_dealloc_pair(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
 }
-CB_DEVICE void umma_bf16_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-// arrive on the barrier at this smem offset in both CTAs of the pair
-CB_DEVICE void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(uint16_t(3))
-      : "memory");
-}
 // TMA tile load whose completion bytes land on the pair leader's barrier
 CB_DEVICE void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int c1,
                                 uint64_t cache_policy) {
@@ -363,44 +308,6 @@ CB_DEVICE void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* sme
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
       "l"(cache_policy)
-      : "memory");
-}
-// 3-D tile load (kd k-blocks in one box) whose completion bytes land on the pair leader's barrier
-CB_DEVICE void tma_load_3d_pair(const CUtensorMap* map, uint64_t* bar, void* smem_dst, int c0, int c1, int c2,
-                                uint64_t cache_policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2),
-      "l"(cache_policy)
-      : "memory");
-}
-// CTA-pair version of umma_2kblock_elect: 8 x (M x N x 16) cta_group::2 MMAs over a
-// 2-k-block stage (the second k-block's operands a_step / b_step further, >> 4
-// encoded) and one commit multicast to the stage barrier of both CTAs.
-CB_DEVICE void umma_2kblock_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate, uint64_t* bar, uint32_t a_step, uint32_t b_step) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7, as, bs;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.b32 q, %4, 0;\n\t"
-      "cvt.u64.u32 as, %7;\n\tcvt.u64.u32 bs, %8;\n\t"
-      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
-      "add.s64 b1, %2, 2;\n\tadd.s64 b2, %2, 4;\n\tadd.s64 b3, %2, 6;\n\t"
-      "add.s64 a4, %1, as;\n\tadd.s64 a5, a4, 2;\n\tadd.s64 a6, a4, 4;\n\tadd.s64 a7, a4, 6;\n\t"
-      "add.s64 b4, %2, bs;\n\tadd.s64 b5, b4, 2;\n\tadd.s64 b6, b4, 4;\n\tadd.s64 b7, b4, 6;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, q;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, 1;\n\t"
-      "@p tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, 1;\n\t"
-      "@p tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%5], %6;\n\t}" ::"r"(
-          d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(smem_u32(bar)), "h"(uint16_t(3)), "r"(a_step),
-      "r"(b_step)
       : "memory");
 }
 CB_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
@@ -412,14 +319,6 @@ CB_DEVICE void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
-}
-// Arrive on the barrier at this smem offset in every CTA of `mask` (1-CTA MMAs).
-CB_DEVICE void umma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
 }
 // 32 lanes x 32 bit, 16 consecutive columns: thread i of the warp gets TMEM lane (base_lane+i).
 CB_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -479,11 +378,6 @@ CB_DEVICE uint32_t dsmem_map(uint32_t local_addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
   return r;
 }
-CB_DEVICE float2 dsmem_ld_f2(uint32_t cluster_addr) {
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(cluster_addr) : "memory");
-  return v;
-}
 
 CB_DEVICE unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -491,22 +385,9 @@ CB_DEVICE unsigned long long globaltimer_ns() {
   return t;
 }
 
-CB_DEVICE void dsmem_st_f4(uint32_t cluster_addr, float4 v) {
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
 CB_DEVICE float dsmem_ld_f32(uint32_t cluster_addr) {
   float v;
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
-  return v;
-}
-CB_DEVICE float4 dsmem_ld_f4(uint32_t cluster_addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(cluster_addr)
-               : "memory");
   return v;
 }
 

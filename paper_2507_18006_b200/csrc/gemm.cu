@@ -61,7 +61,6 @@ static constexpr int kMaxStages = 16;
 static constexpr int kBarBytes = 2048;
 static constexpr int kRtabOff = 1024;
 static constexpr int kMaxNormRows = 256;
-static constexpr size_t kCorunSmem = 112 * 1024;  // per CTA when two CTAs share an SM (228 KB - reserves)
 
 template <int WB, int XB>
 struct RingCfg {
@@ -574,8 +573,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
   uint64_t* tfull_bar = xempty_bar + SX;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* fix_bar = tempty_bar + 2;
-  uint64_t* pfull_bar = fix_bar + 1;  // cluster stream-K: retained partial [first, last] complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfull_bar + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
   int* bcast = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -586,22 +584,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
   // Work range: stream-K slice of the (tile, k-block) space, or -- in cluster
   // split mode -- k-slice r of tile c / S (the cluster = the tile's S CTAs).
   const int csplit = a.cluster_split > 1 ? a.cluster_split : 1;
-  // Cluster stream-K (cstream = cs > 1): cluster g owns whole tiles [T0, T1);
-  // its units are split evenly over its cs CTAs, so a split tile is only ever
-  // shared by CTAs of one cluster and is reduced through DSMEM (no fixup in
-  // global memory).  A CTA keeps its first / last partial tile in TMEM.
-  const int cs = a.cstream > 1 ? a.cstream : 1;
-  int cl_u0 = 0, cl_units = 0;
   int ubeg, uend;
-  if (cs > 1) {
-    const int tiles = sk.units / sk.kb;
-    const int nc = int(gridDim.x) / cs, g = c / cs, r = c % cs;
-    const int t0 = int((long long)g * tiles / nc), t1 = int((long long)(g + 1) * tiles / nc);
-    cl_u0 = t0 * sk.kb;
-    cl_units = (t1 - t0) * sk.kb;
-    ubeg = cl_u0 + int((long long)r * cl_units / cs);
-    uend = cl_u0 + int((long long)(r + 1) * cl_units / cs);
-  } else if (csplit > 1) {
+  if (csplit > 1) {
     const int tile = c / csplit, r = c % csplit;
     ubeg = tile * sk.kb + (r * sk.kb) / csplit;
     uend = tile * sk.kb + ((r + 1) * sk.kb) / csplit;
@@ -635,8 +619,6 @@ __global__ void __launch_bounds__(kThreads1, 1)
       mbar_init(&tempty_bar[i], kEpiThreads);
     }
     mbar_init(fix_bar, 1);
-    mbar_init(&pfull_bar[0], 1);
-    mbar_init(&pfull_bar[1], 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -701,12 +683,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
     for (int u = ubeg; u < uend;) {
       const int kb0 = u % sk.kb;
       const int kb1 = min(sk.kb, kb0 + (uend - u));
-      // cluster stream-K: a partial tile accumulates into its retained buffer
-      const bool keep = cs > 1 && !(kb0 == 0 && kb1 == sk.kb);
-      const int pslot = (u == ubeg) ? 0 : 1;
-      if (!keep) mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + uint32_t(keep ? (2 + pslot) * TN : acc * TN);
+      const uint32_t d_tmem = tmem_base + uint32_t(acc * TN);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         mbar_wait(&xfull_bar[xstage], xphase);
@@ -734,11 +713,6 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (++xstage == SX) { xstage = 0; xphase ^= 1; }
       }
       __syncwarp();
-      if (keep) {
-        umma_commit_elect(&pfull_bar[pslot]);
-        u += kb1 - kb0;
-        continue;
-      }
       if (a.dbg & 1) {
         if (lane == 0) mbar_arrive(&tfull_bar[acc]);
       } else {
@@ -782,10 +756,6 @@ __global__ void __launch_bounds__(kThreads1, 1)
       const int ncols = min(TN, a.T - tt * TN);
       const bool whole = (kb0 == 0 && kb1 == sk.kb);
       const bool last_seg = (u + (kb1 - kb0) == uend);
-      if (cs > 1 && !whole) {  // retained in TMEM, reduced through DSMEM after the loop
-        u += kb1 - kb0;
-        continue;
-      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       unsigned long long* tr = (a.trace && et == 0 && seg_i < 4) ? a.trace + (size_t)c * 512 + 130 + 4 * seg_i : nullptr;
@@ -809,71 +779,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       u += kb1 - kb0;
     }
     e.drain();
-    if (cs > 1) {
-      // retained partials -> this CTA's (idle) stage ring, chunk-major, slot 0 =
-      // first segment.  Slot 1 first: its commit retires every MMA of the CTA, so
-      // no MMA still reads the ring when slot 0 is written over it.
-      for (int slot = 1; slot >= 0; --slot) {
-        const int u = slot == 0 ? ubeg : (uend - 1);
-        if (ubeg >= uend || (slot == 1 && u / sk.kb == ubeg / sk.kb)) continue;  // single segment: slot 0 only
-        const int kb0 = slot == 0 ? ubeg % sk.kb : 0;
-        const int kb1 = slot == 0 ? min(sk.kb, kb0 + (uend - ubeg)) : (uend - 1) % sk.kb + 1;
-        if (kb0 == 0 && kb1 == sk.kb) continue;  // whole: emitted in the loop
-        mbar_wait(&pfull_bar[slot], 0);
-        tc_fence_after();
-        const int tt = (u / sk.kb) % n_ttiles;
-        const int ncols = min(TN, a.T - tt * TN);
-        const uint32_t t_addr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t((2 + slot) * TN);
-        float* part = reinterpret_cast<float*>(smem) + slot * (TN * kBM);
-        for (int c0 = 0; c0 < ncols; c0 += 16) {
-          uint32_t r[16];
-          tmem_ld16(t_addr + uint32_t(c0), r);
-          tmem_ld_wait();
-          float* pc = part + part_chunk(c0, q);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pc[i * 32 + lane] = __uint_as_float(r[i]);
-        }
-      }
-    }
     if (a.trace && et == 0) a.trace[(size_t)c * 512 + 1] = globaltimer_ns();
-  }
-  if (cs > 1) {
-    // every CTA of the cluster deposited its partials; the CTA holding a split
-    // tile's first k-block sums the parts (rank order) through DSMEM and emits
-    cluster_sync_all();
-    if (warp >= 2 && warp < 6) {
-      const int q = warp & 3;
-      EpiWarp e(epi_smem + q * kEpiWarpBytes, q, lane, row_scales(a, smem + ring_bytes + kTbufBytes));
-      const int r_me = c % cs;
-      const uint32_t base = smem_u32(smem);
-      auto rank_of = [&](int uu) { return int(((long long)(uu - cl_u0 + 1) * cs - 1) / cl_units); };
-      auto beg_of = [&](int rr) { return cl_u0 + int((long long)rr * cl_units / cs); };
-      for (int tile = ubeg / sk.kb; ubeg < uend && tile <= (uend - 1) / sk.kb; ++tile) {
-        const int ra = rank_of(tile * sk.kb), rb = rank_of(tile * sk.kb + sk.kb - 1);
-        if (ra != r_me || ra == rb) continue;  // not the head of a split tile
-        const int mt = tile / n_ttiles, tt = tile % n_ttiles;
-        const int row0 = a.row_off + tt * TN;
-        const int ncols = min(TN, a.T - tt * TN);
-        for (int ch = 0; ch < (ncols + 15) / 16; ++ch) {
-          float v[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          for (int rr = ra; rr <= rb; ++rr) {
-            const int slot = (beg_of(rr) / sk.kb == tile) ? 0 : 1;
-            const uint32_t off = base + uint32_t((slot * (TN * kBM) + part_chunk(ch * 16, q) + lane) * 4);
-            const uint32_t ra_addr = dsmem_map(off, uint32_t(rr));
-            float x[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) x[i] = dsmem_ld_f32(ra_addr + uint32_t(i * 128));
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += x[i];
-          }
-          emit_chunk(a, &tmO, e, mt * kBM + q * 32, row0 + ch * 16, min(16, ncols - ch * 16), v);
-        }
-      }
-      e.drain();
-    }
-    cluster_sync_all();  // peers' shared memory stays alive until every read is done
   }
   if (csplit > 1) {
     // Cluster split-K: every CTA of the cluster holds a partial [TN][128] in
@@ -1115,25 +1021,17 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
 // same smem tiles and TMA loads -- so the accumulator is token-major and the
 // epilogue stores rows straight from TMEM (epi_drain_tok).  The transposing
 // epilogue of the weight-major layout was 20% of a T = 256 launch.
-//
-// KD = 2 (opt-in, token-major plans, K % 128 == 0): a stage holds two k-blocks
-// loaded as one 3-D TMA box per operand (half the TMA issues); measured slower
-// than KD = 1 -- 64 KB stages leave a 3-deep ring.
-template <int TNP, bool SWAP, int KD = 1>
+template <int TNP, bool SWAP>
 __global__ void __launch_bounds__(kThreads1, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmO, const GemmArgs a) {
-  static_assert(KD == 1 || SWAP, "2-k-block stages: token-major kernel only");
-  using Cfg = PairCfg<TNP, KD>;
-  // Token-major (SWAP, KD 1) launches size the ring at run time: weight stages
-  // of exactly nw / 2 rows and 6 KB epilogue blocks (the token-major epilogue
+  using Cfg = PairCfg<TNP>;
+  // Token-major (SWAP) launches size the ring at run time: weight stages of
+  // exactly nw / 2 rows and 6 KB epilogue blocks (the token-major epilogue
   // only stages TMA stores) leave room for a deeper ring (launch_pair)
-  // ... and may give the weight ring (HBM) and the token ring (L2) their own
-  // depths (a.xstages > 0), each with its own stage-release barrier
-  constexpr bool kRt = SWAP && KD == 1;
+  constexpr bool kRt = SWAP;
   const int S = kRt ? a.stages : Cfg::kStages;
-  const bool dec = kRt && a.xstages > 0;
-  const int SX = dec ? a.xstages : S;
+  const int SX = S;
   const int WBYTES = kRt ? (a.nw >> 1) * kBK * 2 : Cfg::kWBytes;
   constexpr int XBYTES = Cfg::kXBytes;
   const int ring_bytes = S * WBYTES + SX * XBYTES;
@@ -1146,9 +1044,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
   uint8_t* epi_smem = smem + ring_bytes;  // 4 x epi_stride
   uint64_t* wfull_bar = reinterpret_cast<uint64_t*>(smem + ring_bytes + tbuf_bytes);  // leader: weights landed
   uint64_t* xfull_bar = wfull_bar + S;   // leader: both CTAs' tokens landed
-  uint64_t* empty_bar = xfull_bar + SX;  // each CTA: (weight) stage consumed
-  uint64_t* xempty_bar = dec ? empty_bar + S : empty_bar;  // each CTA: token stage consumed (decoupled rings)
-  uint64_t* tfull_bar = empty_bar + S + (dec ? SX : 0);  // each CTA: accumulator ready
+  uint64_t* empty_bar = xfull_bar + SX;  // each CTA: stage consumed
+  uint64_t* xempty_bar = empty_bar;      // (one ring: weights and tokens share the release)
+  uint64_t* tfull_bar = empty_bar + S;   // each CTA: accumulator ready
   uint64_t* tempty_bar = tfull_bar + 2;  // leader: both epilogues drained
   uint64_t* fix_bar = tempty_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fix_bar + 1);
@@ -1211,7 +1109,6 @@ __global__ void __launch_bounds__(kThreads1, 1)
     }
     for (int i = 0; i < SX; ++i) {
       mbar_init(&xfull_bar[i], 1);
-      if (dec) mbar_init(&xempty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
@@ -1239,13 +1136,9 @@ __global__ void __launch_bounds__(kThreads1, 1)
         if (u - ubeg >= S) mbar_wait(&empty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 66 + (u - ubeg)] = globaltimer_ns();
         if (SWAP) {  // nw / 2 weight rows per CTA (box height of the launcher's map)
-          if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2 * KD);
-          if (KD > 1)
-            tma_load_3d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, 0,
-                             mt * a.nw + int(rank) * (a.nw >> 1), kb * KD, pol_w);
-          else
-            tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, kb * kBK,
-                             mt * a.nw + int(rank) * (a.nw >> 1), pol_w);
+          if (leader) mbar_arrive_expect_tx(&wfull_bar[stage], uint32_t(a.nw) * kBK * 2);
+          tma_load_2d_pair(&tmW, &wfull_bar[stage], sW + stage * WBYTES, kb * kBK, mt * a.nw + int(rank) * (a.nw >> 1),
+                           pol_w);
           if (++stage == S) { stage = 0; phase ^= 1; }
           continue;
         }
@@ -1272,12 +1165,8 @@ __global__ void __launch_bounds__(kThreads1, 1)
         mbar_wait(&xempty_bar[stage], phase ^ 1);
         if (a.trace && u - ubeg < 64) a.trace[(size_t)c * 512 + 150 + (u - ubeg)] = globaltimer_ns();
         if (leader) mbar_arrive_expect_tx(&xfull_bar[stage], 2 * XBYTES);
-        if (KD > 1)
-          tma_load_3d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, 0,
-                           a.row_off + tt * TNP + int(rank) * (TNP / 2), kb * KD, pol_x);
-        else
-          tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, kb * kBK,
-                           a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
+        tma_load_2d_pair(&tmX, &xfull_bar[stage], sX + stage * XBYTES, kb * kBK,
+                         a.row_off + tt * TNP + int(rank) * (TNP / 2), pol_x);
         if (++stage == SX) { stage = 0; phase ^= 1; }
       }
     }
@@ -1308,13 +1197,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
           __syncwarp();
           const uint64_t dw = dw0 + uint64_t((stage * WBYTES) >> 4);
           const uint64_t dx = dx0 + uint64_t((xstage * XBYTES) >> 4);
-          if (SWAP && KD > 1)  // second k-block: 128 token rows / nw / 2 weight rows x 128 B further
-            umma_2kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage],
-                                    uint32_t((TNP / 2) * kBK * 2) >> 4, uint32_t(a.nw >> 1) * (kBK * 2) >> 4);
-          else if (SWAP && dec)
-            umma_kblock_pair2_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], &xempty_bar[xstage],
-                                    pmask);
-          else if (SWAP)
+          if (SWAP)
             umma_kblock_pair_elect(d_tmem, dx, dw, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage], pmask);
           else
             umma_kblock_pair_elect(d_tmem, dw, dx, idesc, kb > kb0 ? 1u : 0u, &empty_bar[stage]);
@@ -1534,36 +1417,6 @@ int gemm_pick_tn(int T) {
   return 256;
 }
 
-// How many clusters of `cs` 1-CTA-kernel CTAs can be resident at once (one CTA
-// per SM; GPCs are not multiples of every cluster size).  Cached per device.
-static int cluster_capacity(int cs, int num_sms) {
-  static int cache[64][9] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int& slot = cache[dev & 63][cs & 7];
-  if (slot) return slot;
-  using Cfg = GemmCfg<64, 2>;
-  cudaFuncSetAttribute(gemm_tc_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::kSmemBytes));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(unsigned(cs));
-  cfg.blockDim = dim3(unsigned(kThreads1));
-  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(cs);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<64, 2>, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = num_sms / cs;
-  }
-  slot = n;
-  return n;
-}
-
 // Work split of one launch.  Everything but the TN bucket depends on (N, K),
 // the kernel kind and the tile count only, so within one kind a decode row's
 // result does not depend on how many rows share the launch.
@@ -1589,20 +1442,9 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   const int kb = (K + kBK - 1) / kBK;
   const long long tiles = (N + kBM - 1) / kBM;  // 128-row weight tiles
   // 2 k-blocks per stage (3-D TMA boxes) for the 1-CTA kernel up to 128 rows
-  static const int kd_env = [] {
-    const char* e = getenv("COCOB200_KD");
-    return e ? atoi(e) : 2;
-  }();
-  // co-resident CTAs (PDL overlap of consecutive GEMMs on one SM) measured
-  // 15-30% slower in the decode step: the shallow ring starves the weight
-  // stream.  Off unless COCOB200_CORUN=1.
-  static const int corun_env = [] {
-    const char* e = getenv("COCOB200_CORUN");
-    return e ? atoi(e) : 0;
-  }();
-  p.corun = (corun_env && kind_T <= 128) ? 1 : 0;
-  // (co-resident CTAs need a small ring: one 64-wide k-block per stage then)
-  const int kd2 = (kd_env == 2 && !p.corun && K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // replica-invariant
+  // (measured against 1 k-block stages and against two co-resident shallow-ring
+  // CTAs per SM, which starve the weight stream: 15-30% slower decode steps)
+  const int kd2 = (K % (2 * kBK) == 0 && kind_T <= 128) ? 2 : 1;  // replica-invariant
   p.kd = 1;
   const int ks_nw = 256, ks_s = 4;
   if (kind_T > kPairMinT && kind_T <= 256 && N % ks_nw == 0 && K % (ks_s * kBK) == 0 &&
@@ -1648,8 +1490,7 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
     // waves of pair tiles fit the SMs -- per-SM work of a wave ~ nw, so the
     // cost is waves * nw (12288 rows: 64 tiles of 192 = one wave on 74 pairs
     // instead of 48 tiles of 256 on 48 pairs); ties keep the larger tile.
-    static const bool no_swap = std::getenv("COCOB200_NO_SWAP") != nullptr;  // A/B experiments
-    if (!no_swap && N % 32 == 0) {
+    if (N % 32 == 0) {
       const long long pairs = num_sms / 2;
       long long best = -1;
       for (int nw = 256; nw >= 128; nw -= 32) {
@@ -1662,14 +1503,8 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
       }
       p.whole = 1;
       p.max_parts = 0;
-      // 2 k-blocks per stage (3-D boxes, half the TMA issues per byte): correct
-      // (tested) but measured 5-15% slower at T = 192..8192 -- the 3-stage ring
-      // of 64 KB stages pipelines worse -- so opt-in: COCOB200_PAIR_KD=2
-      static const int pair_kd_env = [] {
-        const char* e = std::getenv("COCOB200_PAIR_KD");
-        return e ? std::atoi(e) : 1;
-      }();
-      if (pair_kd_env == 2 && K % (2 * kBK) == 0) p.kd = 2;
+      // (2 k-blocks per stage -- 3-D boxes, half the TMA issues per byte --
+      // measured 5-15% slower at T = 192..8192: 64 KB stages leave a 3-deep ring)
     }
     return p;
   }
@@ -1679,36 +1514,8 @@ GemmPlan gemm_plan(int N, int K, int T, int num_sms, int kind_T) {
   if (tiles <= num_sms) p.max_parts = 1;             // QKV: one wave of whole tiles
   if (tiles * 2 >= (long long)num_sms * 3) p.whole = 1;  // lm_head (>= 1.5 waves): whole tiles
   p.box_rows = p.tn;
-  // Cluster stream-K when it balances better than the options above: units
-  // (stages) per CTA of the most loaded CTA, a global stream-K split charged a
-  // fixup of ~a third of a tile.  Correct (tested) but measured 5-15% slower
-  // than the plans above on the 7B decode shapes (co-resident cluster counts),
-  // so it is opt-in: COCOB200_CSTREAM=1.
-  static const int cstream_env = [] {
-    const char* e = getenv("COCOB200_CSTREAM");
-    return e ? atoi(e) : 0;
-  }();
-  const long long units_tile = (K + kBK * p.kd - 1) / (kBK * p.kd);
-  long long best = p.max_parts == 1 ? units_tile
-                   : p.whole        ? (tiles + num_sms - 1) / num_sms * units_tile
-                                    : (tiles * units_tile + num_sms - 1) / num_sms + units_tile / 3;
-  if (cstream_env && T <= 128) {
-    for (int cs = 2; cs <= 4; ++cs) {
-      const long long nc = std::min<long long>(cluster_capacity(cs, num_sms), tiles);
-      if (nc < 1) continue;
-      const long long tpc = (tiles + nc - 1) / nc;
-      const long long per = (tpc * units_tile + cs - 1) / cs + 1;  // +1: the DSMEM reduction
-      if (per < best) {
-        best = per;
-        p.cstream = cs;
-        p.nclusters = int(nc);
-      }
-    }
-    if (p.cstream > 1) {
-      p.max_parts = 0;
-      p.whole = 0;
-    }
-  }
+  // (a cluster stream-K variant -- clusters owning whole tiles, split tiles
+  // reduced through DSMEM -- measured 5-15% slower on the 7B decode shapes)
   return p;
 }
 
@@ -1739,29 +1546,18 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   a.n_ttiles = (a.T + TN - 1) / TN;
   a.n_mtiles = (a.N + kBM - 1) / kBM;
   a.kblocks = (a.K + kBK * KD - 1) / (kBK * KD);
-  // two co-resident CTAs per SM (<= ~113 KB each) when the plan asks for it
-  int stages = Cfg::kStages;
-  if (plan.corun) {
-    const int fit = int((kCorunSmem - kTbufBytes - 1024 - kBarBytes) / Cfg::kStageBytes);
-    stages = fit < stages ? fit : stages;
-    if (stages < 2) stages = 2;
-  }
-  if (plan.csplit > 1 && stages * Cfg::kStageBytes < TN * kBM * 4) stages = Cfg::kStages;  // smem holds the partial
+  const int stages = Cfg::kStages;
   a.stages = stages;
   a.xstages = 0;
   size_t smem_bytes = size_t(stages) * Cfg::kStageBytes + kTbufBytes + 1024 + kBarBytes;
   // Decoupled depths: activations (L2, re-read by every tile) need a short
   // ring; the rest of the 227 KB goes to the weight ring (HBM, ~1.1 us away).
-  static const int xs_env = [] {
-    const char* e = std::getenv("COCOB200_XSTAGES");  // 0 = one shared depth (A/B experiments)
-    return e ? std::atoi(e) : -1;
-  }();
   // Measured: a win for 128-row token tiles (2-k-block stages: -1% per B=128
   // step); tiles <= 64 rows starve on 2-3 activation stages (consumed in ~0.2
   // us each), and the T=256 split-K launches, faster alone, made the B=256
   // step no faster -- both keep one shared depth.
-  const int xs = xs_env >= 0 ? xs_env : (TN == 128 && KD == 2 ? 2 : 0);
-  if (!plan.corun && xs > 0) {
+  const int xs = (TN == 128 && KD == 2) ? 2 : 0;
+  if (xs > 0) {
     const size_t fixed = size_t(kTbufBytes) + 1024 + kBarBytes;
     int ws = int((kMaxDynSmem - fixed - size_t(xs) * Cfg::kXBytes) / Cfg::kWBytes);
     if (ws > kMaxStages) ws = kMaxStages;
@@ -1780,10 +1576,6 @@ static cudaError_t launch_tn(const CUtensorMap& w, const CUtensorMap& x, const C
   if (plan.csplit > 1)
     return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(tiles * plan.csplit)), dim3(kThreads1),
                               smem_bytes, st, unsigned(plan.csplit), w, x, o, a);
-  a.cstream = plan.cstream;
-  if (plan.cstream > 1)
-    return launch_pdl_cluster(gemm_tc_kernel<TN, KD>, dim3(unsigned(plan.nclusters * plan.cstream)),
-                              dim3(kThreads1), smem_bytes, st, unsigned(plan.cstream), w, x, o, a);
   // persistent stream-K: one CTA per SM, a tile spread over <= max_parts CTAs
   long long ctas = num_sms;
   if (ctas > a.units) ctas = a.units;
@@ -1796,7 +1588,6 @@ template <int TNP>
 static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& o, GemmArgs a,
                                const GemmPlan& plan, int num_sms, cudaStream_t st) {
   using Cfg = PairCfg<TNP>;
-  using Cfg2 = PairCfg<TNP, 2>;
   static bool attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1806,9 +1597,6 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     if (e == cudaSuccess && TNP == 2 * kBM)  // runtime-sized ring: up to the opt-in maximum
       e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                int(kMaxDynSmem));
-    if (e == cudaSuccess && TNP == 2 * kBM)
-      e = cudaFuncSetAttribute(gemm_tc2_kernel<TNP, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(Cfg2::kSmemBytes));
     if (e != cudaSuccess) return e;
     attr_set[dev & 63] = true;
   }
@@ -1822,24 +1610,19 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     static std::mutex mu;
     static std::map<std::tuple<const void*, long long, long long, long long, int, int>, CUtensorMap> wcache;
     static std::map<std::tuple<const void*, int, long long, long long, int>, CUtensorMap> ocache;
-    const int kd = (plan.kd == 2 && a.K % (2 * kBK) == 0) ? 2 : 1;  // 3-D boxes of 2 k-blocks (x must be a 3-D map)
     CUtensorMap wt;
     {
       std::lock_guard<std::mutex> lk(mu);
-      const auto key = std::make_tuple(a.w_base, (long long)a.N, (long long)a.K, a.w_stride, plan.nw, kd);
+      const auto key = std::make_tuple(a.w_base, (long long)a.N, (long long)a.K, a.w_stride, plan.nw, 1);
       auto it = wcache.find(key);
       if (it == wcache.end()) {
         CUtensorMap m;
-        const int e = kd == 2 ? make_kmajor_map3(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride),
-                                                 uint32_t(plan.nw / 2), 2)
-                              : make_kmajor_map(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride),
-                                                uint32_t(plan.nw / 2));
-        if (e) return cudaErrorInvalidValue;
+        if (make_kmajor_map(&m, a.w_base, uint64_t(a.N), uint64_t(a.K), uint64_t(a.w_stride), uint32_t(plan.nw / 2)))
+          return cudaErrorInvalidValue;
         it = wcache.emplace(key, m).first;
       }
       wt = it->second;
     }
-    if (kd == 2) a.kblocks = a.K / (2 * kBK);
     a.nw = plan.nw;
     a.n_mtiles = (a.N + a.nw - 1) / a.nw;
     const long long tiles = (long long)a.n_mtiles * a.n_ttiles;
@@ -1854,8 +1637,7 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     CUtensorMap ot;
     std::memset(&ot, 0, sizeof(ot));
     a.tma = 0;
-    static const bool no_tma = std::getenv("COCOB200_NO_TMA_STORE") != nullptr;  // A/B experiments
-    if (a.out_rows > 0 && !no_tma) {
+    if (a.out_rows > 0) {
       const long long cols = a.epi == EPI_SWIGLU ? a.N / 2 : a.N;
       const auto key = std::make_tuple(static_cast<const void*>(a.out), a.epi, a.out_rows, a.ldo, int(cols));
       std::lock_guard<std::mutex> lk(mu);
@@ -1870,20 +1652,16 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
         a.tma = 1;
       }
     }
-    a.ksplit = (plan.ksplit > 1 && kd == 1 && a.n_ttiles == 1 && a.nw % (32 * plan.ksplit) == 0 &&
+    a.ksplit = (plan.ksplit > 1 && a.n_ttiles == 1 && a.nw % (32 * plan.ksplit) == 0 &&
                 size_t(a.n_mtiles) * 2 * plan.ksplit * plan.ksplit * kBM * (a.nw / plan.ksplit) <=
                     gemm_ws_floats(num_sms))
                    ? plan.ksplit
                    : 0;
-    if (kd == 2)
-      return launch_pdl_cluster(gemm_tc2_kernel<TNP, true, 2>, dim3(unsigned(2 * pairs)), dim3(kThreads1),
-                                Cfg2::kSmemBytes, st, 2u, wt, x, ot, a);
     // ring of exactly-sized stages (nw / 2 weight rows + TNP / 2 token rows per
     // k-block) in whatever the 6 KB-per-warp epilogue and the barriers leave
-    static const size_t budget = [] {
-      const char* e = std::getenv("COCOB200_PAIR_SMEM_KB");  // A/B experiments: the old 224 KB budget
-      return e ? size_t(std::atoi(e)) * 1024 : kMaxDynSmem;
-    }();
+    // (decoupled weight / token ring depths measured no better: the shared
+    // 7-stage ring is balanced)
+    const size_t budget = kMaxDynSmem;
     const size_t wbytes = size_t(plan.nw / 2) * kBK * 2;
     const size_t stage_bytes = wbytes + Cfg::kXBytes;
     const size_t fixed = size_t(4) * kTokEpiWarpBytes + 1024 + kBarBytes;
@@ -1892,21 +1670,7 @@ static cudaError_t launch_pair(const CUtensorMap& w, const CUtensorMap& x, const
     if (stages < 2) return cudaErrorInvalidValue;
     a.stages = stages;
     a.xstages = 0;
-    size_t smem = size_t(stages) * stage_bytes + fixed;
-    // decoupled depths: a short token ring (L2), the rest to weights (HBM)
-    static const int pxs = [] {
-      const char* e = std::getenv("COCOB200_PAIR_XSTAGES");  // 0 = one shared depth
-      return e ? std::atoi(e) : 0;
-    }();
-    if (pxs > 0) {
-      int ws = int((budget - fixed - size_t(pxs) * Cfg::kXBytes) / wbytes);
-      if (ws > kMaxStages) ws = kMaxStages;
-      if (ws >= 2) {
-        a.stages = ws;
-        a.xstages = pxs;
-        smem = size_t(ws) * wbytes + size_t(pxs) * Cfg::kXBytes + fixed;
-      }
-    }
+    const size_t smem = size_t(stages) * stage_bytes + fixed;
     if (a.ksplit > 1 && size_t(stages) * stage_bytes < size_t(2) * (a.ksplit - 1) * kBM * (a.nw / a.ksplit) * 4)
       a.ksplit = 0;  // the exchange blocks must fit the stage ring
     if (a.ksplit > 1) {  // ksplit pairs per tile, one K part each

@@ -36,7 +36,6 @@ struct GemmArgs {
   int whole_tiles;    // set from the plan: CTA (pair) ranges rounded to whole tiles
   int stages;         // set by the launcher: pipeline ring depth (1-CTA kernel: the weight ring)
   int xstages;        // set by the launcher: activation ring depth (1-CTA kernel; 0 = stages)
-  int cstream;        // set from the plan: cluster stream-K cluster size (> 1)
   int dbg;            // experiments only: bit0 = skip the MMAs, bit1 = skip the epilogue
   // Fused RMSNorm (decode passes, T <= 256; SURVEY.md §8(a) rmsnorm):
   //  consumer (ssq_in != null): X rows are h' = bf16(x * gamma); output row t is
@@ -78,9 +77,6 @@ struct GemmPlan {
   int max_parts; // stream-K: max CTAs (pairs) sharing a tile (0 = no cap; 1 = one tile per CTA, no fixups)
   int whole;     // 1 = persistent over whole tiles (contiguous tile ranges per CTA / pair, no fixups)
   int kd;        // k-blocks (64 wide) per pipeline stage: 2 = 3-D TMA maps (make_kmajor_map3), 1-CTA kernel only
-  int corun;     // 1 = shallow ring so two CTAs (this kernel's and the next one's) share an SM
-  int cstream;   // > 1: cluster stream-K, clusters of cstream CTAs each owning whole tiles (DSMEM reduce)
-  int nclusters; // cluster stream-K: number of clusters
   int nw;        // > 0: token-major CTA-pair kernel, whole tiles of nw weight rows (32..256, multiple of 32)
   int ksplit;    // token-major pair kernel: 2 = each tile's K halves on two pairs of a 4-CTA cluster
 };

@@ -642,13 +642,12 @@ int gemm(cb_model* m, int dev, const OpMap& w, const OpMap* xmaps, int N, int K,
   const uint64_t orows = out == ws.logits ? uint64_t(m->d.max_slots) : uint64_t(m->d.max_tokens);
   const auto key = std::make_tuple(static_cast<const void*>(out), epi, ocols, uint64_t(ldo), orows);
   const CUtensorMap* om = nullptr;
-  static const bool no_tma_store = std::getenv("COCOB200_NO_TMA_STORE") != nullptr;  // A/B experiments
-  auto it = no_tma_store ? ws.out_maps.end() : ws.out_maps.find(key);
+  auto it = ws.out_maps.find(key);
   if (it != ws.out_maps.end()) {
     om = &it->second;
   } else {
     CUtensorMap mo;
-    if (!no_tma_store && cb::make_out_map(&mo, out, epi, orows, ocols, uint64_t(ldo)) == 0)
+    if (cb::make_out_map(&mo, out, epi, orows, ocols, uint64_t(ldo)) == 0)
       om = &(ws.out_maps[key] = mo);
   }
   ProfScope ps(m, dev, CB_KCLASS_GEMM, dc.compute, bytes, 2.0 * N * K * T);
@@ -848,8 +847,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
     CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
                                d.max_ctx, ac.compute));
   }
-  static const bool pf_rows = std::getenv("COCOB200_PREFILL_ROWS") != nullptr;  // A/B: row-parallel prefill
-  if (!fused && !pf_rows) {
+  if (!fused) {
     // prefill: causal tensor-core attention over the segment's sequences' 64-row blocks
     const int b0 = m->seq_blk[s.s0], b1 = m->seq_blk[s.s1];
     const int4* blocks = reinterpret_cast<const int4*>(wa.meta + ((3 * m->cur_T + m->cur_bs + 3) & ~3)) + b0;

@@ -112,13 +112,11 @@ int cbt_gemm(const void* w, const void* x, int64_t x_rows, int32_t N, int32_t K,
   return finish(cb::gemm_launch(mw, mx, a, plan, ws->sms, 0, tma ? &mo : nullptr));
 }
 
-// The plan gemm_plan picks (host-only): tn, pair, box_rows, csplit, max_parts, whole, kd, corun, cstream,
-// nclusters, nw.
+// The plan gemm_plan picks (host-only): tn, pair, box_rows, csplit, max_parts, whole, kd, nw, ksplit.
 int cbt_gemm_plan(int32_t N, int32_t K, int32_t T, int32_t num_sms, int32_t kind_T, int32_t* out) {
   const cb::GemmPlan p = cb::gemm_plan(N, K, T, num_sms, kind_T);
-  const int32_t v[11] = {p.tn, p.pair, p.box_rows, p.csplit, p.max_parts, p.whole, p.kd, p.corun, p.cstream,
-                         p.nclusters, p.nw};
-  for (int i = 0; i < 11; ++i) out[i] = v[i];
+  const int32_t v[9] = {p.tn, p.pair, p.box_rows, p.csplit, p.max_parts, p.whole, p.kd, p.nw, p.ksplit};
+  for (int i = 0; i < 9; ++i) out[i] = v[i];
   return CB_OK;
 }
 

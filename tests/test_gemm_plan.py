@@ -15,11 +15,11 @@ import pytest
 from paper_2507_18006_b200 import ops
 
 SHAPES = [(12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008), (32000, 4096), (1536, 512), (384, 256)]
-FIELDS = ["tn", "pair", "box_rows", "csplit", "max_parts", "whole", "kd", "corun", "cstream", "nclusters", "nw"]
+FIELDS = ["tn", "pair", "box_rows", "csplit", "max_parts", "whole", "kd", "nw", "ksplit"]
 
 
 def _plan(lib, N, K, T, kind_T, sms=148):
-    out = np.zeros(11, np.int32)
+    out = np.zeros(len(FIELDS), np.int32)
     assert lib.cbt_gemm_plan(N, K, T, sms, kind_T, out.ctypes.data_as(C.c_void_p)) == 0
     return dict(zip(FIELDS, out.tolist()))
 
@@ -33,7 +33,7 @@ def test_replica_share_runs_the_unreplicated_split(lib, N, K, bs):
             if share == 0:
                 continue
             sub = _plan(lib, N, K, share, bs)
-            for f in ("pair", "csplit", "max_parts", "whole", "kd", "nw", "cstream"):
+            for f in ("pair", "csplit", "max_parts", "whole", "kd", "nw", "ksplit"):
                 assert sub[f] == full[f], (N, K, bs, p, share, f, sub, full)
 
 
@@ -46,6 +46,8 @@ def test_plan_fields_are_sane(lib, N, K):
         if pl["pair"]:
             assert T > 128 and pl["box_rows"] == pl["tn"] // 2
             assert pl["nw"] == 0 or (128 <= pl["nw"] <= 256 and pl["nw"] % 32 == 0)
+            if pl["ksplit"]:  # split-K token-major pairs: 64-column parts, one token tile
+                assert pl["nw"] % (32 * pl["ksplit"]) == 0 and T <= 256 and (K // 64) % pl["ksplit"] == 0
         else:
             assert pl["box_rows"] == pl["tn"] and pl["tn"] >= min(T, 256) // 2
         if pl["csplit"] > 1:  # cluster split-K: every CTA of the cluster gets >= 1 k-block

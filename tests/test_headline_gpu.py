@@ -13,9 +13,10 @@ oracle, which is pinned to transformers):
 * logits within the north star's 2e-2 max-abs at every step;
 * greedy tokens identical wherever the oracle's top-2 margin exceeds 2x that.
 
-At B = 256 the decode GEMMs run the token-major CTA-pair kernel and RMSNorm is
-fused into the GEMM epilogues (asserted from the plan); B = 1 / 16 / 64 / 128
-are the bench's sweep points (1-CTA kernel plans).  A replicated variant
+At B = 256 the decode GEMMs run the token-major CTA-pair kernel (O / down
+split over K in 4 parts) and RMSNorm is fused into the GEMM epilogues
+(asserted from the plan); B = 1 / 16 / 64 / 128 are the bench's sweep points
+(1-CTA kernel plans).  A replicated variant
 splits layer 2 over two logical devices (split_batch(256, 2) = [128, 128]).
 Reference semantics: sim.py:269-300 (prefill then decode), ops.py:151-158.
 """
@@ -57,10 +58,10 @@ def _bench_cfg(batch: int) -> ExecutorConfig:
 
 
 def _plan(lib, N, K, T):
-    out = np.zeros(11, np.int32)
+    names = ["tn", "pair", "box_rows", "csplit", "max_parts", "whole", "kd", "nw", "ksplit"]
+    out = np.zeros(len(names), np.int32)
     assert lib.cbt_gemm_plan(N, K, T, 148, T, out.ctypes.data_as(C.c_void_p)) == 0
-    return dict(zip(["tn", "pair", "box_rows", "csplit", "max_parts", "whole", "kd", "corun", "cstream",
-                     "nclusters", "nw"], out.tolist()))
+    return dict(zip(names, out.tolist()))
 
 
 def _run(runtime, weights, batch, replicate_layer2=False):
@@ -109,14 +110,16 @@ def _run(runtime, weights, batch, replicate_layer2=False):
 def test_headline_plans(lib):
     """The plans the B = 256 case exercises (host-only choice, csrc/gemm.cu
     gemm_plan): QKV, gate/up and lm_head run the token-major CTA-pair kernel
-    (wave-fitted nw-row weight tiles); O and down the 1-CTA kernel with a
-    4-CTA cluster split-K over 256-token tiles."""
+    (wave-fitted nw-row weight tiles); O and down the same kernel with 256-row
+    weight tiles split over K in 4 parts (parts exchanged through L2)."""
     for N, K in ((12288, 4096), (22016, 4096), (32000, 4096)):
         pl = _plan(lib, N, K, 256)
-        assert pl["pair"] == 1 and pl["nw"] > 0 and pl["whole"] == 1, (N, K, pl)
+        assert pl["pair"] == 1 and pl["nw"] > 0 and pl["whole"] == 1 and pl["ksplit"] == 0, (N, K, pl)
     for N, K in ((4096, 4096), (4096, 11008)):
         pl = _plan(lib, N, K, 256)
-        assert pl["pair"] == 0 and pl["csplit"] == 4 and pl["tn"] == 256, (N, K, pl)
+        assert pl["pair"] == 1 and pl["ksplit"] == 4 and pl["nw"] == 256, (N, K, pl)
+        pl = _plan(lib, N, K, 128)  # <= 128 rows: the 1-CTA kernel, cluster split-K
+        assert pl["pair"] == 0 and pl["csplit"] == 4, (N, K, pl)
     assert _plan(lib, 12288, 4096, 64)["pair"] == 0
 
 
