@@ -109,12 +109,15 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ CPU baseline (oracle port)
 class CpuDecodeSample:
-    """The fp32 numpy oracle on a bounded sample of one 7B decode step.
+    """The fp32 numpy oracle on one 7B decode step.
 
     TEST INFRASTRUCTURE: the oracle is the timed CPU baseline here, never the
-    product path.  Sample = ``sample_layers`` of the 32 decoder layers (KV of
-    ``ctx`` random tokens per sequence) + the lm_head, timed and scaled to 32
-    layers.  Built once; ``step()`` times one sampled decode step."""
+    product path.  ``sample_layers`` distinct decoder layers are held in
+    memory (KV of ``ctx`` random tokens per sequence); ``step(full=True)``
+    runs all 32 decoder layers by cycling through them (layer i uses sampled
+    layer i % sample_layers: same shapes, same arithmetic) + the lm_head +
+    argmax -- a complete decode step of the workload, nothing scaled;
+    ``step(full=False)`` runs the sampled layers once and scales."""
 
     def __init__(self, batch: int, ctx: int, sample_layers: int = 2):
         from oracle.cpu_llama import LLAMA2_7B as CFG, OracleModel, init_weights
@@ -133,20 +136,24 @@ class CpuDecodeSample:
         self.x = self.m.embed[rng.integers(0, CFG.vocab, batch)]
         self.pos = np.full(batch, ctx, dtype=np.int64)
 
-    def step(self) -> float:
+    def step(self, full: bool = True) -> float:
         t0 = time.perf_counter()
         h = self.x
-        for li in range(self.sample_layers):
-            h = self.m.layer_forward(li, h, self.slots, self.pos)
+        n = self.cfg.n_layers if full else self.sample_layers
+        for li in range(n):
+            h = self.m.layer_forward(li % self.sample_layers, h, self.slots, self.pos)
         t1 = time.perf_counter()
         _ = (h @ self.m.lm_head.T).argmax(-1)
         t2 = time.perf_counter()
-        return (t1 - t0) * self.cfg.n_layers / self.sample_layers + (t2 - t1)
+        return (t1 - t0) * (1 if full else self.cfg.n_layers / self.sample_layers) + (t2 - t1)
 
-    def describe(self, repeats: int) -> str:
-        return (f"numpy fp32 oracle (oracle/cpu_llama.py), one decode step at batch {self.batch}, ctx {self.ctx}: "
-                f"{self.sample_layers} of {self.cfg.n_layers} decoder layers + lm_head timed ({repeats} samples), "
-                f"layer time scaled x{self.cfg.n_layers // self.sample_layers}; BLAS threads = all host cores")
+    def describe(self, steps: int, full: bool = True) -> str:
+        what = (f"all {self.cfg.n_layers} decoder layers executed (cycling {self.sample_layers} distinct "
+                f"layers' weights) + lm_head + argmax, nothing extrapolated" if full else
+                f"{self.sample_layers} of {self.cfg.n_layers} decoder layers + lm_head timed, layer time "
+                f"scaled x{self.cfg.n_layers // self.sample_layers}")
+        return (f"numpy fp32 oracle (oracle/cpu_llama.py), {steps} decode step(s) at batch {self.batch}, "
+                f"ctx {self.ctx}: {what}; BLAS threads = all host cores")
 
 
 def blas_all_cores():
@@ -160,39 +167,56 @@ def blas_all_cores():
     return ctx, used
 
 
-def cpu_decode_sample(batch: int, ctx: int, repeats: int = 2) -> dict:
+def cpu_decode_sample(batch: int, ctx: int, repeats: int = 1) -> dict:
+    """cpu_baseline of our arm's line: one complete 32-layer decode step (~15 s at B=256)."""
     lim, cores = blas_all_cores()
     with lim:
         s = CpuDecodeSample(batch, ctx)
-        s.step()  # warm
-        step_s = min(s.step() for _ in range(repeats))
+        s.step(full=False)  # warm
+        step_s = min(s.step(full=True) for _ in range(repeats))
     return {"value": batch / step_s, "unit": "tokens/s", "cores": cores, "kind": "port",
             "sample": s.describe(repeats)}
+
+
+def headline_config(args, world: int) -> dict:
+    """The N=1 workload both arms report (BASELINE config 2)."""
+    return {"workload": "config 2: Llama-2-7B shape decode, no replication", "batch": args.batch,
+            "prompt_len": args.prompt, "gen_len": args.gen, "ctx_at_mid_step": args.prompt + args.gen // 2,
+            "parallelism": "single instance",
+            "l2": "weights 13.2 GB >> 126 MB L2: every step streams from HBM (no flush needed)"}
 
 
 def run_reference(args, rank: int, world: int) -> None:
     """--impl reference: the reference has no forward pass, so its
     CPU path for this tier is the oracle port of the decoder step, timed with all
-    host cores on a bounded sample of the same workload."""
+    host cores.  N=1: exactly K complete decode steps of config 2 (all 32
+    layers, batch 256, ctx = prompt + gen/2), each ~15 s; the W warm-up steps
+    are sampled (2 layers) -- a CPU needs no warm-up beyond first touch.  N>1
+    (config 3's global batch would take minutes per step): rank 0 times
+    sampled steps (2 of 32 layers, scaled) of the per-GPU batch, bounded."""
     if rank != 0:
         return
     t_all = time.perf_counter()
     lim, cores = blas_all_cores()
+    full = world == 1
+    ctx = args.prompt + args.gen // 2
     with lim:
-        s = CpuDecodeSample(args.batch, args.prompt)
-        for _ in range(max(1, min(args.warmup, 2))):
-            s.step()
-        steps = max(1, min(args.steps, 3 if args.batch > 64 else 10))  # bounded: each sampled step is 1-10 s of CPU work
-        steps_s = [s.step() for _ in range(steps)]
+        s = CpuDecodeSample(args.batch, ctx)
+        for _ in range(args.warmup):
+            s.step(full=False)
+        steps = args.steps if full else max(1, min(args.steps, 3))
+        steps_s = [s.step(full=full) for _ in range(steps)]
     value = args.batch * len(steps_s) / sum(steps_s)
+    cfg = headline_config(args, world)
+    if not full:
+        cfg = dict(cfg, workload=f"config 3 per-GPU batch ({args.batch}) on the CPU, sampled")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(steps_s) / len(steps_s),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "config 2 decode step (Llama-2-7B shape), bounded CPU sample", "batch": args.batch,
-                   "ctx": args.prompt, "parallelism": "cpu"},
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
-                         "sample": s.describe(steps)},
+                         "sample": s.describe(steps, full)},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "the reference (modscale) has no forward pass (SPEC.md:136); its CPU path for this tier is the "
                 "oracle port of the decoder layer, timed with all host cores",
@@ -210,7 +234,11 @@ def build_instance(args, n_dev: int, ordinal0: int):
     batch = args.batch * n_dev
     sweep = [s * n_dev for s in args.sweep if s * n_dev != batch]
     sweep_tokens = sum(args.sweep_steps + max(3, args.warmup) for _ in sweep)
-    max_ctx = max(args.prompt + args.warmup + 2 * args.steps + sweep_tokens, args.prompt + args.serve_gen) + 8
+    # decode steps the headline slots take (run_single): warm-up, an early-ctx
+    # window, generation up to the mid-generation context, the headline window
+    # and the profiled pass; the sweep slots then continue
+    headline_tokens = max(args.warmup + 2 * args.steps, args.gen // 2 + args.steps // 2 + 1) + args.steps
+    max_ctx = max(args.prompt + headline_tokens + sweep_tokens, args.prompt + args.serve_gen) + 8
     max_slots = max([batch] + sweep)
     # two logical devices on one GPU at N=1 so the replication/migration copy
     # engine can be measured too (device 1 holds no layer during decode)
@@ -244,12 +272,12 @@ def measure_migration(ex, cat, cluster, n_dev: int) -> dict:
             "nvlink_peak_gbps_per_dir": 900.0}
 
 
-def serving_window(ex, args, batch: int) -> dict:
+def serving_window(ex, args, batch: int, rps: float) -> dict:
     """Continuous batching (reference Engine semantics, serving.py) under Poisson
     arrivals for a bounded window: per-request p50/p99 latency and tok/s."""
     from paper_2507_18006_b200.serving import InstanceState, ServingEngine, poisson_arrivals
 
-    reqs = poisson_arrivals(args.serve_rps, args.serve_s, args.prompt, args.serve_gen, seed=7)
+    reqs = poisson_arrivals(rps, args.serve_s, args.prompt, args.serve_gen, seed=7)
     inst = InstanceState(0, ex, max_batch_size=batch)
     eng = ServingEngine([inst], seed=7)
     res = eng.run(reqs)
@@ -261,11 +289,69 @@ def serving_window(ex, args, batch: int) -> dict:
         T.write_run(args.telemetry, trace, ops, [], T.summary(trace, ops, res.completed, 7, args.serve_s,
                                                               {"0": list(ex.placement.p_vector())}))
     s = res.summary()
-    s.update({"rps": args.serve_rps, "arrival_window_s": args.serve_s, "requests": len(reqs),
+    s.update({"rps": rps, "arrival_window_s": args.serve_s, "requests": len(reqs),
               "prompt_len": args.prompt, "gen_len": args.serve_gen, "max_batch_size": batch,
               "what": "wall-clock serving run: Poisson arrivals (seed 7), FIFO admission, prefill-then-decode "
                       "continuous batching (sim.py:624-736 semantics); latency = completion - arrival"})
     return s
+
+
+def timed_steps(ex, slots, nxt, steps: int):
+    """K synchronous decode calls: device ms (CUDA events inside cb_step) and host wall seconds."""
+    dev_ms, wall_s = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        nxt, _, ms = ex.decode(slots, nxt)
+        wall_s.append(time.perf_counter() - t0)
+        dev_ms.append(ms)
+    return nxt, dev_ms, wall_s
+
+
+def parity_spot_check(batch: int, prompt: int) -> dict:
+    """Outside every timed region: the headline plans (7B geometry, the bench's
+    batch and prompt, 2 decoder layers + lm_head) with oracle weights, prefill +
+    2 decode steps, teacher-forced against the fp32 oracle (oracle/torch_llama.py
+    on cuda, IEEE fp32; pinned to the numpy oracle in tests/).  Test
+    infrastructure used as a checker, never as the measured path."""
+    from oracle.cpu_llama import LlamaConfig, init_weights
+    from oracle.torch_llama import TorchOracle
+    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
+
+    cfg_o = LlamaConfig(2, LLAMA2_7B["d_model"], LLAMA2_7B["d_ff"], LLAMA2_7B["n_heads"], LLAMA2_7B["n_heads"],
+                        LLAMA2_7B["vocab"])
+    w = init_weights(cfg_o, seed=21)
+    cfg = ExecutorConfig(n_layers=2, d_model=cfg_o.d_model, d_ff=cfg_o.d_ff, n_heads=cfg_o.n_heads,
+                         vocab=cfg_o.vocab, max_slots=batch, max_ctx=prompt + 8,
+                         max_tokens=max(min(batch, 64) * prompt, 256))
+    rt = Runtime([0])
+    ex = Executor(rt, cfg)
+    ex.load_model(w, device_of_layer=0)
+    ref = TorchOracle(cfg_o, w, max_ctx=cfg.max_ctx, max_slots=batch, device="cuda")
+    rng = np.random.default_rng(batch)
+    prompts = rng.integers(0, cfg_o.vocab, batch * prompt).astype(np.int32)
+    slots = np.arange(batch, dtype=np.int32)
+    lens = np.full(batch, prompt, np.int32)
+    _, lg, _ = ex.prefill(slots, prompts, lens, want_logits=True)
+    want = ref.forward(slots, prompts, lens)
+    worst, sure_n, same_n = 0.0, 0, 0
+    for step in range(3):
+        worst = max(worst, float(np.abs(lg - want).max()))
+        srt = np.sort(want, axis=1)
+        sure = (srt[:, -1] - srt[:, -2]) > 4e-2
+        sure_n += int(sure.sum())
+        same_n += int((lg.argmax(1)[sure] == want.argmax(1)[sure]).sum())
+        if step == 2:
+            break
+        inp = want.argmax(1).astype(np.int32)
+        _, lg, _ = ex.decode(slots, inp, want_logits=True)
+        want = ref.forward(slots, inp, None)
+    ex.close()
+    rt.close()
+    del ref
+    return {"max_abs_logit_err": worst, "tol": 2e-2, "pass": bool(worst <= 2e-2 and same_n == sure_n),
+            "confident_decisions": sure_n, "identical": same_n,
+            "what": f"7B geometry, batch {batch}, prompt {prompt}, 2 layers + lm_head with oracle weights, "
+                    "prefill + 2 decode steps vs the fp32 oracle (same GEMM / attention plans as the headline)"}
 
 
 def run_single(args) -> None:
@@ -286,16 +372,20 @@ def run_single(args) -> None:
     nxt = all_next[:batch]
     for _ in range(args.warmup):
         nxt, _, _ = ex.decode(slots, nxt)
-    dev_ms, wall_s = [], []
+    # early-context point (ctx = prompt + W .. + K): the round-1 headline
+    ctx_early = args.prompt + args.warmup + args.steps // 2
+    nxt, early_ms, _ = timed_steps(ex, slots, nxt, args.steps)
+    # generate on to the middle of a prompt/gen request (BASELINE config 2:
+    # prompt 128, gen 256 -> mean attended context 256), then the headline K
+    done = args.warmup + args.steps
+    for _ in range(max(0, args.gen // 2 - args.steps // 2 - done)):
+        nxt, _, _ = ex.decode(slots, nxt)
+        done += 1
+    ctx_mid = args.prompt + done + args.steps // 2
     with ClockSampler(0) as clocks:
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            nxt, _, ms = ex.decode(slots, nxt)
-            wall_s.append(time.perf_counter() - t0)
-            dev_ms.append(ms)
+        nxt, dev_ms, wall_s = timed_steps(ex, slots, nxt, args.steps)
     # decode throughput at other batch sizes on the same instance (slot
-    # subsets), after the headline loop: right after the long prefill the
-    # power controller still holds the clocks down (first steps measured slow)
+    # subsets, their context continues from the headline's)
     all_next[:batch] = nxt
     sweep_res = {}
     for sb in sorted(sweep):
@@ -303,10 +393,7 @@ def run_single(args) -> None:
         s_next = all_next[:sb]
         for _ in range(max(3, args.warmup)):
             s_next, _, _ = ex.decode(s_slots, s_next)
-        ms = []
-        for _ in range(args.sweep_steps):
-            s_next, _, m = ex.decode(s_slots, s_next)
-            ms.append(m)
+        s_next, ms, _ = timed_steps(ex, s_slots, s_next, args.sweep_steps)
         all_next[:sb] = s_next
         sweep_res[str(sb)] = {"tokens_per_s": sb * len(ms) / (sum(ms) / 1e3), "ms_per_step": float(np.mean(ms))}
     nxt = all_next[:batch]
@@ -322,7 +409,10 @@ def run_single(args) -> None:
     ex.profile(False)
     mig = measure_migration(ex, cat, cluster, n_dev)
     ex.release_all()
-    serving = serving_window(ex, args, batch) if args.serve_s > 0 else None
+    serving = None
+    if args.serve_s > 0:
+        serving = {"moderate": serving_window(ex, args, batch, args.serve_rps),
+                   "saturated": serving_window(ex, args, batch, args.serve_rps_sat)}
     total_dev_s = sum(dev_ms) / 1e3
     value = batch * args.steps / total_dev_s
     e2e = batch * args.steps / sum(wall_s)
@@ -331,34 +421,37 @@ def run_single(args) -> None:
     ncu_path = ROOT / "profiles" / "ncu_summary.json"
     if ncu_path.exists():
         ncu = json.loads(ncu_path.read_text())
-    ctx_mid = args.prompt + args.warmup + args.steps // 2
+    cfg = headline_config(args, world)
+    cfg["ctx_at_mid_step"] = ctx_mid
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sum(dev_ms) / len(dev_ms), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random prompts)",
-        "config": {"workload": "config 2: Llama-2-7B shape decode, no replication" if world == 1 else
-                   f"config 3: Llama-2-7B shape, layers 1..{args.replicate_layers} replicated on {world} GPUs",
-                   "batch": batch, "prompt_len": args.prompt, "ctx_at_mid_step": ctx_mid,
-                   "parallelism": "single instance" if world == 1 else f"module replication x{world}",
-                   "l2": "weights 13.2 GB >> 126 MB L2: every step streams from HBM (no flush needed)"},
+        "config": cfg,
         "latency_ms": {"p50": float(np.percentile(np.array(wall_s) * 1e3, 50)),
                        "p99": float(np.percentile(np.array(wall_s) * 1e3, 99)),
                        "what": "per-token decode step latency through the public API (e2e)",
-                       "prefill_ms": prefill_ms},
+                       "prefill_ms": prefill_ms, "prefill_tokens": n_slots * args.prompt},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": (3 * batch + batch) * 4,
                 "d2h_bytes_per_step": batch * 4},
         "gpu_launches": launches,
         "roofline": gemm_roofline(prof, prof_ms, peaks, ncu),
+        "ctx_points": {str(ctx_early): {"tokens_per_s": batch * len(early_ms) / (sum(early_ms) / 1e3),
+                                        "ms_per_step": float(np.mean(early_ms))},
+                       str(ctx_mid): {"tokens_per_s": value, "ms_per_step": sum(dev_ms) / len(dev_ms)}},
         "batch_sweep": sweep_res,
         "migrate": mig,
         "serving": serving,
         "clocks": clocks.summary(),
     }
+    ex.close()
+    rt.close()
+    torch.cuda.empty_cache()
+    if not args.no_spot_check:
+        line["parity_spot_check"] = parity_spot_check(batch, args.prompt)
     if world == 1 and not args.no_cpu_baseline:
-        ex.close()
-        rt.close()
         try:
-            line["cpu_baseline"] = cpu_decode_sample(batch, args.prompt)
+            line["cpu_baseline"] = cpu_decode_sample(batch, args.prompt + args.gen // 2)
         except MemoryError:
             line["cpu_baseline"] = None
     print(json.dumps(line), flush=True)
@@ -564,8 +657,11 @@ def main() -> None:
     ap.add_argument("--churn-steps", type=int, default=12, help="N>1: continuous-batching steps after the timed region")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--serve-s", type=float, default=8.0, help="serving window (0 = skip)")
-    ap.add_argument("--serve-rps", type=float, default=40.0)
-    ap.add_argument("--serve-gen", type=int, default=64)
+    ap.add_argument("--serve-rps", type=float, default=50.0, help="moderate load (config 2 lists rps 3..50)")
+    ap.add_argument("--serve-rps-sat", type=float, default=200.0, help="saturating load (batch cap reached)")
+    ap.add_argument("--serve-gen", type=int, default=256)
+    ap.add_argument("--gen", type=int, default=256, help="generation length: the headline is timed at mid-generation")
+    ap.add_argument("--no-spot-check", action="store_true")
     ap.add_argument("--telemetry", default="", help="write the serving window's trace/ops/summary (reference schema) here")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
