@@ -153,7 +153,7 @@ _SIGS = {
                                       C.c_int32, C.c_int32, _F32P]),
     "cbt_argmax": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),
     "cbt_prefill_attention": (C.c_int, [_P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                        C.c_int32]),
+                                        C.c_int32, C.c_int32]),
     "cbt_gemm_trace": (C.c_int, [_P, C.c_int32]),
     "cbt_mma_probe": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
     "cbt_gemm_set_wcopies": (C.c_int, [C.c_int32, C.c_int64]),

@@ -125,14 +125,17 @@ struct AttnArgs {
   int T, row_off, H, Hkv, hd, max_ctx, max_len;
   float scale;  // 1/sqrt(hd)
   int prefetch_pos;  // set by the launcher: cached positions per CTA prefetched to L2 before the PDL wait
+  int qkv_rows;      // prefill: rows of the qkv buffer (TMA bounds)
+  int kv_slots;      // prefill: slots of the KV block (TMA bounds: kv_slots * max_ctx positions)
 };
 cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
 
 // act = bf16(silu(gate) * act) over rows [row_off, row_off + T) of [rows][d_ff] buffers (d_ff % 8 == 0)
 cudaError_t swiglu_launch(const uint16_t* gate, uint16_t* act, int T, int d_ff, int row_off, cudaStream_t st);
-// Causal prefill attention on the tensor cores: blocks[i] = (first row relative to
-// a.row_off, rows (<= 64), slot, first position) of one sequence; q already rotated
-// and the block's K/V already in the cache (rope_kv_launch).  Grid (blocks, H).
+// Causal prefill attention on the tcgen05 tensor cores: blocks[i] = (first row
+// relative to a.row_off, rows (<= 128), slot, first position) of one sequence; q
+// already rotated and the block's K/V already in the cache (rope_kv_launch).
+// Grid (blocks, H); a.qkv_rows / a.kv_slots bound the TMA views.
 cudaError_t prefill_attention_launch(const AttnArgs& a, const int4* blocks, int nblocks, cudaStream_t st);
 // dst[i, :] = src[idx[i], :] (bf16 rows; prefill keeps only each sequence's last row)
 cudaError_t gather_rows_launch(const uint16_t* src, const int32_t* idx, uint16_t* dst, int n, int d,

@@ -1,242 +1,359 @@
-// Causal prefill attention on the tensor cores (flash-attention forward).
+// Causal prefill attention on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
 // Prefill rows of one sequence are contiguous in qkv and their K/V were just
-// appended to the slot's cache (rope_kv_kernel), so a block of 64 consecutive
-// query rows of one sequence attends to cache positions [0, p0 + 63] of its
-// slot.  CTA = (q block, q head), 4 warps x 16 query rows.  Per 64-position
-// K/V block: S = Q K^T and O += P V with mma.sync.m16n8k16 (bf16 in, fp32
-// accumulate), online softmax in registers (exp2), causal mask on the diagonal
-// block only.  K/V blocks are staged in shared memory with cp.async (double
-// buffered, 16-byte chunks XOR-swizzled against bank conflicts) and read back
-// with ldmatrix (.trans for V).  The decode path keeps attention.cu (one query
-// row per sequence: HBM-bound, no tensor-core work to do).
+// appended to the slot's cache (rope_kv_kernel).  CTA = (128-row query block of
+// one sequence, q head); 6 warps, warp-specialised:
 //
-// Replaces the row-parallel prefill use of attn_kernel: at 2048-token prompts
-// that path ran at ~10 TFLOP/s and was 81% of the prefill time.
+//   warp 0      TMA producer: the Q tile once, then K and V blocks of 128
+//               cached positions (SWIZZLE_128B boxes of 64 columns x 128 rows
+//               straight from the [slot][pos][k|v] cache) into a 3-stage K
+//               ring (freed when S_j retires) and a 2-stage V ring (freed when
+//               PV_j retires), K one block ahead of V
+//   warp 1      MMA issuer (one elected lane of a converged warp):
+//               S_j = Q K_j^T   (M 128 x N 128 x K hd, both K-major) into one of
+//                                two TMEM S buffers, issued one block ahead;
+//               O  += P_j V_j   (M 128 x N hd x K 128; P K-major from smem, V
+//                                MN-major: the cache's [pos][hd] rows as is)
+//   warps 2..5  softmax, one thread per query row = one TMEM lane: S row ->
+//               registers (tcgen05.ld), causal mask, online softmax in the
+//               exp2 domain with lazy rescaling (O in TMEM is rescaled with
+//               tcgen05.ld/st only when a row max grows by > 2^8), P as bf16
+//               into smem in the 128-byte-swizzled K-major layout the MMA
+//               reads; finally O / l -> bf16 -> global.
+//
+// TMEM: S double buffer (2 x 128 columns) + O (hd columns).  Smem (hd 128):
+// Q 32 KB + 3 x K 32 KB + 2 x V 32 KB + P 32 KB = 224 KB.  Positions past the
+// sequence's last row inside the last key block are masked in S, and their V
+// rows are zeroed in smem before the PV MMA (stale cache bytes could hold
+// non-finite values; 0 * NaN would poison the row).
+//
+// Replaces the mma.sync (HMMA.16816) flash-attention forward of round 1.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace cb {
 
-static constexpr int kPfRows = 64;  // query rows per CTA (4 warps x 16)
-static constexpr int kPfKeys = 64;  // key positions per block
+static constexpr int kPfRows = 128;  // query rows per CTA = UMMA M = TMEM lanes
+static constexpr int kPfKeys = 128;  // cached positions per K/V block = UMMA N of S = UMMA K of PV
+static constexpr int kPfThreads = 192;
 
-CB_DEVICE void cp_async16(void* smem_dst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
-}
-CB_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-CB_DEVICE void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+template <int HD>
+struct PfCfg {
+  static constexpr int kRegion = kPfRows * 128;  // one [128 rows][64 bf16] swizzled box: 16 KB
+  static constexpr int kQ = kPfRows * HD * 2;
+  static constexpr int kK = kPfKeys * HD * 2;
+  static constexpr int kV = kPfKeys * HD * 2;
+  static constexpr int kP = kPfRows * kPfKeys * 2;
+  static constexpr int kBars = 16 * 8;
+  static constexpr int kKStages = 3, kVStages = 2;  // K is released after S, V after PV
+  static constexpr int kSmem = 1024 + kQ + kKStages * kK + kVStages * kV + kP + kBars;
+  static constexpr uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256 + HD)
+};
 
-CB_DEVICE void ldmatrix_x4(uint32_t (&r)[4], const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(p)));
-}
-CB_DEVICE void ldmatrix_x4_trans(uint32_t (&r)[4], const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(p)));
-}
-// D (16x8 fp32) += A (16x16 bf16, row) * B (16x8 bf16, col)
-CB_DEVICE void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+CB_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+      "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+      "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+CB_DEVICE float fast_exp2(float x) {  // ex2.approx.ftz: one MUFU.EX2, exp2(-inf) = 0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+CB_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// MN-major operand (the contiguous dimension is N) in 128-byte-swizzled
+// [k rows][64 n] boxes: SBO = 1024 B between 8-row k groups, LBO = bytes
+// between consecutive 64-column n boxes.
+CB_DEVICE uint64_t make_sw128_mn_desc(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((smem_addr & 0x3ffff) >> 4);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3fff) << 16;
+  d |= uint64_t(1024 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
 }
 
-// row-major [rows][HD] bf16 tile in smem, 16-byte chunk c of row r at chunk c ^ (r & 7)
 template <int HD>
-CB_DEVICE uint16_t* swz(uint16_t* base, int r, int c) {
-  return base + r * HD + ((c ^ (r & 7)) << 3);
-}
+__global__ void __launch_bounds__(kPfThreads, 1)
+    prefill_attn_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mkv,
+                           const AttnArgs a, const int4* __restrict__ blocks) {
+  using C = PfCfg<HD>;
+  constexpr int NR = HD / 64;  // 64-column boxes per Q / K / V tile
+  extern __shared__ uint8_t pf_raw[];
+  uint8_t* sm = pf_raw + ((1024 - (smem_u32(pf_raw) & 1023)) & 1023);
+  uint8_t* sQ = sm;
+  uint8_t* sK = sQ + C::kQ;                 // [3 stages]
+  uint8_t* sV = sK + C::kKStages * C::kK;   // [2 stages]
+  uint8_t* sP = sV + C::kVStages * C::kV;   // [2 boxes of 64 keys]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::kP);
+  uint64_t* bar_q = bars + 0;
+  uint64_t* k_full = bars + 1;   // [3]
+  uint64_t* k_empty = bars + 4;  // [3]
+  uint64_t* v_full = bars + 7;   // [2]
+  uint64_t* v_empty = bars + 9;  // [2]
+  uint64_t* s_full = bars + 11;  // [2]
+  uint64_t* s_free = bars + 13;  // [2]
+  uint64_t* p_full = bars + 15;
+  uint64_t* o_done = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
-template <int HD>
-__global__ void __launch_bounds__(128) prefill_attn_kernel(const AttnArgs a, const int4* blocks) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(k_full + i, 1);
+      mbar_init(k_empty + i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(v_full + i, 1);
+      mbar_init(v_empty + i, 1);
+      mbar_init(s_full + i, 1);
+      mbar_init(s_free + i, 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+    tma_prefetch_desc(&mq);
+    tma_prefetch_desc(&mkv);
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
   pdl_trigger();
-  pdl_wait();
-  constexpr int CH = HD / 8;  // 16-byte chunks per row
-  extern __shared__ __align__(128) uint8_t pf_smem[];
-  uint16_t* sQ = reinterpret_cast<uint16_t*>(pf_smem);  // [64][HD]
-  uint16_t* sK = sQ + kPfRows * HD;                     // [2][64][HD]
-  uint16_t* sV = sK + 2 * kPfKeys * HD;                 // [2][64][HD]
-  const int4 blk = blocks[blockIdx.x];                  // (first row, rows, slot, first position)
+  pdl_wait();  // q rotated and K/V appended by rope_kv_kernel
+
+  const int4 blk = blocks[blockIdx.x];  // (first row, rows, slot, first position)
   const int row0 = a.row_off + blk.x, nrows = blk.y, slot = blk.z, p0 = blk.w;
   const int qh = blockIdx.y;
-  const int gq = a.H / a.Hkv;
-  const int hk = qh / gq;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
-  const size_t kvd = size_t(a.Hkv) * HD;
-  const uint16_t* kv_slot = a.kv + (size_t)slot * a.max_ctx * 2 * kvd + (size_t)hk * HD;
-
-  // Q tile -> smem (rows beyond the block read row0 .. clamp: masked at the store)
-  for (int i = threadIdx.x; i < kPfRows * CH; i += 128) {
-    const int r = i / CH, c = i % CH;
-    const int rr = min(r, nrows - 1);
-    cp_async16(swz<HD>(sQ, r, c), a.qkv + (size_t)(row0 + rr) * qkv_ld + (size_t)qh * HD + c * 8);
-  }
+  const int hk = qh / (a.H / a.Hkv);
   const int last_pos = p0 + nrows - 1;
   const int nkb = last_pos / kPfKeys + 1;
-  auto load_kv = [&](int kb, int buf) {
-    uint16_t* dk = sK + buf * kPfKeys * HD;
-    uint16_t* dv = sV + buf * kPfKeys * HD;
-    for (int i = threadIdx.x; i < kPfKeys * CH; i += 128) {
-      const int r = i / CH, c = i % CH;
-      const int pos = min(kb * kPfKeys + r, last_pos);  // beyond the causal range: masked
-      const uint16_t* src = kv_slot + (size_t)pos * 2 * kvd + c * 8;
-      cp_async16(swz<HD>(dk, r, c), src);
-      cp_async16(swz<HD>(dv, r, c), src + kvd);
-    }
-  };
-  load_kv(0, 0);
-  cp_async_commit();
 
-  const float sl2 = a.scale * 1.4426950408889634f;
-  float o[HD / 8][4];
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+      mbar_arrive_expect_tx(bar_q, C::kQ);
 #pragma unroll
-  for (int j = 0; j < HD / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows g and g + 8 of this warp
-  const int qr0 = warp * 16 + g;                            // local query rows of this thread
-  const int qp0 = p0 + qr0, qp1 = qp0 + 8;                  // their positions
-  uint32_t qa[HD / 16][4];
-  bool q_loaded = false;
+      for (int r = 0; r < NR; ++r) tma_load_2d(&mq, bar_q, sQ + r * C::kRegion, qh * HD + r * 64, row0, pol_q);
+      const int kv_row0 = slot * a.max_ctx;
+      auto load_k = [&](int j) {  // stage j % 3, free once S_{j-3} retired
+        const int s = j % 3;
+        if (j >= 3) mbar_wait(k_empty + s, ((j / 3) + 1) & 1);
+        mbar_arrive_expect_tx(k_full + s, C::kK);
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          tma_load_2d(&mkv, k_full + s, sK + s * C::kK + r * C::kRegion, hk * HD + r * 64, kv_row0 + j * kPfKeys,
+                      pol_kv);
+      };
+      load_k(0);
+      for (int j = 0; j < nkb; ++j) {  // K runs one block ahead of V (S_j precedes PV_j)
+        if (j + 1 < nkb) load_k(j + 1);
+        const int s = j & 1;
+        if (j >= 2) mbar_wait(v_empty + s, ((j >> 1) + 1) & 1);
+        mbar_arrive_expect_tx(v_full + s, C::kV);
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          tma_load_2d(&mkv, v_full + s, sV + s * C::kV + r * C::kRegion, (a.Hkv + hk) * HD + r * 64,
+                      kv_row0 + j * kPfKeys, pol_kv);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = make_idesc_bf16(kPfRows, kPfKeys);
+    constexpr uint32_t idesc_o = make_idesc_bf16(kPfRows, HD) | (1u << 16);  // B (V) MN-major
+    const uint32_t tO = tmem + 256;
+    mbar_wait(bar_q, 0);
+    auto issue_s = [&](int j) {
+      const int s = j & 1, ks = j % 3;
+      mbar_wait(k_full + ks, (j / 3) & 1);
+      if (j >= 2) mbar_wait(s_free + s, ((j >> 1) + 1) & 1);
+      tc_fence_after();
+      const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + ks * C::kK);
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const uint32_t off = (kk >> 2) * C::kRegion + (kk & 3) * 32;
+        umma_bf16_elect(tmem + s * 128, make_sw128_desc(q0 + off), make_sw128_desc(k0 + off), idesc_s, kk > 0);
+      }
+      umma_commit_elect(s_full + s);
+      umma_commit_elect(k_empty + ks);
+    };
+    issue_s(0);
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      if (j + 1 < nkb) issue_s(j + 1);
+      mbar_wait(p_full, j & 1);
+      mbar_wait(v_full + s, (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t p0a = smem_u32(sP), v0 = smem_u32(sV + s * C::kV);
+#pragma unroll
+      for (int kk = 0; kk < kPfKeys / 16; ++kk) {
+        const uint32_t poff = (kk >> 2) * C::kRegion + (kk & 3) * 32;
+        umma_bf16_elect(tO, make_sw128_desc(p0a + poff), make_sw128_mn_desc(v0 + kk * 2048, C::kRegion), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      umma_commit_elect(o_done);
+      umma_commit_elect(v_empty + s);
+    }
+    __syncwarp();
+  } else {
+    // softmax: thread = query row r = TMEM lane (warp w may touch lanes 32 (w % 4) ..)
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_off = uint32_t(q4 * 32) << 16;
+    const int qp = p0 + r;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    float m_used = -INFINITY, l = 0.f;
+    uint8_t* prow = sP + r * 128;
+    const int rsw = r & 7;
+    for (int j = 0; j < nkb; ++j) {
+      const int s = j & 1;
+      mbar_wait(s_full + s, (j >> 1) & 1);
+      tc_fence_after();
+      float v[kPfKeys];
+#pragma unroll
+      for (int c = 0; c < kPfKeys / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld32(tmem + lane_off + s * 128 + c * 32, u);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[c * 32 + e] = __uint_as_float(u[e]);
+      }
+      tc_fence_before();
+      mbar_arrive(s_free + s);
+      const int kbase = j * kPfKeys;
+      const bool mask = kbase + kPfKeys - 1 > p0;  // the block reaches past some row's position
+      if (mask) {  // (block-uniform) causal mask on raw scores
+#pragma unroll
+        for (int c = 0; c < kPfKeys; ++c)
+          if (kbase + c > qp) v[c] = -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kPfKeys; ++c) mx = fmaxf(mx, v[c]);
+      mx *= sl2;  // row max in the scaled log2 domain
+      float alpha = 1.f;
+      bool need = false;
+      if (j == 0) {
+        m_used = mx;
+      } else {
+        need = mx > m_used + 8.f;
+        if (need) {
+          alpha = fast_exp2(m_used - mx);
+          m_used = mx;
+        }
+      }
+      // P = exp2(S - m) packed to bf16 in registers while PV_{j-1} may still run
+      float rs = 0.f;
+      uint32_t pk[kPfKeys / 2];
+#pragma unroll
+      for (int e = 0; e < kPfKeys / 2; ++e) {
+        const float e0 = fast_exp2(fmaf(v[2 * e], sl2, -m_used));  // FFMA + MUFU.EX2 per score
+        const float e1 = fast_exp2(fmaf(v[2 * e + 1], sl2, -m_used));
+        rs += e0 + e1;
+        pk[e] = pack_bf16x2(e0, e1);
+      }
+      if (j > 0) {
+        mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} retired: O is final for j-1 and P is free
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {  // lazy rescale: only when a row max grew by > 2^8
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t u[32];
+            tmem_ld32(tmem + lane_off + 256 + c * 32, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
+            tmem_st32(tmem + lane_off + 256 + c * 32, u);
+          }
+          tmem_st_wait();
+        }
+      }
+#pragma unroll
+      for (int ch = 0; ch < kPfKeys / 8; ++ch) {  // 16-byte chunks of 8 keys, 128-byte swizzle
+        uint8_t* dst = prow + (ch >> 3) * C::kRegion + (((ch & 7) ^ rsw) << 4);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      }
+      l = l * alpha + rs;
+      if (kbase + kPfKeys - 1 > last_pos) {
+        // last block: V rows past the sequence's last position -> 0 (P is 0 there)
+        mbar_wait(v_full + s, (j >> 1) & 1);
+        if (kbase + r > last_pos) {
+          uint8_t* vrow = sV + s * C::kV + r * 128;
+#pragma unroll
+          for (int b = 0; b < NR; ++b)
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              *reinterpret_cast<uint4*>(vrow + b * C::kRegion + ch * 16) = make_uint4(0, 0, 0, 0);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_done, (nkb - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    uint16_t* out = a.out + (size_t)(row0 + r) * a.H * HD + (size_t)qh * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t u[32];
+      tmem_ld32(tmem + lane_off + 256 + c * 32, u);
+      tmem_ld_wait();
+      if (r < nrows) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(u[8 * e + 0]) * inv, __uint_as_float(u[8 * e + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(u[8 * e + 2]) * inv, __uint_as_float(u[8 * e + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(u[8 * e + 4]) * inv, __uint_as_float(u[8 * e + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(u[8 * e + 6]) * inv, __uint_as_float(u[8 * e + 7]) * inv);
+          *reinterpret_cast<uint4*>(out + c * 32 + e * 8) = w;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
+}
 
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nkb) {
-      load_kv(kb + 1, buf ^ 1);
-      cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    if (!q_loaded) {  // A fragments of this warp's 16 query rows, all k-chunks
-#pragma unroll
-      for (int kc = 0; kc < HD / 16; ++kc) {
-        const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int c = kc * 2 + (lane >> 4);
-        ldmatrix_x4(qa[kc], swz<HD>(sQ, r, c));
-      }
-      q_loaded = true;
-    }
-    const uint16_t* k_s = sK + buf * kPfKeys * HD;
-    const uint16_t* v_s = sV + buf * kPfKeys * HD;
-    // S = Q K^T for 64 key positions: 8 n-tiles of 8
-    float s[8][4];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-#pragma unroll
-    for (int kc = 0; kc < HD / 16; ++kc) {
-#pragma unroll
-      for (int jp = 0; jp < 4; ++jp) {  // n-tiles 2jp, 2jp+1 (positions 16jp .. 16jp+15)
-        uint32_t b[4];
-        const int r = jp * 16 + (lane & 7) + (lane >> 4) * 8;
-        const int c = kc * 2 + ((lane >> 3) & 1);
-        ldmatrix_x4(b, swz<HD>(const_cast<uint16_t*>(k_s), r, c));
-        mma16816(s[2 * jp], qa[kc], b[0], b[1]);
-        mma16816(s[2 * jp + 1], qa[kc], b[2], b[3]);
-      }
-    }
-    // causal mask (diagonal block), scale, online softmax
-    const int kbase = kb * kPfKeys;
-    float mx0 = m0, mx1 = m1;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int kp = kbase + j * 8 + 2 * t;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        s[j][e] = (kp + e <= qp0) ? s[j][e] * sl2 : -INFINITY;
-        s[j][2 + e] = (kp + e <= qp1) ? s[j][2 + e] * sl2 : -INFINITY;
-        mx0 = fmaxf(mx0, s[j][e]);
-        mx1 = fmaxf(mx1, s[j][2 + e]);
-      }
-    }
-#pragma unroll
-    for (int o2 = 1; o2 < 4; o2 <<= 1) {
-      mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o2));
-      mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o2));
-    }
-    const float c0 = (mx0 == -INFINITY) ? 1.f : exp2f(m0 - mx0);
-    const float c1 = (mx1 == -INFINITY) ? 1.f : exp2f(m1 - mx1);
-    m0 = mx0;
-    m1 = mx1;
-    float rs0 = 0.f, rs1 = 0.f;
-    uint32_t pa[4][4];  // P as A fragments: k-chunk kk covers n-tiles 2kk, 2kk+1
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float e0 = (m0 == -INFINITY) ? 0.f : exp2f(s[j][0] - m0);
-      const float e1 = (m0 == -INFINITY) ? 0.f : exp2f(s[j][1] - m0);
-      const float e2 = (m1 == -INFINITY) ? 0.f : exp2f(s[j][2] - m1);
-      const float e3 = (m1 == -INFINITY) ? 0.f : exp2f(s[j][3] - m1);
-      rs0 += e0 + e1;
-      rs1 += e2 + e3;
-      const int kk = j >> 1, hi = j & 1;
-      pa[kk][hi * 2 + 0] = pack_bf16x2(e0, e1);
-      pa[kk][hi * 2 + 1] = pack_bf16x2(e2, e3);
-    }
-    l0 = l0 * c0 + rs0;
-    l1 = l1 * c1 + rs1;
-#pragma unroll
-    for (int j = 0; j < HD / 8; ++j) {
-      o[j][0] *= c0;
-      o[j][1] *= c0;
-      o[j][2] *= c1;
-      o[j][3] *= c1;
-    }
-    // O += P V: k = 64 positions (4 chunks of 16), n = HD dims
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-#pragma unroll
-      for (int jd = 0; jd < HD / 16; ++jd) {  // dim tiles 2jd, 2jd+1
-        uint32_t b[4];
-        const int r = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int c = jd * 2 + (lane >> 4);
-        ldmatrix_x4_trans(b, swz<HD>(const_cast<uint16_t*>(v_s), r, c));
-        mma16816(o[2 * jd], pa[kk], b[0], b[1]);
-        mma16816(o[2 * jd + 1], pa[kk], b[2], b[3]);
-      }
-    }
-    __syncthreads();  // the buffer is refilled two blocks later
+template <int HD>
+static cudaError_t launch_hd(const AttnArgs& a, const int4* blocks, int nblocks, cudaStream_t st) {
+  using C = PfCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
-  // row sums across the quad, normalise, store
-#pragma unroll
-  for (int o2 = 1; o2 < 4; o2 <<= 1) {
-    l0 += __shfl_xor_sync(0xffffffffu, l0, o2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, o2);
-  }
-  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-  uint16_t* out0 = a.out + (size_t)(row0 + qr0) * a.H * HD + (size_t)qh * HD;
-  uint16_t* out1 = out0 + (size_t)8 * a.H * HD;
-#pragma unroll
-  for (int j = 0; j < HD / 8; ++j) {
-    const int d = j * 8 + 2 * t;
-    if (qr0 < nrows) *reinterpret_cast<uint32_t*>(out0 + d) = pack_bf16x2(o[j][0] * inv0, o[j][1] * inv0);
-    if (qr0 + 8 < nrows) *reinterpret_cast<uint32_t*>(out1 + d) = pack_bf16x2(o[j][2] * inv1, o[j][3] * inv1);
-  }
+  const uint64_t qkv_n = uint64_t(a.H + 2 * a.Hkv) * HD;
+  const uint64_t kv_n = uint64_t(2 * a.Hkv) * HD;
+  CUtensorMap mq, mkv;
+  if (make_kmajor_map(&mq, a.qkv, uint64_t(a.qkv_rows), qkv_n, qkv_n, kPfRows) != 0 ||
+      make_kmajor_map(&mkv, a.kv, uint64_t(a.kv_slots) * a.max_ctx, kv_n, kv_n, kPfKeys) != 0)
+    return cudaErrorInvalidValue;
+  const dim3 grid(unsigned(nblocks), unsigned(a.H));
+  return launch_pdl(prefill_attn_tc_kernel<HD>, grid, dim3(kPfThreads), size_t(C::kSmem), st, mq, mkv, a, blocks);
 }
 
 cudaError_t prefill_attention_launch(const AttnArgs& a, const int4* blocks, int nblocks, cudaStream_t st) {
   if (nblocks <= 0) return cudaSuccess;
-  const dim3 grid(unsigned(nblocks), unsigned(a.H));
+  if (a.qkv_rows <= 0 || a.kv_slots <= 0) return cudaErrorInvalidValue;
   switch (a.hd) {
-    case 64: {
-      const size_t smem = size_t(kPfRows + 4 * kPfKeys) * 64 * 2;
-      return launch_pdl(prefill_attn_kernel<64>, grid, dim3(128), smem, st, a, blocks);
-    }
-    case 128: {
-      const size_t smem = size_t(kPfRows + 4 * kPfKeys) * 128 * 2;
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(prefill_attn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        attr = true;
-      }
-      return launch_pdl(prefill_attn_kernel<128>, grid, dim3(128), smem, st, a, blocks);
-    }
+    case 64: return launch_hd<64>(a, blocks, nblocks, st);
+    case 128: return launch_hd<128>(a, blocks, nblocks, st);
   }
   return cudaErrorInvalidValue;
 }

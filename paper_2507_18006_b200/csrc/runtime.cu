@@ -848,7 +848,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
                                d.max_ctx, ac.compute));
   }
   if (!fused) {
-    // prefill: causal tensor-core attention over the segment's sequences' 64-row blocks
+    // prefill: causal tensor-core attention over the segment's sequences' 128-row blocks
     const int b0 = m->seq_blk[s.s0], b1 = m->seq_blk[s.s1];
     const int4* blocks = reinterpret_cast<const int4*>(wa.meta + ((3 * m->cur_T + m->cur_bs + 3) & ~3)) + b0;
     cb::AttnArgs pa{};
@@ -861,6 +861,8 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
     pa.Hkv = d.n_kv_heads;
     pa.hd = m->hd;
     pa.max_ctx = d.max_ctx;
+    pa.qkv_rows = m->cur_T;
+    pa.kv_slots = d.max_slots;
     pa.scale = 1.0f / std::sqrt(float(m->hd));
     double flops = 0;  // QK^T + PV over the causal prefix of every row
     for (int r = s.r0; r < s.r1; ++r) flops += 4.0 * (row_pos[r] + 1) * m->q_n;
@@ -1188,7 +1190,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       meta[2 * T + r] = pos;
     }
   for (int i = 0; i < bs; ++i) meta[3 * T + i] = seq_row[i + 1] - 1;
-  // prefill: 64-row query blocks of every sequence for the tensor-core attention
+  // prefill: 128-row query blocks of every sequence for the tensor-core attention
   m->cur_bs = bs;
   m->seq_blk.assign(bs + 1, 0);
   int nblk = 0;
@@ -1198,9 +1200,9 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     for (int i = 0; i < bs; ++i) {
       m->seq_blk[i] = nblk;
       const int len = seq_row[i + 1] - seq_row[i];
-      for (int b0 = 0; b0 < len; b0 += 64, ++nblk) {
+      for (int b0 = 0; b0 < len; b0 += 128, ++nblk) {
         blk[4 * nblk + 0] = seq_row[i] + b0;
-        blk[4 * nblk + 1] = std::min(64, len - b0);
+        blk[4 * nblk + 1] = std::min(128, len - b0);
         blk[4 * nblk + 2] = slots[i];
         blk[4 * nblk + 3] = b0;
       }

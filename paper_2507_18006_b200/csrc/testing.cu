@@ -577,10 +577,11 @@ extern "C" int cbt_mma_probe(int32_t N, int32_t n, int32_t grid, int32_t kstep, 
 }
 
 // causal prefill attention: rows [0, T) of qkv hold consecutive prompts; blocks_dev
-// = int4 (row, rows, slot, first position) per 64-row block; K/V already in kv.
+// = int4 (row, rows, slot, first position) per 128-row block; K/V already in kv
+// ([n_slots][max_ctx][2][Hkv hd]).
 extern "C" int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
                                      int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd,
-                                     int32_t max_ctx) {
+                                     int32_t max_ctx, int32_t n_slots) {
   cb::AttnArgs a{};
   a.qkv = qkv;
   a.kv = kv;
@@ -590,6 +591,8 @@ extern "C" int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, ui
   a.Hkv = Hkv;
   a.hd = hd;
   a.max_ctx = max_ctx;
+  a.qkv_rows = T;
+  a.kv_slots = n_slots;
   a.scale = 1.0f / std::sqrt(float(hd));
   return finish(cb::prefill_attention_launch(a, reinterpret_cast<const int4*>(blocks_dev), nblocks, 0));
 }

@@ -1,0 +1,18 @@
+#!/bin/bash
+# Ad-hoc GPU session: the tests and measurements named in $1 (comma list).
+set -u
+mkdir -p gpurun_out
+IFS=',' read -ra JOBS <<< "${1:-}"
+for j in "${JOBS[@]}"; do
+  case $j in
+    pftest) timeout 600 python -m pytest tests/test_kernels_gpu.py -k prefill -q -x 2>&1 | tail -5 > gpurun_out/pf_test.txt
+            timeout 600 python -m pytest tests/test_model_gpu.py -k "prefill" -q -x 2>&1 | tail -5 >> gpurun_out/pf_test.txt ;;
+    pfperf) for L in 128 512 2048 4096; do B=$((8192 / L)); timeout 300 python scripts/prefill_profile.py $B $L; done > gpurun_out/pf_perf.txt 2>&1 ;;
+    pfncu) timeout 300 ncu --set full --clock-control none --import-source on -k regex:prefill_attn -c 1 \
+             -o gpurun_out/prof_pf -f python scripts/prefill_profile.py 4 2048 > gpurun_out/ncu_pf.log 2>&1 ;;
+    gemmod) timeout 600 python scripts/gemm_perf.py 0,411,512411,401,512401,412,421 256 --real-epi --norm > gpurun_out/gemm_od.txt 2>&1 ;;
+    gputests) timeout 1200 python -m pytest tests -m gpu -q -rA 2>&1 | tail -60 > gpurun_out/pytest_gpu.txt ;;
+    bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ;;
+  esac
+done
+ls gpurun_out

@@ -355,26 +355,32 @@ def test_gemm_pair_kernel_row_count_invariant(lib, cuda, N, K):
     assert (a.double().cpu() - ref).abs().max().item() <= 2e-5 * K ** 0.5 * ref.abs().max().item() + 1e-4
 
 
-@pytest.mark.parametrize("H,Hkv,hd,lens", [(4, 4, 64, [1, 63, 64, 65]), (32, 32, 128, [200, 7, 130]),
-                                           (8, 2, 128, [129, 64]), (64, 8, 128, [300])])
+@pytest.mark.parametrize("H,Hkv,hd,lens", [(4, 4, 64, [1, 63, 64, 65, 128, 129]), (32, 32, 128, [200, 7, 130]),
+                                           (8, 2, 128, [129, 64, 256]), (64, 8, 128, [300]),
+                                           (4, 4, 128, [1000, 128, 255])])
 def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
-    """Tensor-core causal prefill attention (mma.sync flash-attention forward)
-    vs a float64 causal softmax reference: every row of every prompt, 64-row
-    blocks incl. ragged tails, GQA, head dims 64/128."""
+    """tcgen05 causal prefill attention (TMA-fed Q/K/V, S and O in TMEM, softmax
+    warps one row per thread) vs a float64 causal softmax reference: every row
+    of every prompt, 128-row blocks incl. ragged tails, multi-block prompts
+    (lazy O rescaling in TMEM), GQA, head dims 64/128.  The cache holds NaN
+    past each prompt (stale / uninitialised bytes must not leak into rows)."""
     torch = cuda
     T = sum(lens)
-    max_ctx = max(lens) + 4
+    max_ctx = max(lens) + 132
     qkv = _bf16(torch, (T, (H + 2 * Hkv) * hd), 1.0, 31).cuda()
     kv = _bf16(torch, (len(lens), max_ctx, 2, Hkv * hd), 1.0, 32).cuda()
+    for sl, L in enumerate(lens):
+        kv[sl, L:] = float("nan")
     out = torch.zeros(T, H * hd, dtype=torch.bfloat16, device="cuda")
     blocks, row = [], 0
     for sl, L in enumerate(lens):
-        for b0 in range(0, L, 64):
-            blocks.append((row + b0, min(64, L - b0), sl, b0))
+        for b0 in range(0, L, 128):
+            blocks.append((row + b0, min(128, L - b0), sl, b0))
         row += L
     bl = torch.tensor(blocks, dtype=torch.int32, device="cuda")
     assert lib.cbt_prefill_attention(_ptr(qkv), _ptr(kv), _ptr(out), _ptr(bl), len(blocks), T, H, Hkv, hd,
-                                     max_ctx) == 0
+                                     max_ctx, len(lens)) == 0
+    torch.cuda.synchronize()
     q = qkv[:, : H * hd].double().cpu().numpy().reshape(T, H, hd)
     kvn = kv.double().cpu().numpy()
     g = H // Hkv
@@ -388,5 +394,6 @@ def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
         p /= p.sum(-1, keepdims=True)
         ref = np.einsum("htl,lhd->thd", p, v).reshape(L, -1)
         got = out[row:row + L].double().cpu().numpy()
+        assert np.isfinite(got).all(), sl
         assert np.abs(got - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max()), (sl, np.abs(got - ref).max())
         row += L

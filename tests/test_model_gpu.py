@@ -365,19 +365,38 @@ def test_kv_offload_to_host_and_back_matches_oracle(runtime, confident):
 
 
 def test_ragged_long_prompts_prefill_matches_oracle(runtime, confident):
-    """Ragged prompts longer than one 64-row prefill block (1 .. 150 tokens) in
-    one pass, layer 2 replicated (prompts split across the two replicas): the
-    tensor-core causal prefill attention + decode continue to match the fp32
+    """Ragged prompts spanning several 128-row prefill blocks (1 .. 300 tokens)
+    in one pass, layer 2 replicated (prompts split across the two replicas):
+    the tcgen05 causal prefill attention + decode continue to match the fp32
     oracle (tokens equal, logits within 2e-2)."""
     rng = np.random.default_rng(5)
-    lens = [150, 1, 64, 65, 130, 7]
+    lens = [150, 1, 64, 65, 130, 7, 300, 128, 129]
     prompts = [rng.integers(0, TINY.vocab, L).astype(np.int32) for L in lens]
-    ex = Executor(runtime, _tiny_cfg(max_ctx=192, max_tokens=512))
+    ex = Executor(runtime, _tiny_cfg(max_ctx=320, max_tokens=1024))
     ex.load_model(confident, device_of_layer=0)
     cat, cl = _catalog_cluster()
     ex.apply(O.ReplicateLayer(2, 1), cat, cl)
     got, logits = _greedy_gpu(ex, prompts, 6)
-    ref, ref_logits = greedy_generate(OracleModel(TINY, confident, 192), prompts, 6, replicas={1: 2})
+    ref, ref_logits = greedy_generate(OracleModel(TINY, confident, 320), prompts, 6, replicas={1: 2})
+    assert np.array_equal(got, ref)
+    assert max(np.abs(a - b).max() for a, b in zip(logits, ref_logits)) <= LOGIT_TOL
+    ex.close()
+
+
+def test_prefill_into_offloaded_kv_matches_oracle(runtime, confident):
+    """Phase-3 offload before the prefill: half the layers' KV blocks live in
+    mapped pinned host memory, so the prefill's rope_kv appends and the tcgen05
+    attention's TMA loads of K/V go to host memory over PCIe; tokens and logits
+    still match the fp32 oracle."""
+    rng = np.random.default_rng(9)
+    lens = [40, 200, 3]
+    prompts = [rng.integers(0, TINY.vocab, L).astype(np.int32) for L in lens]
+    ex = Executor(runtime, _tiny_cfg(max_ctx=224, max_tokens=512))
+    ex.load_model(confident, device_of_layer=0)
+    ex.set_kv_offload(0.5)
+    assert ex.kv_offloaded(1) and ex.kv_offloaded(2)
+    got, logits = _greedy_gpu(ex, prompts, 5)
+    ref, ref_logits = greedy_generate(OracleModel(TINY, confident, 224), prompts, 5)
     assert np.array_equal(got, ref)
     assert max(np.abs(a - b).max() for a, b in zip(logits, ref_logits)) <= LOGIT_TOL
     ex.close()
