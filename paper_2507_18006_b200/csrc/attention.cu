@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     const int cur = a.row_pos[row];
     const int p0 = int(blockIdx.z) * chunk, p1 = min(cur, p0 + min(chunk, a.prefetch_pos));
     const size_t kvd = size_t(a.Hkv) * HD, pos_stride = 2 * kvd;
-    const uint16_t* kb = a.kv + (size_t)a.row_slot[row] * a.max_ctx * pos_stride + (size_t)blockIdx.x * HD;
+    const int ks = a.kv_map ? a.kv_map[a.row_slot[row]] : a.row_slot[row];
+    const uint16_t* kb = a.kv + (size_t)ks * a.max_ctx * pos_stride + (size_t)blockIdx.x * HD;
     const int part = threadIdx.x & 3;
     for (int p = p0 + int(threadIdx.x >> 2); p < p1; p += int(blockDim.x >> 2))
       prefetch_l2(kb + (size_t)p * pos_stride + (part >> 1) * kvd + (part & 1) * 64);
@@ -61,7 +62,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lg = lane % G, pg = lane / G;
   const int grp = warp * P + pg;
-  const int slot = a.row_slot[row];
+  const int slot = a.kv_map ? a.kv_map[a.row_slot[row]] : a.row_slot[row];  // index in this KV block
   const int len = a.row_pos[row] + 1;
   const int cur = len - 1;
   const int p_begin = split * chunk;

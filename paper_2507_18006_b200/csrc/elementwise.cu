@@ -178,13 +178,14 @@ cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, i
 // (rotate-half convention).  q is rotated in place; rotated k and raw v are
 // appended at cache[slot][pos].
 __global__ void rope_kv_kernel(uint16_t* __restrict__ qkv, uint16_t* __restrict__ kv,
-                               const float2* __restrict__ rope, const int32_t* __restrict__ row_slot,
+                               const int32_t* __restrict__ kv_map, const float2* __restrict__ rope,
+                               const int32_t* __restrict__ row_slot,
                                const int32_t* __restrict__ row_pos, int row_off, int H, int Hkv, int hd,
                                int max_ctx) {
   pdl_trigger();
   pdl_wait();
   const int row = row_off + blockIdx.x;
-  const int slot = row_slot[row];
+  const int slot = kv_map ? kv_map[row_slot[row]] : row_slot[row];  // index in this KV block
   const int pos = row_pos[row];
   const int half = hd / 2;
   const int cph = half / 8;  // 8-element chunks per half head
@@ -232,12 +233,12 @@ __global__ void rope_kv_kernel(uint16_t* __restrict__ qkv, uint16_t* __restrict_
   }
 }
 
-cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const float2* rope, const int32_t* row_slot,
-                           const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd, int max_ctx,
-                           cudaStream_t st) {
+cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const int32_t* kv_map, const float2* rope,
+                           const int32_t* row_slot, const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd,
+                           int max_ctx, cudaStream_t st) {
   if (T <= 0) return cudaSuccess;
-  return launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, st, qkv, kv, rope, row_slot, row_pos, row_off, H, Hkv,
-                    hd, max_ctx);
+  return launch_pdl(rope_kv_kernel, dim3(T), dim3(256), 0, st, qkv, kv, kv_map, rope, row_slot, row_pos, row_off, H,
+                    Hkv, hd, max_ctx);
 }
 
 // ---------------------------------------------------------------- row gather

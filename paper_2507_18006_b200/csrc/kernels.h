@@ -106,10 +106,11 @@ cudaError_t embed_norm_launch(const uint16_t* table, const int32_t* tokens, floa
 cudaError_t rmsnorm_launch(const float* x, const uint16_t* gamma, uint16_t* y, int T, int d, float eps,
                            int row_off, cudaStream_t st);
 // In place RoPE of q,k inside qkv rows and append of (k, v) to the slot KV cache.
-// qkv row = [q: H*hd | k: Hkv*hd | v: Hkv*hd]; cache = [slot][max_ctx][2][Hkv*hd].
-cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const float2* rope, const int32_t* row_slot,
-                           const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd, int max_ctx,
-                           cudaStream_t st);
+// qkv row = [q: H*hd | k: Hkv*hd | v: Hkv*hd]; cache = [index][max_ctx][2][Hkv*hd]
+// with index = kv_map[slot] (a share-sized replica block's slot table) or slot (kv_map null).
+cudaError_t rope_kv_launch(uint16_t* qkv, uint16_t* kv, const int32_t* kv_map, const float2* rope,
+                           const int32_t* row_slot, const int32_t* row_pos, int T, int row_off, int H, int Hkv, int hd,
+                           int max_ctx, cudaStream_t st);
 // Row-parallel causal attention over the slot KV cache: row r attends to
 // positions [0, row_pos[r]] of its slot.  Decode (one row per sequence) and
 // prefill (one row per prompt token) share this kernel.
@@ -118,6 +119,7 @@ struct AttnArgs {
   const uint16_t* kv;
   uint16_t* out;  // [row][H*hd]
   const int32_t* row_slot;
+  const int32_t* kv_map;  // slot -> index in this KV block (null: the slot itself)
   const int32_t* row_pos;
   float* ws;       // split-context partials
   size_t ws_floats;

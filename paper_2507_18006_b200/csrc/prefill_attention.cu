@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   pdl_wait();  // q rotated and K/V appended by rope_kv_kernel
 
   const int4 blk = blocks[blockIdx.x];  // (first row, rows, slot, first position)
-  const int row0 = a.row_off + blk.x, nrows = blk.y, slot = blk.z, p0 = blk.w;
+  const int row0 = a.row_off + blk.x, nrows = blk.y, p0 = blk.w;
+  const int slot = a.kv_map ? a.kv_map[blk.z] : blk.z;  // index in this KV block
   const int qh = blockIdx.y;
   const int hk = qh / (a.H / a.Hkv);
   const int last_pos = p0 + nrows - 1;

@@ -131,14 +131,32 @@ struct ModCopy {
 };
 constexpr int kModKinds = CB_FFN_PROJ_DOWN + 1;
 
+// One (layer, device) KV block: [cap][max_ctx][2][Hkv hd] bf16.  The layer's
+// KV device keeps every slot at its own index (cap = max_slots, no table).  A
+// replica's block is sized for its split_batch share -- cap = ceil(max_slots /
+// p), the reference keeps KV only on the KV device (domain.py:380-383) -- and
+// maps slot -> local index through a slot table (pinned host copy + device
+// copy the attention kernels read), growing by an eighth when a re-split brings
+// more sequences than it holds.  An index released during a step is reusable
+// from the next step on (a copy on another stream may still read it).
+struct KvBlock {
+  uint16_t* p = nullptr;
+  int cap = 0;                 // slots
+  bool host = false;           // offloaded: mapped pinned host memory (Phase 3)
+  bool table = false;          // share-sized, slot table in use
+  int32_t* map_h = nullptr;    // slot -> local index (-1 = none); pinned, the authoritative copy
+  int32_t* map_d = nullptr;    // device copy read by the kernels
+  bool dirty = false;
+  std::vector<int> free_idx, pending;
+};
+
 struct LayerState {
   std::vector<LayerCopy> reps;      // original first (Replica order, domain.py:306-317)
   int kv_override = -1;             // device holding KV when overridden, else -1
-  std::map<int, uint16_t*> kv;      // device -> KV block
+  std::map<int, KvBlock> kv;        // device -> KV block
   std::vector<int> owner;           // slot -> device holding that slot's KV (-1 none)
   ModCopy mod[kModKinds];           // projection / self-attention overrides
   bool proj_ov = false;             // any entry of mod[] in use
-  std::map<int, bool> kv_host;      // device -> its KV block lives in mapped pinned host memory (offloaded)
   std::vector<std::pair<int, int>> pend;  // uncommitted scaling ops on this layer: (OpKind, dst or module kind)
 };
 
@@ -524,30 +542,149 @@ int make_layer_maps(cb_model* m, LayerCopy& c) {
 
 // st != null: stream-ordered reservation for a scaling op (no host sync);
 // *created tells the caller whether this call allocated the block.
+size_t kv_token_bytes(cb_model* m);
+size_t kv_slot_bytes(cb_model* m) { return size_t(m->d.max_ctx) * kv_token_bytes(m); }
+int kv_device(const LayerState& L);
+void sync_all_devices(cb_model* m);
+
+// Slots a new KV block on `dev` holds: everything on the layer's KV device (and
+// for unreplicated layers), the split_batch share ceil(max_slots / p) on a
+// replica, p counting the replications still pending.
+int kv_cap_for(cb_model* m, const LayerState& L, int dev) {
+  const int ms = m->d.max_slots;
+  if (L.reps.empty() || dev == kv_device(L)) return ms;
+  int p = int(L.reps.size());
+  for (const auto& pk : L.pend) p += pk.first == OPK_REPLICATE ? 1 : 0;
+  bool replica = false;
+  for (size_t j = 1; j < L.reps.size(); ++j) replica |= L.reps[j].dev == dev;
+  for (const auto& pk : L.pend) replica |= pk.first == OPK_REPLICATE && pk.second == dev;
+  if (!replica || p <= 1) return ms;
+  return std::min(ms, (ms + p - 1) / p);
+}
+
+int kv_alloc_bytes(cb_model* m, DeviceCtx& dc, bool host, size_t bytes, uint16_t** p, uint64_t* shortfall,
+                   cudaStream_t st) {
+  if (host) {
+    CB_CUDA(cudaHostAlloc((void**)p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    return CB_OK;
+  }
+  return dev_alloc(dc, (void**)p, bytes, shortfall, MEM_KV, st);
+}
+
+// st != null: stream-ordered reservation for a scaling op (no host sync);
+// *created tells the caller whether this call allocated the block.
 int ensure_kv(cb_model* m, LayerState& L, int dev, uint64_t* shortfall = nullptr, cudaStream_t st = nullptr,
-              bool* created = nullptr) {
+              bool* created = nullptr, int cap = 0) {
   if (created) *created = false;
   if (L.kv.count(dev) || !is_local(m, dev)) return CB_OK;
-  void* p = nullptr;
-  CB_TRY(dev_alloc(devctx(m, dev), &p, m->kv_block_bytes, shortfall, MEM_KV, st));
-  L.kv[dev] = static_cast<uint16_t*>(p);
+  const int ms = m->d.max_slots;
+  if (cap <= 0) cap = kv_cap_for(m, L, dev);
+  DeviceCtx& dc = devctx(m, dev);
+  KvBlock b;
+  b.cap = cap;
+  CB_TRY(kv_alloc_bytes(m, dc, false, size_t(cap) * kv_slot_bytes(m), &b.p, shortfall, st));
+  if (cap < ms) {
+    b.table = true;
+    CB_TRY(use(dc));
+    if (cudaHostAlloc((void**)&b.map_h, size_t(ms) * 4, cudaHostAllocPortable) != cudaSuccess ||
+        cudaMalloc((void**)&b.map_d, size_t(ms) * 4) != cudaSuccess) {
+      cudaGetLastError();
+      dev_free(m, dev, b.p);
+      return fail(CB_ENOMEM, "KV slot table allocation failed");
+    }
+    for (int i = 0; i < ms; ++i) b.map_h[i] = -1;
+    for (int i = cap - 1; i >= 0; --i) b.free_idx.push_back(i);
+    b.dirty = true;
+  }
+  L.kv[dev] = b;
   if (created) *created = true;
   return CB_OK;
 }
 
-int kv_device(const LayerState& L);
-void sync_all_devices(cb_model* m);
+size_t kv_block_bytes_of(cb_model* m, const KvBlock& b) { return size_t(b.cap) * kv_slot_bytes(m); }
 
-// Free a device's KV block for the layer once no slot's KV lives there and the
-// device no longer runs the layer's attention.
-void free_kv_block(cb_model* m, LayerState& L, int dev, uint16_t* p) {
-  if (L.kv_host.count(dev) && L.kv_host[dev]) {
+// Free a device's KV block (and its slot table).
+void free_kv_block(cb_model* m, LayerState& L, int dev, KvBlock& b) {
+  (void)L;
+  if (b.host) {
     sync_all_devices(m);
-    cudaFreeHost(p);
-    L.kv_host.erase(dev);
+    cudaFreeHost(b.p);
   } else {
-    dev_free(m, dev, p);
+    dev_free(m, dev, b.p);
   }
+  if (b.table && is_local(m, dev)) {
+    sync_all_devices(m);
+    cudaFreeHost(b.map_h);
+    cudaSetDevice(devctx(m, dev).ordinal);
+    cudaFree(b.map_d);
+  }
+  b = KvBlock{};
+}
+
+// Local index of `slot` in a block (the slot itself without a table).
+int kv_index(const KvBlock& b, int slot) { return b.table ? b.map_h[slot] : slot; }
+
+// Grow a table block by an eighth (at least one slot): new block, the old one
+// copied whole on the device's compute stream (every write into a block is
+// issued on its device's compute stream), the old freed stream-ordered.
+int kv_grow(cb_model* m, KvBlock& b, int dev) {
+  DeviceCtx& dc = devctx(m, dev);
+  const int ncap = std::min(m->d.max_slots, b.cap + std::max(1, b.cap / 8));
+  uint16_t* np = nullptr;
+  CB_TRY(kv_alloc_bytes(m, dc, b.host, size_t(ncap) * kv_slot_bytes(m), &np, nullptr, nullptr));
+  CB_TRY(use(dc));
+  CB_CUDA(cudaMemcpyAsync(np, b.p, kv_block_bytes_of(m, b), cudaMemcpyDefault, dc.compute));
+  if (b.host) {
+    sync_all_devices(m);
+    cudaFreeHost(b.p);
+  } else {
+    dev_free(m, dev, b.p);
+  }
+  b.p = np;
+  for (int i = ncap - 1; i >= b.cap; --i) b.free_idx.push_back(i);
+  b.cap = ncap;
+  return CB_OK;
+}
+
+// `slot`'s KV is (about to be) held by `dev`: give it a local index there.
+int kv_assign(cb_model* m, LayerState& L, int dev, int slot) {
+  auto it = L.kv.find(dev);
+  if (it == L.kv.end() || !it->second.table) return CB_OK;
+  KvBlock& b = it->second;
+  if (b.map_h[slot] >= 0) return CB_OK;
+  if (b.free_idx.empty()) {
+    if (b.cap >= m->d.max_slots) return fail(CB_ESTATE, "KV slot table full");
+    CB_TRY(kv_grow(m, b, dev));
+  }
+  b.map_h[slot] = b.free_idx.back();
+  b.free_idx.pop_back();
+  b.dirty = true;
+  return CB_OK;
+}
+
+// `slot`'s KV left `dev` (or the slot was released): its index becomes
+// reusable at the next step.
+void kv_unassign(LayerState& L, int dev, int slot) {
+  auto it = L.kv.find(dev);
+  if (it == L.kv.end() || !it->second.table) return;
+  KvBlock& b = it->second;
+  if (b.map_h[slot] < 0) return;
+  b.pending.push_back(b.map_h[slot]);
+  b.map_h[slot] = -1;
+  b.dirty = true;
+}
+
+// the slot table the kernels of (layer, dev) read this step (null: identity)
+int kv_table_for_launch(KvBlock& b, DeviceCtx& dc, cudaStream_t st, const int32_t** out, int n) {
+  *out = nullptr;
+  if (!b.table) return CB_OK;
+  if (b.dirty) {
+    CB_TRY(use(dc));
+    CB_CUDA(cudaMemcpyAsync(b.map_d, b.map_h, size_t(n) * 4, cudaMemcpyHostToDevice, st));
+    b.dirty = false;
+  }
+  *out = b.map_d;
+  return CB_OK;
 }
 
 void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
@@ -564,10 +701,29 @@ void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
   L.kv.erase(it);
 }
 
+// indices released during the previous step become reusable (cb_step entry:
+// the previous step and every copy it issued have completed)
+void kv_release_pending(cb_model* m) {
+  for (auto& L : m->layers)
+    for (auto& kv : L.kv) {
+      KvBlock& b = kv.second;
+      b.free_idx.insert(b.free_idx.end(), b.pending.begin(), b.pending.end());
+      b.pending.clear();
+    }
+}
+
 int kv_device(const LayerState& L) { return L.kv_override >= 0 ? L.kv_override : L.reps[0].dev; }
 
 size_t kv_token_bytes(cb_model* m) { return size_t(2) * m->kv_n * 2; }
-size_t kv_slot_offset(cb_model* m, int slot) { return size_t(slot) * m->d.max_ctx * m->kv_n * 2; }  // elements
+size_t kv_slot_offset(cb_model* m, int idx) { return size_t(idx) * m->d.max_ctx * m->kv_n * 2; }  // elements
+// element offset of `slot`'s position p0 inside dev's block (null block: another rank's)
+uint16_t* kv_ptr(cb_model* m, LayerState& L, int dev, int slot, int p0) {
+  if (!is_local(m, dev)) return nullptr;
+  KvBlock& b = L.kv.at(dev);
+  const int idx = kv_index(b, slot);
+  if (idx < 0) return nullptr;
+  return b.p + kv_slot_offset(m, idx) + size_t(p0) * m->kv_n * 2;
+}
 
 // copy KV positions [p0, p1) of `slot` from src's block to dst's block (on
 // st, a stream of dst; across processes: channel ch, the sender on src_st)
@@ -575,15 +731,17 @@ int kv_copy(cb_model* m, LayerState& L, int slot, int src, int dst, int p0, int 
             uint64_t* bytes, int ch = 0, cudaStream_t src_st = nullptr) {
   if (p1 <= p0 || src == dst) return CB_OK;
   const size_t tb = kv_token_bytes(m);
-  const size_t off = kv_slot_offset(m, slot) + size_t(p0) * tb / 2;  // elements
+  CB_TRY(kv_assign(m, L, dst, slot));
+  uint16_t* sp = kv_ptr(m, L, src, slot, p0);
+  uint16_t* dp = kv_ptr(m, L, dst, slot, p0);
+  if ((is_local(m, src) && !sp) || (is_local(m, dst) && !dp)) return fail(CB_ESTATE, "KV slot has no index");
   if (crosses(m, src, dst)) {
     if (bytes) *bytes += size_t(p1 - p0) * tb;
-    return xmove(m, ch, src, is_local(m, src) ? L.kv[src] + off : nullptr,
-                 src_st ? src_st : (is_local(m, src) ? devctx(m, src).compute : nullptr), dst,
-                 is_local(m, dst) ? L.kv[dst] + off : nullptr, st, size_t(p1 - p0) * tb);
+    return xmove(m, ch, src, sp, src_st ? src_st : (is_local(m, src) ? devctx(m, src).compute : nullptr), dst, dp,
+                 st, size_t(p1 - p0) * tb);
   }
   // cudaMemcpyDefault: either block may be offloaded to mapped pinned host memory
-  CB_CUDA(cudaMemcpyAsync(L.kv[dst] + off, L.kv[src] + off, size_t(p1 - p0) * tb, cudaMemcpyDefault, st));
+  CB_CUDA(cudaMemcpyAsync(dp, sp, size_t(p1 - p0) * tb, cudaMemcpyDefault, st));
   if (bytes) *bytes += size_t(p1 - p0) * tb;
   return CB_OK;
 }
@@ -837,15 +995,18 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
   }
   CB_TRY(ensure_kv(m, L, ad));
   CB_TRY(use(ac));
-  uint16_t* kv = L.kv[ad];
+  KvBlock& kvb = L.kv.at(ad);
+  uint16_t* kv = kvb.p;
+  const int32_t* kv_map = nullptr;  // slot -> local index in a share-sized replica block
+  CB_TRY(kv_table_for_launch(kvb, ac, ac.compute, &kv_map, d.max_slots));
   const int32_t* row_slot = wa.meta + m->cur_T;
   const int32_t* rpos = wa.meta + 2 * m->cur_T;
   // decode rows are one per sequence: RoPE + KV append fuse into the attention kernel
   const bool fused = m->cur_phase == CB_PHASE_DECODE;
   if (!fused) {
     ProfScope ps(m, ad, CB_KCLASS_ELEMWISE, ac.compute, double(T) * m->qkv_n * 4);
-    CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads, m->hd,
-                               d.max_ctx, ac.compute));
+    CB_CUDA(cb::rope_kv_launch(wa.qkv, kv, kv_map, wa.rope, row_slot, rpos, T, s.r0, d.n_heads, d.n_kv_heads,
+                               m->hd, d.max_ctx, ac.compute));
   }
   if (!fused) {
     // prefill: causal tensor-core attention over the segment's sequences' 128-row blocks
@@ -862,7 +1023,8 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
     pa.hd = m->hd;
     pa.max_ctx = d.max_ctx;
     pa.qkv_rows = m->cur_T;
-    pa.kv_slots = d.max_slots;
+    pa.kv_slots = kvb.cap;
+    pa.kv_map = kv_map;
     pa.scale = 1.0f / std::sqrt(float(m->hd));
     double flops = 0;  // QK^T + PV over the causal prefix of every row
     for (int r = s.r0; r < s.r1; ++r) flops += 4.0 * (row_pos[r] + 1) * m->q_n;
@@ -888,6 +1050,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
   aa.kv = kv;
   aa.out = wa.att;
   aa.row_slot = row_slot;
+  aa.kv_map = kv_map;
   aa.row_pos = rpos;
   aa.ws = wa.attn_ws;
   aa.ws_floats = wa.attn_ws_floats;
@@ -946,6 +1109,8 @@ int kv_follow(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& 
         CB_TRY(kv_move(m, L, slot, owner, ad, ac.compute, nullptr));
       }
     }
+    if (owner != ad && owner >= 0) kv_unassign(L, owner, slot);
+    CB_TRY(kv_assign(m, L, ad, slot));
     L.owner[slot] = ad;
   }
   return CB_OK;
@@ -1580,6 +1745,8 @@ int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
     const int have = fresh ? std::min(op.snap_len[slot], len) : 0;
     CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, lt ? tc.compute : nullptr, &op.catchup_bytes, 0,
                    lf ? fc.compute : nullptr));
+    CB_TRY(kv_assign(m, L, op.kv_to, slot));
+    kv_unassign(L, op.kv_from, slot);
     L.owner[slot] = op.kv_to;
   }
   CB_TRY(grp.close());
@@ -1603,7 +1770,7 @@ void op_release_reservation(cb_model* m, PendingOp& op) {
   if (op.kv_new && op.kv_to >= 0) {
     auto it = L.kv.find(op.kv_to);
     if (it != L.kv.end()) {
-      dev_free(m, op.kv_to, it->second);
+      free_kv_block(m, L, op.kv_to, it->second);
       L.kv.erase(it);
     }
   }
@@ -1631,7 +1798,11 @@ int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shor
   PendingOp op = new_op(m, OPK_REPLICATE, layer, dst, dst);
   int r = reserve_block(m, op, dst, shortfall);
   if (r == CB_OK) {
-    r = ensure_kv(m, L, dst, shortfall, is_local(m, dst) ? devctx(m, dst).copy : nullptr, &op.kv_new);
+    // the replica's KV block holds its split_batch share: ceil(max_slots / p) slots
+    int p = int(L.reps.size()) + 1;
+    for (const auto& pk : L.pend) p += pk.first == OPK_REPLICATE ? 1 : 0;
+    const int cap = (m->d.max_slots + p - 1) / p;
+    r = ensure_kv(m, L, dst, shortfall, is_local(m, dst) ? devctx(m, dst).copy : nullptr, &op.kv_new, cap);
     op.kv_to = dst;  // (no KV moves at issue: rows move with split_batch once serving)
   }
   if (r == CB_OK) r = ensure_ws(m, dst);
@@ -1640,7 +1811,7 @@ int issue_replicate(cb_model* m, int layer, int dst, int64_t* id, uint64_t* shor
     op_release_reservation(m, op);
     return fail(r, err);
   }
-  op.reserved = m->layer_bytes + (op.kv_new ? m->kv_block_bytes : 0);
+  op.reserved = m->layer_bytes + (op.kv_new ? kv_block_bytes_of(m, L.kv.at(dst)) : 0);
   op.src_dev = L.reps[0].dev;
   op.xsrc = L.reps[0].block;
   op.xdst = op.copy.block;
@@ -1884,28 +2055,24 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
   float ms = 0.f;
   for (auto& kv : L.kv) {
     const int dev = kv.first;
-    const bool on_host = L.kv_host.count(dev) && L.kv_host[dev];
-    if (on_host == to_host) continue;
+    KvBlock& b = kv.second;
+    if (b.host == to_host) continue;
     DeviceCtx& dc = devctx(m, dev);
     CB_TRY(use(dc));
     uint16_t* nb = nullptr;
-    if (to_host) {
-      CB_CUDA(cudaHostAlloc((void**)&nb, m->kv_block_bytes, cudaHostAllocMapped | cudaHostAllocPortable));
-    } else {
-      uint64_t shortfall = 0;
-      int r = dev_alloc(dc, (void**)&nb, m->kv_block_bytes, &shortfall, MEM_KV);
-      if (r != CB_OK) {
-        if (st) st->shortfall_bytes = shortfall;
-        return r;
-      }
+    uint64_t shortfall = 0;
+    int r = kv_alloc_bytes(m, dc, to_host, kv_block_bytes_of(m, b), &nb, &shortfall, nullptr);
+    if (r != CB_OK) {
+      if (st) st->shortfall_bytes = shortfall;
+      return r;
     }
     CB_TRY(use(dc));
     CB_CUDA(cudaEventRecord(dc.t0, dc.copy));
-    for (int slot = 0; slot < m->d.max_slots; ++slot) {
-      if (L.owner[slot] != dev || m->slot_len[slot] <= 0) continue;
+    for (int slot = 0; slot < m->d.max_slots; ++slot) {  // live prefixes, same local indices
+      if (L.owner[slot] != dev || m->slot_len[slot] <= 0 || kv_index(b, slot) < 0) continue;
       const size_t nbytes = size_t(m->slot_len[slot]) * kv_token_bytes(m);
-      const size_t off = kv_slot_offset(m, slot);
-      CB_CUDA(cudaMemcpyAsync(nb + off, kv.second + off, nbytes, cudaMemcpyDefault, dc.copy));
+      const size_t off = kv_slot_offset(m, kv_index(b, slot));
+      CB_CUDA(cudaMemcpyAsync(nb + off, b.p + off, nbytes, cudaMemcpyDefault, dc.copy));
       moved += nbytes;
     }
     CB_CUDA(cudaEventRecord(dc.t1, dc.copy));
@@ -1913,10 +2080,13 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
     float one = 0.f;
     CB_CUDA(cudaEventElapsedTime(&one, dc.t0, dc.t1));
     ms += one;
-    uint16_t* old = kv.second;
-    free_kv_block(m, L, dev, old);
-    kv.second = nb;
-    if (to_host) L.kv_host[dev] = true;
+    if (b.host) {
+      cudaFreeHost(b.p);
+    } else {
+      dev_free(m, dev, b.p);
+    }
+    b.p = nb;
+    b.host = to_host;
   }
   if (st) {
     st->kv_bytes = moved;
@@ -2322,7 +2492,9 @@ int cb_kv_read(cb_model* m, int32_t layer, int32_t slot, void* dst, uint64_t nby
   if (!is_local(m, owner)) return fail(CB_EINVAL, "the slot's KV lives on another rank's device " + std::to_string(owner));
   sync_all(m);
   CB_TRY(use(devctx(m, owner)));
-  CB_CUDA(cudaMemcpy(dst, L.kv[owner] + kv_slot_offset(m, slot), want, cudaMemcpyDefault));
+  const uint16_t* src = kv_ptr(m, L, owner, slot, 0);
+  if (!src) return fail(CB_ESTATE, "slot has no KV index on its owner");
+  CB_CUDA(cudaMemcpy(dst, src, want, cudaMemcpyDefault));
   if (dev_out) *dev_out = owner;
   return CB_OK;
 }
@@ -2358,6 +2530,7 @@ int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const 
     return fail(CB_EINVAL, "bad batch arguments");
   if (phase != CB_PHASE_PREFILL && phase != CB_PHASE_DECODE) return fail(CB_EINVAL, "unknown phase");
   if (!m->head_loaded) return fail(CB_ESTATE, "embedding / lm_head not loaded");
+  kv_release_pending(m);
   for (auto& L : m->layers)
     if (L.reps.empty()) return fail(CB_ESTATE, "a decoder layer is not loaded");
   std::vector<char> seen(m->d.max_slots, 0);
@@ -2412,7 +2585,10 @@ int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots) {
     m->slot_len[slots[i]] = 0;
     m->slot_epoch[slots[i]] += 1;
     for (auto& L : m->layers)
-      if (!L.owner.empty()) L.owner[slots[i]] = -1;
+      if (!L.owner.empty()) {
+        if (L.owner[slots[i]] >= 0) kv_unassign(L, L.owner[slots[i]], slots[i]);
+        L.owner[slots[i]] = -1;
+      }
   }
   return CB_OK;
 }
@@ -2445,8 +2621,8 @@ int cb_kv_offloaded(cb_model* m, int32_t layer, int32_t* out) {
   CB_TRY(check_layer(m, layer));
   const LayerState& L = m->layers[layer - 1];
   *out = 0;
-  for (auto& h : L.kv_host)
-    if (h.second) *out = 1;
+  for (auto& kv : L.kv)
+    if (kv.second.host) *out = 1;
   return CB_OK;
 }
 

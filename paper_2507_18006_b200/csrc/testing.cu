@@ -288,7 +288,7 @@ int cbt_rope_kv(uint16_t* qkv, uint16_t* kv, const int32_t* row_slot, const int3
   float2* dtab = nullptr;
   if (cudaMalloc(&dtab, tab.size() * sizeof(float2)) != cudaSuccess) return CB_ECUDA;
   cudaMemcpy(dtab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice);
-  int r = finish(cb::rope_kv_launch(qkv, kv, dtab, row_slot, row_pos, T, 0, H, Hkv, hd, max_ctx, 0));
+  int r = finish(cb::rope_kv_launch(qkv, kv, nullptr, dtab, row_slot, row_pos, T, 0, H, Hkv, hd, max_ctx, 0));
   cudaFree(dtab);
   return r;
 }

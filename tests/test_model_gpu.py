@@ -207,6 +207,55 @@ def test_shrinking_batch_moves_kv_with_rows(runtime, confident):
     ex.close()
 
 
+def test_replica_kv_sized_by_share(cuda, confident):
+    """A replica's KV block holds its split_batch share, not max_slots: layer 2
+    replicated x3 on three logical devices, the replicas' blocks hold
+    ceil(32 / 2) and ceil(32 / 3) slots (p at their replication) behind slot
+    tables, the original keeps all 32.  Requests finish (the split moves
+    sequences and their KV between replicas), one replica is evicted (the
+    survivors' shares grow: their tables grow), and every step's tokens and
+    logits match the fp32 oracle."""
+    rt = Runtime([0, 0, 0])
+    ex = Executor(rt, _tiny_cfg())
+    ex.load_model(confident, device_of_layer=0)
+    cat, cl = _catalog_cluster(3)
+    slot_kv = 64 * 2 * TINY.d_model * 2  # max_ctx x KV bytes per token of one layer
+    ex.apply(O.ReplicateLayer(2, 1), cat, cl)
+    ex.apply(O.ReplicateLayer(2, 2), cat, cl)
+    assert ex.mem_usage(0)["kv_bytes"] == TINY.n_layers * 32 * slot_kv
+    assert ex.mem_usage(1)["kv_bytes"] == 16 * slot_kv
+    assert ex.mem_usage(2)["kv_bytes"] == 11 * slot_kv
+    rng = np.random.default_rng(3)
+    n = 30
+    prompts = [rng.integers(0, TINY.vocab, PROMPT).astype(np.int32) for _ in range(n)]
+    oracle = OracleModel(TINY, confident, 64)
+    live = list(range(n))
+    nxt, _, _ = ex.prefill(np.array(live, np.int32), np.concatenate(prompts), np.full(n, PROMPT, np.int32))
+    assert np.array_equal(nxt, oracle.forward(live, np.concatenate(prompts), [PROMPT] * n).argmax(-1))
+    last = dict(zip(live, nxt))
+    drop_plan = {2: [0, 11, 12], 4: [29], 6: [3, 4, 5, 6], 9: [20, 21]}
+    for step in range(1, 14):
+        for s_ in drop_plan.get(step, []):
+            live.remove(s_)
+            ex.release([Request(s_, 0.0, PROMPT, 1, slot=s_)])
+        if step == 7:  # p 3 -> 2: the rows of device 2 move back, the survivors' shares grow
+            ex.apply(O.EvictReplica(2, 2), cat, cl)
+        inp = np.array([last[s_] for s_ in live], np.int32)
+        nxt, lg, _ = ex.decode(np.array(live, np.int32), inp, want_logits=True)
+        ref_lg = oracle.forward(live, inp, None)
+        assert np.array_equal(nxt, ref_lg.argmax(-1)), step
+        assert np.abs(lg - ref_lg).max() <= LOGIT_TOL, step
+        last.update(zip(live, nxt))
+        p = 3 if step < 7 else 2
+        shares = O.split_batch(len(live), p)
+        assert [c for _, _, c in ex.last_routing(2)] == shares
+        # every replica block holds at least its share, never all 32 slots
+        assert shares[1] * slot_kv <= ex.mem_usage(1)["kv_bytes"] < 32 * slot_kv
+    assert ex.mem_usage(2)["kv_bytes"] == 0  # evicted: its block is gone
+    ex.close()
+    rt.close()
+
+
 def test_migration_moves_weights_and_kv_bit_exact(runtime, confident):
     prompts = config1_prompts()
     ex = _executor(runtime, confident)
