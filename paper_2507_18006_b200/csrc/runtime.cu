@@ -547,16 +547,17 @@ size_t kv_slot_bytes(cb_model* m) { return size_t(m->d.max_ctx) * kv_token_bytes
 int kv_device(const LayerState& L);
 void sync_all_devices(cb_model* m);
 
-// Slots a new KV block on `dev` holds: everything on the layer's KV device (and
-// for unreplicated layers), the split_batch share ceil(max_slots / p) on a
-// replica, p counting the replications still pending.
+// Slots a new KV block on `dev` holds: every slot for an unreplicated layer's
+// KV device; the split_batch share ceil(max_slots / p) on each device of a
+// replicated layer (the original included: see kv_shrink_empty), p counting
+// the replications still pending.
 int kv_cap_for(cb_model* m, const LayerState& L, int dev) {
   const int ms = m->d.max_slots;
-  if (L.reps.empty() || dev == kv_device(L)) return ms;
+  if (L.reps.empty()) return ms;
   int p = int(L.reps.size());
   for (const auto& pk : L.pend) p += pk.first == OPK_REPLICATE ? 1 : 0;
   bool replica = false;
-  for (size_t j = 1; j < L.reps.size(); ++j) replica |= L.reps[j].dev == dev;
+  for (const auto& c : L.reps) replica |= c.dev == dev;
   for (const auto& pk : L.pend) replica |= pk.first == OPK_REPLICATE && pk.second == dev;
   if (!replica || p <= 1) return ms;
   return std::min(ms, (ms + p - 1) / p);
@@ -662,6 +663,18 @@ int kv_assign(cb_model* m, LayerState& L, int dev, int slot) {
   return CB_OK;
 }
 
+// Grow dev's table block (if any) until `need` more slots fit.  Called before a
+// batch of copies into the block is queued: inside a transport group
+// (SPMD) the copies run at the group's close, so the block must not be
+// replaced while they are queued.
+int kv_reserve(cb_model* m, LayerState& L, int dev, int need) {
+  auto it = L.kv.find(dev);
+  if (it == L.kv.end() || !it->second.table) return CB_OK;
+  KvBlock& b = it->second;
+  while (int(b.free_idx.size()) < need && b.cap < m->d.max_slots) CB_TRY(kv_grow(m, b, dev));
+  return CB_OK;
+}
+
 // `slot`'s KV left `dev` (or the slot was released): its index becomes
 // reusable at the next step.
 void kv_unassign(LayerState& L, int dev, int slot) {
@@ -699,6 +712,25 @@ void drop_kv_if_unused(cb_model* m, LayerState& L, int dev) {
   if (attn_here) return;
   free_kv_block(m, L, dev, it->second);
   L.kv.erase(it);
+}
+
+// After a replication commits: a block of the layer that holds no live KV and
+// more slots than the new share is dropped; it is re-created at its first use,
+// sized for the share (a layer replicated before serving -- config 3 -- so
+// never keeps a full block on its original).
+void kv_shrink_empty(cb_model* m, LayerState& L) {
+  for (auto it = L.kv.begin(); it != L.kv.end();) {
+    const int dev = it->first;
+    KvBlock& b = it->second;
+    bool live = false;
+    for (int slot = 0; slot < m->d.max_slots && !live; ++slot) live = L.owner[slot] == dev;
+    if (!b.host && !live && b.cap > kv_cap_for(m, L, dev)) {
+      free_kv_block(m, L, dev, b);
+      it = L.kv.erase(it);
+    } else {
+      ++it;
+    }
+  }
 }
 
 // indices released during the previous step become reusable (cb_step entry:
@@ -1086,7 +1118,13 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
 int kv_follow(cb_model* m, LayerState& L, const Seg& s, const std::vector<int>& seq_slot) {
   const int ad = L.reps.size() > 1 ? s.dev : kv_device(L);
   const bool la = is_local(m, ad);
-  if (la) CB_TRY(ensure_kv(m, L, ad));
+  if (la) {
+    CB_TRY(ensure_kv(m, L, ad));
+    const KvBlock& b = L.kv.at(ad);
+    int need = 0;
+    for (int q = s.s0; q < s.s1 && b.table; ++q) need += b.map_h[seq_slot[q]] < 0;
+    CB_TRY(kv_reserve(m, L, ad, need));
+  }
   for (int q = s.s0; q < s.s1; ++q) {
     const int slot = seq_slot[q];
     const int owner = L.owner[slot];
@@ -1544,8 +1582,7 @@ int finish_layer_load(cb_model* m, int layer, LayerCopy& c) {
   L.reps.push_back(c);
   m->norm_ready = false;
   L.owner.assign(m->d.max_slots, -1);
-  CB_TRY(ensure_kv(m, L, c.dev));
-  CB_TRY(ensure_ws(m, c.dev));
+  CB_TRY(ensure_ws(m, c.dev));  // (the KV block is created at its first use, sized for the placement then)
   return CB_OK;
 }
 
@@ -1736,6 +1773,15 @@ int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
     CB_CUDA(cudaEventCreate(&op.c0));
     CB_CUDA(cudaEventCreate(&op.c1));
     CB_CUDA(cudaEventRecord(op.c0, tc.compute));
+  }
+  if (lt) {
+    auto it = L.kv.find(op.kv_to);
+    if (it != L.kv.end() && it->second.table) {
+      int need = 0;
+      for (int slot = 0; slot < m->d.max_slots; ++slot)
+        need += L.owner[slot] == op.kv_from && it->second.map_h[slot] < 0;
+      CB_TRY(kv_reserve(m, L, op.kv_to, need));
+    }
   }
   XGroup grp(m, 0);
   for (int slot = 0; slot < m->d.max_slots; ++slot) {
@@ -1999,6 +2045,7 @@ int op_commit(cb_model* m, PendingOp& op) {
   op.copy.block = nullptr;  // owned by the layer now
   op.mod.buf = nullptr;
   op_unlock(L, op);
+  if (op.kind == OPK_REPLICATE) kv_shrink_empty(m, L);
   if (op.dst >= 0) devctx(m, op.dst).reserved -= op.reserved;
   op.committed = true;
   return CB_OK;
@@ -2051,6 +2098,7 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
   if (m->rt->spmd) return fail(CB_ENOTSUP, "SPMD runtime: KV offload needs the single-process runtime");
   CB_TRY(check_idle(L, layer, OPK_MIGRATE));
   sync_all(m);  // Phase-3 relief (rare): a blocking move keeps the host-memory swap simple
+  if (to_host && is_local(m, kv_device(L))) CB_TRY(ensure_kv(m, L, kv_device(L)));  // not used yet: offload it empty
   uint64_t moved = 0;
   float ms = 0.f;
   for (auto& kv : L.kv) {
