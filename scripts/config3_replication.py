@@ -61,11 +61,20 @@ def main() -> None:
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--out", default="gpurun_out/config3.json")
     args = ap.parse_args()
+    from _oracle_check import check
+
+    def scenario(ex, cat, cluster, step):  # the hot layer replicated on every other device before serving
+        if step == 0:
+            for dv in range(1, args.devices):
+                ex.apply(O.ReplicateLayer(1, dv), cat, cluster)
+
+    parity = check(dict(d_model=4096, d_ff=11008, n_heads=32), args.devices, 48, 64, 6, scenario,
+                   release={2: [0, 7, 30], 4: [11, 12, 13, 47]})
     base = run(1, 0, args.duration, args.batch)
     repl = run(args.devices, args.hot, args.duration, args.batch)
     res = {"config": "config 3: Llama-2-7B, hot layers replicated, bursty trace (5 rps 4 s / 50 rps 2 s)",
            "note": "logical devices share one B200: replication adds no compute here; shows correctness + overhead",
-           "baseline_no_replication": base, "replicated": repl}
+           "parity": parity, "baseline_no_replication": base, "replicated": repl}
     Path(args.out).parent.mkdir(parents=True, exist_ok=True)
     Path(args.out).write_text(json.dumps(res, indent=1))
     print(json.dumps(res))

@@ -35,6 +35,17 @@ def main() -> None:
     ap.add_argument("--out", default="gpurun_out/config4.json")
     args = ap.parse_args()
     ordinals = [int(x) for x in args.ordinals.split(",")]
+    from _oracle_check import check
+
+    def scenario(ex, cat, cluster, step):  # migrations with KV mid-decode: one synchronous, one asynchronous
+        if step == 2:
+            ex.apply(O.MigrateLayer(1, 1, with_kv=True), cat, cluster)
+        if step == 3:
+            ex.issue(O.MigrateLayer(2, 1, with_kv=True), cat, cluster)  # copies run while step 3 decodes
+        if step == 4:
+            ex.commit(wait=True)
+
+    parity = check(dict(d_model=5120, d_ff=13824, n_heads=40), 2, 24, 48, 6, scenario, release={3: [5, 6]})
     rt = Runtime(ordinals)
     geom = dict(n_layers=40, d_model=5120, d_ff=13824, n_heads=40)
     ex = Executor(rt, ExecutorConfig(**geom, vocab=32000, max_slots=args.batch, max_ctx=args.prompt + 96,
@@ -82,6 +93,7 @@ def main() -> None:
     analytic = O.batch_apply(D.PlacementState.sequential(40, 0), batch_ops, cat, D.ClusterSpec.b200(2))[1]
     res = {
         "config": "config 4: Llama-2-13B shape, migration mid-serving (weights + KV)",
+        "parity": parity,
         "logical_devices": ordinals,
         "path": "same-GPU D2D (HBM)" if len(set(ordinals)) == 1 else "NVLink P2P",
         "batch": args.batch, "ctx_at_migration": args.prompt + 10,

@@ -20,6 +20,7 @@ import numpy as np
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 from paper_2507_18006_b200 import domain as D  # noqa: E402
+from paper_2507_18006_b200 import ops as O  # noqa: E402
 from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime  # noqa: E402
 
 
@@ -32,6 +33,14 @@ def main() -> None:
     ap.add_argument("--out", default="gpurun_out/config5.json")
     args = ap.parse_args()
     ordinals = [int(x) for x in args.ordinals.split(",")]
+    from _oracle_check import check
+
+    def scenario(ex, cat, cluster, step):  # sharded layers + the controller's projection migration
+        if step == 2:
+            ex.apply(O.MigrateSubModule(2, D.ModuleKind.FFN_PROJ_GATE, 0), cat, cluster)
+
+    parity = check(dict(d_model=8192, d_ff=28672, n_heads=64, n_kv_heads=8), 2, 8, 32, 5, scenario,
+                   device_of_layer=lambda li: li - 1)
     rt = Runtime(ordinals)
     cfg = ExecutorConfig(n_layers=80, d_model=8192, d_ff=28672, n_heads=64, n_kv_heads=8, vocab=32000,
                          max_slots=args.batch, max_ctx=args.prompt + args.steps + 8,
@@ -56,6 +65,7 @@ def main() -> None:
     mha = D.ModuleCatalog.from_model(D.ModelSpec(80, 8192, 28672, 64))
     res = {
         "config": "config 5: Llama-2-70B shape (GQA 8 KV heads), 80 layers sharded 10 per logical device",
+        "parity": parity,
         "logical_devices": ordinals, "batch": args.batch, "prompt": args.prompt,
         "original_layers_per_device": {d: len(p.original_layers_on(d)) for d in range(len(ordinals))},
         "decode_ms_per_step": step, "tokens_per_s": args.batch / step * 1e3, "prefill_ms": prefill_ms,

@@ -13,6 +13,10 @@ for j in "${JOBS[@]}"; do
     gemmod) timeout 600 python scripts/gemm_perf.py 0,411,512411,401,512401,412,421 256 --real-epi --norm > gpurun_out/gemm_od.txt 2>&1 ;;
     gputests) timeout 1200 python -m pytest tests -m gpu -q -rA 2>&1 | tail -60 > gpurun_out/pytest_gpu.txt ;;
     bench) timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err ;;
+    configs) timeout 900 python scripts/config3_replication.py --out gpurun_out/config3.json > gpurun_out/config3.log 2>&1
+             timeout 900 python scripts/config4_migration.py --out gpurun_out/config4.json > gpurun_out/config4.log 2>&1
+             timeout 900 python scripts/config5_70b_sharded.py --out gpurun_out/config5.json > gpurun_out/config5.log 2>&1 ;;
+    gemmsmall) timeout 600 python scripts/gemm_perf.py 0,2,3,4,99 1,16 --real-epi --norm > gpurun_out/gemm_small.txt 2>&1 ;;
   esac
 done
 ls gpurun_out
