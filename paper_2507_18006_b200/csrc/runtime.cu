@@ -1370,8 +1370,13 @@ std::vector<int> split_batch_vec(int bs, int p) {
 // One pass over a group of sequences whose rows fit max_tokens.
 double g_last_enqueue_ms = 0.0;  // experiments: host time to enqueue the last pass (cbt_last_enqueue_ms)
 
+// One pass over sequences [g_off, g_off + bs) of a step of g_bs sequences (a
+// prefill longer than max_tokens rows runs in several passes): each layer's
+// rows are routed by split_batch over the WHOLE step (sim.py:717-725: one
+// prefill of all fresh requests), so a sequence lands on the same replica as in
+// the decode steps that follow and its KV does not move.
 int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_t* tokens, const int32_t* lens,
-              int32_t* next_out, float* logits_out, float* ms_out) {
+              int32_t* next_out, float* logits_out, float* ms_out, int g_off, int g_bs) {
   const auto enq0 = std::chrono::steady_clock::now();
   const cb_model_desc& d = m->d;
   const bool prefill = phase == CB_PHASE_PREFILL;
@@ -1487,13 +1492,14 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
   for (int li = 0; li < d.n_layers; ++li) {
     LayerState& L = m->layers[li];
     const int p = int(L.reps.size());
-    const std::vector<int> shares = split_batch_vec(bs, p);
+    const std::vector<int> shares = split_batch_vec(g_bs, p);
     std::vector<Seg> segs;
-    int s0 = 0;
+    int g0 = 0;  // replica j's sequences: [g0, g0 + shares[j]) of the whole step
     for (int j = 0; j < p; ++j) {
-      m->last_routing[li].push_back({L.reps[j].dev, s0, shares[j]});
-      if (shares[j] > 0) segs.push_back({L.reps[j].dev, j, seq_row[s0], seq_row[s0 + shares[j]], s0, s0 + shares[j]});
-      s0 += shares[j];
+      m->last_routing[li].push_back({L.reps[j].dev, g0, shares[j]});
+      const int s0 = std::max(g0, g_off) - g_off, s1 = std::min(g0 + shares[j], g_off + bs) - g_off;
+      if (s1 > s0) segs.push_back({L.reps[j].dev, j, seq_row[s0], seq_row[s1], s0, s1});
+      g0 += shares[j];
     }
     CB_TRY(reshard(m, layout, segs, m->fin[li]));
     {
@@ -2598,7 +2604,7 @@ int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const 
   };
   if (phase == CB_PHASE_DECODE) {
     if (bad_tokens(bs)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
-    return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out);
+    return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out, 0, bs);
   }
   if (!prompt_lens) return fail(CB_EINVAL, "prefill needs prompt_lens");
   {
@@ -2619,7 +2625,7 @@ int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const 
     }
     if (j == i) return fail(CB_EINVAL, "prompt longer than max_tokens");
     CB_TRY(step_pass(m, phase, j - i, slots + i, tokens + tok_off, prompt_lens + i, next_out + i,
-                     logits_out ? logits_out + size_t(i) * m->d.vocab : nullptr, ms_out));
+                     logits_out ? logits_out + size_t(i) * m->d.vocab : nullptr, ms_out, i, bs));
     tok_off += rows;
     i = j;
   }

@@ -262,6 +262,39 @@ def test_replica_kv_sized_by_share(cuda, confident):
     rt.close()
 
 
+def test_prefill_in_several_passes_routes_like_one(runtime, confident):
+    """A prefill larger than max_tokens rows runs in several passes; each
+    layer's sequences are still routed by split_batch over the whole step
+    (sim.py:717-725: one prefill of all fresh requests), so every sequence's KV
+    lands on the replica that decodes it and the decode steps move exactly the
+    bytes of a single-pass prefill's (activation rows only, no KV prefix)."""
+    prompts = config1_prompts()
+    cat, cl = _catalog_cluster()
+    moved = {}
+    for max_tokens in (64, 512):  # 4 prompts of 16 tokens per pass / one pass
+        ex = Executor(runtime, _tiny_cfg(max_tokens=max_tokens))
+        ex.load_model(confident, device_of_layer=0)
+        ex.apply(O.ReplicateLayer(2, 1), cat, cl)
+        oracle = OracleModel(TINY, confident, 64)
+        slots = np.arange(N_REQ, dtype=np.int32)
+        nxt, lg, _ = ex.prefill(slots, np.concatenate(prompts), np.full(N_REQ, PROMPT, np.int32), want_logits=True)
+        ref = oracle.forward(list(range(N_REQ)), np.concatenate(prompts), [PROMPT] * N_REQ)
+        assert np.abs(lg - ref).max() <= LOGIT_TOL
+        assert ex.last_routing(2) == [(0, 0, 7), (1, 7, 8)]
+        assert [ex.read_kv(2, s_)[1] for s_ in range(N_REQ)] == [0] * 7 + [1] * 8
+        moved[max_tokens] = []
+        for step in range(3):
+            inp = ref.argmax(-1).astype(np.int32)
+            ex.profile(True)
+            nxt, lg, _ = ex.decode(slots, inp, want_logits=True)
+            moved[max_tokens].append(ex.profile_read()["copy"]["bytes"])
+            ex.profile(False)
+            ref = oracle.forward(list(range(N_REQ)), inp, None)
+            assert np.array_equal(nxt, ref.argmax(-1)) and np.abs(lg - ref).max() <= LOGIT_TOL
+        ex.close()
+    assert moved[64] == moved[512], moved
+
+
 def test_migration_moves_weights_and_kv_bit_exact(runtime, confident):
     prompts = config1_prompts()
     ex = _executor(runtime, confident)
