@@ -4,14 +4,15 @@
 // appended to the slot's cache (rope_kv_kernel).  CTA = (128-row query block of
 // one sequence, q head); 6 warps, warp-specialised:
 //
-//   warp 0      TMA producer: the Q tile once, then K and V blocks of 128
+//   warps 0, 6  TMA producers: the Q tile once, then K and V blocks of 128
 //               cached positions (SWIZZLE_128B boxes of 64 columns x 128 rows
 //               straight from the [slot][pos][k|v] cache) into a 3-stage K
-//               ring (freed when S_j retires) and a 2-stage V ring (freed when
-//               PV_j retires), K one block ahead of V
+//               ring (freed when S_j retires, warp 0) and a 2-stage V ring
+//               (freed when PV_j retires, warp 6)
 //   warp 1      MMA issuer (one elected lane of a converged warp):
 //               S_j = Q K_j^T   (M 128 x N 128 x K hd, both K-major) into one of
-//                                two TMEM S buffers, issued one block ahead;
+//                                two TMEM S buffers, issued one block ahead
+//                                when K_j has landed (else after PV_{j-1});
 //               O  += P_j V_j   (M 128 x N hd x K 128; P K-major from smem, V
 //                                MN-major: the cache's [pos][hd] rows as is)
 //   warps 2..5  softmax, one thread per query row = one TMEM lane: S row ->
@@ -31,11 +32,27 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifdef PF_TRACE  // timeline probe (scripts/pf_trace.py builds a separate library with it)
+__device__ unsigned long long* g_pf_trace = nullptr;
+#define PFT(slot, j)                                                                          \
+  do {                                                                                        \
+    if (g_pf_trace && blockIdx.y == 0 && blockIdx.x == gridDim.x - 1 && (j) < 32)             \
+      g_pf_trace[(slot) * 32 + (j)] = clock64();                                       \
+  } while (0)
+extern "C" int cbt_pf_trace_set(unsigned long long* p) {
+  return cudaMemcpyToSymbol(g_pf_trace, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
+}
+#else
+#define PFT(slot, j) \
+  do {               \
+  } while (0)
+#endif
+
 namespace cb {
 
 static constexpr int kPfRows = 128;  // query rows per CTA = UMMA M = TMEM lanes
 static constexpr int kPfKeys = 128;  // cached positions per K/V block = UMMA N of S = UMMA K of PV
-static constexpr int kPfThreads = 192;
+static constexpr int kPfThreads = 224;
 
 template <int HD>
 struct PfCfg {
@@ -65,6 +82,39 @@ CB_DEVICE float fast_exp2(float x) {  // ex2.approx.ftz: one MUFU.EX2, exp2(-inf
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// Four K=16 MMAs from one asm block (one elected lane of a converged warp):
+// A advances 32 bytes per MMA (a K-major 128-byte-swizzled box), B by
+// BSTEP (>> 4 encoded): 2 for a K-major box, 128 for an MN-major operand
+// (16 rows of 128 bytes).  Per-MMA asm blocks cost ~120 clk of descriptor moves
+// each (measured with scripts/pf_trace.py: 0.5 us for 8 MMAs).
+template <int BSTEP>
+CB_DEVICE void umma4_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 a1, a2, a3, b1, b2, b3;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 a2, %1, 4;\n\tadd.s64 a3, %1, 6;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, %2, %6;\n\tadd.s64 b3, %2, %7;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP)
+      : "memory");
+}
+
+// non-blocking: has the phase with this parity completed?
+CB_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 CB_DEVICE void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -131,6 +181,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // q rotated and K/V appended by rope_kv_kernel
+  if (threadIdx.x == 0) PFT(9, 0);
 
   const int4 blk = blocks[blockIdx.x];  // (first row, rows, slot, first position)
   const int row0 = a.row_off + blk.x, nrows = blk.y, p0 = blk.w;
@@ -155,10 +206,16 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         for (int r = 0; r < NR; ++r)
           tma_load_2d(&mkv, k_full + s, sK + s * C::kK + r * C::kRegion, hk * HD + r * 64, kv_row0 + j * kPfKeys,
                       pol_kv);
+        PFT(0, j);
       };
-      load_k(0);
-      for (int j = 0; j < nkb; ++j) {  // K runs one block ahead of V (S_j precedes PV_j)
-        if (j + 1 < nkb) load_k(j + 1);
+      for (int j = 0; j < nkb; ++j) load_k(j);
+    }
+    __syncwarp();
+  } else if (warp == 6) {  // V producer: its ring waits on PV, which must not hold back the K loads
+    if (elect_one()) {
+      const uint64_t pol_kv = policy_evict_last();
+      const int kv_row0 = slot * a.max_ctx;
+      for (int j = 0; j < nkb; ++j) {
         const int s = j & 1;
         if (j >= 2) mbar_wait(v_empty + s, ((j >> 1) + 1) & 1);
         mbar_arrive_expect_tx(v_full + s, C::kV);
@@ -166,6 +223,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         for (int r = 0; r < NR; ++r)
           tma_load_2d(&mkv, v_full + s, sV + s * C::kV + r * C::kRegion, (a.Hkv + hk) * HD + r * 64,
                       kv_row0 + j * kPfKeys, pol_kv);
+        PFT(1, j);
       }
     }
     __syncwarp();
@@ -181,32 +239,43 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       tc_fence_after();
       const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + ks * C::kK);
 #pragma unroll
-      for (int kk = 0; kk < HD / 16; ++kk) {
-        const uint32_t off = (kk >> 2) * C::kRegion + (kk & 3) * 32;
-        umma_bf16_elect(tmem + s * 128, make_sw128_desc(q0 + off), make_sw128_desc(k0 + off), idesc_s, kk > 0);
-      }
+      for (int g = 0; g < NR; ++g)  // 64 head dims (one box) per group of 4 MMAs
+        umma4_elect<2>(tmem + s * 128, make_sw128_desc(q0 + g * C::kRegion), make_sw128_desc(k0 + g * C::kRegion),
+                       idesc_s, g > 0);
       umma_commit_elect(s_full + s);
       umma_commit_elect(k_empty + ks);
+      if (lane == 0) PFT(2, j);
     };
     issue_s(0);
     for (int j = 0; j < nkb; ++j) {
       const int s = j & 1;
-      if (j + 1 < nkb) issue_s(j + 1);
+      // S_{j+1} ahead of PV_j (the softmax of j+1 then starts as soon as j's is
+      // done) -- unless K_{j+1} has not landed: PV_j must not wait on that load
+      bool ahead = false;
+      if (j + 1 < nkb) {
+        const int n = j + 1;
+        bool ok = mbar_test(k_full + n % 3, (n / 3) & 1) && (n < 2 || mbar_test(s_free + (n & 1), ((n >> 1) + 1) & 1));
+        ahead = __shfl_sync(0xffffffffu, ok, 0);
+        if (ahead) issue_s(n);
+      }
       mbar_wait(p_full, j & 1);
+      if (lane == 0) PFT(3, j);
       mbar_wait(v_full + s, (j >> 1) & 1);
+      if (lane == 0) PFT(10, j);
       tc_fence_after();
       const uint32_t p0a = smem_u32(sP), v0 = smem_u32(sV + s * C::kV);
 #pragma unroll
-      for (int kk = 0; kk < kPfKeys / 16; ++kk) {
-        const uint32_t poff = (kk >> 2) * C::kRegion + (kk & 3) * 32;
-        umma_bf16_elect(tO, make_sw128_desc(p0a + poff), make_sw128_mn_desc(v0 + kk * 2048, C::kRegion), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-      }
+      for (int g = 0; g < kPfKeys / 64; ++g)  // 64 keys (one P box, 64 V rows) per group of 4 MMAs
+        umma4_elect<128>(tO, make_sw128_desc(p0a + g * C::kRegion), make_sw128_mn_desc(v0 + g * 8192, C::kRegion),
+                         idesc_o, (j > 0 || g > 0) ? 1u : 0u);
+      if (lane == 0) PFT(11, j);
       umma_commit_elect(o_done);
       umma_commit_elect(v_empty + s);
+      if (lane == 0) PFT(4, j);
+      if (j + 1 < nkb && !ahead) issue_s(j + 1);
     }
     __syncwarp();
-  } else {
+  } else if (warp >= 2 && warp <= 5) {
     // softmax: thread = query row r = TMEM lane (warp w may touch lanes 32 (w % 4) ..)
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;
@@ -219,6 +288,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     for (int j = 0; j < nkb; ++j) {
       const int s = j & 1;
       mbar_wait(s_full + s, (j >> 1) & 1);
+      if (warp == 2 && lane == 0) PFT(5, j);
       tc_fence_after();
       float v[kPfKeys];
 #pragma unroll
@@ -263,8 +333,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         rs += e0 + e1;
         pk[e] = pack_bf16x2(e0, e1);
       }
+      if (warp == 2 && lane == 0) PFT(6, j);
       if (j > 0) {
         mbar_wait(o_done, (j - 1) & 1);  // PV_{j-1} retired: O is final for j-1 and P is free
+        if (warp == 2 && lane == 0) PFT(7, j);
         tc_fence_after();
         if (__any_sync(0xffffffffu, need)) {  // lazy rescale: only when a row max grew by > 2^8
 #pragma unroll
@@ -300,6 +372,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(p_full);
+      if (warp == 2 && lane == 0) PFT(8, j);
     }
     mbar_wait(o_done, (nkb - 1) & 1);
     tc_fence_after();
@@ -326,6 +399,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) PFT(9, 1);
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
