@@ -334,32 +334,10 @@ cudaError_t init_uniform_launch(uint16_t* dst, size_t n, uint64_t seed, float st
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- segment copy
-// One CTA per segment, 128-bit loads with 4-way unroll; src may live on a peer.
-__global__ void copy_segments_kernel(const CopySeg* __restrict__ segs) {
-  const CopySeg s = segs[blockIdx.y];
-  const size_t n16 = s.bytes / 16;
-  const uint4* src = reinterpret_cast<const uint4*>(s.src);
-  uint4* dst = reinterpret_cast<uint4*>(s.dst);
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    uint4 a = src[i], b = src[i + stride], c = src[i + 2 * stride], d = src[i + 3 * stride];
-    dst[i] = a;
-    dst[i + stride] = b;
-    dst[i + 2 * stride] = c;
-    dst[i + 3 * stride] = d;
-  }
-  for (; i < n16; i += stride) dst[i] = src[i];
-}
-
-cudaError_t copy_segments_launch(const CopySeg* segs_dev, int nseg, cudaStream_t st) {
-  if (nseg <= 0) return cudaSuccess;
-  dim3 grid(8, nseg);
-  copy_segments_kernel<<<grid, 256, 0, st>>>(segs_dev);
-  return cudaGetLastError();
-}
-
+// ---------------------------------------------------------------- SM copy engine
+// Transfer mode 2 of the scaling ops (cb_set_copy_mode): launched on the SOURCE
+// GPU, 128-bit streaming loads and stores, 4-way unrolled; dst may be a peer
+// pointer (NVLink writes need no round trip).
 __global__ void __launch_bounds__(512) copy_bulk_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
                                                           size_t n16) {
   const size_t stride = (size_t)gridDim.x * blockDim.x;

@@ -146,14 +146,6 @@ cudaError_t gather_rows_launch(const uint16_t* src, const int32_t* idx, uint16_t
 cudaError_t argmax_launch(const float* logits, int32_t* out, int T, int V, cudaStream_t st);
 // deterministic counter-based init: uniform with the given std, plus `mean`
 cudaError_t init_uniform_launch(uint16_t* dst, size_t n, uint64_t seed, float std, float mean, cudaStream_t st);
-// SM-driven gather copy of (src, dst, bytes) segments (16-byte aligned), used for
-// KV row moves; src/dst may be peer pointers.
-struct CopySeg {
-  const void* src;
-  void* dst;
-  unsigned long long bytes;
-};
-cudaError_t copy_segments_launch(const CopySeg* segs_dev, int nseg, cudaStream_t st);
 // Contiguous copy by the SMs of the launching GPU (dst and/or src may be peer
 // memory): 16-byte vectors, 4 in flight per thread.  bytes % 16 == 0, 16-byte aligned.
 cudaError_t copy_bulk_launch(void* dst, const void* src, size_t bytes, int num_sms, cudaStream_t st);
