@@ -2,31 +2,34 @@
 //
 // Prefill rows of one sequence are contiguous in qkv and their K/V were just
 // appended to the slot's cache (rope_kv_kernel).  CTA = (128-row query block of
-// one sequence, q head); 6 warps, warp-specialised:
+// one sequence, q head); 11 warps, warp-specialised:
 //
-//   warps 0, 6  TMA producers: the Q tile once, then K and V blocks of 128
+//   warps 0, 10 TMA producers: the Q tile once, then K and V blocks of 128
 //               cached positions (SWIZZLE_128B boxes of 64 columns x 128 rows
-//               straight from the [slot][pos][k|v] cache) into a 3-stage K
-//               ring (freed when S_j retires, warp 0) and a 2-stage V ring
-//               (freed when PV_j retires, warp 6)
+//               straight from the [slot][pos][k|v] cache) into a K ring
+//               (freed when S_j retires, warp 0) and a 2-stage V ring
+//               (freed when PV_j retires, warp 10)
 //   warp 1      MMA issuer (one elected lane of a converged warp):
 //               S_j = Q K_j^T   (M 128 x N 128 x K hd, both K-major) into one of
 //                                two TMEM S buffers, issued one block ahead
 //                                when K_j has landed (else after PV_{j-1});
 //               O  += P_j V_j   (M 128 x N hd x K 128; P K-major from smem, V
 //                                MN-major: the cache's [pos][hd] rows as is)
-//   warps 2..5  softmax, one thread per query row = one TMEM lane: S row ->
-//               registers (tcgen05.ld), causal mask, online softmax in the
-//               exp2 domain with lazy rescaling (O in TMEM is rescaled with
+//   warps 2..9  softmax, two threads per query row (TMEM lane), one per half
+//               of the block's columns: S half-row -> registers (tcgen05.ld),
+//               causal mask, row max exchanged between the halves through
+//               smem, online softmax in the exp2 domain (one FFMA + MUFU.EX2 per
+//               score) with lazy rescaling (O in TMEM is rescaled with
 //               tcgen05.ld/st only when a row max grows by > 2^8), P as bf16
 //               into smem in the 128-byte-swizzled K-major layout the MMA
-//               reads; finally O / l -> bf16 -> global.
+//               reads; finally O / l -> bf16 -> global.  Two warps per SM
+//               sub-partition hide the MUFU / FFMA latencies one warp could not.
 //
 // TMEM: S double buffer (2 x 128 columns) + O (hd columns).  Smem (hd 128):
-// Q 32 KB + 3 x K 32 KB + 2 x V 32 KB + P 32 KB = 224 KB.  Positions past the
-// sequence's last row inside the last key block are masked in S, and their V
-// rows are zeroed in smem before the PV MMA (stale cache bytes could hold
-// non-finite values; 0 * NaN would poison the row).
+// Q 32 KB + 2 x K 32 KB + 2 x V 32 KB + P 32 KB = 192 KB (hd 64: 3 K stages).
+// Positions past the sequence's last row inside the last key block are masked
+// in S, and their V rows are zeroed in smem before the PV MMA (stale cache
+// bytes could hold non-finite values; 0 * NaN would poison the row).
 //
 // Replaces the mma.sync (HMMA.16816) flash-attention forward of round 1.
 #include "common.cuh"
@@ -52,7 +55,7 @@ namespace cb {
 
 static constexpr int kPfRows = 128;  // query rows per CTA = UMMA M = TMEM lanes
 static constexpr int kPfKeys = 128;  // cached positions per K/V block = UMMA N of S = UMMA K of PV
-static constexpr int kPfThreads = 224;
+static constexpr int kPfThreads = 352;  // 11 warps: K producer, MMA, 8 softmax, V producer
 
 template <int HD>
 struct PfCfg {
@@ -61,8 +64,8 @@ struct PfCfg {
   static constexpr int kK = kPfKeys * HD * 2;
   static constexpr int kV = kPfKeys * HD * 2;
   static constexpr int kP = kPfRows * kPfKeys * 2;
-  static constexpr int kBars = 16 * 8;
-  static constexpr int kKStages = 3, kVStages = 2;  // K is released after S, V after PV
+  static constexpr int kBars = 18 * 8 + 6 * 128 * 4;  // barriers + the softmax halves' max / sum exchange
+  static constexpr int kKStages = HD == 64 ? 3 : 2, kVStages = 2;  // K is released after S, V after PV
   static constexpr int kSmem = 1024 + kQ + kKStages * kK + kVStages * kV + kP + kBars;
   static constexpr uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256 + HD)
 };
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   extern __shared__ uint8_t pf_raw[];
   uint8_t* sm = pf_raw + ((1024 - (smem_u32(pf_raw) & 1023)) & 1023);
   uint8_t* sQ = sm;
-  uint8_t* sK = sQ + C::kQ;                 // [3 stages]
+  uint8_t* sK = sQ + C::kQ;                 // [kKStages]
   uint8_t* sV = sK + C::kKStages * C::kK;   // [2 stages]
   uint8_t* sP = sV + C::kVStages * C::kV;   // [2 boxes of 64 keys]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + C::kP);
@@ -158,7 +161,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     mbar_init(bar_q, 1);
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < C::kKStages; ++i) {
       mbar_init(k_full + i, 1);
       mbar_init(k_empty + i, 1);
     }
@@ -166,9 +169,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_init(v_full + i, 1);
       mbar_init(v_empty + i, 1);
       mbar_init(s_full + i, 1);
-      mbar_init(s_free + i, 128);
+      mbar_init(s_free + i, 256);
     }
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(o_done, 1);
     fence_barrier_init();
     tma_prefetch_desc(&mq);
@@ -198,9 +201,10 @@ __global__ void __launch_bounds__(kPfThreads, 1)
 #pragma unroll
       for (int r = 0; r < NR; ++r) tma_load_2d(&mq, bar_q, sQ + r * C::kRegion, qh * HD + r * 64, row0, pol_q);
       const int kv_row0 = slot * a.max_ctx;
-      auto load_k = [&](int j) {  // stage j % 3, free once S_{j-3} retired
-        const int s = j % 3;
-        if (j >= 3) mbar_wait(k_empty + s, ((j / 3) + 1) & 1);
+      constexpr int KS = C::kKStages;
+      auto load_k = [&](int j) {  // stage j % KS, free once S_{j-KS} retired
+        const int s = j % KS;
+        if (j >= KS) mbar_wait(k_empty + s, ((j / KS) + 1) & 1);
         mbar_arrive_expect_tx(k_full + s, C::kK);
 #pragma unroll
         for (int r = 0; r < NR; ++r)
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       for (int j = 0; j < nkb; ++j) load_k(j);
     }
     __syncwarp();
-  } else if (warp == 6) {  // V producer: its ring waits on PV, which must not hold back the K loads
+  } else if (warp == 10) {  // V producer: its ring waits on PV, which must not hold back the K loads
     if (elect_one()) {
       const uint64_t pol_kv = policy_evict_last();
       const int kv_row0 = slot * a.max_ctx;
@@ -233,8 +237,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const uint32_t tO = tmem + 256;
     mbar_wait(bar_q, 0);
     auto issue_s = [&](int j) {
-      const int s = j & 1, ks = j % 3;
-      mbar_wait(k_full + ks, (j / 3) & 1);
+      const int s = j & 1, ks = j % C::kKStages;
+      mbar_wait(k_full + ks, (j / C::kKStages) & 1);
       if (j >= 2) mbar_wait(s_free + s, ((j >> 1) + 1) & 1);
       tc_fence_after();
       const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + ks * C::kK);
@@ -254,7 +258,8 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       bool ahead = false;
       if (j + 1 < nkb) {
         const int n = j + 1;
-        bool ok = mbar_test(k_full + n % 3, (n / 3) & 1) && (n < 2 || mbar_test(s_free + (n & 1), ((n >> 1) + 1) & 1));
+        bool ok = mbar_test(k_full + n % C::kKStages, (n / C::kKStages) & 1) &&
+                  (n < 2 || mbar_test(s_free + (n & 1), ((n >> 1) + 1) & 1));
         ahead = __shfl_sync(0xffffffffu, ok, 0);
         if (ahead) issue_s(n);
       }
@@ -275,43 +280,53 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       if (j + 1 < nkb && !ahead) issue_s(j + 1);
     }
     __syncwarp();
-  } else if (warp >= 2 && warp <= 5) {
-    // softmax: thread = query row r = TMEM lane (warp w may touch lanes 32 (w % 4) ..)
-    const int q4 = warp & 3;
+  } else if (warp >= 2 && warp <= 9) {
+    // softmax: two warps per query row quarter (warp w may touch TMEM lanes
+    // 32 (w % 4) ..); thread = (row r = TMEM lane, column half hh): 64 of the
+    // block's 128 scores and hd / 2 of the O columns.  The two halves of a row
+    // exchange their partial row max through smem each block (named barrier
+    // of the quarter's 64 threads) and their partial sums at the end.
+    constexpr int KH = kPfKeys / 2, OH = HD / 2;
+    const int q4 = warp & 3, hh = (warp - 2) >> 2;
     const int r = q4 * 32 + lane;
     const uint32_t lane_off = uint32_t(q4 * 32) << 16;
     const int qp = p0 + r;
     const float sl2 = a.scale * 1.4426950408889634f;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + r * 128;
+    uint8_t* prow = sP + hh * C::kRegion + r * 128;
     const int rsw = r & 7;
+    float* red = reinterpret_cast<float*>(bars + 18);  // [2 blocks][2 halves][128 rows]
     for (int j = 0; j < nkb; ++j) {
       const int s = j & 1;
       mbar_wait(s_full + s, (j >> 1) & 1);
       if (warp == 2 && lane == 0) PFT(5, j);
       tc_fence_after();
-      float v[kPfKeys];
-#pragma unroll
-      for (int c = 0; c < kPfKeys / 32; ++c) {
-        uint32_t u[32];
-        tmem_ld32(tmem + lane_off + s * 128 + c * 32, u);
+      float v[KH];
+      {
+        uint32_t u0[32], u1[32];
+        tmem_ld32(tmem + lane_off + s * 128 + hh * KH, u0);
+        tmem_ld32(tmem + lane_off + s * 128 + hh * KH + 32, u1);
         tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[c * 32 + e] = __uint_as_float(u[e]);
+        for (int e = 0; e < 32; ++e) {
+          v[e] = __uint_as_float(u0[e]);
+          v[32 + e] = __uint_as_float(u1[e]);
+        }
       }
       tc_fence_before();
       mbar_arrive(s_free + s);
-      const int kbase = j * kPfKeys;
-      const bool mask = kbase + kPfKeys - 1 > p0;  // the block reaches past some row's position
-      if (mask) {  // (block-uniform) causal mask on raw scores
+      const int kbase = j * kPfKeys + hh * KH;
+      if (j * kPfKeys + kPfKeys - 1 > p0) {  // (block-uniform) causal mask on raw scores
 #pragma unroll
-        for (int c = 0; c < kPfKeys; ++c)
+        for (int c = 0; c < KH; ++c)
           if (kbase + c > qp) v[c] = -INFINITY;
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kPfKeys; ++c) mx = fmaxf(mx, v[c]);
-      mx *= sl2;  // row max in the scaled log2 domain
+      for (int c = 0; c < KH; ++c) mx = fmaxf(mx, v[c]);
+      red[((j & 1) * 2 + hh) * 128 + r] = mx;
+      named_bar_sync(1 + q4, 64);
+      mx = fmaxf(mx, red[((j & 1) * 2 + (hh ^ 1)) * 128 + r]) * sl2;  // row max, scaled log2 domain
       float alpha = 1.f;
       bool need = false;
       if (j == 0) {
@@ -325,9 +340,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       }
       // P = exp2(S - m) packed to bf16 in registers while PV_{j-1} may still run
       float rs = 0.f;
-      uint32_t pk[kPfKeys / 2];
+      uint32_t pk[KH / 2];
 #pragma unroll
-      for (int e = 0; e < kPfKeys / 2; ++e) {
+      for (int e = 0; e < KH / 2; ++e) {
         const float e0 = fast_exp2(fmaf(v[2 * e], sl2, -m_used));  // FFMA + MUFU.EX2 per score
         const float e1 = fast_exp2(fmaf(v[2 * e + 1], sl2, -m_used));
         rs += e0 + e1;
@@ -340,33 +355,34 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         tc_fence_after();
         if (__any_sync(0xffffffffu, need)) {  // lazy rescale: only when a row max grew by > 2^8
 #pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
+          for (int c = 0; c < OH / 32; ++c) {
             uint32_t u[32];
-            tmem_ld32(tmem + lane_off + 256 + c * 32, u);
+            tmem_ld32(tmem + lane_off + 256 + hh * OH + c * 32, u);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) u[e] = __float_as_uint(__uint_as_float(u[e]) * alpha);
-            tmem_st32(tmem + lane_off + 256 + c * 32, u);
+            tmem_st32(tmem + lane_off + 256 + hh * OH + c * 32, u);
           }
           tmem_st_wait();
         }
       }
 #pragma unroll
-      for (int ch = 0; ch < kPfKeys / 8; ++ch) {  // 16-byte chunks of 8 keys, 128-byte swizzle
-        uint8_t* dst = prow + (ch >> 3) * C::kRegion + (((ch & 7) ^ rsw) << 4);
+      for (int ch = 0; ch < KH / 8; ++ch) {  // 16-byte chunks of 8 keys, 128-byte swizzle
+        uint8_t* dst = prow + ((ch ^ rsw) << 4);
         *reinterpret_cast<uint4*>(dst) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
       }
       l = l * alpha + rs;
-      if (kbase + kPfKeys - 1 > last_pos) {
+      if (j * kPfKeys + kPfKeys - 1 > last_pos) {
         // last block: V rows past the sequence's last position -> 0 (P is 0 there)
         mbar_wait(v_full + s, (j >> 1) & 1);
-        if (kbase + r > last_pos) {
+        if (j * kPfKeys + r > last_pos) {
           uint8_t* vrow = sV + s * C::kV + r * 128;
 #pragma unroll
           for (int b = 0; b < NR; ++b)
+            if ((b & 1) == hh)
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-              *reinterpret_cast<uint4*>(vrow + b * C::kRegion + ch * 16) = make_uint4(0, 0, 0, 0);
+              for (int ch = 0; ch < 8; ++ch)
+                *reinterpret_cast<uint4*>(vrow + b * C::kRegion + ch * 16) = make_uint4(0, 0, 0, 0);
         }
       }
       fence_proxy_async_smem();
@@ -374,14 +390,17 @@ __global__ void __launch_bounds__(kPfThreads, 1)
       mbar_arrive(p_full);
       if (warp == 2 && lane == 0) PFT(8, j);
     }
+    red[(4 + hh) * 128 + r] = l;  // the two halves' row sums
+    named_bar_sync(1 + q4, 64);
+    l += red[(4 + (hh ^ 1)) * 128 + r];
     mbar_wait(o_done, (nkb - 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
-    uint16_t* out = a.out + (size_t)(row0 + r) * a.H * HD + (size_t)qh * HD;
+    uint16_t* out = a.out + (size_t)(row0 + r) * a.H * HD + (size_t)qh * HD + hh * OH;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < OH / 32; ++c) {
       uint32_t u[32];
-      tmem_ld32(tmem + lane_off + 256 + c * 32, u);
+      tmem_ld32(tmem + lane_off + 256 + hh * OH + c * 32, u);
       tmem_ld_wait();
       if (r < nrows) {
 #pragma unroll
