@@ -11,8 +11,9 @@
 // covers 32/(hd/8) positions per step, 4 warps stride the context.  Scores use
 // exp2 with q pre-scaled by log2(e)/sqrt(hd); online softmax in fp32; the
 // partial states are merged across lane groups (shuffles), warps (smem) and --
-// for short batches with long context -- across context splits (a second
-// combine kernel).  Decode attention is HBM-bound: every K/V byte is read once.
+// for short batches with long context -- across context splits (the last
+// split CTA of a (row, kv head) to arrive merges the partials, in split
+// order).  Decode attention is HBM-bound: every K/V byte is read once.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -261,25 +262,38 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       }
     }
   }
-}
-
-template <int HD>
-__global__ void attn_combine_kernel(const AttnArgs a, int nsplit) {
-  pdl_trigger();
-  pdl_wait();
-  const int rl = blockIdx.x, qh = blockIdx.y, i = threadIdx.x;
-  const float* st = a.ws + ((size_t)rl * a.H + qh) * nsplit * (HD + 2);
-  float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, st[s * (HD + 2)]);
-  float L = 0.f, o = 0.f;
-  for (int s = 0; s < nsplit; ++s) {
-    const float ms = st[s * (HD + 2)];
-    const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
-    L += st[s * (HD + 2) + 1] * c;
-    o += st[s * (HD + 2) + 2 + i] * c;
+  if (nsplit > 1) {
+    // the last split CTA of (row, kv head) merges every split's partial state
+    // (fixed split order: deterministic whatever the arrival order)
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      int* cnt = a.counters + (size_t)rl * a.Hkv + hk;
+      s_last = atomicAdd(cnt, 1) == nsplit - 1;
+      if (s_last) *cnt = 0;  // every split arrived: ready for the next launch
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int row = a.row_off + rl;
+      for (int idx = threadIdx.x; idx < GQ * HD; idx += kAttnWarps * 32) {
+        const int h = idx / HD, i = idx % HD;
+        const int qh = hk * GQ + h;
+        const float* st = a.ws + ((size_t)rl * a.H + qh) * nsplit * (HD + 2);
+        float M = -INFINITY;
+        for (int s = 0; s < nsplit; ++s) M = fmaxf(M, __ldcg(st + s * (HD + 2)));
+        float L = 0.f, o = 0.f;
+        for (int s = 0; s < nsplit; ++s) {
+          const float ms = __ldcg(st + s * (HD + 2));
+          const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+          L += __ldcg(st + s * (HD + 2) + 1) * c;
+          o += __ldcg(st + s * (HD + 2) + 2 + i) * c;
+        }
+        a.out[(size_t)row * a.H * HD + (size_t)qh * HD + i] = f_to_bf16(o / L);
+      }
+    }
   }
-  const int row = a.row_off + rl;
-  a.out[(size_t)row * a.H * HD + (size_t)qh * HD + i] = f_to_bf16(o / L);
 }
 
 template <int HD>
@@ -292,16 +306,21 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
   constexpr int NG = kAttnWarps * (32 / (HD / 8));
   if (gq < 1 || NG % gq != 0) return cudaErrorInvalidValue;
   int nsplit = 1;
-  const long long ctas = (long long)a.T * a.Hkv;
+  // the split is decided from the rows of the whole pass (kind_T), so a
+  // replica's share of the rows splits its contexts exactly like the
+  // unreplicated pass (same summation order: replication stays bit-identical)
+  const long long ctas = (long long)(a.kind_T > 0 ? a.kind_T : a.T) * a.Hkv;
   // enough CTAs to keep HBM busy: MHA needs 2 waves; a GQA CTA carries gq
-  // heads' work, so aim for 8 waves of CTAs there
+  // heads' work, so aim for 8 waves of CTAs there.  The merge runs in the last
+  // split CTA (no second launch), so short chunks only cost partial traffic.
   const long long want = (gq > 1 ? 8LL : 2LL) * num_sms;
-  const int min_chunk = gq > 1 ? 128 : 256;
+  const int min_chunk = gq > 1 ? 128 : 64;
   if (ctas < want && a.max_len > min_chunk) {
     nsplit = int((want + ctas - 1) / ctas);
     nsplit = min(nsplit, (a.max_len + min_chunk - 1) / min_chunk);
     nsplit = min(nsplit, 32);
     while (nsplit > 1 && (size_t)a.T * a.H * nsplit * (HD + 2) > a.ws_floats) --nsplit;
+    if (!a.counters) nsplit = 1;  // (the merge needs the arrival counters)
   }
   const int chunk = (a.max_len + nsplit - 1) / nsplit;
   // positions in flight per lane group: 4 when there are enough CTAs to fill
@@ -322,8 +341,7 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
       default: e = cudaErrorInvalidValue;
     }
   }
-  if (e != cudaSuccess || nsplit == 1) return e;
-  return launch_pdl(attn_combine_kernel<HD>, dim3(a.T, a.H), dim3(HD), 0, st, a, nsplit);
+  return e;
 }
 
 cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st) {

@@ -123,6 +123,8 @@ struct AttnArgs {
   const int32_t* row_pos;
   float* ws;       // split-context partials
   size_t ws_floats;
+  int* counters;   // split-context arrivals per (row, kv head), zero between launches
+  int kind_T;      // rows of the whole pass (the split decision; 0 = T): replicas split like the unreplicated pass
   const float2* rope;  // non-null: fused decode path (RoPE of q/k + KV append inside the kernel)
   int T, row_off, H, Hkv, hd, max_ctx, max_len;
   float scale;  // 1/sqrt(hd)

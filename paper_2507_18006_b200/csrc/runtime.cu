@@ -204,6 +204,7 @@ struct Workspace {
   int* gemm_cnt = nullptr;
   float* attn_ws = nullptr;
   size_t attn_ws_floats = 0;
+  int* attn_cnt = nullptr;  // split-context arrivals per (row, kv head)
   float2* rope = nullptr;
   OpMap map_h[kTnCount], map_hl[kTnCount], map_att[kTnCount], map_act[kTnCount];
   // TMA-store epilogue maps by (output base, epi, cols, ldo, rows), built on first use
@@ -507,6 +508,8 @@ int ensure_ws(cb_model* m, int dev) {
   CB_CUDA(cudaMemset(w.gemm_cnt, 0, size_t(cb::kGemmMaxTiles) * 4));
   w.attn_ws_floats = size_t(4 * dc.num_sms) * 8 * (m->hd + 2) * 4;
   CB_TRY(dev_alloc(dc, (void**)&w.attn_ws, w.attn_ws_floats * 4));
+  CB_TRY(dev_alloc(dc, (void**)&w.attn_cnt, size_t(std::max(d.max_tokens, d.max_slots)) * d.n_kv_heads * 4));
+  CB_CUDA(cudaMemset(w.attn_cnt, 0, size_t(std::max(d.max_tokens, d.max_slots)) * d.n_kv_heads * 4));
   // RoPE table, rotate-half convention: angle(pos, i) = pos * theta^(-2i/hd)
   const int half = m->hd / 2;
   std::vector<float2> tab(size_t(d.max_ctx) * half);
@@ -1086,6 +1089,8 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
   aa.row_pos = rpos;
   aa.ws = wa.attn_ws;
   aa.ws_floats = wa.attn_ws_floats;
+  aa.counters = wa.attn_cnt;
+  aa.kind_T = m->cur_T;  // the split decision follows the whole pass, not this replica's rows
   aa.T = T;
   aa.row_off = s.r0;
   aa.H = d.n_heads;
@@ -2364,7 +2369,7 @@ int cb_model_destroy(cb_model* m) {
   for (auto& kv : m->ws) {
     Workspace& w = kv.second;
     void* ptrs[] = {w.x, w.h, w.hl, w.qkv, w.att, w.act, w.gbuf, w.logits, w.meta, w.next, w.gemm_ws, w.gemm_cnt,
-                    w.attn_ws, w.rope};
+                    w.attn_ws, w.attn_cnt, w.rope};
     for (void* p : ptrs) dev_free(m, kv.first, p);
   }
   dev_free(m, m->home, m->embed);

@@ -19,6 +19,7 @@ struct TestWs {
   int* cnt = nullptr;
   float* attn_ws = nullptr;
   size_t attn_floats = 0;
+  int* attn_cnt = nullptr;
   int sms = 148;
 };
 
@@ -38,6 +39,8 @@ int ws_for_current(TestWs** out) {
     cudaMemset(w.cnt, 0, size_t(cb::kGemmMaxTiles) * 4);
     w.attn_floats = size_t(1) << 24;
     if (cudaMalloc(&w.attn_ws, w.attn_floats * 4) != cudaSuccess) return CB_ECUDA;
+    if (cudaMalloc(&w.attn_cnt, size_t(1 << 16) * 4) != cudaSuccess) return CB_ECUDA;
+    cudaMemset(w.attn_cnt, 0, size_t(1 << 16) * 4);
   }
   *out = &w;
   return CB_OK;
@@ -260,6 +263,7 @@ extern "C" int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* 
   a.row_slot = row_slot;
   a.row_pos = row_pos;
   a.ws = ws->attn_ws;
+  a.counters = ws->attn_cnt;
   a.ws_floats = ws->attn_floats;
   a.T = T;
   a.H = H;
@@ -309,6 +313,7 @@ int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const 
   a.row_slot = row_slot;
   a.row_pos = row_pos;
   a.ws = ws->attn_ws;
+  a.counters = ws->attn_cnt;
   a.ws_floats = ws->attn_floats;
   a.T = T;
   a.H = H;
@@ -333,6 +338,7 @@ int cbt_attention_bench(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, 
   a.row_slot = row_slot;
   a.row_pos = row_pos;
   a.ws = ws->attn_ws;
+  a.counters = ws->attn_cnt;
   a.ws_floats = ws->attn_floats;
   a.T = T;
   a.H = H;
