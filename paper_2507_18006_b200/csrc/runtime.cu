@@ -2157,6 +2157,113 @@ int kv_offload(cb_model* m, int layer, bool to_host, cb_op_stats* st) {
 }  // namespace
 
 // ============================================================== C-ABI
+namespace {
+// Routing order of a step's sequences (SURVEY §7 hard part 1, option A: sticky
+// assignment).  split_batch fixes how MANY sequences each replica of a layer
+// serves (ops.py:151-158, bit-exact); which ones is the executor's choice.  In
+// the first replicated layer's run, a sequence whose KV already lives on one of
+// the replicas stays there while that replica's share has room (earliest in
+// batch order first); the rest -- fresh prompts and the overflow of shrunken
+// shares -- fill the replicas with room in replica order, in batch order.
+// The step then runs on the sequences in that order (each replica's rows
+// contiguous) and the outputs return in the caller's order.  Under continuous
+// batching only the share changes move KV, not every shifted range boundary.
+// Deterministic from the replicated owner bookkeeping: every SPMD rank derives
+// the same order.
+std::vector<int> routing_order(cb_model* m, int bs, const int32_t* slots) {
+  std::vector<int> perm(bs);
+  for (int i = 0; i < bs; ++i) perm[i] = i;
+  const LayerState* L = nullptr;
+  for (const auto& l : m->layers)
+    if (l.reps.size() > 1) {
+      L = &l;
+      break;
+    }
+  if (!L || L->owner.empty()) return perm;
+  const int p = int(L->reps.size());
+  const std::vector<int> shares = split_batch_vec(bs, p);
+  std::vector<std::vector<int>> groups(p);
+  std::vector<int> pool;
+  for (int i = 0; i < bs; ++i) {
+    const int o = L->owner[slots[i]];
+    int j = -1;
+    for (int r = 0; r < p && o >= 0; ++r)
+      if (L->reps[r].dev == o) j = r;
+    if (j >= 0 && int(groups[j].size()) < shares[j]) {
+      groups[j].push_back(i);
+    } else {
+      pool.push_back(i);
+    }
+  }
+  size_t next = 0;
+  for (int j = 0; j < p; ++j)
+    while (int(groups[j].size()) < shares[j]) groups[j].push_back(pool[next++]);
+  int k = 0;
+  for (const auto& g : groups)
+    for (int i : g) perm[k++] = i;
+  return perm;
+}
+
+// cb_step on the sequences in the given order (each layer's replicas take
+// contiguous split_batch ranges of it)
+int step_ordered(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const int32_t* tokens,
+                 const int32_t* prompt_lens, int32_t* next_out, float* logits_out, float* ms_out) {
+  if (!m) return fail(CB_EINVAL, "null model");
+  if (ms_out) *ms_out = 0.f;
+  if (bs == 0) return CB_OK;
+  if (bs < 0 || bs > m->d.max_slots || !slots || !tokens || !next_out)
+    return fail(CB_EINVAL, "bad batch arguments");
+  if (phase != CB_PHASE_PREFILL && phase != CB_PHASE_DECODE) return fail(CB_EINVAL, "unknown phase");
+  if (!m->head_loaded) return fail(CB_ESTATE, "embedding / lm_head not loaded");
+  kv_release_pending(m);
+  for (auto& L : m->layers)
+    if (L.reps.empty()) return fail(CB_ESTATE, "a decoder layer is not loaded");
+  std::vector<char> seen(m->d.max_slots, 0);
+  for (int i = 0; i < bs; ++i) {
+    if (slots[i] < 0 || slots[i] >= m->d.max_slots) return fail(CB_EINVAL, "slot out of range");
+    if (seen[slots[i]]++) return fail(CB_EINVAL, "duplicate slot in batch");
+    const int len = m->slot_len[slots[i]];
+    if (phase == CB_PHASE_PREFILL && len != 0) return fail(CB_EINVAL, "prefill into a non-empty slot");
+    if (phase == CB_PHASE_DECODE && len == 0) return fail(CB_EINVAL, "decode on an empty slot");
+  }
+  // token ids index the embedding table on the device: reject out-of-range ids
+  // before any launch (an out-of-bounds gather would poison the context)
+  auto bad_tokens = [&](long long n) {
+    for (long long t = 0; t < n; ++t)
+      if (tokens[t] < 0 || tokens[t] >= m->d.vocab) return true;
+    return false;
+  };
+  if (phase == CB_PHASE_DECODE) {
+    if (bad_tokens(bs)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
+    return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out, 0, bs);
+  }
+  if (!prompt_lens) return fail(CB_EINVAL, "prefill needs prompt_lens");
+  {
+    long long total = 0;
+    for (int t = 0; t < bs; ++t) {
+      if (prompt_lens[t] < 1 || prompt_lens[t] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
+      total += prompt_lens[t];
+    }
+    if (bad_tokens(total)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
+  }
+  // prefill: group sequences so each pass fits max_tokens rows
+  int i = 0, tok_off = 0;
+  while (i < bs) {
+    int j = i, rows = 0;
+    while (j < bs && rows + prompt_lens[j] <= m->d.max_tokens) {
+      if (prompt_lens[j] < 1 || prompt_lens[j] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
+      rows += prompt_lens[j++];
+    }
+    if (j == i) return fail(CB_EINVAL, "prompt longer than max_tokens");
+    CB_TRY(step_pass(m, phase, j - i, slots + i, tokens + tok_off, prompt_lens + i, next_out + i,
+                     logits_out ? logits_out + size_t(i) * m->d.vocab : nullptr, ms_out, i, bs));
+    tok_off += rows;
+    i = j;
+  }
+  return CB_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int cb_abi_version(void) { return CB_ABI_VERSION; }
@@ -2580,59 +2687,40 @@ int cb_get_placement(cb_model* m, int64_t* layer_ptr, int32_t* replica_dev, int3
   return CB_OK;
 }
 
+
 int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const int32_t* tokens,
             const int32_t* prompt_lens, int32_t* next_out, float* logits_out, float* ms_out) {
   if (!m) return fail(CB_EINVAL, "null model");
-  if (ms_out) *ms_out = 0.f;
-  if (bs == 0) return CB_OK;
-  if (bs < 0 || bs > m->d.max_slots || !slots || !tokens || !next_out)
-    return fail(CB_EINVAL, "bad batch arguments");
-  if (phase != CB_PHASE_PREFILL && phase != CB_PHASE_DECODE) return fail(CB_EINVAL, "unknown phase");
-  if (!m->head_loaded) return fail(CB_ESTATE, "embedding / lm_head not loaded");
-  kv_release_pending(m);
-  for (auto& L : m->layers)
-    if (L.reps.empty()) return fail(CB_ESTATE, "a decoder layer is not loaded");
-  std::vector<char> seen(m->d.max_slots, 0);
-  for (int i = 0; i < bs; ++i) {
+  if (bs <= 0 || bs > m->d.max_slots || !slots || !tokens || !next_out || (phase == CB_PHASE_PREFILL && !prompt_lens))
+    return step_ordered(m, phase, bs, slots, tokens, prompt_lens, next_out, logits_out, ms_out);
+  for (int i = 0; i < bs; ++i)
     if (slots[i] < 0 || slots[i] >= m->d.max_slots) return fail(CB_EINVAL, "slot out of range");
-    if (seen[slots[i]]++) return fail(CB_EINVAL, "duplicate slot in batch");
-    const int len = m->slot_len[slots[i]];
-    if (phase == CB_PHASE_PREFILL && len != 0) return fail(CB_EINVAL, "prefill into a non-empty slot");
-    if (phase == CB_PHASE_DECODE && len == 0) return fail(CB_EINVAL, "decode on an empty slot");
-  }
-  // token ids index the embedding table on the device: reject out-of-range ids
-  // before any launch (an out-of-bounds gather would poison the context)
-  auto bad_tokens = [&](long long n) {
-    for (long long t = 0; t < n; ++t)
-      if (tokens[t] < 0 || tokens[t] >= m->d.vocab) return true;
-    return false;
-  };
-  if (phase == CB_PHASE_DECODE) {
-    if (bad_tokens(bs)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
-    return step_pass(m, phase, bs, slots, tokens, nullptr, next_out, logits_out, ms_out, 0, bs);
-  }
-  if (!prompt_lens) return fail(CB_EINVAL, "prefill needs prompt_lens");
-  {
-    long long total = 0;
-    for (int t = 0; t < bs; ++t) {
-      if (prompt_lens[t] < 1 || prompt_lens[t] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
-      total += prompt_lens[t];
+  const std::vector<int> perm = routing_order(m, bs, slots);
+  bool ident = true;
+  for (int i = 0; i < bs; ++i) ident &= perm[i] == i;
+  if (ident) return step_ordered(m, phase, bs, slots, tokens, prompt_lens, next_out, logits_out, ms_out);
+  std::vector<int32_t> ps(bs), pl, pt, pn(bs);
+  for (int k = 0; k < bs; ++k) ps[k] = slots[perm[k]];
+  if (phase == CB_PHASE_PREFILL) {
+    std::vector<long long> off(bs + 1, 0);
+    for (int i = 0; i < bs; ++i) off[i + 1] = off[i] + std::max(0, prompt_lens[i]);
+    pl.resize(bs);
+    for (int k = 0; k < bs; ++k) {
+      pl[k] = prompt_lens[perm[k]];
+      pt.insert(pt.end(), tokens + off[perm[k]], tokens + off[perm[k] + 1]);
     }
-    if (bad_tokens(total)) return fail(CB_EINVAL, "token id out of range [0, vocab)");
+  } else {
+    pt.resize(bs);
+    for (int k = 0; k < bs; ++k) pt[k] = tokens[perm[k]];
   }
-  // prefill: group sequences so each pass fits max_tokens rows
-  int i = 0, tok_off = 0;
-  while (i < bs) {
-    int j = i, rows = 0;
-    while (j < bs && rows + prompt_lens[j] <= m->d.max_tokens) {
-      if (prompt_lens[j] < 1 || prompt_lens[j] > m->d.max_ctx) return fail(CB_EINVAL, "bad prompt length");
-      rows += prompt_lens[j++];
-    }
-    if (j == i) return fail(CB_EINVAL, "prompt longer than max_tokens");
-    CB_TRY(step_pass(m, phase, j - i, slots + i, tokens + tok_off, prompt_lens + i, next_out + i,
-                     logits_out ? logits_out + size_t(i) * m->d.vocab : nullptr, ms_out, i, bs));
-    tok_off += rows;
-    i = j;
+  std::vector<float> plog(logits_out ? size_t(bs) * m->d.vocab : 0);
+  CB_TRY(step_ordered(m, phase, bs, ps.data(), pt.data(), pl.empty() ? nullptr : pl.data(), pn.data(),
+                         logits_out ? plog.data() : nullptr, ms_out));
+  for (int k = 0; k < bs; ++k) {
+    next_out[perm[k]] = pn[k];
+    if (logits_out)
+      std::memcpy(logits_out + size_t(perm[k]) * m->d.vocab, plog.data() + size_t(k) * m->d.vocab,
+                  size_t(m->d.vocab) * 4);
   }
   return CB_OK;
 }
