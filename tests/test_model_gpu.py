@@ -295,6 +295,57 @@ def test_prefill_in_several_passes_routes_like_one(runtime, confident):
     assert moved[64] == moved[512], moved
 
 
+def test_sticky_routing_moves_only_rebalanced_kv(runtime, confident):
+    """Sticky routing order: split_batch counts stay exact, but sequences keep
+    the replica holding their KV.  Two requests of replica 0 finish, two fresh
+    ones are prefilled (split 1 / 1) and appended: contiguous ranges would move
+    three sequences' KV on the next decode, the sticky order moves one (the
+    latest overflow of replica 1); tokens stay equal to the oracle."""
+    rng = np.random.default_rng(4)
+    prompts = {s_: rng.integers(0, TINY.vocab, PROMPT).astype(np.int32) for s_ in range(18)}
+    ex = _executor(runtime, confident)  # layer 2 replicated x2
+    oracle = OracleModel(TINY, confident, 64)
+    live = list(range(16))
+    nxt, _, _ = ex.prefill(np.array(live, np.int32), np.concatenate([prompts[s_] for s_ in live]),
+                           np.full(16, PROMPT, np.int32))
+    oracle.forward(live, np.concatenate([prompts[s_] for s_ in live]), [PROMPT] * 16)
+    last = dict(zip(live, nxt))
+
+    def decode():
+        inp = np.array([last[s_] for s_ in live], np.int32)
+        ex.profile(True)
+        out, lg, _ = ex.decode(np.array(live, np.int32), inp, want_logits=True)
+        moved = ex.profile_read()["copy"]["bytes"]
+        ex.profile(False)
+        ref = oracle.forward(live, inp, None)
+        assert np.array_equal(out, ref.argmax(-1)) and np.abs(lg - ref).max() <= LOGIT_TOL
+        last.update(zip(live, out))
+        return moved
+
+    base = decode()  # activation rows only (scatter / gather of the replicated run)
+    assert [ex.read_kv(2, s_)[1] for s_ in live] == [0] * 8 + [1] * 8
+    for s_ in (0, 1):
+        live.remove(s_)
+        ex.release([Request(s_, 0.0, PROMPT, 1, slot=s_)])
+        oracle.release([s_])
+    fresh = [16, 17]
+    out, _, _ = ex.prefill(np.array(fresh, np.int32), np.concatenate([prompts[s_] for s_ in fresh]),
+                           np.full(2, PROMPT, np.int32))
+    oracle.forward(fresh, np.concatenate([prompts[s_] for s_ in fresh]), [PROMPT] * 2)
+    assert [ex.read_kv(2, s_)[1] for s_ in fresh] == [0, 1]
+    live += fresh
+    last.update(zip(fresh, out))
+    moved = decode()
+    q, r = divmod(len(live), 2)
+    assert [c for _, _, c in ex.last_routing(2)] == [q, q + r]
+    owners = [ex.read_kv(2, s_)[1] for s_ in live]
+    assert owners.count(0) == 8 and owners.count(1) == 8
+    assert ex.read_kv(2, 17)[1] == 0  # the one sequence that moved
+    one_seq = PROMPT * 2 * TINY.d_model * 2  # its KV prefix (the prompt) in layer 2
+    assert moved - base == one_seq, (moved, base, one_seq)
+    ex.close()
+
+
 def test_migration_moves_weights_and_kv_bit_exact(runtime, confident):
     prompts = config1_prompts()
     ex = _executor(runtime, confident)
