@@ -5,11 +5,12 @@
 
 Metric (BASELINE.json): tokens/s and p50/p99 latency; module-migrate GB/s.
 N=1 workload = BASELINE config 2: Llama-2-7B shape, bf16, synthetic requests
-(prompt 128), no replication, one B200.  A "step" is one decode pass of the
-whole batch through all 32 decoder layers + lm_head + greedy sampling.
-Weights are random-init on the device (no checkpoints offline); they total
-13.2 GB, far larger than the 126 MB L2, so every step streams them from HBM
-(no L2 flush needed).
+(prompt 128, gen 256), batch 256, no replication, one B200.  A "step" is one
+decode pass of the whole batch through all 32 decoder layers + lm_head +
+greedy sampling, timed at mid-generation (attended context = prompt + gen/2 =
+256; the ctx-148 point is reported beside it).  Weights are random-init on the
+device (no checkpoints offline); they total 13.2 GB, far larger than the 126
+MB L2, so every step streams them from HBM (no L2 flush needed).
 
 * ``value``   = batch * K / (sum of device-timed step durations), CUDA events
   on the launching stream inside libcocob200 (inputs resident in HBM).
@@ -17,23 +18,31 @@ Weights are random-init on the device (no checkpoints offline); they total
   cb_step) with host token buffers: H2D of the step's metadata and D2H of the
   sampled tokens inside the timed region, host wall clock around K
   synchronous calls.
-* ``roofline``: the dominant kernel class (the tcgen05 GEMMs streaming the
-  weights) -- algorithmic bytes per launch / average launch time, both
-  measured live with CUDA events bracketing every launch in a second pass of
-  the same K steps right after the timed region (the events serialise the
-  programmatic-dependent-launch overlap, so they stay out of the timed
-  region); peak = MEASURED_PEAKS.json hbm_gbs.
-* ``cpu_baseline``: the CPU oracle (numpy fp32, all host cores) on a bounded
-  sample of the same decode step (2 of 32 layers + lm_head), scaled.
+* ``roofline``: the dominant kernel class (the tcgen05 GEMMs) -- algorithmic
+  bytes and FLOPs per launch / average launch time, measured live with CUDA
+  events bracketing every launch in a second pass of K steps right after the
+  timed region (the events serialise the programmatic-dependent-launch
+  overlap, so they stay out of the timed region); the binding roof is the
+  larger of bytes / HBM peak and FLOPs / sustained bf16 peak
+  (MEASURED_PEAKS.json).  ``in_step`` attributes the timed steps by the class
+  shares of that pass.  ``traffic`` = ncu DRAM bytes per GEMM launch
+  (profiles/ncu_summary.json).
+* ``parity_spot_check``: outside every timed region, the headline plans with
+  oracle weights vs the fp32 oracle (test infrastructure as a checker).
+* ``cpu_baseline``: the CPU oracle (numpy fp32, all host cores), one complete
+  32-layer decode step of the same workload.
+* ``serving``: continuous batching under Poisson arrivals at a moderate and a
+  saturating rate (per-request p50 / p99).
 
-For N>1 (torchrun, one process per GPU) every decoder layer is replicated on
-every GPU (BASELINE config 3 with all layers hot): that is ONE replicated run,
-so each rank serves its split_batch share of the global batch on its own GPU
-(``dist.ReplicaGroup``) and the run-boundary scatter / gather
-are NCCL collectives of the step metadata and sampled tokens.  Per-GPU batch
-is fixed (weak scaling); value = global tokens / max-over-ranks device time.
-Rank 0 then measures a cross-GPU layer migration over NVLink (one process,
-two GPUs, cudaMemcpyPeerAsync of the layer block).
+For N>1 (torchrun, one process per GPU): BASELINE config 3 on the SPMD
+runtime -- the originals on GPU 0, hot layers 1..k (k = 28 by default)
+replicated on every other GPU by the scaling operator (NVLink, NCCL), so each
+step scatters the batch rows to the replicas at the run's first layer and
+gathers them after its last; the cold layers and the head run
+on GPU 0 over the whole batch.  Per-GPU batch fixed (weak scaling); value =
+global tokens / max-over-ranks device time; then a continuous-batching window
+(KV following re-split sequences across ranks) and one 7B layer replicated
+over NVLink and evicted (``migrate``).
 """
 from __future__ import annotations
 
@@ -539,7 +548,9 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
     k = args.replicate_layers if args.replicate_layers is not None else n_layers - 4
     k = max(1, min(k, n_layers))
     churn_steps = args.churn_steps
-    max_ctx = args.prompt + args.warmup + 2 * args.steps + churn_steps + 16
+    # timed at mid-generation like N=1 (prompt + gen / 2), then <= 10 profiled steps and the churn window
+    advance = max(0, args.gen // 2 - args.steps // 2 - args.warmup)
+    max_ctx = args.prompt + args.warmup + advance + args.steps + min(args.steps, 10) + churn_steps + 16
     # KV on GPU 0: the cold layers' blocks hold the whole global batch, the hot
     # layers' blocks their split_batch share (+ 1/8 growth slack) -- cap the
     # per-GPU batch so that fits in 110 GB
@@ -564,8 +575,9 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
     slots = np.arange(gbatch, dtype=np.int32)
     prompts = rng.integers(0, cfg.vocab, gbatch * args.prompt).astype(np.int32)
     nxt, _, _ = ex.prefill(slots, prompts, np.full(gbatch, args.prompt, np.int32))
-    for _ in range(args.warmup):
+    for _ in range(args.warmup + advance):
         nxt, _, _ = ex.decode(slots, nxt)
+    ctx_mid = args.prompt + args.warmup + advance + args.steps // 2
     group.barrier()
     torch.cuda.synchronize()
     dev_ms, t0 = [], time.perf_counter()
@@ -640,7 +652,8 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
             "data": "synthetic (random-init weights, random prompts)",
             "config": {"workload": f"config 3: Llama-2-7B shape, hot layers 1..{k} replicated on all {world} GPUs "
                                    f"(one process per GPU), layers {k + 1}..{n_layers} + head on GPU 0",
-                       "batch": gbatch, "batch_per_gpu": per, "prompt_len": args.prompt,
+                       "batch": gbatch, "batch_per_gpu": per, "prompt_len": args.prompt, "gen_len": args.gen,
+                       "ctx_at_mid_step": ctx_mid,
                        "replicated_layers": k,
                        "parallelism": f"module replication x{world} (SPMD, NCCL scatter/gather at run boundaries)",
                        "l2": "weights 13.2 GB >> 126 MB L2 per GPU: every step streams from HBM"},
