@@ -6,6 +6,7 @@ and the softmax warp's phases, in SM clock cycles from the CTA's start.
 
     python scripts/pf_trace.py [L]"""
 import ctypes as C
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -23,7 +24,7 @@ out.mkdir(parents=True, exist_ok=True)
 objs = []
 for src in _build._sources():
     obj = out / (src.stem + ".o")
-    extra = ["-DPF_TRACE"] if src.stem == "prefill_attention" else []
+    extra = (["-DPF_TRACE"] + os.environ.get("PF_FLAGS", "").split()) if src.stem == "prefill_attention" else []
     subprocess.run([_build._nvcc(), *_build.ARCH, *_build.FLAGS, *extra, "-c", str(src), "-o", str(obj)], check=True)
     objs.append(str(obj))
 lib_path = out / "libcocob200_pftrace.so"
