@@ -31,7 +31,7 @@ int cbt_attention_bench(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, 
                         const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,
                         int32_t max_len, int32_t iters, float* ms_per_launch);
 int cbt_argmax(const float* logits, int32_t* out, int32_t T, int32_t V);
-/* causal tcgen05 prefill attention: blocks_dev = int4 (row, rows <= 128, slot, first position) per block;
+/* causal tcgen05 prefill attention: blocks_dev = int4 (row, rows <= 256, slot, first position) per block;
    the KV cache holds n_slots x max_ctx positions */
 int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
                           int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,

@@ -137,7 +137,7 @@ cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
 // act = bf16(silu(gate) * act) over rows [row_off, row_off + T) of [rows][d_ff] buffers (d_ff % 8 == 0)
 cudaError_t swiglu_launch(const uint16_t* gate, uint16_t* act, int T, int d_ff, int row_off, cudaStream_t st);
 // Causal prefill attention on the tcgen05 tensor cores: blocks[i] = (first row
-// relative to a.row_off, rows (<= 128), slot, first position) of one sequence; q
+// relative to a.row_off, rows (<= 256), slot, first position) of one sequence; q
 // already rotated and the block's K/V already in the cache (rope_kv_launch).
 // Grid (blocks, H); a.qkv_rows / a.kv_slots bound the TMA views.
 cudaError_t prefill_attention_launch(const AttnArgs& a, const int4* blocks, int nblocks, cudaStream_t st);

@@ -1044,7 +1044,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
                                m->hd, d.max_ctx, ac.compute));
   }
   if (!fused) {
-    // prefill: causal tensor-core attention over the segment's sequences' 128-row blocks
+    // prefill: causal tensor-core attention over the segment's sequences' 256-row blocks
     const int b0 = m->seq_blk[s.s0], b1 = m->seq_blk[s.s1];
     const int4* blocks = reinterpret_cast<const int4*>(wa.meta + ((3 * m->cur_T + m->cur_bs + 3) & ~3)) + b0;
     cb::AttnArgs pa{};
@@ -1403,7 +1403,7 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
       meta[2 * T + r] = pos;
     }
   for (int i = 0; i < bs; ++i) meta[3 * T + i] = seq_row[i + 1] - 1;
-  // prefill: 128-row query blocks of every sequence for the tensor-core attention
+  // prefill: 256-row query blocks (two 128-row tiles) of every sequence for the tensor-core attention
   m->cur_bs = bs;
   m->seq_blk.assign(bs + 1, 0);
   int nblk = 0;
@@ -1413,9 +1413,9 @@ int step_pass(cb_model* m, int phase, int bs, const int32_t* slots, const int32_
     for (int i = 0; i < bs; ++i) {
       m->seq_blk[i] = nblk;
       const int len = seq_row[i + 1] - seq_row[i];
-      for (int b0 = 0; b0 < len; b0 += 128, ++nblk) {
+      for (int b0 = 0; b0 < len; b0 += 256, ++nblk) {
         blk[4 * nblk + 0] = seq_row[i] + b0;
-        blk[4 * nblk + 1] = std::min(128, len - b0);
+        blk[4 * nblk + 1] = std::min(256, len - b0);
         blk[4 * nblk + 2] = slots[i];
         blk[4 * nblk + 3] = b0;
       }

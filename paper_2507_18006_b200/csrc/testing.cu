@@ -583,7 +583,7 @@ extern "C" int cbt_mma_probe(int32_t N, int32_t n, int32_t grid, int32_t kstep, 
 }
 
 // causal prefill attention: rows [0, T) of qkv hold consecutive prompts; blocks_dev
-// = int4 (row, rows, slot, first position) per 128-row block; K/V already in kv
+// = int4 (row, rows, slot, first position) per 256-row block; K/V already in kv
 // ([n_slots][max_ctx][2][Hkv hd]).
 extern "C" int cbt_prefill_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* blocks_dev,
                                      int32_t nblocks, int32_t T, int32_t H, int32_t Hkv, int32_t hd,

@@ -34,7 +34,7 @@ H, Hkv, hd = 32, 32, 128
 qkv = (torch.randn(L, (H + 2 * Hkv) * hd, device="cuda")).to(torch.bfloat16)
 kv = (torch.randn(1, L + 8, 2, Hkv * hd, device="cuda")).to(torch.bfloat16)
 out_t = torch.zeros(L, H * hd, dtype=torch.bfloat16, device="cuda")
-blocks = torch.tensor([(b0, min(128, L - b0), 0, b0) for b0 in range(0, L, 128)], dtype=torch.int32, device="cuda")
+blocks = torch.tensor([(b0, min(256, L - b0), 0, b0) for b0 in range(0, L, 256)], dtype=torch.int32, device="cuda")
 tr = torch.zeros(12 * 32, dtype=torch.int64, device="cuda")
 P = C.c_void_p
 lib.cbt_prefill_attention.argtypes = [P, P, P, P] + [C.c_int32] * 7
@@ -49,10 +49,11 @@ torch.cuda.synchronize()
 t = tr.cpu().numpy().reshape(12, 32).astype(np.float64)
 t0 = t[9, 0]
 rel = np.where(t > 0, (t - t0), np.nan)  # SM clock cycles (clock64: one SM, one counter)
-names = ["K issued", "V issued", "S issued", "P ready@MMA", "PV committed", "S ready@smx", "exp done",
-         "PV(j-1) done", "P arrive", "-", "V ready@MMA", "PV issued"]
-nkb = (L - 1) // 128 + 1
-print(f"L={L}: CTA of the last query block, {nkb} key blocks; SM cycles from the CTA start; end at {rel[9, 1]:.0f}")
-print("j   " + " ".join(f"{n:>12s}" for i, n in enumerate(names) if i != 9))
+names = ["-", "-", "S_A issued", "S_B issued", "PV_A issued", "PV_B issued", "S_A ready@smx", "A exp done",
+         "P_A arrive", "-", "S_B ready@smx", "P_B arrive"]
+nkb = (L - 1) // 64 + 1
+print(f"L={L}: CTA of the last 256-row query block (tiles A, B), {nkb} key blocks of 64; SM cycles from the CTA start; "
+      f"end at {rel[9, 1]:.0f}")
+print("j   " + " ".join(f"{n:>12s}" for n in names if n != "-"))
 for j in range(min(nkb, 32)):
-    print(f"{j:2d}  " + " ".join(f"{rel[k, j]:12.0f}" for k in range(12) if k != 9))
+    print(f"{j:2d}  " + " ".join(f"{rel[k, j]:12.0f}" for k in range(12) if names[k] != "-"))

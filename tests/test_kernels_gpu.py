@@ -361,7 +361,8 @@ def test_gemm_pair_kernel_row_count_invariant(lib, cuda, N, K):
 def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
     """tcgen05 causal prefill attention (TMA-fed Q/K/V, S and O in TMEM, softmax
     warps one row per thread) vs a float64 causal softmax reference: every row
-    of every prompt, 128-row blocks incl. ragged tails, multi-block prompts
+    of every prompt, 256-row blocks (two 128-row tiles) incl. ragged tails and
+    single-tile blocks, multi-block prompts
     (lazy O rescaling in TMEM), GQA, head dims 64/128.  The cache holds NaN
     past each prompt (stale / uninitialised bytes must not leak into rows)."""
     torch = cuda
@@ -374,8 +375,8 @@ def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
     out = torch.zeros(T, H * hd, dtype=torch.bfloat16, device="cuda")
     blocks, row = [], 0
     for sl, L in enumerate(lens):
-        for b0 in range(0, L, 128):
-            blocks.append((row + b0, min(128, L - b0), sl, b0))
+        for b0 in range(0, L, 256):
+            blocks.append((row + b0, min(256, L - b0), sl, b0))
         row += L
     bl = torch.tensor(blocks, dtype=torch.int32, device="cuda")
     assert lib.cbt_prefill_attention(_ptr(qkv), _ptr(kv), _ptr(out), _ptr(bl), len(blocks), T, H, Hkv, hd,
