@@ -12,20 +12,21 @@
 //   warp 1      MMA issuer (one elected lane of a converged warp, four MMAs per
 //               asm block), per key block j: S_A(j), S_B(j) = Q K_j^T (M 128 x
 //               N 64, K-major, double-buffered in TMEM per tile), then
-//               PV_A(j-1), PV_B(j-1) (M 128 x N hd; P K-major from smem, V
-//               MN-major: the cache's [pos][hd] rows as they are)
+//               PV_A(j-1), PV_B(j-1) (M 128 x N hd; P from TMEM, V MN-major:
+//               the cache's [pos][hd] rows as they are)
 //   warps 2..5  softmax of tile A, warps 6..9 of tile B: one thread per query
 //               row (TMEM lane): S row -> registers (tcgen05.ld), causal mask
 //               on diagonal blocks only, online softmax in the exp2 domain (one
 //               FFMA + MUFU.EX2 per score) with lazy rescaling (O in TMEM is
 //               rescaled with tcgen05.ld/st only when a row max grows by > 2^8),
-//               P as bf16 into smem in the 128-byte-swizzled K-major layout the
-//               MMA reads; finally O / l -> bf16 -> global.
+//               P as bf16 pairs over the S columns just read (tcgen05.st): the
+//               PV MMA's A operand straight from TMEM, as FlashAttention-4
+//               does; finally O / l -> bf16 -> global.
 //
 // Ping-pong: while one tile's softmax runs, the tensor pipe executes the other
 // tile's MMAs, and the two warpgroups take turns on each sub-partition's MUFU.
 // TMEM: S_A[2 x 64] S_B[2 x 64] O_A[hd] O_B[hd] = 512 columns.  Smem (hd 128):
-// Q 2 x 32 KB + K 3 x 16 KB + V 3 x 16 KB + P 2 x 16 KB = 192 KB.  Positions
+// Q 2 x 32 KB + K 3 x 16 KB + V 3 x 16 KB = 160 KB.  Positions
 // past the sequence inside its last key block are masked in S, and their V
 // rows are zeroed in smem before the PV MMAs (stale cache bytes could hold
 // non-finite values; 0 * NaN would poison the row).  The tensor pipe is the
@@ -99,6 +100,33 @@ CB_DEVICE void umma4_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, ui
       : "memory");
 }
 
+// Four K=16 MMAs with A in tensor memory (M lanes x K/2 columns: two bf16 of
+// a row per 32-bit column, so +8 columns per K=16 step) and B from smem.
+template <int BSTEP>
+CB_DEVICE void umma4_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.s64 b1, %2, %5;\n\tadd.s64 b2, %2, %6;\n\tadd.s64 b3, %2, %7;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, q;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "n"(BSTEP), "n"(2 * BSTEP), "n"(3 * BSTEP)
+      : "memory");
+}
+CB_DEVICE void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
 // non-blocking: has the phase with this parity completed?
 CB_DEVICE bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -142,10 +170,9 @@ struct PpCfg {
   static constexpr int kQ = 2 * (HD / 64) * kQBox;  // two tiles
   static constexpr int kK = (HD / 64) * kKVBox;
   static constexpr int kV = kK;
-  static constexpr int kP = kQBox;                  // [128 rows][64 keys] per tile
   static constexpr int kStages = 3;
   static constexpr int kBars = 32 * 8;
-  static constexpr int kSmem = 1024 + kQ + kStages * (kK + kV) + 2 * kP + kBars;
+  static constexpr int kSmem = 1024 + kQ + kStages * (kK + kV) + kBars;
 };
 
 template <int HD>
@@ -161,8 +188,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
   uint8_t* sQ = sm;                      // [tile][NR boxes]
   uint8_t* sK = sQ + C::kQ;              // [ST][NR boxes]
   uint8_t* sV = sK + ST * C::kK;         // [ST][NR boxes]
-  uint8_t* sP = sV + ST * C::kV;         // [tile]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * C::kP);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + ST * C::kV);
   uint64_t* bar_q = bars + 0;
   uint64_t* k_full = bars + 1;   // [3]
   uint64_t* k_empty = bars + 4;  // [3]
@@ -284,8 +310,9 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           if (jj >= (t ? nk_b : nk_a)) continue;
           mbar_wait(p_full + t, jj & 1);
           tc_fence_after();
-          umma4_elect<128>(tmem + 256 + t * 128, make_sw128_desc(smem_u32(sP + t * C::kP)),
-                           make_sw128_mn_desc(v0, C::kKVBox), idesc_o, jj > 0 ? 1u : 0u);
+          // P(jj) lives in the first 32 columns of tile t's S buffer jj & 1
+          umma4_ts_elect<128>(tmem + 256 + t * 128, tmem + t * 128 + (jj & 1) * 64,
+                              make_sw128_mn_desc(v0, C::kKVBox), idesc_o, jj > 0 ? 1u : 0u);
           umma_commit_elect(o_done + t);
           if (lane == 0) PFT(4 + t, jj);
         }
@@ -304,8 +331,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     const int qp = pt + r;
     const float sl2 = a.scale * 1.4426950408889634f;
     float m_used = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + t * C::kP + r * 128;
-    const int rsw = r & 7;
     const uint32_t tS = tmem + lane_off + t * 128, tO = tmem + lane_off + 256 + t * 128;
     for (int j = 0; j < nk_t; ++j) {
       const int b = j & 1;
@@ -357,10 +382,21 @@ __global__ void __launch_bounds__(kPfThreads, 1)
         pk[e] = pack_bf16x2(e0, e1);
       }
       if (t == 0 && q4 == 0 && lane == 0) PFT(7, j);
+      // P(j) as bf16 pairs over the S(j) columns just read: the A operand of PV(j)
+      // (S(j+2) overwrites them only after PV(j): the tensor pipe runs in order)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t ph[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) ph[e] = pk[h * 16 + e];
+        tmem_st16(tS + b * 64 + h * 16, ph);
+      }
       if (j > 0) {
-        mbar_wait(o_done + t, (j - 1) & 1);  // PV(j-1) retired: O final for j-1, P free
+        // every PV completion is consumed in order (an mbarrier parity wait is only
+        // valid one phase ahead); the lazy rescale needs PV(j-1) retired anyway
+        mbar_wait(o_done + t, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {  // lazy rescale
+        if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
           for (int c = 0; c < HD / 32; ++c) {
             uint32_t u[32];
@@ -373,10 +409,7 @@ __global__ void __launch_bounds__(kPfThreads, 1)
           tmem_st_wait();
         }
       }
-#pragma unroll
-      for (int ch = 0; ch < KB / 8; ++ch)
-        *reinterpret_cast<uint4*>(prow + ((ch ^ rsw) << 4)) =
-            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      tmem_st_wait();
       l = l * alpha + rs;
       if (t == zt && j == nk - 1 && kbase + KB - 1 > last_pos) {
         // last block: V rows past the sequence's last position -> 0 (P is 0 there)
