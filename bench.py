@@ -281,6 +281,43 @@ def measure_migration(ex, cat, cluster, n_dev: int) -> dict:
             "nvlink_peak_gbps_per_dir": 900.0}
 
 
+def measure_p2p_copy_engine(reps: int = 3, ordinals=(0, 1)) -> dict:
+    """N>1, rank 0: the single-process copy engine between GPUs 0 and 1 over
+    NVLink -- one 7B layer block (404,766,720 B) replicated GPU 0 -> GPU 1 and
+    evicted, per transfer mode (cudaMemcpyPeerAsync / chunks over two copy
+    engines / SM 16-byte push), best of `reps`, device-timed on the copy stream."""
+    from paper_2507_18006_b200 import domain as D
+    from paper_2507_18006_b200 import ops as O
+    from paper_2507_18006_b200.executor import Executor, ExecutorConfig, Runtime
+
+    rt = Runtime(list(ordinals))
+    ex = Executor(rt, ExecutorConfig(n_layers=1, d_model=LLAMA2_7B["d_model"], d_ff=LLAMA2_7B["d_ff"],
+                                     n_heads=LLAMA2_7B["n_heads"], vocab=LLAMA2_7B["vocab"], max_slots=1,
+                                     max_ctx=16, max_tokens=256), home_device=0, seed=3)
+    ex.init_layer_random(1, 0, std=0.02)
+    cat = D.ModuleCatalog.from_model(D.ModelSpec(1, LLAMA2_7B["d_model"], LLAMA2_7B["d_ff"], LLAMA2_7B["n_heads"]))
+    cluster = D.ClusterSpec.b200(2)
+    out = {}
+    for mode, name in ((Runtime.COPY_SINGLE, "one_copy_engine"), (Runtime.COPY_CHUNKED, "two_copy_engines"),
+                       (Runtime.COPY_SM, "sm_push")):
+        rt.set_copy_mode(mode, 64 << 20)
+        best = None
+        for _ in range(reps):
+            ex.apply(O.ReplicateLayer(1, 1), cat, cluster)
+            m = ex.op_log[-1]
+            ex.apply(O.EvictReplica(1, 1), cat, cluster)
+            if best is None or m.device_ms < best[1]:
+                best = (m.weight_bytes, m.device_ms)
+        gbps = best[0] / (best[1] * 1e6)
+        out[name] = {"bytes": best[0], "ms": best[1], "gbps": gbps, "frac": gbps / 900.0}
+    rt.set_copy_mode(Runtime.COPY_CHUNKED, 64 << 20)
+    ex.close()
+    rt.close()
+    out["what"] = ("single-process P2P copy engine GPU 0 -> GPU 1 (NVLink 5 through NVSwitch), one 7B layer "
+                   "block, best of %d; frac of 900 GB/s per direction" % reps)
+    return out
+
+
 def serving_window(ex, args, batch: int, rps: float) -> dict:
     """Continuous batching (reference Engine semantics, serving.py) under Poisson
     arrivals for a bounded window: per-request p50/p99 latency and tok/s."""
@@ -641,6 +678,12 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
                "path": "NCCL send/recv over NVLink between the ranks' copy streams (receiver-timed)",
                "bulk_replication": {"layers": k, "replicas_per_layer": world - 1, "wall_s": rep_s,
                                     "median_gbps_this_rank": statistics.median(rep_gbps) if rep_gbps else None}}
+    p2p = None
+    if rank == 0 and not same_gpu and torch.cuda.device_count() > 1:
+        try:
+            p2p = measure_p2p_copy_engine()
+        except Exception as e:  # the probe must not sink the bench line
+            p2p = {"error": repr(e)[:200]}
     group.barrier()
     if rank == 0:
         value = gbatch * args.steps / dev_s
@@ -668,6 +711,7 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
                                       step_ms=float(np.mean(dev_ms))),
             "continuous_batching": churn,
             "migrate": mig,
+            "p2p_copy_engine": p2p,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -77,6 +77,15 @@ class Runtime:
         _lib.check(self.lib.cb_device_info(self.handle, dev, C.byref(sms), C.byref(free), C.byref(total)))
         return {"num_sms": sms.value, "free_bytes": free.value, "total_bytes": total.value}
 
+    COPY_SINGLE, COPY_CHUNKED, COPY_SM = 0, 1, 2
+
+    def set_copy_mode(self, mode: int, chunk_bytes: int = 0) -> None:
+        """Transfer engine of the scaling ops (cb_set_copy_mode): COPY_SINGLE = one
+        cudaMemcpyPeerAsync, COPY_CHUNKED = chunks alternating over two copy
+        engines (default, 64 MB), COPY_SM = an SM kernel on the source GPU pushing
+        16-byte stores into the destination."""
+        _lib.check(self.lib.cb_set_copy_mode(self.handle, int(mode), int(chunk_bytes)), "cb_set_copy_mode")
+
     def close(self) -> None:
         if self.handle:
             for ex in list(self._models):  # a model must never outlive its runtime

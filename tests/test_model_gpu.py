@@ -346,6 +346,25 @@ def test_sticky_routing_moves_only_rebalanced_kv(runtime, confident):
     ex.close()
 
 
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_copy_engine_modes_bytes_identical(runtime, confident, mode):
+    """The scaling ops' transfer engine (cb_set_copy_mode): one copy, chunks over
+    two copy lanes (1 MB chunks here, so the 1.7 MB layer block splits), and the
+    SM push kernel -- the replicated layer block is byte-identical each way."""
+    ex = _executor(runtime, confident, replicate_layer2=False)
+    cat, cl = _catalog_cluster()
+    runtime.set_copy_mode(mode, 1 << 20)
+    try:
+        ex.apply(O.ReplicateLayer(3, 1), cat, cl)
+        assert np.array_equal(ex.read_module(3, 1, "decoder_layer"), ex.read_module(3, 0, "decoder_layer"))
+        m = ex.op_log[-1]
+        assert m.weight_bytes == 1704960 and m.device_ms > 0
+        ex.apply(O.EvictReplica(3, 1), cat, cl)
+    finally:
+        runtime.set_copy_mode(Runtime.COPY_CHUNKED, 64 << 20)
+    ex.close()
+
+
 def test_migration_moves_weights_and_kv_bit_exact(runtime, confident):
     prompts = config1_prompts()
     ex = _executor(runtime, confident)
