@@ -194,9 +194,12 @@ int cb_get_placement(cb_model* m, int64_t* layer_ptr, int32_t* replica_dev, int3
  * One pass over `bs` sequences in admission order.  Prefill: tokens holds the
  * concatenated prompts (prompt_lens[i] each) and the slots must be empty.
  * Decode: one token per sequence, appended at the slot's current length.
- * Rows are routed to each layer's replicas with cb_split_batch over sequences
- * (contiguous ranges in replica order), activations move between devices at
- * placement changes, and KV rows follow their sequence's replica.
+ * Rows are routed to each layer's replicas with cb_split_batch counts over the
+ * step's sequences in a sticky routing order (a sequence stays on the replica
+ * holding its KV while that replica's share has room; fresh and overflow
+ * sequences fill the rest in replica order), each replica taking a contiguous
+ * range of that order; activations move between devices at placement changes,
+ * and KV rows follow their sequence's replica.  Outputs are in the caller's order.
  * Outputs: greedy next token per sequence, optional fp32 logits [bs][vocab],
  * device time of the pass.  CB_EINVAL before any launch for: slots out of range
  * or repeated, token ids outside [0, vocab), prompt lengths outside
@@ -206,7 +209,8 @@ int cb_step(cb_model* m, int32_t phase, int32_t bs, const int32_t* slots, const 
             const int32_t* prompt_lens, int32_t* next_tokens_out, float* logits_out, float* device_ms_out);
 int cb_release_slots(cb_model* m, int32_t n, const int32_t* slots);
 /* Routing the last step used for `layer`: per replica (device, first sequence,
- * sequence count).  p_out = number of replicas. */
+ * sequence count), the sequences counted in the step's routing order.  p_out =
+ * number of replicas. */
 int cb_last_routing(cb_model* m, int32_t layer, int32_t* dev_out, int32_t* seq_begin_out, int32_t* seq_count_out,
                     int32_t cap, int32_t* p_out);
 

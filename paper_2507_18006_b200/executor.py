@@ -493,6 +493,8 @@ class Executor:
         return out, dev.value
 
     def last_routing(self, layer: int) -> list[tuple[int, int, int]]:
+        """(device, first sequence, count) per replica of `layer` in the last step:
+        split_batch counts over the step's sticky routing order (cb_step)."""
         cap = max(1, self.rt.n_devices)
         d, s, c, p = (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)(), C.c_int32()
         _lib.check(self.lib.cb_last_routing(self.handle, layer, d, s, c, cap, C.byref(p)))
