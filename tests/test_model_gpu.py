@@ -365,6 +365,51 @@ def test_copy_engine_modes_bytes_identical(runtime, confident, mode):
     ex.close()
 
 
+def test_share_sized_kv_through_offload_migration_and_eviction(cuda, confident):
+    """Slot tables under the other KV paths: layer 2 replicated on a second
+    logical device (share-sized blocks on both), half the layers' KV offloaded
+    to host memory and back (table blocks copied with their indices), the
+    replicated layer's original migrated with its KV to a third device, then
+    the replica evicted (its rows return to the new original's full block);
+    tokens equal the fp32 oracle at every step."""
+    rt = Runtime([0, 0, 0])
+    ex = Executor(rt, _tiny_cfg())
+    ex.load_model(confident, device_of_layer=0)
+    cat, cl = _catalog_cluster(3)
+    ex.apply(O.ReplicateLayer(2, 1), cat, cl)
+    prompts = config1_prompts()
+    oracle = OracleModel(TINY, confident, 64)
+    live = list(range(N_REQ))
+    nxt, _, _ = ex.prefill(np.array(live, np.int32), np.concatenate(prompts), np.full(N_REQ, PROMPT, np.int32))
+    assert np.array_equal(nxt, oracle.forward(live, np.concatenate(prompts), [PROMPT] * N_REQ).argmax(-1))
+    slot_kv = 64 * 2 * TINY.d_model * 2
+    assert ex.mem_usage(1)["kv_bytes"] == 16 * slot_kv  # the replica's share: ceil(32 / 2) slots
+    last = dict(zip(live, nxt))
+    for step in range(1, 9):
+        if step == 2:
+            ex.set_kv_offload(0.5)
+            assert ex.kv_offloaded(2)
+        if step == 3:
+            ex.set_kv_offload(0.0)
+        if step == 4:
+            ex.release([Request(3, 0.0, PROMPT, 1, slot=3)])
+            live.remove(3)
+        if step == 5:
+            ex.apply(O.MigrateLayer(2, 2, with_kv=True), cat, cl)
+            assert ex.placement.replicas[1][0].device_id == 2
+        if step == 7:
+            ex.apply(O.EvictReplica(2, 1), cat, cl)
+            assert all(ex.read_kv(2, s_)[1] == 2 for s_ in live)
+        inp = np.array([last[s_] for s_ in live], np.int32)
+        nxt, lg, _ = ex.decode(np.array(live, np.int32), inp, want_logits=True)
+        ref = oracle.forward(live, inp, None)
+        assert np.array_equal(nxt, ref.argmax(-1)), step
+        assert np.abs(lg - ref).max() <= LOGIT_TOL, step
+        last.update(zip(live, nxt))
+    ex.close()
+    rt.close()
+
+
 def test_migration_moves_weights_and_kv_bit_exact(runtime, confident):
     prompts = config1_prompts()
     ex = _executor(runtime, confident)
