@@ -561,7 +561,7 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
     """N>1 (BASELINE config 3): one process per GPU, the SPMD runtime.  The
     model's originals live on GPU 0 (the router's home); the hot layers
     1..k (--replicate-layers, k < 32) are replicated onto every other GPU by
-    the scaling operator (ReplicateLayer over NVLink, NCCL send/recv), so each
+    the scaling operator (ReplicateLayer over NVLink: a CUDA IPC pull), so each
     step scatters the batch rows to the replicas at the run's first layer and
     gathers them back after its last; the cold layers and the
     head run on GPU 0 over the whole batch.  Per-GPU batch fixed (weak
@@ -665,19 +665,23 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
              "transport_messages": transport.messages - moved0, "transport_bytes": transport.bytes - bytes0,
              "what": "continuous batching: each step releases 1/16 of the batch, prefills as many fresh "
                      "requests, then decodes the whole batch (sequences re-split; KV rows follow over NCCL)"}
-    # one more cold layer replicated to GPU 1 and evicted: a 7B layer block over NVLink (NCCL send/recv)
+    # one more cold layer replicated to GPU 1 and evicted: a 7B layer block over NVLink (CUDA IPC pull)
     mig = None
     if k < n_layers:
         ex.apply(O.ReplicateLayer(n_layers, 1), cat, cluster)
         m = ex.op_log[-1]
         ex.apply(O.EvictReplica(n_layers, 1), cat, cluster)
-        g = group.allgather([int(m.weight_bytes), int(m.device_ms * 1e6)])
+        med = statistics.median(rep_gbps) if rep_gbps else 0.0
+        g = group.allgather([int(m.weight_bytes), int(m.device_ms * 1e6), int(med * 1e3)])
         b1, ms1 = int(g[1, 0]), g[1, 1] / 1e6  # rank 1 = the receiver
         gbps = b1 / (ms1 * 1e6) if ms1 > 0 else 0.0
         mig = {"bytes": b1, "ms": ms1, "gbps": gbps, "frac": gbps / 900.0, "nvlink_peak_gbps_per_dir": 900.0,
-               "path": "NCCL send/recv over NVLink between the ranks' copy streams (receiver-timed)",
+               "path": "CUDA IPC pull of the source rank's block by the receiver's two copy engines over NVLink "
+                       "(receiver-timed)",
                "bulk_replication": {"layers": k, "replicas_per_layer": world - 1, "wall_s": rep_s,
-                                    "median_gbps_this_rank": statistics.median(rep_gbps) if rep_gbps else None}}
+                                    "median_gbps_receivers": [float(v) / 1e3 for v in g[1:, 2]],
+                                    "what": "hot layers replicated before serving; per receiving rank the median "
+                                            "GB/s of its pulls"}}
     p2p = None
     if rank == 0 and not same_gpu and torch.cuda.device_count() > 1:
         try:

@@ -77,6 +77,8 @@ struct DeviceCtx {
   cudaEvent_t t0 = nullptr, t1 = nullptr;  // timing events
   std::map<void*, std::pair<size_t, int>> allocs;  // live allocations: bytes, MemCat
   size_t mem[MEM_CATS] = {0, 0, 0};
+  bool ipc_weights = false;  // SPMD: weight blocks from cudaMalloc, exportable with CUDA IPC
+  std::map<void*, bool> ipc_allocs;
   size_t reserved = 0;  // bytes held by pending (uncommitted) scaling ops
 };
 
@@ -189,6 +191,7 @@ struct PendingOp {
   size_t xbytes = 0;
   bool strided_gu = false;       // gate / up rows of the interleaved block (row pitch 2x)
   bool precopy = false;          // pre-copy the KV kv_from holds into kv_to
+  void* ipc_base = nullptr;      // SPMD destination: the source block mapped with CUDA IPC (closed at commit / abort)
 };
 
 struct Workspace {
@@ -420,8 +423,11 @@ int dev_alloc(DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullpt
               cudaStream_t st = nullptr) {
   CB_TRY(use(d));
   *p = nullptr;
-  cudaError_t e = cudaMallocAsync(p, bytes, st ? st : d.alloc);
-  if (e == cudaSuccess && !st) e = cudaStreamSynchronize(d.alloc);  // usable from every stream from here on
+  // SPMD weight blocks: plain cudaMalloc, so another process can map them (CUDA
+  // IPC) and pull a replicated / migrated layer with its copy engines
+  const bool ipc = d.ipc_weights && cat == MEM_WEIGHTS;
+  cudaError_t e = ipc ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, st ? st : d.alloc);
+  if (e == cudaSuccess && !st && !ipc) e = cudaStreamSynchronize(d.alloc);  // usable from every stream from here on
   if (e != cudaSuccess) {
     cudaGetLastError();
     size_t free_b = 0, total_b = 0;
@@ -433,6 +439,7 @@ int dev_alloc(DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullpt
   }
   d.allocs[*p] = {bytes, cat};
   d.mem[cat] += bytes;
+  if (ipc) d.ipc_allocs[*p] = true;
   return CB_OK;
 }
 
@@ -458,7 +465,12 @@ void dev_free(cb_model* m, int dev, void* p) {
     if (o.local)
       for (cudaStream_t s : {o.compute, o.copy, o.copy2}) join(d, d.compute, o, s);
   cudaSetDevice(d.ordinal);
-  cudaFreeAsync(p, d.compute);
+  if (d.ipc_allocs.erase(p)) {
+    cudaStreamSynchronize(d.compute);  // (the joins above: every stream that may read it is done)
+    cudaFree(p);
+  } else {
+    cudaFreeAsync(p, d.compute);
+  }
   auto it = d.allocs.find(p);
   if (it != d.allocs.end()) {
     d.mem[it->second.second] -= it->second.first;
@@ -1742,6 +1754,68 @@ int op_precopy_kv(cb_model* m, PendingOp& op, LayerState& L) {
   return grp.close();
 }
 
+// ---- between processes (SPMD): a layer block moves as a P2P copy-engine pull
+// over NVLink, not through the collective library.  The source's rank exports
+// the block (CUDA IPC handle, after its compute stream drained: every write into
+// the block has landed) and sends the handle over the host transport; the
+// destination's rank maps it and pulls it in chunks alternating over its two
+// copy lanes.  Weight blocks are static while they serve, and the SPMD commit
+// is preceded by a barrier of every rank's part, so the source block outlives
+// the pull.  (KV pre-copies / catch-ups and per-step rows stay on the transport.)
+struct IpcMsg {
+  cudaIpcMemHandle_t h;
+  uint64_t offset;
+};
+
+int host_msg(cb_model* m, bool send, int peer_rank, void* buf, size_t n) {
+  cb_runtime* rt = m->rt;
+  if (rt->xfer(rt->xfer_ctx, 2, send ? 4 : 5, peer_rank, buf, n, nullptr) != 0)
+    return fail(CB_ECOMM, std::string("transport host message ") + (send ? "to" : "from") + " rank " +
+                              std::to_string(peer_rank) + " failed");
+  return CB_OK;
+}
+
+int ipc_pull(cb_model* m, PendingOp& op) {
+  DeviceCtx& sc = devctx(m, op.src_dev);
+  DeviceCtx& dc = devctx(m, op.dst);
+  if (sc.local) {
+    auto it = sc.allocs.upper_bound(const_cast<void*>(op.xsrc));
+    if (it == sc.allocs.begin()) return fail(CB_ESTATE, "IPC source is not a tracked allocation");
+    --it;
+    if (!sc.ipc_allocs.count(it->first)) return fail(CB_ESTATE, "IPC source block is not exportable");
+    CB_TRY(use(sc));
+    CB_CUDA(cudaStreamSynchronize(sc.compute));
+    IpcMsg msg{};
+    CB_CUDA(cudaIpcGetMemHandle(&msg.h, it->first));
+    msg.offset = uint64_t(static_cast<const uint8_t*>(op.xsrc) - static_cast<const uint8_t*>(it->first));
+    CB_TRY(host_msg(m, true, dc.rank, &msg, sizeof msg));
+  }
+  if (dc.local) {
+    IpcMsg msg{};
+    CB_TRY(host_msg(m, false, sc.rank, &msg, sizeof msg));
+    CB_TRY(use(dc));
+    CB_CUDA(cudaIpcOpenMemHandle(&op.ipc_base, msg.h, cudaIpcMemLazyEnablePeerAccess));
+    const uint8_t* src = static_cast<const uint8_t*>(op.ipc_base) + msg.offset;
+    uint8_t* dst = static_cast<uint8_t*>(op.xdst);
+    const size_t chunk = std::max<size_t>(m->rt->copy_chunk, 1 << 20);
+    if (op.e0 && op.ev_dev == op.dst) CB_CUDA(cudaEventRecord(op.e0, dc.copy));  // time the pull, not the handshake
+    CB_TRY(join(dc, dc.copy2, dc, dc.copy));
+    int lane = 0;
+    for (size_t off = 0; off < op.xbytes; off += chunk, lane ^= 1)
+      CB_CUDA(cudaMemcpyAsync(dst + off, src + off, std::min(chunk, op.xbytes - off), cudaMemcpyDeviceToDevice,
+                              lane ? dc.copy2 : dc.copy));
+    CB_TRY(join(dc, dc.copy, dc, dc.copy2));
+  }
+  return CB_OK;
+}
+
+void ipc_close(PendingOp& op) {
+  if (!op.ipc_base) return;
+  if (op.e1) cudaEventSynchronize(op.e1);
+  cudaIpcCloseMemHandle(op.ipc_base);
+  op.ipc_base = nullptr;
+}
+
 // Enqueue an op's data movement: the weight transfer (+ KV pre-copy) on the
 // copy streams; e1 marks this rank's part done.
 int op_run(cb_model* m, PendingOp& op) {
@@ -1752,6 +1826,8 @@ int op_run(cb_model* m, PendingOp& op) {
       const size_t row = size_t(m->d.d_model) * 2;
       CB_TRY(use(dc));
       CB_CUDA(cudaMemcpy2DAsync(op.xdst, row, op.xsrc, 2 * row, row, m->d.d_ff, cudaMemcpyDefault, dc.copy));
+    } else if (crosses(m, op.src_dev, op.dst)) {
+      CB_TRY(ipc_pull(m, op));
     } else {
       CB_TRY(transfer(m, op.dst, op.xdst, op.src_dev, op.xsrc, op.xbytes));
     }
@@ -2008,6 +2084,7 @@ int issue_evict(cb_model* m, int layer, int dev, int64_t* id) {
 int op_commit(cb_model* m, PendingOp& op) {
   LayerState& L = m->layers[op.layer - 1];
   if (!op.started) return fail(CB_ESTATE, "op " + std::to_string(op.id) + " was never started (cb_op_start)");
+  ipc_close(op);
   if (op.e1)
     for (auto& o : m->rt->devs) {
       if (!o.local) continue;
@@ -2063,6 +2140,7 @@ int op_commit(cb_model* m, PendingOp& op) {
 }
 
 int op_abort(cb_model* m, PendingOp& op) {
+  ipc_close(op);
   op_release_reservation(m, op);
   op_unlock(m->layers[op.layer - 1], op);
   if (op.dst >= 0) devctx(m, op.dst).reserved -= op.reserved;
@@ -2362,6 +2440,7 @@ int cb_runtime_create_spmd(int32_t n_devices, const int32_t* rank_of_device, int
     }
     rt->devs[i].id = i;
     rt->devs[i].rank = rank_of_device[i];
+    rt->devs[i].ipc_weights = true;
     rt->ranks.push_back(rank_of_device[i]);
   }
   std::sort(rt->ranks.begin(), rt->ranks.end());

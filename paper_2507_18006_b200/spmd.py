@@ -14,8 +14,10 @@ own process, and every process runs the SAME program:
 * ``Transport`` -- the ``cb_xfer_fn`` the runtime calls for each byte range that
   crosses a process boundary, in the same global order on every rank:
   activation rows at replica-run boundaries, KV prefixes following their
-  sequence when ``split_batch`` re-assigns it, layer blocks of replicate /
-  migrate, KV pre-copies and catch-ups.  ``mode="nccl"``: zero-copy views of
+  sequence when ``split_batch`` re-assigns it, KV pre-copies and catch-ups;
+  and host messages: the CUDA IPC handle of a layer block being replicated /
+  migrated, which the destination's rank maps and pulls with its own copy
+  engines over NVLink (not through the collective library).  ``mode="nccl"``: zero-copy views of
   the library's device buffers, ``batch_isend_irecv`` on the stream the library
   names (NCCL over NVLink; one communicator per channel: per-step exchanges on
   the compute streams, op transfers on the copy streams).  ``mode="host"``:
@@ -58,7 +60,9 @@ class Transport:
 
     GROUP_BEGIN, GROUP_END = 2, 3
 
-    def __init__(self, dist, mode: str, device_index: int, groups: Sequence):
+    HOST_SEND, HOST_RECV = 4, 5
+
+    def __init__(self, dist, mode: str, device_index: int, groups: Sequence, host_group=None):
         import torch
 
         if mode not in ("nccl", "host"):
@@ -68,6 +72,7 @@ class Transport:
         self.mode = mode
         self.device_index = device_index
         self.groups = list(groups)  # one per channel
+        self.host_group = host_group  # gloo: host messages (CUDA IPC handles of layer blocks)
         self._batch: dict[int, list | None] = {0: None, 1: None}
         self.error: BaseException | None = None
         self.messages = 0
@@ -89,6 +94,9 @@ class Transport:
                 ops, self._batch[channel] = self._batch[channel] or [], None
                 self._flush(channel, ops)
                 return 0
+            if send in (self.HOST_SEND, self.HOST_RECV):
+                self._host_msg(send == self.HOST_SEND, int(peer), int(ptr), int(nbytes))
+                return 0
             item = (bool(send), int(peer), int(ptr or 0), int(nbytes), int(stream or 0))
             self.messages += 1
             self.bytes += int(nbytes)
@@ -101,6 +109,18 @@ class Transport:
             self.error = e
             traceback.print_exc()
             return 1
+
+    def _host_msg(self, send: bool, peer: int, ptr: int, n: int) -> None:
+        torch = self.torch
+        if send:
+            buf = torch.frombuffer(bytearray(C.string_at(ptr, n)), dtype=torch.uint8)
+            self.dist.send(buf, peer, group=self.host_group)
+        else:
+            buf = torch.empty(n, dtype=torch.uint8)
+            self.dist.recv(buf, peer, group=self.host_group)
+            C.memmove(ptr, buf.data_ptr(), n)
+        self.messages += 1
+        self.bytes += n
 
     def _flush(self, channel: int, ops: list) -> None:
         if not ops:
@@ -263,6 +283,17 @@ class SpmdExecutor(Executor):
         self._pending_placement = new_p
         return oid.value
 
+    def commit(self, wait: bool = False):
+        """Every rank's part of every pending op finishes before any rank
+        switches: a layer block is pulled by the destination's rank straight
+        from the source's memory (CUDA IPC), and a migration frees the source
+        block at the switch."""
+        for _, oid in self._pending:
+            _lib.check(self.lib.cb_op_wait(self.handle, oid, None), "cb_op_wait")
+        if self._pending:
+            self.group.barrier()
+        return super().commit(wait)
+
     def apply(self, op, catalog: ModuleCatalog, cluster: ClusterSpec, cost_model: O.OpCostModel = O.DEFAULT_COST_MODEL,
               extra_used_mb: Mapping[int, float] | None = None,
               kv_mb_by_layer: Mapping[int, float] | None = None):
@@ -307,6 +338,7 @@ def init_spmd(dist, rank: int, world: int, cuda_ordinal: int, mode: str = "nccl"
     backend = "nccl" if mode == "nccl" else "gloo"
     meta = dist.new_group(backend="gloo")
     chans = [dist.new_group(backend=backend) for _ in range(2)]
-    transport = Transport(dist, mode, cuda_ordinal, chans)
+    host = dist.new_group(backend="gloo")
+    transport = Transport(dist, mode, cuda_ordinal, chans, host_group=host)
     rank_of_device = [r for r in range(world) for _ in range(devices_per_rank)]
     return SpmdGroup(dist, meta), transport, rank_of_device
