@@ -148,12 +148,14 @@ int cb_runtime_create(int32_t n_devices, const int32_t* cuda_ordinals, cb_runtim
  * streams (activation rows at replica-run boundaries = the reference's
  * scatter/gather, _kernels.py:41-51; KV rows following their sequence; norm
  * vectors at the first step), channel 1 = scaling-op transfers on copy streams
- * (KV pre-copies and catch-ups).  Markers: send == 2 / 3 open / close a group of
+ * (unused when both sides are on GPUs: layer blocks and the KV of scaling ops
+ * move as CUDA IPC pulls, see below).  Markers: send == 2 / 3 open / close a group of
  * exchanges the transport may batch.  Host messages (channel 2): send == 4 sends
  * `bytes` of HOST memory at dev_ptr to peer_rank, send == 5 receives them, both
- * complete on return -- used for the CUDA IPC handle of a layer block, which the
- * destination's rank maps and pulls with its copy engines over NVLink (weight
- * blocks of an SPMD runtime are cudaMalloc allocations, exportable; the host
+ * complete on return -- used for the CUDA IPC handle of a layer block or KV
+ * block, which the destination's rank maps and pulls with its copy engines over
+ * NVLink (weight and KV blocks of an SPMD runtime are cudaMalloc allocations,
+ * exportable; the host
  * must not commit an op on any rank before every rank's part finished, e.g. a
  * barrier after cb_op_wait).  A non-zero return fails the call with CB_ECOMM.  The Python host implements it with torch.distributed (NCCL over
  * NVLink on a B200 box).  Not supported in this mode: projection / KV-cache

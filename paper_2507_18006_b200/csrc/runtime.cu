@@ -423,9 +423,9 @@ int dev_alloc(DeviceCtx& d, void** p, size_t bytes, uint64_t* shortfall = nullpt
               cudaStream_t st = nullptr) {
   CB_TRY(use(d));
   *p = nullptr;
-  // SPMD weight blocks: plain cudaMalloc, so another process can map them (CUDA
-  // IPC) and pull a replicated / migrated layer with its copy engines
-  const bool ipc = d.ipc_weights && cat == MEM_WEIGHTS;
+  // SPMD weight and KV blocks: plain cudaMalloc, so another process can map them
+  // (CUDA IPC) and pull a replicated / migrated layer or its KV with its copy engines
+  const bool ipc = d.ipc_weights && (cat == MEM_WEIGHTS || cat == MEM_KV);
   cudaError_t e = ipc ? cudaMalloc(p, bytes) : cudaMallocAsync(p, bytes, st ? st : d.alloc);
   if (e == cudaSuccess && !st && !ipc) e = cudaStreamSynchronize(d.alloc);  // usable from every stream from here on
   if (e != cudaSuccess) {
@@ -1735,8 +1735,18 @@ int op_register(cb_model* m, PendingOp& op, int64_t* id_out) {
 // valid and the commit copies only what was appended since (a slot released
 // and refilled meanwhile has a new epoch and is copied whole).  Only used when
 // nothing else writes kv_to's block for this layer while the op is pending.
+int kv_ipc_pull(cb_model* m, PendingOp& op, LayerState& L, bool catchup, cudaStream_t dst_st, uint64_t* bytes);
+
 int op_precopy_kv(cb_model* m, PendingOp& op, LayerState& L) {
   const bool lt = is_local(m, op.kv_to), lf = is_local(m, op.kv_from);
+  if (crosses(m, op.kv_from, op.kv_to)) {  // between processes: a CUDA IPC pull (every rank keeps the snapshot)
+    for (int slot = 0; slot < m->d.max_slots; ++slot) {
+      if (L.owner[slot] != op.kv_from || m->slot_len[slot] <= 0) continue;
+      op.snap_len[slot] = m->slot_len[slot];
+      op.snap_epoch[slot] = int(m->slot_epoch[slot]);
+    }
+    return kv_ipc_pull(m, op, L, false, lt ? devctx(m, op.kv_to).copy : nullptr, &op.kv_bytes);
+  }
   cudaStream_t dst_st = lt ? devctx(m, op.kv_to).copy : nullptr;
   cudaStream_t src_st = nullptr;
   if (crosses(m, op.kv_from, op.kv_to) && lf) {  // the sender orders its copy lane after its compute stream
@@ -1816,6 +1826,77 @@ void ipc_close(PendingOp& op) {
   op.ipc_base = nullptr;
 }
 
+// KV of a scaling op between processes (pre-copy at the start, catch-up at the
+// commit): the source's rank drains its compute stream and sends its KV
+// block's IPC handle with its slot table; the destination's rank maps the
+// block, pulls each slot kv_from holds -- positions [0, len) for the pre-copy,
+// [snapshot, len) for the catch-up -- with its copy engine on dst_st, waits,
+// unmaps and acknowledges.  The source waits for the acknowledgement: its block
+// may be regrown or freed right after.
+int kv_ipc_pull(cb_model* m, PendingOp& op, LayerState& L, bool catchup, cudaStream_t dst_st, uint64_t* bytes) {
+  DeviceCtx& fc = devctx(m, op.kv_from);
+  DeviceCtx& tc = devctx(m, op.kv_to);
+  const int ms = m->d.max_slots;
+  // message: [has_block][IPC handle][slot -> index table]
+  std::vector<uint8_t> msg(8 + sizeof(cudaIpcMemHandle_t) + size_t(ms) * 4, 0);
+  int32_t* has = reinterpret_cast<int32_t*>(msg.data());
+  cudaIpcMemHandle_t* hdl = reinterpret_cast<cudaIpcMemHandle_t*>(msg.data() + 8);
+  int32_t* map = reinterpret_cast<int32_t*>(msg.data() + 8 + sizeof(cudaIpcMemHandle_t));
+  uint8_t ack = 1;
+  if (fc.local) {
+    auto it = L.kv.find(op.kv_from);
+    if (it != L.kv.end()) {  // (no block: the layer never held KV there)
+      KvBlock& b = it->second;
+      if (!fc.ipc_allocs.count(b.p)) return fail(CB_ESTATE, "KV block is not exportable");
+      CB_TRY(use(fc));
+      CB_CUDA(cudaStreamSynchronize(fc.compute));
+      CB_CUDA(cudaIpcGetMemHandle(hdl, b.p));
+      *has = 1;
+      for (int slot = 0; slot < ms; ++slot) map[slot] = kv_index(b, slot);
+    }
+    CB_TRY(host_msg(m, true, tc.rank, msg.data(), msg.size()));
+    CB_TRY(host_msg(m, false, tc.rank, &ack, 1));
+  }
+  if (tc.local) {
+    CB_TRY(host_msg(m, false, fc.rank, msg.data(), msg.size()));
+    if (!*has) return host_msg(m, true, fc.rank, &ack, 1);
+    CB_TRY(use(tc));
+    void* base = nullptr;
+    CB_CUDA(cudaIpcOpenMemHandle(&base, *hdl, cudaIpcMemLazyEnablePeerAccess));
+    const size_t tb = kv_token_bytes(m);
+    for (int slot = 0; slot < ms; ++slot) {
+      if (L.owner[slot] != op.kv_from) continue;
+      const int len = m->slot_len[slot];
+      int p0 = 0;
+      if (catchup) {
+        const bool fresh = op.snap_len[slot] >= 0 && op.snap_epoch[slot] == int(m->slot_epoch[slot]);
+        p0 = fresh ? std::min(op.snap_len[slot], len) : 0;
+      }
+      if (len <= p0 || map[slot] < 0) continue;
+      CB_TRY(kv_assign(m, L, op.kv_to, slot));
+      uint16_t* dst = kv_ptr(m, L, op.kv_to, slot, p0);
+      const uint16_t* src = static_cast<const uint16_t*>(base) + kv_slot_offset(m, map[slot]) + size_t(p0) * tb / 2;
+      CB_CUDA(cudaMemcpyAsync(dst, src, size_t(len - p0) * tb, cudaMemcpyDeviceToDevice, dst_st));
+      if (bytes) *bytes += size_t(len - p0) * tb;
+    }
+    CB_CUDA(cudaStreamSynchronize(dst_st));
+    CB_CUDA(cudaIpcCloseMemHandle(base));
+    CB_TRY(host_msg(m, true, fc.rank, &ack, 1));
+  } else if (bytes) {  // (the byte count is bookkeeping on every rank)
+    for (int slot = 0; slot < ms; ++slot) {
+      if (L.owner[slot] != op.kv_from) continue;
+      const int len = m->slot_len[slot];
+      int p0 = 0;
+      if (catchup) {
+        const bool fresh = op.snap_len[slot] >= 0 && op.snap_epoch[slot] == int(m->slot_epoch[slot]);
+        p0 = fresh ? std::min(op.snap_len[slot], len) : 0;
+      }
+      if (len > p0) *bytes += size_t(len - p0) * kv_token_bytes(m);
+    }
+  }
+  return CB_OK;
+}
+
 // Enqueue an op's data movement: the weight transfer (+ KV pre-copy) on the
 // copy streams; e1 marks this rank's part done.
 int op_run(cb_model* m, PendingOp& op) {
@@ -1870,14 +1951,17 @@ int op_catchup_kv(cb_model* m, PendingOp& op, LayerState& L) {
       CB_TRY(kv_reserve(m, L, op.kv_to, need));
     }
   }
+  const bool ipc = crosses(m, op.kv_from, op.kv_to);
+  if (ipc) CB_TRY(kv_ipc_pull(m, op, L, true, lt ? tc.compute : nullptr, &op.catchup_bytes));
   XGroup grp(m, 0);
   for (int slot = 0; slot < m->d.max_slots; ++slot) {
     if (L.owner[slot] != op.kv_from) continue;
     const int len = m->slot_len[slot];
     const bool fresh = op.snap_len[slot] >= 0 && op.snap_epoch[slot] == int(m->slot_epoch[slot]);
     const int have = fresh ? std::min(op.snap_len[slot], len) : 0;
-    CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, lt ? tc.compute : nullptr, &op.catchup_bytes, 0,
-                   lf ? fc.compute : nullptr));
+    if (!ipc)
+      CB_TRY(kv_copy(m, L, slot, op.kv_from, op.kv_to, have, len, lt ? tc.compute : nullptr, &op.catchup_bytes, 0,
+                     lf ? fc.compute : nullptr));
     CB_TRY(kv_assign(m, L, op.kv_to, slot));
     kv_unassign(L, op.kv_from, slot);
     L.owner[slot] = op.kv_to;

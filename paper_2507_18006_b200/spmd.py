@@ -14,10 +14,10 @@ own process, and every process runs the SAME program:
 * ``Transport`` -- the ``cb_xfer_fn`` the runtime calls for each byte range that
   crosses a process boundary, in the same global order on every rank:
   activation rows at replica-run boundaries, KV prefixes following their
-  sequence when ``split_batch`` re-assigns it, KV pre-copies and catch-ups;
-  and host messages: the CUDA IPC handle of a layer block being replicated /
-  migrated, which the destination's rank maps and pulls with its own copy
-  engines over NVLink (not through the collective library).  ``mode="nccl"``: zero-copy views of
+  sequence when ``split_batch`` re-assigns it; and host messages: the CUDA
+  IPC handle of a layer block being replicated / migrated or of a KV block a
+  scaling op moves, which the destination's rank maps and pulls with its own
+  copy engines over NVLink (not through the collective library).  ``mode="nccl"``: zero-copy views of
   the library's device buffers, ``batch_isend_irecv`` on the stream the library
   names (NCCL over NVLink; one communicator per channel: per-step exchanges on
   the compute streams, op transfers on the copy streams).  ``mode="host"``:
