@@ -428,11 +428,13 @@ def run_single(args) -> None:
     # generate on to the middle of a prompt/gen request (BASELINE config 2:
     # prompt 128, gen 256 -> mean attended context 256), then the headline K
     done = args.warmup + args.steps
-    for _ in range(max(0, args.gen // 2 - args.steps // 2 - done)):
-        nxt, _, _ = ex.decode(slots, nxt)
-        done += 1
-    ctx_mid = args.prompt + done + args.steps // 2
+    # (clocks sampled from here: nvidia-smi needs a few hundred ms to start,
+    # the generation steps before the timed ones keep the GPU under the same load)
     with ClockSampler(0) as clocks:
+        for _ in range(max(0, args.gen // 2 - args.steps // 2 - done)):
+            nxt, _, _ = ex.decode(slots, nxt)
+            done += 1
+        ctx_mid = args.prompt + done + args.steps // 2
         nxt, dev_ms, wall_s = timed_steps(ex, slots, nxt, args.steps)
     # decode throughput at other batch sizes on the same instance (slot
     # subsets, their context continues from the headline's)
