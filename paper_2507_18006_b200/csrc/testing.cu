@@ -141,11 +141,11 @@ int cbt_gemm_bench(const void* w, const void* x, int64_t x_rows, int32_t N, int3
     plan = cb::GemmPlan{256, 1, 128, 1, 0};
     plan.whole = 1;
     plan.nw = 32 * (max_parts - 300);
-  } else if (max_parts == 352 || max_parts == 354) {  // token-major pairs of 256 weight rows, K split in 2 / 4
-    plan = cb::GemmPlan{256, 1, 128, 1, 0};
+  } else if (max_parts == 352 || max_parts == 354 || max_parts == 362) {  // token-major pairs, K split
+    plan = cb::GemmPlan{256, 1, 128, 1, 0};   // 35x: 256 weight rows, K split in 2 / 4; 362: 128 rows, split 2
     plan.whole = 1;
-    plan.nw = 256;
-    plan.ksplit = max_parts - 350;
+    plan.nw = max_parts == 362 ? 128 : 256;
+    plan.ksplit = max_parts % 10;
   } else if (max_parts > 400 && max_parts <= 408) {  // 1-CTA kernel, 128-token tiles, cluster split (knob - 400)
     plan = cb::GemmPlan{128, 0, 128, max_parts - 400, 0};
   } else if (max_parts > 410 && max_parts <= 418) {  // 1-CTA kernel, 64-token tiles, cluster split (knob - 410)
