@@ -18,14 +18,13 @@ full model:
 
 The collectives run over ``torch.distributed``: NCCL on the GPU box (the
 messages are a few KB of int32 per step, latency-bound), gloo in the CPU tests.
-Partial replication (hot layers only) and module migration keep the
-single-process multi-device executor, where rows and layer blocks move
-peer-to-peer over NVLink.
 
-Sequence -> rank assignment follows ``split_batch`` over the live batch, like
-the reference.  A re-split that would move a sequence to another rank (the
-batch shrank) needs its KV moved between processes; this mode raises instead
-(the single-process executor moves KV rows itself, ``kv_move`` in runtime.cu).
+This is the light mode for the one placement where every rank holds the whole
+model and sequences never change rank.  The general multi-GPU path is the SPMD
+runtime (``spmd.py``): partial (hot-layer) replication, layer / sub-module
+migration and KV following re-split sequences across processes, which is what
+``bench.py --gpus N`` runs.  Here a re-split that would move a sequence to
+another rank (the batch shrank) raises and names that path.
 """
 from __future__ import annotations
 
@@ -90,7 +89,7 @@ class ReplicaGroup:
             elif self.owner.get(g, r) != r:
                 raise NotImplementedError(
                     f"slot {g} would move from rank {self.owner[g]} to rank {r}: cross-process KV moves are "
-                    "not implemented in the replica-group mode")
+                    "not done by the replica-group mode; use spmd.SpmdExecutor, which moves KV across ranks")
         mine = []
         for g in slots[s0:s1]:
             g = int(g)

@@ -1,8 +1,13 @@
-"""Multi-process plumbing on CPU (gloo, world_size 2).
+"""Multi-process plumbing on CPU (gloo, world_size 2-3).
 
-``bench.py`` under ``torch.distributed.run`` with two ranks: the reference arm
-must run on rank 0 only and print exactly one JSON line; the rendezvous uses
-127.0.0.1.  (The GPU arm's N>1 path needs GPUs and is exercised on the box.)
+* ``bench.py`` under ``torch.distributed.run`` with two ranks: the reference
+  arm runs on rank 0 only and prints exactly one JSON line; the rendezvous
+  uses 127.0.0.1.
+* The SPMD runtime's host side (``spmd.py``): lockstep broadcasts / votes,
+  host messages and transfer batching through the ``cb_xfer_fn`` pointer.
+* ``dist.ReplicaGroup``'s scatter / gather by ``split_batch``.
+The device side of the N>1 path needs GPUs and is exercised on the box
+(tests/test_spmd_gpu.py, tests/test_dist_gpu.py).
 """
 from __future__ import annotations
 
@@ -80,3 +85,20 @@ def test_replica_group_world3_uneven_shares():
     assert out.returncode == 0, out.stderr[-3000:]
     rec = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
     assert rec["equal"] and rec["shares"] == [1, 2, 2]
+
+
+def test_spmd_host_plumbing_world2():
+    """The SPMD runtime's host side over gloo (tests/spmd_host_worker.py):
+    lockstep broadcast / all-gather, host messages through the cb_xfer_fn
+    function pointer, transfer batching and error return."""
+    out = _torchrun(ROOT / "tests" / "spmd_host_worker.py", 2)
+    assert out.returncode == 0, out.stderr[-3000:]
+    rec = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
+    assert rec["rank_of_device"] == [0, 0, 1, 1]
+    assert rec["bcast"] == [5, 6, 7, 101]
+    assert rec["allgather"] == [[0, 3], [1, 13]]
+    assert rec["host_rc"] == 0 and rec["host_equal"]
+    assert rec["host_counted"] == [1, 64 + 9 * 4]
+    assert rec["flush_before_end"] == 0
+    assert rec["flushed"] == [[0, [[True, 1, 0x1000, 256], [False, 1, 0x2000, 128]]], [1, [[True, 1, 0x3000, 64]]]]
+    assert rec["err_rc"] == 1 and rec["err_kept"]
