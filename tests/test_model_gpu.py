@@ -687,3 +687,53 @@ def test_llama2_geometries_match_oracle(runtime, shape, B):
     assert worst <= LOGIT_TOL, worst
     assert checked >= steps * B // 2
     ex.close()
+
+
+def test_context_and_slot_capacity_edges(runtime, confident):
+    """Capacity edges (max_ctx 64, max_slots 32): a full-length prompt and a
+    decode that fills the last cache position match the oracle; one more
+    position, a prompt past max_ctx, a slot id past max_slots and an empty
+    batch are handled without a launch on bad input (OpError / empty result),
+    and the executor keeps serving afterwards."""
+    ex = _executor(runtime, confident)
+    oracle = OracleModel(TINY, confident, 64)
+    rng = np.random.default_rng(11)
+    lens = [64, 60, 56, 1]  # one prompt fills the whole context, one is a single token
+    slots = np.array([31, 0, 7, 30], np.int32)  # highest slot id included
+    toks = rng.integers(0, TINY.vocab, sum(lens)).astype(np.int32)
+    with pytest.raises(O.OpError):  # prompt one past max_ctx
+        ex.prefill(np.array([5], np.int32), rng.integers(0, TINY.vocab, 65).astype(np.int32),
+                   np.array([65], np.int32))
+    with pytest.raises(O.OpError):  # slot id past max_slots
+        ex.prefill(np.array([32], np.int32), toks[:4], np.array([4], np.int32))
+    _, lg, _ = ex.prefill(slots, toks, np.array(lens, np.int32), want_logits=True)
+    want = oracle.forward(list(slots), toks, lens)
+    assert np.abs(lg - want).max() <= LOGIT_TOL
+    # slot 31 is at max_ctx: it cannot decode; the others can until they reach it
+    with pytest.raises(O.OpError):
+        ex.decode(slots, np.zeros(4, np.int32))
+    live = [0, 7, 30]
+    nxt = dict(zip(live, want[1:].argmax(1).astype(np.int32)))
+    steps = 0
+    while True:
+        s = np.array(live, np.int32)
+        inp = np.array([nxt[q] for q in live], np.int32)
+        _, lg, _ = ex.decode(s, inp, want_logits=True)
+        want = oracle.forward(live, inp, None)
+        assert np.abs(lg - want).max() <= LOGIT_TOL
+        nxt = dict(zip(live, want.argmax(1).astype(np.int32)))
+        steps += 1
+        if 0 in live and oracle.lens[0] == 64:  # slot 0 just filled position 63
+            break
+    assert steps == 4
+    with pytest.raises(O.OpError):  # one position past max_ctx
+        ex.decode(np.array([0], np.int32), np.array([nxt[0]], np.int32))
+    out, _, _ = ex.decode(np.zeros(0, np.int32), np.zeros(0, np.int32))  # empty batch
+    assert len(out) == 0
+    # the remaining sequences keep decoding like the oracle
+    live = [7, 30]
+    s = np.array(live, np.int32)
+    inp = np.array([nxt[q] for q in live], np.int32)
+    _, lg, _ = ex.decode(s, inp, want_logits=True)
+    assert np.abs(lg - oracle.forward(live, inp, None)).max() <= LOGIT_TOL
+    ex.close()
