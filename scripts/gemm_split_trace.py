@@ -1,6 +1,6 @@
 """Per-CTA timeline of the token-major split-K pair GEMM (O / down at T > 128):
-k-block landing times, then the DSMEM exchange: tfull (own K half done),
-barrier A (all MMAs retired), push of the peer's half done, barrier B, end.
+k-block landing times, then the L2 part exchange: tfull (own K part done),
+parts stored (bulk stores of the other column parts done), parts arrived (counter wait over, loads issued), drained, end.
     python scripts/gemm_split_trace.py N K T [epi]"""
 import ctypes as C
 import sys
@@ -38,7 +38,7 @@ for c in np.nonzero(valid)[0]:
     ev = rel[c, 130:134]
     rows.append((rel[c, 0], mma[0] if len(mma) else np.nan, mma[-1] if len(mma) else np.nan, len(mma), *ev, rel[c, 1]))
 a = np.array(rows)
-names = ["start", "kb0 landed", "kb63 landed", "n kb traced", "tfull", "barrier A", "pushed", "barrier B", "end"]
+names = ["start", "kb0 landed", "kb63 landed", "n kb traced", "tfull", "parts stored", "parts arrived", "drained", "end"]
 for i, nme in enumerate(names):
     col = a[:, i]
     print(f"  {nme:12s} min {np.nanmin(col):7.2f}  median {np.nanmedian(col):7.2f}  max {np.nanmax(col):7.2f}")

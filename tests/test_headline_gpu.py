@@ -129,7 +129,7 @@ def test_headline_b256_matches_oracle(runtime, weights):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("batch", [1, 16, 64, 128])
+@pytest.mark.parametrize("batch", [1, 2, 16, 64, 128])
 def test_sweep_batches_match_oracle(runtime, weights, batch):
     _run(runtime, weights, batch)
 
