@@ -18,15 +18,17 @@ MB L2, so every step streams them from HBM (no L2 flush needed).
   cb_step) with host token buffers: H2D of the step's metadata and D2H of the
   sampled tokens inside the timed region, host wall clock around K
   synchronous calls.
-* ``roofline``: the dominant kernel class (the tcgen05 GEMMs) -- algorithmic
-  bytes and FLOPs per launch / average launch time, measured live with CUDA
-  events bracketing every launch in a second pass of K steps right after the
-  timed region (the events serialise the programmatic-dependent-launch
-  overlap, so they stay out of the timed region); the binding roof is the
-  larger of bytes / HBM peak and FLOPs / sustained bf16 peak
-  (MEASURED_PEAKS.json).  ``in_step`` attributes the timed steps by the class
-  shares of that pass.  ``traffic`` = ncu DRAM bytes per GEMM launch
-  (profiles/ncu_summary.json).
+* ``roofline``: the dominant kernel class of the step (largest share of the
+  profiled pass: the decode attention at the headline's context 256, the
+  tcgen05 GEMMs at short contexts), every class's own roofline under
+  ``classes`` -- algorithmic bytes and FLOPs per launch / average launch time,
+  measured live with CUDA events bracketing every launch in a second pass of
+  K steps right after the timed region (the events serialise the
+  programmatic-dependent-launch overlap, so they stay out of the timed
+  region); the binding roof is the larger of bytes / HBM peak and FLOPs /
+  sustained bf16 peak (MEASURED_PEAKS.json).  ``in_step`` attributes the
+  timed steps by the class shares of that pass.  ``traffic`` = ncu DRAM bytes
+  per launch of the class (profiles/ncu_summary.json).
 * ``parity_spot_check``: outside every timed region, the headline plans with
   oracle weights vs the fp32 oracle (test infrastructure as a checker).
 * ``cpu_baseline``: the CPU oracle (numpy fp32, all host cores), one complete
@@ -487,7 +489,7 @@ def run_single(args) -> None:
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": (3 * batch + batch) * 4,
                 "d2h_bytes_per_step": batch * 4},
         "gpu_launches": launches,
-        "roofline": gemm_roofline(prof, prof_ms, peaks, ncu, step_ms=sum(dev_ms) / len(dev_ms)),
+        "roofline": step_roofline(prof, prof_ms, peaks, ncu, step_ms=sum(dev_ms) / len(dev_ms)),
         "ctx_points": {str(ctx_early): {"tokens_per_s": batch * len(early_ms) / (sum(early_ms) / 1e3),
                                         "ms_per_step": float(np.mean(early_ms))},
                        str(ctx_mid): {"tokens_per_s": value, "ms_per_step": sum(dev_ms) / len(dev_ms)}},
@@ -509,54 +511,74 @@ def run_single(args) -> None:
     print(json.dumps(line), flush=True)
 
 
-def gemm_roofline(prof: dict, prof_ms: list, peaks: dict, ncu: dict | None = None,
-                  step_ms: float | None = None) -> dict:
-    """Roofline of the dominant kernel class (the decode GEMMs) from one
-    profiled pass: algorithmic bytes / FLOPs per launch over the average
-    CUDA-event launch time.  The binding roof per launch is the larger of
-    bytes / HBM peak and FLOPs / tensor peak; at B=256 the 7B decode GEMMs sit
-    above the ridge (FLOP-bound)."""
-    g, a = prof["gemm"], prof["attention"]
+def _class_roofline(cls: str, prof: dict, prof_ms: list, peaks: dict, traffic, step_ms: float | None) -> dict:
+    """One kernel class of a profiled pass: algorithmic bytes / FLOPs per
+    launch over the average CUDA-event launch time; the binding roof per launch
+    is the larger of bytes / HBM peak and FLOPs / sustained tensor peak."""
+    g = prof[cls]
     n = max(1, g["launches"])
+    flops = g.get("flops", 0.0)
     gbs = g["bytes"] / (g["ms"] * 1e6) if g["ms"] else 0.0
-    tfs = g.get("flops", 0.0) / (g["ms"] * 1e9) if g["ms"] else 0.0
+    tfs = flops / (g["ms"] * 1e9) if g["ms"] else 0.0
     t_hbm = g["bytes"] / (peaks["hbm_gbs"] * 1e9)
-    t_tc = g.get("flops", 0.0) / (peaks["bf16_tflops_sustained"] * 1e12)
+    t_tc = flops / (peaks["bf16_tflops_sustained"] * 1e12)
     tensor_bound = t_tc > t_hbm
-    attn_gbs = a["bytes"] / (a["ms"] * 1e6) if a["ms"] else 0.0
+    pk = peaks["bf16_tflops_sustained"] if tensor_bound else peaks["hbm_gbs"]
     # Second view: the timed steps' device time attributed by the profiled
-    # pass's class shares (the event-bracketed launches above serialise the
+    # pass's class shares (the event-bracketed launches serialise the
     # programmatic-dependent-launch overlap, so their per-launch time is an
     # upper bound); an estimate, reported beside the measured figure.
     in_step = None
     if step_ms and prof_ms and g["ms"]:
-        share = g["ms"] / sum(prof_ms)
-        lps = g["launches"] / len(prof_ms)
-        ms_l = step_ms * share / lps
-        ach = (g.get("flops", 0.0) / n) / (ms_l * 1e9) if tensor_bound else (g["bytes"] / n) / (ms_l * 1e6)
-        pk = peaks["bf16_tflops_sustained"] if tensor_bound else peaks["hbm_gbs"]
+        ms_l = step_ms * (g["ms"] / sum(prof_ms)) / (g["launches"] / len(prof_ms))
+        ach = (flops / n) / (ms_l * 1e9) if tensor_bound else (g["bytes"] / n) / (ms_l * 1e6)
         in_step = {"ms_per_launch": ms_l, "achieved": ach, "frac": ach / pk,
-                   "how": "timed-region ms/step x the GEMM share of the profiled pass / GEMM launches per step"}
+                   "how": f"timed-region ms/step x the {cls} share of the profiled pass / its launches per step"}
     return {
-        "kernel": "decoder-layer GEMMs (tcgen05 gemm_tc_kernel / gemm_tc2_kernel)",
         "bound": "tensor" if tensor_bound else "hbm",
         "achieved": tfs if tensor_bound else gbs,
-        "peak": peaks["bf16_tflops_sustained"] if tensor_bound else peaks["hbm_gbs"],
+        "peak": pk,
         "unit": "TFLOP/s" if tensor_bound else "GB/s",
-        "frac": (tfs / peaks["bf16_tflops_sustained"]) if tensor_bound else (gbs / peaks["hbm_gbs"]),
+        "frac": (tfs if tensor_bound else gbs) / pk,
         "frac_of_binding_roof": (max(t_hbm, t_tc) * 1e3) / g["ms"] if g["ms"] else 0.0,
         "peak_src": peaks["src"],
-        "bytes_per_launch": g["bytes"] / n, "flops_per_launch": g.get("flops", 0.0) / n,
+        "bytes_per_launch": g["bytes"] / n, "flops_per_launch": flops / n,
         "ms_per_launch": g["ms"] / n,
-        "traffic": (ncu or {}).get("gemm_dram_bytes_per_launch"),
-        "step_share": {k: prof[k]["ms"] / sum(prof_ms) for k in prof} if prof_ms else None,
+        "traffic": traffic,
         "hbm": {"achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"]},
         "tensor": {"achieved": tfs, "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
                    "frac": tfs / peaks["bf16_tflops_sustained"]},
-        "attention": {"achieved": attn_gbs, "unit": "GB/s", "frac": attn_gbs / peaks["hbm_gbs"],
-                      "bytes_per_launch": a["bytes"] / max(1, a["launches"])},
         "in_step": in_step,
     }
+
+
+KERNEL_NAMES = {"gemm": "decoder-layer GEMMs (tcgen05 gemm_tc_kernel / gemm_tc2_kernel)",
+                "attention": "decode attention (attn2_kernel: fused RoPE + KV append, split-context merge)"}
+
+
+def step_roofline(prof: dict, prof_ms: list, peaks: dict, ncu: dict | None = None,
+                  step_ms: float | None = None) -> dict:
+    """Roofline of the dominant kernel class of the step -- the class with the
+    largest share of the profiled pass's device time (the decode GEMMs at short
+    contexts, the decode attention's KV read at the headline's context 256) --
+    with every class's own roofline under ``classes``.  ``traffic`` = ncu DRAM
+    read + write bytes per launch of that class (profiles/ncu_summary.json,
+    one ``--set full`` capture) and, for the attention, the algorithmic bytes
+    of the captured launch beside it (its context differs from this pass's)."""
+    ncu = ncu or {}
+    traffic = {"gemm": ncu.get("gemm_dram_bytes_per_launch"),
+               "attention": ncu.get("attention_dram_bytes_per_launch")}
+    classes = {c: _class_roofline(c, prof, prof_ms, peaks, traffic[c], step_ms) for c in ("gemm", "attention")}
+    if ncu.get("attention_algorithmic_bytes_per_launch"):
+        classes["attention"]["traffic_capture_algorithmic_bytes"] = ncu["attention_algorithmic_bytes_per_launch"]
+    share = {k: prof[k]["ms"] / sum(prof_ms) for k in prof} if prof_ms else None
+    dom = max(classes, key=lambda c: prof[c]["ms"])
+    out = {"kernel": KERNEL_NAMES[dom], "class": dom,
+           "dominant_by": "largest share of the profiled step's device time"}
+    out.update(classes[dom])
+    out["step_share"] = share
+    out["classes"] = {c: dict(classes[c], kernel=KERNEL_NAMES[c]) for c in classes}
+    return out
 
 
 def run_spmd(args, rank: int, world: int, dist) -> None:
@@ -712,7 +734,7 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
             "e2e": {"value": gbatch * args.steps / wall_s, "unit": "tokens/s",
                     "h2d_bytes_per_step": (gbatch * 3 + gbatch) * 4, "d2h_bytes_per_step": gbatch * 4},
             "gpu_launches": launches_per_step * args.steps,
-            "roofline": gemm_roofline(prof, prof_ms, peaks,
+            "roofline": step_roofline(prof, prof_ms, peaks,
                                       json.loads(ncu_path.read_text()) if ncu_path.exists() else None,
                                       step_ms=float(np.mean(dev_ms))),
             "continuous_batching": churn,
