@@ -528,8 +528,11 @@ def _class_roofline(cls: str, prof: dict, prof_ms: list, peaks: dict, traffic, s
     # pass's class shares (the event-bracketed launches serialise the
     # programmatic-dependent-launch overlap, so their per-launch time is an
     # upper bound); an estimate, reported beside the measured figure.
+    # (GEMMs only: their short launches overlap under PDL; a 170+ us attention
+    # launch loses < 1% to the brackets and the proportional attribution would
+    # credit it with the GEMMs' overlap)
     in_step = None
-    if step_ms and prof_ms and g["ms"]:
+    if cls == "gemm" and step_ms and prof_ms and g["ms"]:
         ms_l = step_ms * (g["ms"] / sum(prof_ms)) / (g["launches"] / len(prof_ms))
         ach = (flops / n) / (ms_l * 1e9) if tensor_bound else (g["bytes"] / n) / (ms_l * 1e6)
         in_step = {"ms_per_launch": ms_l, "achieved": ach, "frac": ach / pk,

@@ -69,4 +69,5 @@ def test_roofline_reports_the_dominant_class():
     assert r["achieved"] == pytest.approx(1e9 / (0.7 * 1e6))
     assert r["traffic"] == 1.09e9 and r["traffic_capture_algorithmic_bytes"] == 1.078e9
     assert r["classes"]["gemm"]["bound"] == "tensor" and r["classes"]["gemm"]["traffic"] == 1.1e8
+    assert r["in_step"] is None and r["classes"]["gemm"]["in_step"]["frac"] > 0
     assert r["step_share"]["attention"] > r["step_share"]["gemm"]
