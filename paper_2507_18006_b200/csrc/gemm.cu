@@ -1248,7 +1248,7 @@ __global__ void __launch_bounds__(kThreads1, 1)
       int nb = 0;
       for (int dst = 0; dst < ks; ++dst) {
         if (dst == kh) continue;
-        float4* pp = reinterpret_cast<float4*>(sout + size_t(nb++) * blk) + lt;
+        float4* pp = reinterpret_cast<float4*>(sout + size_t(nb) * blk) + lt;
         for (int c0 = 0; c0 < w; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t_addr + uint32_t(dst * w + c0), r);
@@ -1258,15 +1258,18 @@ __global__ void __launch_bounds__(kThreads1, 1)
             pp[((c0 >> 5) * 8 + j) * 128] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                                         __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
         }
+        // each block leaves for L2 as soon as it is staged (its store overlaps
+        // the staging of the next one)
+        fence_proxy_async_smem();
+        named_bar_sync(1, kEpiThreads);
+        if (et == 0) {
+          bulk_s2g(xb + (dst * ks + kh) * blk, sout + size_t(nb) * blk, uint32_t(blk * 4));
+          bulk_commit();
+        }
+        ++nb;
       }
-      fence_proxy_async_smem();
-      named_bar_sync(1, kEpiThreads);
       int* cnt = a.counters + size_t(pair * 2 + int(rank)) * ks;
       if (et == 0) {
-        nb = 0;
-        for (int dst = 0; dst < ks; ++dst)
-          if (dst != kh) bulk_s2g(xb + (dst * ks + kh) * blk, sout + size_t(nb++) * blk, uint32_t(blk * 4));
-        bulk_commit();
         bulk_wait<0>();
         if (tr) tr[1] = globaltimer_ns();
         fence_proxy_async_global();  // the async-proxy stores, then the generic release below
