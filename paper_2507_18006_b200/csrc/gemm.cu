@@ -858,9 +858,12 @@ CB_DEVICE uint4* stg_chunk(uint8_t* stg, int r, int c) {
 // i + 1), each [32-column chunk][8 float4 groups][128 tokens][float4]; the
 // column sum runs over the parts in K order, this CTA's own accumulator being
 // part xme.
+__device__ const float4 kNoRes[8] = {};
+
 CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, uint32_t t_addr, int n_base,
                              int nw, int row0, int tok0, int ncols, const float* xp = nullptr, int xs = 0,
-                             int xme = 0, size_t xstride = 0) {
+                             int xme = 0, size_t xstride = 0, bool have_first = false,
+                             const float4 (&res_first)[8] = kNoRes) {
   const int tok = tok0 + e.lane;  // tok0: first token of this warp
   const bool ok = tok < ncols;
   // full 32-token groups go out through swizzled staging + one TMA store per
@@ -876,7 +879,9 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
     float4 res[8];
     if (!use_tma && a.epi == EPI_RESID && ok) {  // residual loads in flight during the TMEM load
 #pragma unroll
-      for (int j = 0; j < 8; ++j) res[j] = __ldcg(reinterpret_cast<const float4*>(out_f32(a, n0 + 4 * j, row)));
+      for (int j = 0; j < 8; ++j)
+        res[j] = (c0 == 0 && have_first) ? res_first[j]
+                                        : __ldcg(reinterpret_cast<const float4*>(out_f32(a, n0 + 4 * j, row)));
     }
     uint32_t r[32];
     tmem_ld32(t_addr + uint32_t(c0), r);
@@ -1285,9 +1290,19 @@ __global__ void __launch_bounds__(kThreads1, 1)
           if (src != kh) bulk_g2s(sin + size_t(nb++) * blk, xb + (kh * ks + src) * blk, uint32_t(blk * 4), fix_bar);
         if (tr) tr[2] = globaltimer_ns();
       }
+      // the first chunk's residual rows (this CTA alone updates them) are
+      // loaded while the other parts are still arriving
+      float4 res0[8];
+      const int tok = int(rank) * kBM + q * 32 + lane;
+      const bool pre = a.epi == EPI_RESID && a.h_out && tok < ncols;
+      if (pre) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          res0[j] = __ldcg(reinterpret_cast<const float4*>(out_f32(a, mt * a.nw + kh * w + 4 * j, row0 + tok)));
+      }
       mbar_wait(fix_bar, 0);
       epi_drain_tok(a, &tmO, e, t_addr + uint32_t(kh * w), mt * a.nw + kh * w, w, row0, int(rank) * kBM + q * 32,
-                    ncols, sin, ks, kh, blk);
+                    ncols, sin, ks, kh, blk, pre, res0);
       if (tr) tr[3] = globaltimer_ns();
     }
     for (int u = split ? uend : ubeg; u < uend;) {
