@@ -1,8 +1,8 @@
 #!/bin/bash
-# Interleaved A/B of one decode step (scripts/step_profile.py), R rounds:
-#   bash scripts/ab_step.sh B R "ENV_A" "ENV_B"   (ENV_* = "" or "VAR=1 VAR2=1")
-B=$1; R=${2:-3}; A=$3; BB=$4
+# A/B of two prebuilt libraries (ab/old.so, ab/new.so) on the 7B decode step: alternating runs
+B=${1:-256}; CTX=${2:-256}; R=${3:-4}
 for r in $(seq $R); do
-  echo "A $(env $A timeout 300 python scripts/step_profile.py $B 10 2>&1 | head -1)"
-  echo "B $(env $BB timeout 300 python scripts/step_profile.py $B 10 2>&1 | head -1)"
+  for v in old new; do
+    echo -n "$v "; COCOB200_LIB=ab/$v.so timeout 300 python scripts/step_profile.py $B 5 $CTX 2>&1 | grep "decode step"
+  done
 done
