@@ -603,10 +603,18 @@ def run_spmd(args, rank: int, world: int, dist) -> None:
 
     _lib.load()
     peaks = _peaks()
-    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"  # tests: every rank on cuda:0, host-staged transport
+    same_gpu = os.environ.get("BENCH_SAME_GPU") == "1"  # tests: every rank on cuda:0
     ordinal = 0 if same_gpu else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(ordinal)
-    group, transport, rod = init_spmd(dist, rank, world, ordinal, "host" if same_gpu else "nccl")
+    # transport: NCCL across GPUs; on one GPU (tests) host-staged, or NCCL with
+    # BENCH_TRANSPORT=nccl -- each rank then poses as its own host, since NCCL
+    # refuses two ranks on one device otherwise
+    mode = os.environ.get("BENCH_TRANSPORT") or ("host" if same_gpu else "nccl")
+    if same_gpu and mode == "nccl":
+        os.environ["NCCL_HOSTID"] = f"bench-rank{rank}"
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+        os.environ.setdefault("NCCL_IB_DISABLE", "1")
+    group, transport, rod = init_spmd(dist, rank, world, ordinal, mode)
     rt = SpmdRuntime(rod, rank, ordinal, transport)
     n_layers = LLAMA2_7B["n_layers"]
     k = args.replicate_layers if args.replicate_layers is not None else n_layers - 4

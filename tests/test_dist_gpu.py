@@ -23,15 +23,17 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def test_bench_spmd_world2_same_gpu():
+@pytest.mark.parametrize("transport", ["host", "nccl"])
+def test_bench_spmd_world2_same_gpu(transport):
     """bench.py's N>1 path (config 3, SPMD: hot layers 1..28 replicated on the
     second rank, cold layers + head on rank 0, continuous-batching window with
-    cross-rank KV moves) with both ranks on cuda:0 (host-staged transport)."""
+    cross-rank KV moves) with both ranks on cuda:0: host-staged transport, and
+    the NCCL transport the multi-GPU run uses (each rank its own NCCL host)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "1", "--batch", "8", "--prompt", "16", "--churn-steps", "3"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
-                         env={**os.environ, "BENCH_SAME_GPU": "1"})
+                         env={**os.environ, "BENCH_SAME_GPU": "1", "BENCH_TRANSPORT": transport})
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]
