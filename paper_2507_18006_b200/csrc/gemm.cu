@@ -873,6 +873,77 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
   const int row = row0 + tok;
   const float* rt = e.rt;
   const float sc = (rt && ok) ? rt[row - a.row_off] : 1.0f;
+  if (!xp && use_tma && (a.epi == EPI_BF16 || a.epi == EPI_SWIGLU)) {
+    // bf16 / SwiGLU boxes two chunks at a time: both TMEM loads behind one
+    // wait, both staging slots behind one proxy fence, and the two chunks'
+    // conversions independent (a lone epilogue warp per sub-partition is
+    // latency-bound one chunk at a time, profiles/r02_gemm_epilogue_trace.txt)
+    for (int c0 = 0; c0 < nw; c0 += 64) {
+      const int n0 = n_base + c0;
+      if (n0 >= a.N) break;
+      const bool two = c0 + 32 < nw && n0 + 32 < a.N;
+      uint32_t r[2][32];
+      tmem_ld32(t_addr + uint32_t(c0), r[0]);
+      if (two) tmem_ld32(t_addr + uint32_t(c0 + 32), r[1]);
+      tmem_ld_wait();
+      uint4 o[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = rt ? __uint_as_float(r[h][i]) * sc : __uint_as_float(r[h][i]);
+        if (a.epi == EPI_BF16) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            o[h][c] = make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                                 pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float* g = v + 16 * c;
+            o[h][c] = make_uint4(pack_bf16x2(silu_mul(g[0], g[1]), silu_mul(g[2], g[3])),
+                                 pack_bf16x2(silu_mul(g[4], g[5]), silu_mul(g[6], g[7])),
+                                 pack_bf16x2(silu_mul(g[8], g[9]), silu_mul(g[10], g[11])),
+                                 pack_bf16x2(silu_mul(g[12], g[13]), silu_mul(g[14], g[15])));
+          }
+        }
+      }
+      // slot of the first chunk: <= 2 older stores may still read theirs; the
+      // second chunk's slot was read by the store two chunks back -> <= 1
+      uint8_t* s0 = e.next_stage3();
+      uint8_t* s1 = nullptr;
+      if (two) {
+        if (e.lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        s1 = e.st + e.sb * kChunkBytes;
+        e.sb = e.sb == 2 ? 0 : e.sb + 1;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1 && !two) break;
+        uint8_t* stg = h ? s1 : s0;
+        if (a.epi == EPI_BF16) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) *stg_chunk<64, 3>(stg, e.lane, c) = o[h][c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c) *stg_chunk<32, 1>(stg, e.lane, c) = o[h][c];
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (e.lane == 0) {
+        const int cn = a.epi == EPI_BF16 ? n0 : n0 >> 1;
+        tma_store_2d(tmO, s0, cn, row0 + tok0);
+        bulk_commit();
+        if (two) {
+          tma_store_2d(tmO, s1, a.epi == EPI_BF16 ? n0 + 32 : (n0 + 32) >> 1, row0 + tok0);
+          bulk_commit();
+        }
+      }
+    }
+    return;
+  }
   for (int c0 = 0; c0 < nw; c0 += 32) {
     const int n0 = n_base + c0;
     if (n0 >= a.N) break;  // N % 32 == 0 (launcher)
