@@ -863,7 +863,7 @@ __device__ const float4 kNoRes[8] = {};
 CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp& e, uint32_t t_addr, int n_base,
                              int nw, int row0, int tok0, int ncols, const float* xp = nullptr, int xs = 0,
                              int xme = 0, size_t xstride = 0, bool have_first = false,
-                             const float4 (&res_first)[8] = kNoRes) {
+                             const float4 (&res_first)[8] = kNoRes, const float4 (&res_second)[8] = kNoRes) {
   const int tok = tok0 + e.lane;  // tok0: first token of this warp
   const bool ok = tok < ncols;
   // full 32-token groups go out through swizzled staging + one TMA store per
@@ -951,8 +951,9 @@ CB_DEVICE void epi_drain_tok(const GemmArgs& a, const CUtensorMap* tmO, EpiWarp&
     if (!use_tma && a.epi == EPI_RESID && ok) {  // residual loads in flight during the TMEM load
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        res[j] = (c0 == 0 && have_first) ? res_first[j]
-                                        : __ldcg(reinterpret_cast<const float4*>(out_f32(a, n0 + 4 * j, row)));
+        res[j] = (c0 == 0 && have_first)    ? res_first[j]
+                 : (c0 == 32 && have_first) ? res_second[j]
+                                            : __ldcg(reinterpret_cast<const float4*>(out_f32(a, n0 + 4 * j, row)));
     }
     uint32_t r[32];
     tmem_ld32(t_addr + uint32_t(c0), r);
@@ -1361,19 +1362,21 @@ __global__ void __launch_bounds__(kThreads1, 1)
           if (src != kh) bulk_g2s(sin + size_t(nb++) * blk, xb + (kh * ks + src) * blk, uint32_t(blk * 4), fix_bar);
         if (tr) tr[2] = globaltimer_ns();
       }
-      // the first chunk's residual rows (this CTA alone updates them) are
-      // loaded while the other parts are still arriving
-      float4 res0[8];
+      // the residual rows of both 32-column chunks (this CTA alone updates
+      // them) are loaded while the other parts are still arriving
+      float4 res0[8], res1[8];
       const int tok = int(rank) * kBM + q * 32 + lane;
-      const bool pre = a.epi == EPI_RESID && a.h_out && tok < ncols;
+      const bool pre = a.epi == EPI_RESID && a.h_out && tok < ncols && w == 64;
       if (pre) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < 8; ++j) {
           res0[j] = __ldcg(reinterpret_cast<const float4*>(out_f32(a, mt * a.nw + kh * w + 4 * j, row0 + tok)));
+          res1[j] = __ldcg(reinterpret_cast<const float4*>(out_f32(a, mt * a.nw + kh * w + 32 + 4 * j, row0 + tok)));
+        }
       }
       mbar_wait(fix_bar, 0);
       epi_drain_tok(a, &tmO, e, t_addr + uint32_t(kh * w), mt * a.nw + kh * w, w, row0, int(rank) * kBM + q * 32,
-                    ncols, sin, ks, kh, blk, pre, res0);
+                    ncols, sin, ks, kh, blk, pre, res0, res1);
       if (tr) tr[3] = globaltimer_ns();
     }
     for (int u = split ? uend : ubeg; u < uend;) {
