@@ -15,6 +15,9 @@
 // split CTA of a (row, kv head) to arrive merges the partials, in split
 // order).  Decode attention is HBM-bound: every K/V byte is read once.
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -296,6 +299,300 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
 }
 
+// ---------------------------------------------------------------------------
+// attn_tma: the same CTA, lane-group mapping and arithmetic as attn2 (one
+// context split, hd 128, KV block in device memory), with K and V fed by TMA:
+// boxes of 64 cached positions x one head's 128 dims (16 KB each) from the
+// [slot * max_ctx + pos][k | v] view of the block, two K+V stages per CTA,
+// issued before griddepcontrol.wait (cached positions < cur were written by
+// earlier steps; the row's own k / v are substituted at `cur` as in attn2).
+// Bulk tensor loads read HBM at ~7 TB/s where 16-byte loads top out near
+// 6.2 (profiles/r02_read_bw.txt).
+constexpr int kTmaPos = 64;
+constexpr int kTmaStages = 2;
+
+template <int GQ, int U>
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attn_tma_kernel(const __grid_constant__ CUtensorMap tkv, const AttnArgs a) {
+  constexpr int HD = 128;
+  constexpr int G = HD / 8;           // lanes per group
+  constexpr int P = 32 / G;           // groups per warp
+  constexpr int NG = kAttnWarps * P;  // groups per CTA
+  constexpr uint32_t kBoxBytes = kTmaPos * HD * 2;
+  extern __shared__ __align__(1024) uint8_t smt[];
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smt);  // [stage][K | V][kTmaPos][HD]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smt + kTmaStages * 2 * kBoxBytes);
+  uint64_t* empty = full + kTmaStages;
+  float* sm2 = reinterpret_cast<float*>(empty + kTmaStages);  // [kAttnWarps][GQ][G][10]
+  pdl_trigger();
+  const int hk = blockIdx.x, rl = blockIdx.y;
+  const int row = a.row_off + rl;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lg = lane % G, pg = lane / G;
+  const int grp = warp * P + pg;
+  const int slot = a.kv_map ? a.kv_map[a.row_slot[row]] : a.row_slot[row];
+  const int len = a.row_pos[row] + 1;
+  const int cur = len - 1;
+  const int nbox = (len + kTmaPos - 1) / kTmaPos;
+  const size_t kvd = size_t(a.Hkv) * HD;
+  const int prow = slot * a.max_ctx;  // view row of position 0
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tkv);
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kAttnWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();  // every K / V byte is read once per step
+  auto issue = [&](int b) {
+    const int st = b % kTmaStages;
+    uint16_t* kd = ring + size_t(st) * 2 * kTmaPos * HD;
+    mbar_arrive_expect_tx(&full[st], 2 * kBoxBytes);
+    tma_load_2d(&tkv, &full[st], kd, hk * HD, prow + b * kTmaPos, pol);
+    tma_load_2d(&tkv, &full[st], kd + kTmaPos * HD, int(kvd) + hk * HD, prow + b * kTmaPos, pol);
+  };
+  if (threadIdx.x == 0)
+    for (int b = 0; b < nbox && b < kTmaStages; ++b) issue(b);
+  pdl_wait();
+
+  const float qscale = a.scale * 1.4426950408889634f;
+  const size_t pos_stride = 2 * kvd;
+  const size_t qkv_ld = size_t(a.H + 2 * a.Hkv) * HD;
+  const uint16_t* qrow = a.qkv + row * qkv_ld;
+  const int hl = lg % (G / 2);
+  const bool first_half = lg < G / 2;
+  const float2* rp = a.rope + (size_t)cur * (HD / 2) + hl * 8;
+  auto rope8 = [&](float (&x)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float other = __shfl_xor_sync(0xffffffffu, x[i], G / 2);
+      const float2 cs = rp[i];
+      const float r = first_half ? x[i] * cs.x - other * cs.y : x[i] * cs.x + other * cs.y;
+      x[i] = bf16_to_f(f_to_bf16(r));
+    }
+  };
+  auto load8 = [&](const uint16_t* src, float (&x)[8]) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src);
+    x[0] = bf16_lo(v.x); x[1] = bf16_hi(v.x); x[2] = bf16_lo(v.y); x[3] = bf16_hi(v.y);
+    x[4] = bf16_lo(v.z); x[5] = bf16_hi(v.z); x[6] = bf16_lo(v.w); x[7] = bf16_hi(v.w);
+  };
+  float q[GQ][8];
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+    load8(qrow + (size_t)(hk * GQ + h) * HD + lg * 8, q[h]);
+    rope8(q[h]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[h][i] *= qscale;
+  }
+  uint4 kc, vc;
+  {
+    float k8[8];
+    load8(qrow + (size_t)(a.H + hk) * HD + lg * 8, k8);
+    rope8(k8);
+    kc.x = pack_bf16x2(k8[0], k8[1]); kc.y = pack_bf16x2(k8[2], k8[3]);
+    kc.z = pack_bf16x2(k8[4], k8[5]); kc.w = pack_bf16x2(k8[6], k8[7]);
+    vc = *reinterpret_cast<const uint4*>(qrow + (size_t)(a.H + a.Hkv + hk) * HD + lg * 8);
+    if (grp == 0) {  // append (rotated k, raw v) to the cache for the next steps
+      uint16_t* kcp = const_cast<uint16_t*>(a.kv) + ((size_t)slot * a.max_ctx + cur) * pos_stride + hk * HD + lg * 8;
+      *reinterpret_cast<uint4*>(kcp) = kc;
+      *reinterpret_cast<uint4*>(kcp + kvd) = vc;
+    }
+  }
+
+  float m[GQ], l[GQ], acc[GQ][8];
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+    m[h] = -INFINITY;
+    l[h] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[h][i] = 0.f;
+  }
+  for (int b = 0; b < nbox; ++b) {
+    const int st = b % kTmaStages;
+    mbar_wait(&full[st], uint32_t(b / kTmaStages) & 1u);
+    const uint16_t* ks = ring + size_t(st) * 2 * kTmaPos * HD;
+    const uint16_t* vs = ks + kTmaPos * HD;
+    const int p0 = b * kTmaPos;
+#pragma unroll
+    for (int j0 = 0; j0 < kTmaPos / NG; j0 += U) {
+      uint4 kk[U], vv[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = grp + (j0 + u) * NG;  // row of the box
+        const int pos = p0 + r;
+        ok[u] = pos < len;
+        if (!ok[u]) {  // (stale or out-of-range rows may hold non-finite bytes: 0 * NaN)
+          kk[u] = make_uint4(0, 0, 0, 0);
+          vv[u] = make_uint4(0, 0, 0, 0);
+        } else if (pos == cur) {
+          kk[u] = kc;
+          vv[u] = vc;
+        } else {
+          kk[u] = *reinterpret_cast<const uint4*>(ks + r * HD + lg * 8);
+          vv[u] = *reinterpret_cast<const uint4*>(vs + r * HD + lg * 8);
+        }
+      }
+      float kf[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        kf[u][0] = bf16_lo(kk[u].x); kf[u][1] = bf16_hi(kk[u].x); kf[u][2] = bf16_lo(kk[u].y);
+        kf[u][3] = bf16_hi(kk[u].y); kf[u][4] = bf16_lo(kk[u].z); kf[u][5] = bf16_hi(kk[u].z);
+        kf[u][6] = bf16_lo(kk[u].w); kf[u][7] = bf16_hi(kk[u].w);
+      }
+#pragma unroll
+      for (int h = 0; h < GQ; ++h) {
+        float s[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          s[u] = q[h][0] * kf[u][0] + q[h][1] * kf[u][1] + q[h][2] * kf[u][2] + q[h][3] * kf[u][3] +
+                 q[h][4] * kf[u][4] + q[h][5] * kf[u][5] + q[h][6] * kf[u][6] + q[h][7] * kf[u][7];
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1)
+#pragma unroll
+          for (int u = 0; u < U; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+        float mx = m[h];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!ok[u]) s[u] = -INFINITY;
+          mx = fmaxf(mx, s[u]);
+        }
+        if (mx != -INFINITY) {
+          const float cf = exp2f(m[h] - mx);
+          l[h] *= cf;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[h][i] *= cf;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const float pr = exp2f(s[u] - mx);
+            l[h] += pr;
+            acc[h][0] += pr * bf16_lo(vv[u].x);
+            acc[h][1] += pr * bf16_hi(vv[u].x);
+            acc[h][2] += pr * bf16_lo(vv[u].y);
+            acc[h][3] += pr * bf16_hi(vv[u].y);
+            acc[h][4] += pr * bf16_lo(vv[u].z);
+            acc[h][5] += pr * bf16_hi(vv[u].z);
+            acc[h][6] += pr * bf16_lo(vv[u].w);
+            acc[h][7] += pr * bf16_hi(vv[u].w);
+          }
+          m[h] = mx;
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (threadIdx.x == 0 && b + kTmaStages < nbox) {
+      mbar_wait(&empty[st], uint32_t(b / kTmaStages) & 1u);  // every warp read stage st
+      issue(b + kTmaStages);
+    }
+  }
+  // merge the P groups of a warp, then the warps (as attn2)
+#pragma unroll
+  for (int h = 0; h < GQ; ++h) {
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m[h], o);
+      const float l2 = __shfl_xor_sync(0xffffffffu, l[h], o);
+      const float M = fmaxf(m[h], m2);
+      const float c1 = (m[h] == -INFINITY) ? 0.f : exp2f(m[h] - M);
+      const float c2 = (m2 == -INFINITY) ? 0.f : exp2f(m2 - M);
+      l[h] = l[h] * c1 + l2 * c2;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, acc[h][i], o);
+        acc[h][i] = acc[h][i] * c1 + a2 * c2;
+      }
+      m[h] = M;
+    }
+  }
+  if (pg == 0) {
+#pragma unroll
+    for (int h = 0; h < GQ; ++h) {
+      float* stt = sm2 + ((warp * GQ + h) * G + lg) * 10;
+      stt[0] = m[h];
+      stt[1] = l[h];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) stt[2 + i] = acc[h][i];
+    }
+  }
+  __syncthreads();
+  if (pg == 0) {
+    for (int h = warp; h < GQ; h += kAttnWarps) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int f = 0; f < kAttnWarps; ++f) M = fmaxf(M, sm2[((f * GQ + h) * G + lg) * 10]);
+      float L = 0.f, o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int f = 0; f < kAttnWarps; ++f) {
+        const float* stt = sm2 + ((f * GQ + h) * G + lg) * 10;
+        const float cw = (stt[0] == -INFINITY) ? 0.f : exp2f(stt[0] - M);
+        L += stt[1] * cw;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] += stt[2 + i] * cw;
+      }
+      const int qh = hk * GQ + h;
+      const float inv = 1.f / L;
+      uint4 ov;
+      ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
+      ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
+      ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
+      ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
+      *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
+    }
+  }
+}
+
+// [slot * max_ctx + pos][2 * Hkv * 128] bf16 view of a device KV block, boxes
+// of kTmaPos positions x one head's 128 dims (cached per block)
+static const CUtensorMap* kv_tma_map(const AttnArgs& a) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int, int>, CUtensorMap> cache;
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(static_cast<const void*>(a.kv), a.kv_slots, a.max_ctx, a.Hkv);
+  auto it = cache.find(key);
+  if (it != cache.end()) return &it->second;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const uint64_t cols = uint64_t(2) * a.Hkv * 128;
+  cuuint64_t dims[2] = {cols, uint64_t(a.kv_slots) * a.max_ctx};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {128, uint32_t(kTmaPos)};
+  cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(a.kv), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return nullptr;
+  if (cache.size() > 4096) cache.clear();
+  return &(cache[key] = m);
+}
+
+template <int GQ>
+static cudaError_t launch_attn_tma(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+  const size_t smem = size_t(kTmaStages) * 2 * kTmaPos * 128 * 2 + 2 * kTmaStages * 8 +
+                      size_t(kAttnWarps) * GQ * 16 * 10 * sizeof(float);
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tma_kernel<GQ, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem));
+    if (e != cudaSuccess) return e;
+    attr[dev & 63] = true;
+  }
+  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, 1), dim3(kAttnWarps * 32), smem, st, *tm, a);
+}
+
 template <int HD>
 static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t st) {
   // positions per CTA warmed into L2 before the PDL wait (-1.6% per B=256
@@ -327,6 +624,18 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
   // the GPU (measured best for decode batches), 8 for few long rows
   const long long total = ctas * nsplit;
   const int u = gq == 1 && total >= 8LL * num_sms ? 4 : 8;
+  // one split, hd 128, device-memory KV (kv_slots set by the runtime): the
+  // TMA-fed kernel; the plan depends on kind_T and the block only, so
+  // replicas of a layer run the same kernel as the unreplicated pass
+  if (HD == 128 && nsplit == 1 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4)) {
+    if (const CUtensorMap* tm = kv_tma_map(a)) {
+      switch (gq) {
+        case 1: return launch_attn_tma<1>(tm, a, st);
+        case 2: return launch_attn_tma<2>(tm, a, st);
+        case 4: return launch_attn_tma<4>(tm, a, st);
+      }
+    }
+  }
   cudaError_t e;
   {
     const dim3 g2(a.Hkv, a.T, nsplit);  // head-major grid

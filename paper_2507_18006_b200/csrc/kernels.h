@@ -130,7 +130,7 @@ struct AttnArgs {
   float scale;  // 1/sqrt(hd)
   int prefetch_pos;  // set by the launcher: cached positions per CTA prefetched to L2 before the PDL wait
   int qkv_rows;      // prefill: rows of the qkv buffer (TMA bounds)
-  int kv_slots;      // prefill: slots of the KV block (TMA bounds: kv_slots * max_ctx positions)
+  int kv_slots;      // slots of the KV block (TMA bounds: kv_slots * max_ctx positions); decode: 0 = host-mapped block
 };
 cudaError_t attention_launch(const AttnArgs& a, int num_sms, cudaStream_t st);
 

@@ -1103,6 +1103,7 @@ int attention_part(cb_model* m, LayerState& L, const Seg& s, const std::vector<i
   aa.ws_floats = wa.attn_ws_floats;
   aa.counters = wa.attn_cnt;
   aa.kind_T = m->cur_T;  // the split decision follows the whole pass, not this replica's rows
+  aa.kv_slots = kvb.host ? 0 : kvb.cap;  // device-memory block: the TMA-fed decode kernel may read it
   aa.T = T;
   aa.row_off = s.r0;
   aa.H = d.n_heads;
