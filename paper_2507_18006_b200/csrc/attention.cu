@@ -302,14 +302,17 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 // ---------------------------------------------------------------------------
 // attn_tma: the same CTA, lane-group mapping and arithmetic as attn2 (one
 // context split, hd 128, KV block in device memory), with K and V fed by TMA:
-// boxes of 64 cached positions x one head's 128 dims (16 KB each) from the
-// [slot * max_ctx + pos][k | v] view of the block, two K+V stages per CTA,
-// issued before griddepcontrol.wait (cached positions < cur were written by
-// earlier steps; the row's own k / v are substituted at `cur` as in attn2).
-// Bulk tensor loads read HBM at ~7 TB/s where 16-byte loads top out near
-// 6.2 (profiles/r02_read_bw.txt).
-constexpr int kTmaPos = 64;
-constexpr int kTmaStages = 2;
+// boxes of 32 cached positions x one head's 128 dims (8 KB each) from the
+// [slot * max_ctx + pos][k | v] view of the block, four K+V stages per CTA
+// (64 KB: three CTAs per SM; 2 x 64 positions, 3 x 64 and 8 x 32 measured
+// slower, profiles/r02_attn_tma_ab.txt), the first ones issued before
+// griddepcontrol.wait (cached positions < cur were written by earlier steps;
+// the row's own k / v are substituted at `cur` as in attn2).  Bulk tensor
+// loads read HBM at ~7 TB/s where 16-byte loads top out near 6.2
+// (profiles/r02_read_bw.txt).  A group's positions and their order (chunks of
+// U = 4) are attn2's, so the arithmetic matches attn2 with u = 4.
+constexpr int kTmaPos = 32;
+constexpr int kTmaStages = 4;
 
 template <int GQ, int U>
 __global__ void __launch_bounds__(kAttnWarps * 32)
