@@ -26,6 +26,9 @@ int cbt_attention(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const 
 int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* out, const int32_t* row_slot,
                         const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,
                         float theta);
+/* slots of the KV buffer cbt_attention_fused may view through TMA: 0 (default) = the 16-byte-load kernel,
+   > 0 lets the launcher pick the TMA-fed decode kernel (one context split, hd 128) */
+int cbt_attention_set_kv_slots(int32_t n);
 /* ms per launch of `iters` back-to-back attention launches (max_len given, no host sync inside) */
 int cbt_attention_bench(const uint16_t* qkv, const uint16_t* kv, uint16_t* out, const int32_t* row_slot,
                         const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd, int32_t max_ctx,

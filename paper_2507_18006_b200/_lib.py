@@ -149,6 +149,7 @@ _SIGS = {
     "cbt_attention": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "cbt_attention_fused": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_float]),
+    "cbt_attention_set_kv_slots": (C.c_int, [C.c_int32]),
     "cbt_attention_bench": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_int32, C.c_int32, _F32P]),
     "cbt_argmax": (C.c_int, [_P, _P, C.c_int32, C.c_int32]),

@@ -249,6 +249,14 @@ float2* rope_table_dev(int max_ctx, int hd, float theta) {
 }
 }  // namespace
 
+// slots of the KV buffer the fused decode attention may view through TMA (0 = the
+// 16-byte-load kernel; > 0 lets attention_launch pick the TMA-fed kernel)
+static int g_attn_kv_slots = 0;
+extern "C" int cbt_attention_set_kv_slots(int32_t n) {
+  g_attn_kv_slots = n < 0 ? 0 : n;
+  return CB_OK;
+}
+
 extern "C" int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* out, const int32_t* row_slot,
                                    const int32_t* row_pos, int32_t T, int32_t H, int32_t Hkv, int32_t hd,
                                    int32_t max_ctx, float theta) {
@@ -278,6 +286,7 @@ extern "C" int cbt_attention_fused(const uint16_t* qkv, uint16_t* kv, uint16_t* 
   a.max_len = max_len;
   a.scale = 1.0f / std::sqrt(float(hd));
   a.rope = dtab;
+  a.kv_slots = g_attn_kv_slots;
   r = finish(cb::attention_launch(a, ws->sms, 0));
   cudaFree(dtab);
   return r;

@@ -398,3 +398,46 @@ def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
         assert np.isfinite(got).all(), sl
         assert np.abs(got - ref).max() <= 2e-2 * max(1.0, np.abs(ref).max()), (sl, np.abs(got - ref).max())
         row += L
+
+
+@pytest.mark.parametrize("T,H,Hkv,lens", [(64, 32, 32, None), (48, 32, 8, [1, 31, 32, 33, 64, 100, 128]),
+                                         (40, 32, 32, [1, 31, 32, 33, 200])])
+def test_tma_decode_attention_matches_load_kernel(lib, cuda, T, H, Hkv, lens):
+    """The TMA-fed decode attention (32-position K / V boxes) against the
+    16-byte-load kernel on the same inputs: output and appended cache row
+    bit-identical where the load kernel also takes 4 positions per step (MHA
+    with >= 8 waves of CTAs), within bf16 rounding otherwise; cache rows past
+    each sequence poisoned with NaN (a box may cover them) never reach the
+    output."""
+    torch = cuda
+    hd = 128
+    if lens is None:
+        g = torch.Generator().manual_seed(T)
+        lens = torch.randint(1, 300, (T,), generator=g).tolist()
+    lens = (lens * (T // len(lens) + 1))[:T]
+    max_ctx = max(lens) + 40
+    qkv = _bf16(torch, (T, (H + 2 * Hkv) * hd), 1.0, 41).cuda()
+    kv = _bf16(torch, (T, max_ctx, 2, Hkv * hd), 1.0, 42)
+    for i, L in enumerate(lens):
+        kv[i, L:] = float("nan")  # stale rows past the sequence (the current position is written by the kernel)
+    kv = kv.cuda()
+    row_slot = torch.arange(T, dtype=torch.int32, device="cuda")
+    row_pos = torch.tensor([L - 1 for L in lens], dtype=torch.int32, device="cuda")
+    outs, kvs = [], []
+    for slots in (0, T):
+        q_, kv_ = qkv.clone(), kv.clone()
+        out = torch.zeros(T, H * hd, dtype=torch.bfloat16, device="cuda")
+        assert lib.cbt_attention_set_kv_slots(slots) == 0
+        try:
+            assert lib.cbt_attention_fused(_ptr(q_), _ptr(kv_), _ptr(out), _ptr(row_slot), _ptr(row_pos), T, H, Hkv,
+                                           hd, max_ctx, C.c_float(1e4)) == 0
+        finally:
+            lib.cbt_attention_set_kv_slots(0)
+        outs.append(out)
+        kvs.append(kv_)
+    assert torch.isfinite(outs[1].float()).all()
+    assert torch.equal(kvs[0].nan_to_num(7.0), kvs[1].nan_to_num(7.0))  # the appended rows
+    if Hkv == H and T * Hkv >= 8 * 148:
+        assert torch.equal(outs[0], outs[1])
+    else:
+        assert (outs[0].float() - outs[1].float()).abs().max().item() <= 2e-2
