@@ -550,20 +550,23 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 
 // [slot * max_ctx + pos][2 * Hkv * 128] bf16 view of a device KV block, boxes
 // of kTmaPos positions x one head's 128 dims (cached per block)
-static const CUtensorMap* kv_tma_map(const AttnArgs& a) {
+static bool kv_tma_map(const AttnArgs& a, CUtensorMap* out) {
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, int, int>, CUtensorMap> cache;
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   std::lock_guard<std::mutex> lk(mu);
   const auto key = std::make_tuple(static_cast<const void*>(a.kv), a.kv_slots, a.max_ctx, a.Hkv);
   auto it = cache.find(key);
-  if (it != cache.end()) return &it->second;
+  if (it != cache.end()) {
+    *out = it->second;  // (by value: the cache may be cleared by a later call)
+    return true;
+  }
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
         q != cudaDriverEntryPointSuccess)
-      return nullptr;
+      return false;
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const uint64_t cols = uint64_t(2) * a.Hkv * 128;
@@ -575,13 +578,15 @@ static const CUtensorMap* kv_tma_map(const AttnArgs& a) {
   if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(a.kv), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return nullptr;
+    return false;
   if (cache.size() > 4096) cache.clear();
-  return &(cache[key] = m);
+  cache[key] = m;
+  *out = m;
+  return true;
 }
 
 template <int GQ>
-static cudaError_t launch_attn_tma(const CUtensorMap* tm, const AttnArgs& a, cudaStream_t st) {
+static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, cudaStream_t st) {
   const size_t smem = size_t(kTmaStages) * 2 * kTmaPos * 128 * 2 + 2 * kTmaStages * 8 +
                       size_t(kAttnWarps) * GQ * 16 * 10 * sizeof(float);
   static bool attr[64] = {};
@@ -593,7 +598,7 @@ static cudaError_t launch_attn_tma(const CUtensorMap* tm, const AttnArgs& a, cud
     if (e != cudaSuccess) return e;
     attr[dev & 63] = true;
   }
-  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, 1), dim3(kAttnWarps * 32), smem, st, *tm, a);
+  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, 1), dim3(kAttnWarps * 32), smem, st, tm, a);
 }
 
 template <int HD>
@@ -631,7 +636,8 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
   // TMA-fed kernel; the plan depends on kind_T and the block only, so
   // replicas of a layer run the same kernel as the unreplicated pass
   if (HD == 128 && nsplit == 1 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4)) {
-    if (const CUtensorMap* tm = kv_tma_map(a)) {
+    CUtensorMap tm;
+    if (kv_tma_map(a, &tm)) {
       switch (gq) {
         case 1: return launch_attn_tma<1>(tm, a, st);
         case 2: return launch_attn_tma<2>(tm, a, st);
