@@ -300,8 +300,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 }
 
 // ---------------------------------------------------------------------------
-// attn_tma: the same CTA, lane-group mapping and arithmetic as attn2 (one
-// context split, hd 128, KV block in device memory), with K and V fed by TMA:
+// attn_tma: the same CTA, lane-group mapping and arithmetic as attn2 (hd 128,
+// KV block in device memory; context splits on whole boxes, merged by the
+// last split CTA as in attn2), with K and V fed by TMA:
 // boxes of 32 cached positions x one head's 128 dims (8 KB each) from the
 // [slot * max_ctx + pos][k | v] view of the block, four K+V stages per CTA
 // (64 KB: three CTAs per SM; 2 x 64 positions, 3 x 64 and 8 x 32 measured
@@ -316,7 +317,7 @@ constexpr int kTmaStages = 4;
 
 template <int GQ, int U>
 __global__ void __launch_bounds__(kAttnWarps * 32)
-    attn_tma_kernel(const __grid_constant__ CUtensorMap tkv, const AttnArgs a) {
+    attn_tma_kernel(const __grid_constant__ CUtensorMap tkv, const AttnArgs a, int nsplit, int chunk) {
   constexpr int HD = 128;
   constexpr int G = HD / 8;           // lanes per group
   constexpr int P = 32 / G;           // groups per warp
@@ -328,7 +329,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   uint64_t* empty = full + kTmaStages;
   float* sm2 = reinterpret_cast<float*>(empty + kTmaStages);  // [kAttnWarps][GQ][G][10]
   pdl_trigger();
-  const int hk = blockIdx.x, rl = blockIdx.y;
+  const int hk = blockIdx.x, rl = blockIdx.y, split = blockIdx.z;
   const int row = a.row_off + rl;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lg = lane % G, pg = lane / G;
@@ -336,7 +337,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   const int slot = a.kv_map ? a.kv_map[a.row_slot[row]] : a.row_slot[row];
   const int len = a.row_pos[row] + 1;
   const int cur = len - 1;
-  const int nbox = (len + kTmaPos - 1) / kTmaPos;
+  // this split's positions [p_begin, p_end) (chunk: a multiple of kTmaPos)
+  const int p_begin = split * chunk;
+  const int p_end = min(len, p_begin + chunk);
+  const int box0 = p_begin / kTmaPos;
+  const int nbox = p_end > p_begin ? (p_end - p_begin + kTmaPos - 1) / kTmaPos : 0;
   const size_t kvd = size_t(a.Hkv) * HD;
   const int prow = slot * a.max_ctx;  // view row of position 0
   if (threadIdx.x == 0) {
@@ -353,8 +358,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     const int st = b % kTmaStages;
     uint16_t* kd = ring + size_t(st) * 2 * kTmaPos * HD;
     mbar_arrive_expect_tx(&full[st], 2 * kBoxBytes);
-    tma_load_2d(&tkv, &full[st], kd, hk * HD, prow + b * kTmaPos, pol);
-    tma_load_2d(&tkv, &full[st], kd + kTmaPos * HD, int(kvd) + hk * HD, prow + b * kTmaPos, pol);
+    tma_load_2d(&tkv, &full[st], kd, hk * HD, prow + (box0 + b) * kTmaPos, pol);
+    tma_load_2d(&tkv, &full[st], kd + kTmaPos * HD, int(kvd) + hk * HD, prow + (box0 + b) * kTmaPos, pol);
   };
   if (threadIdx.x == 0)
     for (int b = 0; b < nbox && b < kTmaStages; ++b) issue(b);
@@ -389,8 +394,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[h][i] *= qscale;
   }
-  uint4 kc, vc;
-  {
+  uint4 kc = make_uint4(0, 0, 0, 0), vc = make_uint4(0, 0, 0, 0);
+  if (p_begin <= cur && cur < p_end) {
     float k8[8];
     load8(qrow + (size_t)(a.H + hk) * HD + lg * 8, k8);
     rope8(k8);
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     mbar_wait(&full[st], uint32_t(b / kTmaStages) & 1u);
     const uint16_t* ks = ring + size_t(st) * 2 * kTmaPos * HD;
     const uint16_t* vs = ks + kTmaPos * HD;
-    const int p0 = b * kTmaPos;
+    const int p0 = (box0 + b) * kTmaPos;
 #pragma unroll
     for (int j0 = 0; j0 < kTmaPos / NG; j0 += U) {
       uint4 kk[U], vv[U];
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       for (int u = 0; u < U; ++u) {
         const int r = grp + (j0 + u) * NG;  // row of the box
         const int pos = p0 + r;
-        ok[u] = pos < len;
+        ok[u] = pos < p_end;
         if (!ok[u]) {  // (stale or out-of-range rows may hold non-finite bytes: 0 * NaN)
           kk[u] = make_uint4(0, 0, 0, 0);
           vv[u] = make_uint4(0, 0, 0, 0);
@@ -537,13 +542,52 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         for (int i = 0; i < 8; ++i) o[i] += stt[2 + i] * cw;
       }
       const int qh = hk * GQ + h;
-      const float inv = 1.f / L;
-      uint4 ov;
-      ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
-      ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
-      ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
-      ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
-      *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
+      if (nsplit == 1) {
+        const float inv = 1.f / L;
+        uint4 ov;
+        ov.x = pack_bf16x2(o[0] * inv, o[1] * inv);
+        ov.y = pack_bf16x2(o[2] * inv, o[3] * inv);
+        ov.z = pack_bf16x2(o[4] * inv, o[5] * inv);
+        ov.w = pack_bf16x2(o[6] * inv, o[7] * inv);
+        *reinterpret_cast<uint4*>(a.out + (size_t)row * a.H * HD + (size_t)qh * HD + lg * 8) = ov;
+      } else {
+        float* stt = a.ws + (((size_t)rl * a.H + qh) * nsplit + split) * (HD + 2);
+        if (lg == 0) {
+          stt[0] = M;
+          stt[1] = L;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) stt[2 + lg * 8 + i] = o[i];
+      }
+    }
+  }
+  if (nsplit > 1) {  // the last split CTA of (row, kv head) merges, in split order (as attn2)
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      int* cnt = a.counters + (size_t)rl * a.Hkv + hk;
+      s_last = atomicAdd(cnt, 1) == nsplit - 1;
+      if (s_last) *cnt = 0;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      for (int idx = threadIdx.x; idx < GQ * HD; idx += kAttnWarps * 32) {
+        const int h = idx / HD, i = idx % HD;
+        const int qh = hk * GQ + h;
+        const float* st = a.ws + ((size_t)rl * a.H + qh) * nsplit * (HD + 2);
+        float M = -INFINITY;
+        for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, __ldcg(st + sp * (HD + 2)));
+        float L = 0.f, o = 0.f;
+        for (int sp = 0; sp < nsplit; ++sp) {
+          const float ms = __ldcg(st + sp * (HD + 2));
+          const float c = (ms == -INFINITY) ? 0.f : exp2f(ms - M);
+          L += __ldcg(st + sp * (HD + 2) + 1) * c;
+          o += __ldcg(st + sp * (HD + 2) + 2 + i) * c;
+        }
+        a.out[(size_t)row * a.H * HD + (size_t)qh * HD + i] = f_to_bf16(o / L);
+      }
     }
   }
 }
@@ -586,7 +630,8 @@ static bool kv_tma_map(const AttnArgs& a, CUtensorMap* out) {
 }
 
 template <int GQ>
-static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, cudaStream_t st) {
+static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, int nsplit, int chunk,
+                                   cudaStream_t st) {
   const size_t smem = size_t(kTmaStages) * 2 * kTmaPos * 128 * 2 + 2 * kTmaStages * 8 +
                       size_t(kAttnWarps) * GQ * 16 * 10 * sizeof(float);
   static bool attr[64] = {};
@@ -598,7 +643,8 @@ static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, cud
     if (e != cudaSuccess) return e;
     attr[dev & 63] = true;
   }
-  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, 1), dim3(kAttnWarps * 32), smem, st, tm, a);
+  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, nsplit), dim3(kAttnWarps * 32), smem, st, tm, a,
+                    nsplit, chunk);
 }
 
 template <int HD>
@@ -632,16 +678,19 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
   // the GPU (measured best for decode batches), 8 for few long rows
   const long long total = ctas * nsplit;
   const int u = gq == 1 && total >= 8LL * num_sms ? 4 : 8;
-  // one split, hd 128, device-memory KV (kv_slots set by the runtime): the
-  // TMA-fed kernel; the plan depends on kind_T and the block only, so
-  // replicas of a layer run the same kernel as the unreplicated pass
-  if (HD == 128 && nsplit == 1 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4)) {
+  // hd 128, device-memory KV (kv_slots set by the runtime): the TMA-fed
+  // kernel; the plan depends on kind_T and the block only, so replicas of a
+  // layer run the same kernel as the unreplicated pass
+  if (HD == 128 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4)) {
     CUtensorMap tm;
     if (kv_tma_map(a, &tm)) {
+      // context splits on whole boxes
+      const int tchunk = (chunk + kTmaPos - 1) / kTmaPos * kTmaPos;
+      const int tsplit = (a.max_len + tchunk - 1) / tchunk;
       switch (gq) {
-        case 1: return launch_attn_tma<1>(tm, a, st);
-        case 2: return launch_attn_tma<2>(tm, a, st);
-        case 4: return launch_attn_tma<4>(tm, a, st);
+        case 1: return launch_attn_tma<1>(tm, a, tsplit, tchunk, st);
+        case 2: return launch_attn_tma<2>(tm, a, tsplit, tchunk, st);
+        case 4: return launch_attn_tma<4>(tm, a, tsplit, tchunk, st);
       }
     }
   }

@@ -401,14 +401,16 @@ def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
 
 
 @pytest.mark.parametrize("T,H,Hkv,lens", [(64, 32, 32, None), (48, 32, 8, [1, 31, 32, 33, 64, 100, 128]),
-                                         (40, 32, 32, [1, 31, 32, 33, 200])])
+                                         (40, 32, 32, [1, 31, 32, 33, 200]), (2, 32, 32, [300, 1000]),
+                                         (3, 32, 8, [500, 129, 33]), (1, 32, 32, [4096])])
 def test_tma_decode_attention_matches_load_kernel(lib, cuda, T, H, Hkv, lens):
     """The TMA-fed decode attention (32-position K / V boxes) against the
     16-byte-load kernel on the same inputs: output and appended cache row
     bit-identical where the load kernel also takes 4 positions per step (MHA
-    with >= 8 waves of CTAs), within bf16 rounding otherwise; cache rows past
-    each sequence poisoned with NaN (a box may cover them) never reach the
-    output."""
+    with >= 8 waves of CTAs), within bf16 rounding otherwise (GQA, few rows
+    with long contexts split over whole boxes and merged by the last split);
+    cache rows past each sequence poisoned with NaN (a box may cover them)
+    never reach the output."""
     torch = cuda
     hd = 128
     if lens is None:
