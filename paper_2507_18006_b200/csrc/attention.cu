@@ -629,7 +629,7 @@ static bool kv_tma_map(const AttnArgs& a, CUtensorMap* out) {
   return true;
 }
 
-template <int GQ>
+template <int GQ, int U = 4>
 static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, int nsplit, int chunk,
                                    cudaStream_t st) {
   const size_t smem = size_t(kTmaStages) * 2 * kTmaPos * 128 * 2 + 2 * kTmaStages * 8 +
@@ -638,12 +638,12 @@ static cudaError_t launch_attn_tma(const CUtensorMap& tm, const AttnArgs& a, int
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tma_kernel<GQ, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(attn_tma_kernel<GQ, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;
     attr[dev & 63] = true;
   }
-  return launch_pdl(attn_tma_kernel<GQ, 4>, dim3(a.Hkv, a.T, nsplit), dim3(kAttnWarps * 32), smem, st, tm, a,
+  return launch_pdl(attn_tma_kernel<GQ, U>, dim3(a.Hkv, a.T, nsplit), dim3(kAttnWarps * 32), smem, st, tm, a,
                     nsplit, chunk);
 }
 
@@ -681,7 +681,7 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
   // hd 128, device-memory KV (kv_slots set by the runtime): the TMA-fed
   // kernel; the plan depends on kind_T and the block only, so replicas of a
   // layer run the same kernel as the unreplicated pass
-  if (HD == 128 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4)) {
+  if (HD == 128 && a.rope && a.kv_slots > 0 && (gq == 1 || gq == 2 || gq == 4 || gq == 8)) {
     CUtensorMap tm;
     if (kv_tma_map(a, &tm)) {
       // context splits on whole boxes
@@ -691,6 +691,7 @@ static cudaError_t attention_hd(const AttnArgs& a_in, int num_sms, cudaStream_t 
         case 1: return launch_attn_tma<1>(tm, a, tsplit, tchunk, st);
         case 2: return launch_attn_tma<2>(tm, a, tsplit, tchunk, st);
         case 4: return launch_attn_tma<4>(tm, a, tsplit, tchunk, st);
+        case 8: return launch_attn_tma<8, 2>(tm, a, tsplit, tchunk, st);  // (attn2's 2 positions per step at gq 8)
       }
     }
   }

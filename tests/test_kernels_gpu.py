@@ -402,7 +402,8 @@ def test_prefill_attention_causal(lib, cuda, H, Hkv, hd, lens):
 
 @pytest.mark.parametrize("T,H,Hkv,lens", [(64, 32, 32, None), (48, 32, 8, [1, 31, 32, 33, 64, 100, 128]),
                                          (40, 32, 32, [1, 31, 32, 33, 200]), (2, 32, 32, [300, 1000]),
-                                         (3, 32, 8, [500, 129, 33]), (1, 32, 32, [4096])])
+                                         (3, 32, 8, [500, 129, 33]), (1, 32, 32, [4096]),
+                                         (4, 64, 8, [700, 130, 33, 1]), (40, 64, 8, [1, 32, 64, 100, 128])])
 def test_tma_decode_attention_matches_load_kernel(lib, cuda, T, H, Hkv, lens):
     """The TMA-fed decode attention (32-position K / V boxes) against the
     16-byte-load kernel on the same inputs: output and appended cache row
